@@ -1,0 +1,168 @@
+/*
+ * smpm_b200.h — C ABI of the B200-native deflated block-Jacobi Schur-GMRES
+ * solve (SMPM Poisson-Neumann / per-Fourier-mode Helmholtz).
+ *
+ * Drop-in boundary for the reference library `smpm` (C++20/Eigen,
+ * /root/reference/proj). Each entry point replaces the reference routine
+ * cited beside it. Plain pointers and sizes only; no torch types.
+ *
+ * Layout conventions:
+ *  - A *batch* holds `nsys` independent Schur systems of one geometry
+ *    (n GLL points, m_x strips, m_z elements per strip): the 2D Poisson
+ *    system (nsys = 1) or the per-wavenumber systems of the Fourier
+ *    extension. w = n*m_z, d = m_x-1 interfaces, k = 2*w*d interface slots.
+ *  - Interface vectors use the reference slot order
+ *    (/root/reference/proj/include/smpm/mesh.hpp:43-47): slot
+ *    i*2w + side*w + ez*n + iz. Batched vectors are nsys x k, system-major,
+ *    contiguous. Coarse vectors are nsys x d.
+ *  - Coupling matrices are column-major (Eigen default) per strip kind:
+ *    G_W (w x w)   west-boundary strip: east-readers x east-own columns
+ *    G_I (2w x 2w) interior strip: rows [west-readers; east-readers],
+ *                  cols [west-own; east-own]
+ *    G_E (w x w)   east-boundary strip: west-readers x west-own columns
+ *    exactly the per-kind block `build_kind_coupling` produces
+ *    (/root/reference/proj/src/schur.cpp:19-69).
+ *  - Vector arguments of the operator entry points are DEVICE pointers
+ *    (cudaMalloc'd, 16-byte aligned); `stream` is a cudaStream_t (NULL =
+ *    the context's stream). The *_host solve entry points take host
+ *    pointers and include the copies.
+ *
+ * Errors: every call returns an smpm_status; smpm_last_error() describes the
+ * last failure on the calling thread. SMPM_EINVAL mirrors the reference's
+ * std::invalid_argument, SMPM_ENONFINITE / SMPM_ESINGULAR / SMPM_ERUNTIME
+ * its std::runtime_error cases; non-convergence is reported in
+ * smpm_report.converged, never as an error (proj/src/gmres.cpp:137).
+ * There is no CPU fallback: without a usable sm_100 device every call that
+ * needs one fails with SMPM_ECUDA.
+ */
+#ifndef SMPM_B200_H
+#define SMPM_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SMPM_OK = 0,
+  SMPM_EINVAL = 1,
+  SMPM_ERUNTIME = 2,
+  SMPM_ENONFINITE = 3,
+  SMPM_ESINGULAR = 4,
+  SMPM_ECUDA = 5,
+  SMPM_ENCCL = 6
+} smpm_status;
+
+/* proj/include/smpm/solver.hpp:11 (Method) */
+typedef enum { SMPM_SCHUR = 0, SMPM_BJ = 1, SMPM_DBJ = 2, SMPM_2LAS = 3 } smpm_method;
+
+/* Arnoldi orthogonalization used on the device. The reference uses
+ * Householder reflections (proj/src/gmres.cpp:58-68); both variants span the
+ * same Krylov space. */
+typedef enum { SMPM_ORTH_CGS2 = 0, SMPM_ORTH_MGS = 1 } smpm_orth;
+
+typedef struct smpm_ctx smpm_ctx;
+typedef struct smpm_batch smpm_batch;
+
+/* proj/include/smpm/gmres.hpp:20-28 (KrylovReport) + proj/include/smpm/deflation.hpp:44-48 */
+typedef struct {
+  int iterations;
+  int converged;
+  int mismatch_warning;
+  int history_len;                /* entries written to the history buffer */
+  long long operator_applies;
+  long long krylov_s_applies;     /* S applications inside the GMRES call */
+  double final_rel_residual;
+  double wall_time_s;             /* device time of the whole batched solve */
+} smpm_report;
+
+/* proj/include/smpm/gmres.hpp:12-18 (GmresOptions) + driver arguments of
+ * deflated_solve / two_level_schwarz_solve (proj/include/smpm/deflation.hpp:55-61) */
+typedef struct {
+  double tol;          /* relative to ||b_S|| (proj/src/deflation.cpp:109) */
+  int max_iter;        /* total Arnoldi steps */
+  int restart;         /* 0 = never restart (reference); m = GMRES(m) */
+  int orth;            /* smpm_orth */
+  int fuse_deflation;  /* 1: P applied through O(k) row-sum identities (one S per dbj step); 0: literal */
+  int final_residual_check; /* 1 as the reference default */
+} smpm_solve_options;
+
+const char* smpm_last_error(void);
+/* version string incl. the arch the kernels were built for */
+const char* smpm_version(void);
+
+/* ---- context / batch lifecycle ------------------------------------------ */
+int smpm_ctx_create(int device, smpm_ctx** out);
+int smpm_ctx_destroy(smpm_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) */
+void* smpm_ctx_stream(smpm_ctx* ctx);
+
+int smpm_batch_create(smpm_ctx* ctx, int n, int m_x, int m_z, int nsys, smpm_batch** out);
+int smpm_batch_destroy(smpm_batch* b);
+/* k, d, w of the batch geometry */
+int smpm_batch_dims(const smpm_batch* b, long long* k, int* d, int* w);
+
+/* Per-kind couplings of system `sys` (host pointers, column-major, see
+ * layout above). Replaces the interface-block storage of SchurSystem
+ * (proj/include/smpm/schur.hpp:32-36): the reference copies these blocks
+ * verbatim into every interface (proj/src/schur.cpp:113-124). G_I is
+ * ignored when m_x == 2. */
+int smpm_batch_set_couplings(smpm_batch* b, int sys, const double* G_W, const double* G_I, const double* G_E);
+
+/* Reference-layout import: the d interface blocks of one SchurSystem
+ * (proj/include/smpm/schur.hpp:32-36 / dump format proj/src/schur.cpp:246-297):
+ * entries[i] is column-major rows_i x 2w, segment starts/lengths as in
+ * InterfaceBlock::row_segments. The blocks are verified to be copies of at
+ * most three strip-kind couplings and deduplicated into them. */
+int smpm_batch_set_interface_blocks(smpm_batch* b, int sys, const double* const* entries, const long long* rows,
+                                    const long long* const* seg_start, const long long* const* seg_len,
+                                    const int* nseg);
+
+/* Left null vector u_S of a singular system (the j = 0 / Poisson system):
+ * marks the system singular; the coarse solve uses the rank-one shift
+ * (C + u_C u_C^T) with u_C = normalize(Z^T u_S) (proj/src/deflation.cpp:44-54). */
+int smpm_batch_set_nullspace(smpm_batch* b, int sys, const double* u_S);
+
+/* Uploads, builds the block-Jacobi inverses (proj/src/schur.cpp:188-216),
+ * the coarse matrices C = Z^T S Z and their solvers (proj/src/deflation.cpp:24-69). */
+int smpm_batch_finalize(smpm_batch* b);
+
+/* Coarse matrices (nsys x d x d, column-major) and tridiagonal flags, host out */
+int smpm_batch_coarse_info(smpm_batch* b, double* C, int* tridiagonal, int* singular);
+
+/* ---- operators: device pointers, nsys x k (x_d: nsys x d) ----------------- */
+int smpm_apply_S(smpm_batch* b, const double* v, double* y, void* stream);                 /* proj/src/schur.cpp:143-158 */
+int smpm_apply_St(smpm_batch* b, const double* v, double* y, void* stream);                /* proj/src/schur.cpp:160-175 */
+int smpm_apply_block_jacobi_inv(smpm_batch* b, const double* v, double* y, void* stream);  /* proj/src/schur.cpp:218-225 */
+int smpm_apply_Z(smpm_batch* b, const double* y_d, double* v, void* stream);               /* proj/src/deflation.cpp:8-14 */
+int smpm_apply_Zt(smpm_batch* b, const double* v, double* y_d, void* stream);              /* proj/src/deflation.cpp:16-22 */
+int smpm_coarse_solve(smpm_batch* b, const double* b_d, double* x_d, void* stream);        /* proj/src/deflation.cpp:71-92 */
+int smpm_apply_P(smpm_batch* b, const double* v, double* y, int fused, void* stream);      /* proj/src/deflation.cpp:94-96 */
+int smpm_apply_Q(smpm_batch* b, const double* v, double* y, void* stream);                 /* proj/src/deflation.cpp:98-100 */
+/* out = v - dir (dir . v) per system; dir is nsys x len (proj/src/nullspace.cpp:92) */
+int smpm_project_out(smpm_batch* b, long long len, const double* v, const double* dir, double* out, void* stream);
+
+/* ---- solves --------------------------------------------------------------- */
+/* Batched solve of S x_S = b_S for every system of the batch with `method`
+ * (dbj: proj/src/deflation.cpp:102-122, 2las: :124-143, bj: proj/src/gmres.cpp:144-150,
+ * schur: proj/src/solver.cpp:56-64). b_S, x_S: device, nsys x k. reports: host,
+ * nsys entries (nullable). history: host, nsys x (max_iter + 2) (nullable). */
+int smpm_solve(smpm_batch* b, int method, const double* b_S, double* x_S, const smpm_solve_options* opt,
+               smpm_report* reports, double* history, void* stream);
+int smpm_deflated_solve(smpm_batch* b, const double* b_S, double* x_S, const smpm_solve_options* opt,
+                        smpm_report* reports, double* history, void* stream);
+int smpm_two_level_schwarz_solve(smpm_batch* b, const double* b_S, double* x_S, const smpm_solve_options* opt,
+                                 smpm_report* reports, double* history, void* stream);
+/* Same as smpm_solve with HOST b_S / x_S: the H2D and D2H copies are inside
+ * the call (the reference-facing end-to-end path). */
+int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x_S_host,
+                    const smpm_solve_options* opt, smpm_report* reports, double* history);
+
+/* Number of kernels this library launched since the batch was created
+ * (instrumentation for bench.py's gpu_launches). */
+long long smpm_batch_launch_count(const smpm_batch* b);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMPM_B200_H */

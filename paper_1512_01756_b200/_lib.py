@@ -1,0 +1,105 @@
+"""ctypes binding of the in-tree C-ABI library ``lib/libsmpm_b200.so``.
+
+The product path has no CPU fallback: if the library or a usable sm_100
+device is missing, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libsmpm_b200.so")
+
+SMPM_SCHUR, SMPM_BJ, SMPM_DBJ, SMPM_2LAS = 0, 1, 2, 3
+METHODS = {"schur": SMPM_SCHUR, "bj": SMPM_BJ, "dbj": SMPM_DBJ, "2las": SMPM_2LAS}
+ORTH = {"cgs2": 0, "mgs": 1}
+STATUS = {0: "OK", 1: "EINVAL", 2: "ERUNTIME", 3: "ENONFINITE", 4: "ESINGULAR", 5: "ECUDA", 6: "ENCCL"}
+
+# every symbol include/smpm_b200.h declares
+EXPORTS = [
+    "smpm_last_error", "smpm_version", "smpm_ctx_create", "smpm_ctx_destroy", "smpm_ctx_stream",
+    "smpm_batch_create", "smpm_batch_destroy", "smpm_batch_dims", "smpm_batch_set_couplings",
+    "smpm_batch_set_interface_blocks", "smpm_batch_set_nullspace", "smpm_batch_finalize",
+    "smpm_batch_coarse_info", "smpm_apply_S", "smpm_apply_St", "smpm_apply_block_jacobi_inv", "smpm_apply_Z",
+    "smpm_apply_Zt", "smpm_coarse_solve", "smpm_apply_P", "smpm_apply_Q", "smpm_project_out", "smpm_solve",
+    "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_batch_launch_count",
+]
+
+
+class SmpmError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"smpm_b200 {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Report(C.Structure):
+    """smpm_report (KrylovReport + krylov_s_applies)."""
+    _fields_ = [
+        ("iterations", C.c_int),
+        ("converged", C.c_int),
+        ("mismatch_warning", C.c_int),
+        ("history_len", C.c_int),
+        ("operator_applies", C.c_longlong),
+        ("krylov_s_applies", C.c_longlong),
+        ("final_rel_residual", C.c_double),
+        ("wall_time_s", C.c_double),
+    ]
+
+
+class SolveOptions(C.Structure):
+    _fields_ = [
+        ("tol", C.c_double),
+        ("max_iter", C.c_int),
+        ("restart", C.c_int),
+        ("orth", C.c_int),
+        ("fuse_deflation", C.c_int),
+        ("final_residual_check", C.c_int),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load the library (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise SmpmError(5, f"{LIB_PATH} is missing; run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    vp, dp, ip, llp = C.c_void_p, C.c_void_p, C.c_int, C.c_longlong
+    L.smpm_last_error.restype = C.c_char_p
+    L.smpm_version.restype = C.c_char_p
+    L.smpm_ctx_create.argtypes = [ip, C.POINTER(vp)]
+    L.smpm_ctx_destroy.argtypes = [vp]
+    L.smpm_ctx_stream.restype = vp
+    L.smpm_ctx_stream.argtypes = [vp]
+    L.smpm_batch_create.argtypes = [vp, ip, ip, ip, ip, C.POINTER(vp)]
+    L.smpm_batch_destroy.argtypes = [vp]
+    L.smpm_batch_dims.argtypes = [vp, C.POINTER(llp), C.POINTER(ip), C.POINTER(ip)]
+    L.smpm_batch_set_couplings.argtypes = [vp, ip, dp, dp, dp]
+    L.smpm_batch_set_interface_blocks.argtypes = [vp, ip, C.POINTER(dp), C.POINTER(llp), C.POINTER(C.c_void_p),
+                                                  C.POINTER(C.c_void_p), C.POINTER(ip)]
+    L.smpm_batch_set_nullspace.argtypes = [vp, ip, dp]
+    L.smpm_batch_finalize.argtypes = [vp]
+    L.smpm_batch_coarse_info.argtypes = [vp, dp, C.POINTER(ip), C.POINTER(ip)]
+    for f in ("smpm_apply_S", "smpm_apply_St", "smpm_apply_block_jacobi_inv", "smpm_apply_Z", "smpm_apply_Zt",
+              "smpm_coarse_solve", "smpm_apply_Q"):
+        getattr(L, f).argtypes = [vp, dp, dp, vp]
+    L.smpm_apply_P.argtypes = [vp, dp, dp, ip, vp]
+    L.smpm_project_out.argtypes = [vp, llp, dp, dp, dp, vp]
+    L.smpm_solve.argtypes = [vp, ip, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp, vp]
+    L.smpm_deflated_solve.argtypes = [vp, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp, vp]
+    L.smpm_two_level_schwarz_solve.argtypes = [vp, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp, vp]
+    L.smpm_solve_host.argtypes = [vp, ip, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp]
+    L.smpm_batch_launch_count.restype = llp
+    L.smpm_batch_launch_count.argtypes = [vp]
+    _lib = L
+    return L
+
+
+def check(rc):
+    if rc != 0:
+        raise SmpmError(rc, lib().smpm_last_error().decode())

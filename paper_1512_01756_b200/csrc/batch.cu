@@ -1,0 +1,1312 @@
+// Host side of the B200 Schur-GMRES library: batch setup (uploads, the
+// structured block-Jacobi inverses, coarse spaces), the precomputed GEMM job
+// plans of every operator, the batched GMRES driver and the C ABI declared in
+// include/smpm_b200.h.
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/smpm_b200.h"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "vec.cuh"
+
+using namespace smpm;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct SmpmError : std::runtime_error {
+  int code;
+  SmpmError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& m) { throw SmpmError(code, m); }
+
+#define CUDA_CHECK(x)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) fail(SMPM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define CUSOLVER_CHECK(x)                                                        \
+  do {                                                                           \
+    cusolverStatus_t s_ = (x);                                                   \
+    if (s_ != CUSOLVER_STATUS_SUCCESS) fail(SMPM_ECUDA, std::string(#x) + " failed"); \
+  } while (0)
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SMPM_OK;
+  } catch (const SmpmError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SMPM_ERUNTIME;
+  }
+}
+
+template <class T>
+struct DevArray {
+  T* p = nullptr;
+  size_t n = 0;
+  DevArray() = default;
+  DevArray(const DevArray&) = delete;
+  DevArray& operator=(const DevArray&) = delete;
+  ~DevArray() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    release();
+    if (count == 0) return;
+    CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const std::vector<T>& h, cudaStream_t st) {
+    alloc(h.size());
+    if (!h.empty()) CUDA_CHECK(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+};
+
+View view(int buf, long long off, long long cs = 0, int split = INT_MAX, long long soff = 0) {
+  View v;
+  v.buf = buf;
+  v.off = off;
+  v.cs = cs;
+  v.split = split;
+  v.soff = soff;
+  return v;
+}
+const View kNoView = view(BUF_NONE, 0);
+
+// One GEMM launch worth of jobs (+ split-K reduction items).
+struct Plan {
+  std::vector<GemmJob> jobs;
+  DevArray<GemmJob> djobs;
+  DevArray<GemmTile> dtiles;
+  DevArray<SplitItem> ditems;
+  int ntiles = 0, nitems = 0;
+  long long ws_tiles = 0;
+
+  void add(const double* A, long long lda, bool transA, int M, int N, int K, int sys, View b, View out, View addv,
+           double alpha, double beta) {
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    GemmJob j{};
+    j.A = A;
+    j.lda = lda;
+    j.transA = transA ? 1 : 0;
+    j.M = M;
+    j.N = N;
+    j.K = K;
+    j.sys = sys;
+    j.splitk = 1;
+    j.b = b;
+    j.out = out;
+    j.add = addv;
+    j.alpha = alpha;
+    j.beta = beta;
+    jobs.push_back(j);
+  }
+
+  // split-K when the plan has too few output tiles to fill the GPU
+  void build(int num_sms, cudaStream_t st) {
+    long long tiles = 0;
+    for (const auto& j : jobs)
+      tiles += static_cast<long long>((j.M + GEMM_BM - 1) / GEMM_BM) * ((j.N + GEMM_BN - 1) / GEMM_BN);
+    int split = 1;
+    if (tiles > 0 && tiles < 2LL * num_sms) split = static_cast<int>((2LL * num_sms + tiles - 1) / tiles);
+    std::vector<GemmTile> ht;
+    std::vector<SplitItem> hi;
+    ws_tiles = 0;
+    for (size_t ji = 0; ji < jobs.size(); ++ji) {
+      GemmJob& j = jobs[ji];
+      const int mt = (j.M + GEMM_BM - 1) / GEMM_BM, nt = (j.N + GEMM_BN - 1) / GEMM_BN;
+      j.splitk = std::max(1, std::min(split, j.K / (4 * GEMM_BK)));
+      j.ws_off = 0;
+      if (j.splitk > 1) {
+        j.ws_off = static_cast<int>(ws_tiles);
+        ws_tiles += static_cast<long long>(mt) * nt * j.splitk;
+      }
+      for (int a = 0; a < mt; ++a)
+        for (int b = 0; b < nt; ++b) {
+          for (int ks = 0; ks < j.splitk; ++ks) ht.push_back(GemmTile{static_cast<int>(ji), a * GEMM_BM, b * GEMM_BN, ks});
+          if (j.splitk > 1) hi.push_back(SplitItem{static_cast<int>(ji), a * GEMM_BM, b * GEMM_BN});
+        }
+    }
+    ntiles = static_cast<int>(ht.size());
+    nitems = static_cast<int>(hi.size());
+    djobs.upload(jobs, st);
+    dtiles.upload(ht, st);
+    ditems.upload(hi, st);
+  }
+};
+
+}  // namespace
+
+struct smpm_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+};
+
+struct smpm_batch {
+  smpm_ctx* ctx = nullptr;
+  int n = 0, mx = 0, mz = 0, nsys = 0, w = 0, d = 0;
+  long long k = 0;
+  int nbf = 0;       // block-Jacobi blocks covering two interfaces
+  bool single = false;  // trailing one-interface block (d odd)
+  bool finalized = false;
+
+  // host staging, per system: GW (w*w) | GI (4w*w) | GE (w*w)
+  std::vector<double> hG;
+  std::vector<char> have;
+  std::vector<std::vector<double>> huS;
+
+  // device matrix pool, per system: GW GI GE | K variants (inverses)
+  DevArray<double> dmat;
+  long long mstride = 0;
+  long long oGW = 0, oGI = 0, oGE = 0, oK[4] = {0, 0, 0, 0}, oKs = 0;  // K: [first][last] flags -> index
+  bool kneeded[4] = {false, false, false, false};
+
+  // coarse space
+  DevArray<double> dcinv, duc, dthomas, drowsum;
+  DevArray<int> dcmode, dsingular;
+  std::vector<double> hC;
+  std::vector<int> htri, hsing;
+
+  // operator plans
+  Plan pS, pSt, pBJ1, pBJ2, pBJ3;
+  DevArray<double> dws;  // split-K workspace
+
+  // vectors (nsys x k each)
+  DevArray<double> vbuf[12];
+  DevArray<double> dsmall;  // nsys x (d + misc) scalars
+  DevArray<int> dones, dcount, dsel, dcnt;
+  int* hcnt = nullptr;  // pinned, 4 ints (two in-flight step counters)
+  ~smpm_batch() {
+    if (hcnt) cudaFreeHost(hcnt);
+  }
+  DevArray<double> dpart;
+
+  // GMRES workspace
+  int gm_m = -1, gm_hist = 0, gm_mtot = 0;
+  DevArray<double> dV, dR, dcs, dsn, dg, dh1, dh2, dy, dhist, dgpart, dscal;
+  DevArray<int> dgint;
+  GmState_ G{};
+
+  long long launches = 0;
+
+  cudaStream_t st(void* s) const { return s ? static_cast<cudaStream_t>(s) : ctx->stream; }
+  double* GW(int s) const { return dmat.p + s * mstride + oGW; }
+  double* GI(int s) const { return dmat.p + s * mstride + oGI; }
+  double* GE(int s) const { return dmat.p + s * mstride + oGE; }
+  double* Kinv(int s, int v) const { return dmat.p + s * mstride + oK[v]; }
+  double* Ksingle(int s) const { return dmat.p + s * mstride + oKs; }
+};
+
+namespace {
+
+void check_launch(smpm_batch* b) {
+  ++b->launches;
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void run_plan(smpm_batch* b, Plan& p, const double* in, double* out, double* tmp, const int* active,
+              cudaStream_t st) {
+  if (p.ntiles == 0) return;
+  BufTable t;
+  t.p[BUF_IN] = const_cast<double*>(in);
+  t.p[BUF_OUT] = out;
+  t.p[BUF_TMP] = tmp;
+  t.p[BUF_TMP2] = nullptr;
+  gemm_jobs_kernel<<<p.ntiles, 128, 0, st>>>(p.djobs.p, p.dtiles.p, t, active, b->dws.p);
+  check_launch(b);
+  if (p.nitems > 0) {
+    gemm_splitk_reduce_kernel<<<p.nitems, 256, 0, st>>>(p.djobs.p, p.ditems.p, t, active, b->dws.p);
+    check_launch(b);
+  }
+}
+
+DeflateParams deflate_params(smpm_batch* b, const int* active) {
+  DeflateParams P;
+  P.nsys = b->nsys;
+  P.d = b->d;
+  P.w = b->w;
+  P.k = b->k;
+  P.active = active;
+  P.cmode = b->dcmode.p;
+  P.cinv = b->dcinv.p;
+  P.uc = b->duc.p;
+  P.singular = b->dsingular.p;
+  P.thomas = b->dthomas.p;
+  P.rowsum = b->drowsum.p;
+  P.mx = b->mx;
+  return P;
+}
+
+void run_deflate(smpm_batch* b, int mode, const double* zin, const double* v, double* y, double* cout,
+                 const int* active, cudaStream_t st) {
+  const size_t shm = sizeof(double) * 2 * static_cast<size_t>(b->d);
+  deflate_kernel<<<b->nsys, VEC_THREADS, shm, st>>>(deflate_params(b, active), mode, zin, v, y, cout);
+  check_launch(b);
+}
+
+int grid_for(long long elems) {
+  return static_cast<int>(std::min<long long>((elems + 255) / 256, 148LL * 8));
+}
+
+// --------------------------------------------------------------------------
+// Operators (device vectors nsys x k)
+// --------------------------------------------------------------------------
+void op_S(smpm_batch* b, const double* v, double* y, const int* act, cudaStream_t st) {
+  run_plan(b, b->pS, v, y, nullptr, act, st);
+}
+void op_St(smpm_batch* b, const double* v, double* y, const int* act, cudaStream_t st) {
+  run_plan(b, b->pSt, v, y, nullptr, act, st);
+}
+// structured block-Jacobi: three dependent GEMM stages
+void op_BJ(smpm_batch* b, const double* v, double* y, const int* act, cudaStream_t st) {
+  double* tmp = b->vbuf[9].p;
+  run_plan(b, b->pBJ1, v, y, tmp, act, st);
+  run_plan(b, b->pBJ2, v, y, tmp, act, st);
+  run_plan(b, b->pBJ3, v, y, tmp, act, st);
+}
+// P v = v - S Z c(Z^T v)
+void op_P(smpm_batch* b, const double* v, double* y, bool fused, const int* act, cudaStream_t st) {
+  if (fused) {
+    run_deflate(b, DEFL_P_FUSED, v, v, y, nullptr, act, st);
+    return;
+  }
+  double* c = b->dsmall.p;
+  double* z = b->vbuf[7].p;
+  double* sz = b->vbuf[8].p;
+  run_deflate(b, DEFL_COARSE, v, nullptr, nullptr, c, act, st);
+  zbroadcast_kernel<<<grid_for(b->nsys * b->k), 256, 0, st>>>(b->nsys, b->d, 2 * b->w, b->k, act, c, z);
+  check_launch(b);
+  op_S(b, z, sz, act, st);
+  run_deflate(b, DEFL_SUB_T, sz, v, y, nullptr, act, st);
+}
+// Q v = v - Z c(Z^T S v)
+void op_Q(smpm_batch* b, const double* v, double* y, const int* act, cudaStream_t st) {
+  double* t = b->vbuf[8].p;
+  op_S(b, v, t, act, st);
+  run_deflate(b, DEFL_Q_TAIL, t, v, y, nullptr, act, st);
+}
+
+// --------------------------------------------------------------------------
+// Setup: plans, structured block-Jacobi inverses, coarse spaces
+// --------------------------------------------------------------------------
+void build_plans(smpm_batch* b) {
+  const int w = b->w, d = b->d, mx = b->mx;
+  const long long k = b->k;
+  const long long w2 = 2LL * w;
+  cudaStream_t st = b->ctx->stream;
+  b->pS.jobs.clear();
+  b->pSt.jobs.clear();
+  b->pBJ1.jobs.clear();
+  b->pBJ2.jobs.clear();
+  b->pBJ3.jobs.clear();
+  for (int s = 0; s < b->nsys; ++s) {
+    const long long o = s * k;
+    // ---- S v = v + sum_s G_s [v_{2s-1}; v_{2s}] -> [y_{2s-2}; y_{2s+1}]
+    if (mx >= 3)
+      b->pS.add(b->GI(s), w2, false, 2 * w, mx - 2, 2 * w, s, view(BUF_IN, o + w, w2),
+                view(BUF_OUT, o, w2, w, 2LL * w), view(BUF_IN, o, w2, w, 2LL * w), 1.0, 1.0);
+    b->pS.add(b->GW(s), w, false, w, 1, w, s, view(BUF_IN, o), view(BUF_OUT, o + w), view(BUF_IN, o + w), 1.0, 1.0);
+    b->pS.add(b->GE(s), w, false, w, 1, w, s, view(BUF_IN, o + (2LL * d - 1) * w), view(BUF_OUT, o + (2LL * d - 2) * w),
+              view(BUF_IN, o + (2LL * d - 2) * w), 1.0, 1.0);
+    // ---- S^T: own blocks += G^T reader blocks
+    if (mx >= 3)
+      b->pSt.add(b->GI(s), w2, true, 2 * w, mx - 2, 2 * w, s, view(BUF_IN, o, w2, w, 2LL * w),
+                 view(BUF_OUT, o + w, w2), view(BUF_IN, o + w, w2), 1.0, 1.0);
+    b->pSt.add(b->GW(s), w, true, w, 1, w, s, view(BUF_IN, o + w), view(BUF_OUT, o), view(BUF_IN, o), 1.0, 1.0);
+    b->pSt.add(b->GE(s), w, true, w, 1, w, s, view(BUF_IN, o + (2LL * d - 2) * w), view(BUF_OUT, o + (2LL * d - 1) * w),
+               view(BUF_IN, o + (2LL * d - 1) * w), 1.0, 1.0);
+
+    // ---- block-Jacobi, blocks of two interfaces b = 0..nbf-1 (w-blocks 4b..4b+3):
+    //   r = [v0; v3] - G'[v1; v2] ; [x0; x3] = K_b^{-1} r ; x1 = v1 - Gee x0 ; x2 = v2 - Gww x3
+    const int nbf = b->nbf;
+    const long long w4 = 4LL * w;
+    if (nbf > 0)
+      b->pBJ1.add(b->GI(s), w2, false, 2 * w, nbf, 2 * w, s, view(BUF_IN, o + w, w4), view(BUF_TMP, o, w4),
+                  view(BUF_IN, o, w4, w, 2LL * w), -1.0, 1.0);
+    for (int bb = 0; bb < nbf;) {
+      const bool first = bb == 0;
+      const bool last = 2 * bb + 2 == mx - 1;
+      int e = bb + 1;
+      while (e < nbf && (e == 0) == first && (2 * e + 2 == mx - 1) == last) ++e;
+      const int var = (first ? 1 : 0) | (last ? 2 : 0);
+      b->pBJ2.add(b->Kinv(s, var), w2, false, 2 * w, e - bb, 2 * w, s, view(BUF_TMP, o + bb * w4, w4),
+                  view(BUF_OUT, o + bb * w4, w4, w, 2LL * w), kNoView, 1.0, 0.0);
+      bb = e;
+    }
+    if (nbf > 0) {
+      // x1 = v1 - Gee0 x0 : strip 2b is the west-boundary strip for b = 0
+      b->pBJ3.add(b->GW(s), w, false, w, 1, w, s, view(BUF_OUT, o), view(BUF_OUT, o + w), view(BUF_IN, o + w), -1.0, 1.0);
+      if (nbf > 1)
+        b->pBJ3.add(b->GI(s) + w2 * w + w, w2, false, w, nbf - 1, w, s, view(BUF_OUT, o + w4, w4),
+                    view(BUF_OUT, o + w4 + w, w4), view(BUF_IN, o + w4 + w, w4), -1.0, 1.0);
+      // x2 = v2 - Gww2 x3 : strip 2b+2 is the east-boundary strip when 2b+2 == mx-1
+      const bool last_east = 2 * (nbf - 1) + 2 == mx - 1;
+      const int ninner = last_east ? nbf - 1 : nbf;
+      if (ninner > 0)
+        b->pBJ3.add(b->GI(s), w2, false, w, ninner, w, s, view(BUF_OUT, o + 3LL * w, w4), view(BUF_OUT, o + 2LL * w, w4),
+                    view(BUF_IN, o + 2LL * w, w4), -1.0, 1.0);
+      if (last_east) {
+        const long long ob = o + (nbf - 1) * w4;
+        b->pBJ3.add(b->GE(s), w, false, w, 1, w, s, view(BUF_OUT, ob + 3LL * w), view(BUF_OUT, ob + 2LL * w),
+                    view(BUF_IN, ob + 2LL * w), -1.0, 1.0);
+      }
+    }
+    if (b->single) {
+      // trailing interface d-1 (w-blocks 2d-2, 2d-1): r = v0 - G_E v1 ; x0 = K_s^{-1} r ; x1 = v1 - Gee x0
+      const long long o0 = o + (2LL * d - 2) * w, o1 = o0 + w;
+      b->pBJ1.add(b->GE(s), w, false, w, 1, w, s, view(BUF_IN, o1), view(BUF_TMP, o0), view(BUF_IN, o0), -1.0, 1.0);
+      b->pBJ2.add(b->Ksingle(s), w, false, w, 1, w, s, view(BUF_TMP, o0), view(BUF_OUT, o0), kNoView, 1.0, 0.0);
+      const double* gee = d >= 2 ? b->GI(s) + w2 * w + w : b->GW(s);
+      const long long ldee = d >= 2 ? w2 : w;
+      b->pBJ3.add(gee, ldee, false, w, 1, w, s, view(BUF_OUT, o0), view(BUF_OUT, o1), view(BUF_IN, o1), -1.0, 1.0);
+    }
+  }
+  const int sms = b->ctx->num_sms;
+  b->pS.build(sms, st);
+  b->pSt.build(sms, st);
+  b->pBJ1.build(sms, st);
+  b->pBJ2.build(sms, st);
+  b->pBJ3.build(sms, st);
+  long long wst = std::max({b->pS.ws_tiles, b->pSt.ws_tiles, b->pBJ1.ws_tiles, b->pBJ2.ws_tiles, b->pBJ3.ws_tiles});
+  b->dws.alloc(static_cast<size_t>(std::max(1LL, wst)) * GEMM_BM * GEMM_BN);
+}
+
+__global__ void add_identity_kernel(double* A, long long lda, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) A[i * lda + i] += 1.0;
+}
+__global__ void set_identity_kernel(double* A, long long lda, int n) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(n) * n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long c = e / n, r = e % n;
+    A[c * lda + r] = (r == c) ? 1.0 : 0.0;
+  }
+}
+
+// K = I - G' diag(Gee0, Gww2) (2w x 2w) or K_single = I - G_E Gee (w x w),
+// formed with the GEMM kernel, inverted with cuSOLVER getrf/getrs.
+void build_bj_inverses(smpm_batch* b) {
+  const int w = b->w, mx = b->mx, d = b->d;
+  const long long w2 = 2LL * w;
+  cudaStream_t st = b->ctx->stream;
+  DevArray<double> Kt;
+  Kt.alloc(static_cast<size_t>(4LL * w * w));
+  DevArray<int> ipiv, info;
+  ipiv.alloc(static_cast<size_t>(2 * w));
+  info.alloc(1);
+  int lwork = 0;
+  CUSOLVER_CHECK(cusolverDnDgetrf_bufferSize(b->ctx->solver, 2 * w, 2 * w, Kt.p, 2 * w, &lwork));
+  DevArray<double> work;
+  work.alloc(static_cast<size_t>(std::max(lwork, 1)));
+  auto invert = [&](double* K, int nn, double* out) {
+    CUSOLVER_CHECK(cusolverDnDgetrf(b->ctx->solver, nn, nn, K, nn, work.p, ipiv.p, info.p));
+    set_identity_kernel<<<64, 256, 0, st>>>(out, nn, nn);
+    check_launch(b);
+    CUSOLVER_CHECK(cusolverDnDgetrs(b->ctx->solver, CUBLAS_OP_N, nn, nn, K, nn, ipiv.p, out, nn, info.p));
+    int hinfo = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (hinfo != 0) fail(SMPM_ESINGULAR, "block-Jacobi: singular preconditioner block");
+  };
+  for (int s = 0; s < b->nsys; ++s) {
+    for (int var = 0; var < 4; ++var) {
+      if (!b->kneeded[var]) continue;
+      const bool first = var & 1, last = var & 2;
+      const double* gee = first ? b->GW(s) : b->GI(s) + w2 * w + w;
+      const long long ldee = first ? w : w2;
+      const double* gww = last ? b->GE(s) : b->GI(s);
+      const long long ldww = last ? w : w2;
+      Plan p;
+      // K[:, 0:w] = -G'[:, 0:w] Gee ; K[:, w:2w] = -G'[:, w:2w] Gww ; then + I
+      BufTable t;
+      t.p[BUF_IN] = const_cast<double*>(gee);
+      t.p[BUF_OUT] = Kt.p;
+      t.p[BUF_TMP] = const_cast<double*>(gww);
+      t.p[BUF_TMP2] = nullptr;
+      p.add(b->GI(s), w2, false, 2 * w, w, w, 0, view(BUF_IN, 0, ldee), view(BUF_OUT, 0, w2), kNoView, -1.0, 0.0);
+      p.add(b->GI(s) + w2 * w, w2, false, 2 * w, w, w, 0, view(BUF_TMP, 0, ldww), view(BUF_OUT, w2 * w, w2), kNoView,
+            -1.0, 0.0);
+      p.build(0, st);  // no split-K for setup products
+      gemm_jobs_kernel<<<p.ntiles, 128, 0, st>>>(p.djobs.p, p.dtiles.p, t, nullptr, nullptr);
+      check_launch(b);
+      add_identity_kernel<<<8, 256, 0, st>>>(Kt.p, w2, 2 * w);
+      check_launch(b);
+      invert(Kt.p, 2 * w, b->Kinv(s, var));
+    }
+    if (b->single) {
+      const double* gee = d >= 2 ? b->GI(s) + w2 * w + w : b->GW(s);
+      const long long ldee = d >= 2 ? w2 : w;
+      Plan p;
+      BufTable t;
+      t.p[BUF_IN] = const_cast<double*>(gee);
+      t.p[BUF_OUT] = Kt.p;
+      t.p[BUF_TMP] = nullptr;
+      t.p[BUF_TMP2] = nullptr;
+      p.add(b->GE(s), w, false, w, w, w, 0, view(BUF_IN, 0, ldee), view(BUF_OUT, 0, w), kNoView, -1.0, 0.0);
+      p.build(0, st);
+      gemm_jobs_kernel<<<p.ntiles, 128, 0, st>>>(p.djobs.p, p.dtiles.p, t, nullptr, nullptr);
+      check_launch(b);
+      add_identity_kernel<<<8, 256, 0, st>>>(Kt.p, w, w);
+      check_launch(b);
+      invert(Kt.p, w, b->Ksingle(s));
+    }
+  }
+  (void)mx;
+}
+
+// dense inverse with partial pivoting (host, d <= a few hundred)
+std::vector<double> host_inverse(std::vector<double> A, int n) {
+  std::vector<double> inv(static_cast<size_t>(n) * n, 0.0);
+  for (int i = 0; i < n; ++i) inv[static_cast<size_t>(i) * n + i] = 1.0;
+  auto at = [n](std::vector<double>& M, int r, int c) -> double& { return M[static_cast<size_t>(c) * n + r]; };
+  for (int c = 0; c < n; ++c) {
+    int p = c;
+    for (int r = c + 1; r < n; ++r)
+      if (std::fabs(at(A, r, c)) > std::fabs(at(A, p, c))) p = r;
+    if (at(A, p, c) == 0.0) fail(SMPM_ESINGULAR, "coarse matrix is singular");
+    if (p != c)
+      for (int j = 0; j < n; ++j) {
+        std::swap(at(A, p, j), at(A, c, j));
+        std::swap(at(inv, p, j), at(inv, c, j));
+      }
+    const double piv = at(A, c, c);
+    for (int r = 0; r < n; ++r) {
+      if (r == c) continue;
+      const double f = at(A, r, c) / piv;
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        at(A, r, j) -= f * at(A, c, j);
+        at(inv, r, j) -= f * at(inv, c, j);
+      }
+    }
+  }
+  for (int r = 0; r < n; ++r) {
+    const double piv = at(A, r, r);
+    for (int j = 0; j < n; ++j) at(inv, r, j) /= piv;
+  }
+  return inv;
+}
+
+// C = Z^T S Z from the couplings' row sums (S Z 1_j only touches interfaces
+// j-1, j, j+1; proj/src/deflation.cpp:24-42), rank-one shift or Thomas data.
+void build_coarse(smpm_batch* b) {
+  const int w = b->w, d = b->d, mx = b->mx, nsys = b->nsys;
+  const long long gsz = 6LL * w * w;
+  std::vector<double> rows(static_cast<size_t>(nsys) * 6 * w, 0.0);
+  std::vector<double> cinv(static_cast<size_t>(nsys) * d * d, 0.0), uc(static_cast<size_t>(nsys) * d, 0.0),
+      th(static_cast<size_t>(nsys) * 3 * d, 0.0);
+  std::vector<int> cmode(static_cast<size_t>(nsys), 0);
+  b->hC.assign(static_cast<size_t>(nsys) * d * d, 0.0);
+  b->htri.assign(static_cast<size_t>(nsys), 1);
+  b->hsing.assign(static_cast<size_t>(nsys), 0);
+  for (int s = 0; s < nsys; ++s) {
+    const double* GW = b->hG.data() + s * gsz;
+    const double* GI = GW + static_cast<long long>(w) * w;
+    const double* GE = GI + 4LL * w * w;
+    double* rs = rows.data() + static_cast<size_t>(s) * 6 * w;
+    double* rWI = rs;
+    double* rEI = rs + 2 * w;
+    double* rEW = rs + 4 * w;
+    double* rWE = rs + 5 * w;
+    for (int c = 0; c < w; ++c)
+      for (int r = 0; r < 2 * w; ++r) {
+        rWI[r] += GI[static_cast<long long>(c) * 2 * w + r];
+        rEI[r] += GI[static_cast<long long>(c + w) * 2 * w + r];
+      }
+    for (int c = 0; c < w; ++c)
+      for (int r = 0; r < w; ++r) {
+        rEW[r] += GW[static_cast<long long>(c) * w + r];
+        rWE[r] += GE[static_cast<long long>(c) * w + r];
+      }
+    auto sum = [](const double* p, int n) {
+      double a = 0.0;
+      for (int i = 0; i < n; ++i) a += p[i];
+      return a;
+    };
+    double* C = b->hC.data() + static_cast<size_t>(s) * d * d;
+    auto Cat = [&](int i, int j) -> double& { return C[static_cast<size_t>(j) * d + i]; };
+    for (int j = 0; j < d; ++j) {
+      Cat(j, j) += 2.0 * w;
+      if (j == 0) {
+        Cat(0, 0) += sum(rEW, w);
+      } else {
+        Cat(j - 1, j) += sum(rEI, w);
+        Cat(j, j) += sum(rEI + w, w);
+      }
+      if (j + 1 == mx - 1) {
+        Cat(j, j) += sum(rWE, w);
+      } else {
+        Cat(j, j) += sum(rWI, w);
+        Cat(j + 1, j) += sum(rWI + w, w);
+      }
+    }
+    if (!b->huS[s].empty()) {
+      b->hsing[s] = 1;
+      const std::vector<double>& us = b->huS[s];
+      double* u = uc.data() + static_cast<size_t>(s) * d;
+      double nn = 0.0;
+      for (int i = 0; i < d; ++i) {
+        double a = 0.0;
+        for (int e = 0; e < 2 * w; ++e) a += us[static_cast<size_t>(i) * 2 * w + e];
+        u[i] = a;
+        nn += a * a;
+      }
+      nn = std::sqrt(nn);
+      int imax = 0;
+      for (int i = 0; i < d; ++i) {
+        u[i] /= nn;
+        if (std::fabs(u[i]) > std::fabs(u[imax])) imax = i;
+      }
+      if (u[imax] < 0.0)
+        for (int i = 0; i < d; ++i) u[i] = -u[i];
+      std::vector<double> Cs(C, C + static_cast<size_t>(d) * d);
+      for (int j = 0; j < d; ++j)
+        for (int i = 0; i < d; ++i) Cs[static_cast<size_t>(j) * d + i] += u[i] * u[j];
+      const std::vector<double> inv = host_inverse(Cs, d);
+      std::copy(inv.begin(), inv.end(), cinv.begin() + static_cast<long long>(s) * d * d);
+      cmode[s] = 0;
+    } else {
+      // Thomas pivots (proj/src/deflation.cpp:77-90)
+      double* sub = th.data() + static_cast<size_t>(s) * 3 * d;
+      double* cp = sub + d;
+      double* piv = cp + d;
+      for (int i = 0; i + 1 < d; ++i) sub[i] = Cat(i + 1, i);
+      piv[0] = Cat(0, 0);
+      for (int i = 1; i < d; ++i) {
+        cp[i - 1] = Cat(i - 1, i) / piv[i - 1];
+        piv[i] = Cat(i, i) - sub[i - 1] * cp[i - 1];
+      }
+      for (int i = 0; i < d; ++i)
+        if (piv[i] == 0.0) fail(SMPM_ESINGULAR, "coarse matrix is singular");
+      cmode[s] = 1;
+    }
+  }
+  cudaStream_t st = b->ctx->stream;
+  b->drowsum.upload(rows, st);
+  b->dcinv.upload(cinv, st);
+  b->duc.upload(uc, st);
+  b->dthomas.upload(th, st);
+  b->dcmode.upload(cmode, st);
+  b->dsingular.upload(b->hsing, st);
+}
+
+void finalize(smpm_batch* b) {
+  if (b->finalized) return;
+  for (int s = 0; s < b->nsys; ++s)
+    if (!b->have[s]) fail(SMPM_EINVAL, "smpm_batch_finalize: couplings of system " + std::to_string(s) + " not set");
+  const int w = b->w, mx = b->mx, d = b->d;
+  cudaStream_t st = b->ctx->stream;
+  // which K variants occur ([first][last] over the two-interface blocks)
+  for (int bb = 0; bb < b->nbf; ++bb) b->kneeded[(bb == 0 ? 1 : 0) | (2 * bb + 2 == mx - 1 ? 2 : 0)] = true;
+  long long off = 0;
+  b->oGW = off;
+  off += 1LL * w * w;
+  b->oGI = off;
+  off += 4LL * w * w;
+  b->oGE = off;
+  off += 1LL * w * w;
+  for (int v = 0; v < 4; ++v)
+    if (b->kneeded[v]) {
+      b->oK[v] = off;
+      off += 4LL * w * w;
+    }
+  if (b->single) {
+    b->oKs = off;
+    off += 1LL * w * w;
+  }
+  b->mstride = (off + 31) / 32 * 32;
+  b->dmat.alloc(static_cast<size_t>(b->mstride) * b->nsys);
+  for (int s = 0; s < b->nsys; ++s)
+    CUDA_CHECK(cudaMemcpyAsync(b->GW(s), b->hG.data() + s * 6LL * w * w, sizeof(double) * 6LL * w * w,
+                               cudaMemcpyHostToDevice, st));
+  build_plans(b);
+  build_bj_inverses(b);
+  build_coarse(b);
+  for (auto& v : b->vbuf) v.alloc(static_cast<size_t>(b->nsys) * b->k);
+  b->dsmall.alloc(static_cast<size_t>(b->nsys) * (d + 8));
+  std::vector<int> ones(static_cast<size_t>(b->nsys), 1);
+  b->dones.upload(ones, st);
+  b->dcount.alloc(static_cast<size_t>(b->nsys) + 1);
+  CUDA_CHECK(cudaMemsetAsync(b->dcount.p, 0, sizeof(int) * (b->nsys + 1), st));
+  b->dsel.alloc(static_cast<size_t>(b->nsys));
+  b->dcnt.alloc(4);
+  CUDA_CHECK(cudaMallocHost(&b->hcnt, 4 * sizeof(int)));
+  CUDA_CHECK(cudaStreamSynchronize(st));
+  b->finalized = true;
+}
+
+void need_final(smpm_batch* b) {
+  if (!b || !b->finalized) fail(SMPM_EINVAL, "batch not finalized");
+}
+
+// --------------------------------------------------------------------------
+// Batched reductions
+// --------------------------------------------------------------------------
+struct Chunking {
+  int chunk, nchunk;
+};
+Chunking chunking(const smpm_batch* b) {
+  const long long target_ctas = 4LL * b->ctx->num_sms;
+  long long per_sys = std::max(1LL, target_ctas / b->nsys);
+  long long chunk = (b->k + per_sys - 1) / per_sys;
+  chunk = std::max(128LL, std::min(2048LL, (chunk + 31) / 32 * 32));
+  Chunking c;
+  c.chunk = static_cast<int>(chunk);
+  c.nchunk = static_cast<int>((b->k + chunk - 1) / chunk);
+  return c;
+}
+
+// out[s] = x_s . y_s  (device)
+void batched_dot(smpm_batch* b, const double* x, const double* y, double* out, const int* act, cudaStream_t st) {
+  const Chunking c = chunking(b);
+  b->dpart.alloc(std::max<size_t>(b->dpart.n, static_cast<size_t>(b->nsys) * c.nchunk));
+  dim3 grid(c.nchunk, b->nsys);
+  batched_dot_kernel<<<grid, VEC_THREADS, 0, st>>>(b->nsys, b->k, c.chunk, c.nchunk, act, x, y, b->dpart.p, b->dcount.p,
+                                                   out);
+  check_launch(b);
+}
+
+// --------------------------------------------------------------------------
+// GMRES driver
+// --------------------------------------------------------------------------
+void ensure_gmres(smpm_batch* b, int m, int mtot) {
+  const int histcap = mtot + 2;
+  const Chunking c = chunking(b);
+  if (b->gm_m != m || b->gm_hist != histcap || b->G.nchunk != c.nchunk) {
+    const size_t ns = static_cast<size_t>(b->nsys);
+    b->dV.alloc(ns * (m + 1) * b->k);
+    b->dR.alloc(ns * (m + 1) * m);
+    b->dcs.alloc(ns * m);
+    b->dsn.alloc(ns * m);
+    b->dg.alloc(ns * (m + 1));
+    b->dh1.alloc(ns * (m + 2));
+    b->dh2.alloc(ns * (m + 2));
+    b->dy.alloc(ns * m);
+    b->dhist.alloc(ns * histcap);
+    b->dgpart.alloc(ns * c.nchunk * (m + 2));
+    b->dscal.alloc(ns * 8);
+    b->dgint.alloc(ns * 8);
+    b->gm_m = m;
+    b->gm_hist = histcap;
+  }
+  GmState_& G = b->G;
+  int* ip = b->dgint.p;
+  const int ns = b->nsys;
+  G.jcyc = ip;
+  G.iters = ip + ns;
+  G.state = ip + 2 * ns;
+  G.active = ip + 3 * ns;
+  G.counter = ip + 4 * ns;
+  G.hist_len = ip + 5 * ns;
+  double* dp = b->dscal.p;
+  G.bnorm = dp;
+  G.target = dp + ns;
+  G.hmax = dp + 2 * ns;
+  G.nrm = dp + 3 * ns;
+  G.R = b->dR.p;
+  G.cs = b->dcs.p;
+  G.sn = b->dsn.p;
+  G.g = b->dg.p;
+  G.h1 = b->dh1.p;
+  G.h2 = b->dh2.p;
+  G.y = b->dy.p;
+  G.hist = b->dhist.p;
+  G.part = b->dgpart.p;
+  G.m = m;
+  G.m_total = mtot;
+  G.histcap = histcap;
+  G.k = b->k;
+  G.vstride = static_cast<long long>(m + 1) * b->k;
+  G.chunk = c.chunk;
+  G.nchunk = c.nchunk;
+  G.nsys = ns;
+  b->gm_mtot = mtot;
+  CUDA_CHECK(cudaMemsetAsync(b->dgint.p, 0, sizeof(int) * ns * 8, b->ctx->stream));
+  CUDA_CHECK(cudaMemsetAsync(b->dR.p, 0, sizeof(double) * b->dR.n, b->ctx->stream));
+}
+
+struct SolveCfg {
+  int method;
+  double tol;
+  int max_iter, restart, orth;
+  bool fused, final_check;
+};
+
+// the preconditioned operator GMRES iterates on (proj/src/deflation.cpp:105-107,131; proj/src/gmres.cpp:144-150)
+// returns the number of S applications it made per system
+int apply_op(smpm_batch* b, const SolveCfg& c, const double* vin, double* wout, const int* act, cudaStream_t st) {
+  double* u = b->vbuf[4].p;
+  double* t = b->vbuf[5].p;
+  switch (c.method) {
+    case SMPM_SCHUR:
+      op_S(b, vin, wout, act, st);
+      return 1;
+    case SMPM_BJ:
+      op_BJ(b, vin, u, act, st);
+      op_S(b, u, wout, act, st);
+      return 1;
+    case SMPM_DBJ:
+      op_BJ(b, vin, u, act, st);
+      op_S(b, u, t, act, st);
+      op_P(b, t, wout, c.fused, act, st);
+      return c.fused ? 1 : 2;
+    case SMPM_2LAS: {
+      op_BJ(b, vin, u, act, st);
+      run_deflate(b, DEFL_ADD_ZC, vin, u, t, nullptr, act, st);  // minv = M^{-1} + Z C^{-1} Z^T
+      op_S(b, t, wout, act, st);
+      return 1;
+    }
+  }
+  fail(SMPM_EINVAL, "unknown method");
+}
+
+void arnoldi_step(smpm_batch* b, const SolveCfg& c, cudaStream_t st) {
+  GmState_& G = b->G;
+  double* V = b->dV.p;
+  double* vin = b->vbuf[2].p;
+  double* wv = b->vbuf[3].p;
+  apply_op(b, c, vin, wv, G.active, st);
+  dim3 grid(G.nchunk, b->nsys);
+  const size_t hsm = sizeof(double) * static_cast<size_t>(G.m + 2);
+  if (c.orth == SMPM_ORTH_MGS) {
+    for (int i = 0; i <= std::min(G.m, G.m_total); ++i) {
+      mgs_step_kernel<<<grid, VEC_THREADS, 0, st>>>(G, V, wv, i);
+      check_launch(b);
+    }
+    gm_zero_h2_kernel<<<b->nsys, 128, 0, st>>>(G);
+    check_launch(b);
+    cgs_update_kernel<true><<<grid, VEC_THREADS, hsm, st>>>(G, V, wv, 0);  // norm + Givens only
+    check_launch(b);
+  } else {
+    cgs_dot_kernel<<<grid, VEC_THREADS, 0, st>>>(G, V, wv);
+    check_launch(b);
+    cgs_update_kernel<false><<<grid, VEC_THREADS, hsm, st>>>(G, V, wv, 1);
+    check_launch(b);
+    cgs_update_kernel<true><<<grid, VEC_THREADS, hsm, st>>>(G, V, wv, 1);
+    check_launch(b);
+  }
+  dim3 sg(std::max(1, std::min(G.nchunk, 64)), b->nsys);
+  gm_scale_kernel<<<sg, 256, 0, st>>>(G, V, wv, vin);
+  check_launch(b);
+}
+
+__global__ void count_states_kernel(const int* state, int nsys, int* out) {
+  __shared__ int run, cyc;
+  if (threadIdx.x == 0) {
+    run = 0;
+    cyc = 0;
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < nsys; s += blockDim.x) {
+    if (state[s] == GM_RUN) atomicAdd(&run, 1);
+    if (state[s] == GM_CYCLE) atomicAdd(&cyc, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out[0] = run;
+    out[1] = cyc;
+  }
+}
+
+__global__ void select_state_kernel(const int* state, int nsys, int want, int* sel) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nsys) sel[s] = state[s] == want ? 1 : 0;
+}
+
+void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_report* reps, double* history,
+           cudaStream_t st) {
+  need_final(b);
+  if (c.max_iter < 1) fail(SMPM_EINVAL, "max_iter must be >= 1");
+  const int mtot = static_cast<int>(std::min<long long>(c.max_iter, b->k));
+  int m = c.restart > 0 ? std::min(c.restart, mtot) : mtot;
+  if (m > 4000) fail(SMPM_EINVAL, "Krylov cycle length above 4000 is not supported (use restart)");
+  ensure_gmres(b, m, mtot);
+  GmState_& G = b->G;
+  const int ns = b->nsys;
+  const long long nk = static_cast<long long>(ns) * b->k;
+  double* rhs = b->vbuf[0].p;  // GMRES right-hand side (P b_S for dbj)
+  double* x = b->vbuf[1].p;    // Krylov iterate
+  double* vin = b->vbuf[2].p;
+  double* r = b->vbuf[6].p;
+  double* sc = b->dsmall.p + static_cast<size_t>(ns) * b->d;  // scratch scalars
+  double* nb2 = sc;        // ||b_S||^2
+  double* nr2 = sc + ns;   // ||rhs||^2 / ||r||^2
+  cudaEvent_t e0, e1, ev[2];
+  CUDA_CHECK(cudaEventCreate(&e0));
+  CUDA_CHECK(cudaEventCreate(&e1));
+  CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  int* dsel = b->dsel.p;
+  int* hcnt = b->hcnt;
+  CUDA_CHECK(cudaEventRecord(e0, st));
+  const long long launches0 = b->launches;
+  long long s_applies = 0, op_applies = 0;
+
+  // ---- right-hand side
+  if (c.method == SMPM_DBJ) {
+    op_P(b, bS, rhs, c.fused, nullptr, st);  // pb = P b_S (proj/src/deflation.cpp:110)
+  } else {
+    CUDA_CHECK(cudaMemcpyAsync(rhs, bS, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
+  }
+  batched_dot(b, bS, bS, nb2, nullptr, st);
+  batched_dot(b, rhs, rhs, nr2, nullptr, st);
+  CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double) * nk, st));
+  gm_start_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G, nr2, nb2, c.tol, 1, nullptr);
+  check_launch(b);
+  dim3 vg(std::max(1, std::min(G.nchunk, 64)), ns);
+  gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, rhs, vin);
+  check_launch(b);
+
+  // ---- Arnoldi steps; device flags are polled one step behind the launches
+  // (step i+1 is queued before the host waits on step i's counters; a step
+  // issued after every system finished is a masked no-op)
+  int steps = 0;
+  const int per_sys_applies = c.method == SMPM_DBJ && !c.fused ? 2 : 1;
+  auto issue = [&](int slot) {
+    arnoldi_step(b, c, st);
+    ++steps;
+    count_states_kernel<<<1, 256, 0, st>>>(G.state, ns, b->dcnt.p + 2 * slot);
+    check_launch(b);
+    CUDA_CHECK(cudaMemcpyAsync(hcnt + 2 * slot, b->dcnt.p + 2 * slot, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaEventRecord(ev[slot], st));
+  };
+  int cur = 0;
+  issue(cur);
+  for (;;) {
+    const bool more = steps < mtot + 1;
+    if (more) issue(cur ^ 1);
+    CUDA_CHECK(cudaEventSynchronize(ev[cur]));
+    const int nrun = hcnt[2 * cur], ncyc = hcnt[2 * cur + 1];
+    cur ^= 1;
+    if (nrun > 0 && more) continue;
+    if (more) CUDA_CHECK(cudaEventSynchronize(ev[cur]));  // drain the speculative step
+    const int nrun2 = more ? hcnt[2 * cur] : nrun;
+    const int ncyc2 = more ? hcnt[2 * cur + 1] : ncyc;
+    if (nrun2 > 0 && steps < mtot + 1) {
+      issue(cur);
+      continue;
+    }
+    if (ncyc2 > 0) {
+      // ---- restart (GMRES(m) extension): x += V y ; r = b - op(x) ; new cycle
+      select_state_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, GM_CYCLE, dsel);
+      check_launch(b);
+      gm_backsolve_kernel<<<ns, 32, 0, st>>>(G, dsel);
+      check_launch(b);
+      gm_combine_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, x, dsel, 1);
+      check_launch(b);
+      apply_op(b, c, x, r, dsel, st);
+      ++op_applies;
+      axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, dsel, nullptr, 1.0, rhs, -1.0, r);
+      check_launch(b);
+      batched_dot(b, r, r, nr2, dsel, st);
+      gm_start_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G, nr2, nb2, c.tol, 0, G.state);
+      check_launch(b);
+      gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, r, vin);
+      check_launch(b);
+      issue(cur);
+      continue;
+    }
+    break;
+  }
+  // ---- assemble x' = V y for the last cycle of every system
+  gm_backsolve_kernel<<<ns, 32, 0, st>>>(G, nullptr);
+  check_launch(b);
+  gm_combine_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, x, nullptr, 1);
+  check_launch(b);
+
+  // ---- final residual check (proj/src/gmres.cpp:129-136): r = rhs - op(x')
+  double* nrf = sc + 2 * ns;
+  if (c.final_check) {
+    apply_op(b, c, x, r, nullptr, st);
+    axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, nullptr, nullptr, 1.0, rhs, -1.0, r);
+    check_launch(b);
+    batched_dot(b, r, r, nrf, nullptr, st);
+  }
+  // ---- solution (proj/src/deflation.cpp:118-120, :141; proj/src/gmres.cpp:148)
+  double* u = b->vbuf[4].p;
+  switch (c.method) {
+    case SMPM_SCHUR:
+      CUDA_CHECK(cudaMemcpyAsync(xS, x, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
+      break;
+    case SMPM_BJ:
+      op_BJ(b, x, xS, nullptr, st);
+      break;
+    case SMPM_DBJ: {
+      double* q = b->vbuf[6].p;
+      op_BJ(b, x, u, nullptr, st);
+      op_Q(b, u, q, nullptr, st);
+      run_deflate(b, DEFL_ADD_ZC, bS, q, xS, nullptr, nullptr, st);
+      break;
+    }
+    case SMPM_2LAS:
+      op_BJ(b, x, u, nullptr, st);
+      run_deflate(b, DEFL_ADD_ZC, x, u, xS, nullptr, nullptr, st);
+      break;
+  }
+  CUDA_CHECK(cudaEventRecord(e1, st));
+  CUDA_CHECK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+  CUDA_CHECK(cudaEventDestroy(e0));
+  CUDA_CHECK(cudaEventDestroy(e1));
+  CUDA_CHECK(cudaEventDestroy(ev[0]));
+  CUDA_CHECK(cudaEventDestroy(ev[1]));
+  (void)launches0;
+
+  // ---- reports
+  if (reps || history) {
+    std::vector<int> hint(static_cast<size_t>(ns) * 8);
+    std::vector<double> hsc(static_cast<size_t>(ns) * 8), hg(static_cast<size_t>(ns) * (m + 1)),
+        hsm(static_cast<size_t>(ns) * 3);
+    CUDA_CHECK(cudaMemcpy(hint.data(), b->dgint.p, sizeof(int) * ns * 8, cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaMemcpy(hsc.data(), b->dscal.p, sizeof(double) * ns * 8, cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaMemcpy(hg.data(), b->dg.p, sizeof(double) * ns * (m + 1), cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaMemcpy(hsm.data(), sc, sizeof(double) * ns * 3, cudaMemcpyDeviceToHost));
+    std::vector<double> hh;
+    if (history) {
+      hh.resize(static_cast<size_t>(ns) * G.histcap);
+      CUDA_CHECK(cudaMemcpy(hh.data(), b->dhist.p, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost));
+    }
+    for (int s = 0; s < ns; ++s) {
+      const int iters = hint[static_cast<size_t>(ns) + s];
+      const int jc = hint[static_cast<size_t>(s)];
+      const int hl = hint[static_cast<size_t>(5 * ns) + s];
+      const double bn = hsc[static_cast<size_t>(s)];
+      const double tgt = hsc[static_cast<size_t>(ns) + s];
+      double frel = bn > 0 ? std::fabs(hg[static_cast<size_t>(s) * (m + 1) + jc]) / bn : 0.0;
+      bool mismatch = false;
+      if (c.final_check && bn > 0) {
+        const double true_rel = std::sqrt(hsm[static_cast<size_t>(2 * ns) + s]) / bn;
+        if (true_rel * bn > 10.0 * std::max(tgt, frel * bn)) mismatch = true;
+        frel = true_rel;
+      }
+      const long long apps = iters + (c.final_check ? 1 : 0) + op_applies;
+      if (reps) {
+        smpm_report& R = reps[s];
+        R.iterations = iters;
+        R.history_len = hl;
+        R.final_rel_residual = frel;
+        R.converged = bn > 0 ? (frel * bn <= tgt * (1.0 + 1e-12)) : 1;
+        R.mismatch_warning = mismatch ? 1 : 0;
+        R.operator_applies = apps;
+        R.krylov_s_applies = apps * per_sys_applies;
+        R.wall_time_s = ms * 1e-3;
+      }
+      if (history)
+        for (int i = 0; i < G.histcap; ++i)
+          history[static_cast<size_t>(s) * G.histcap + i] = i < hl ? hh[static_cast<size_t>(s) * G.histcap + i] : 0.0;
+    }
+  }
+  (void)s_applies;
+}
+
+void launch_zt(smpm_batch* b, const double* v, double* y, cudaStream_t st) {
+  zt_kernel<<<(b->nsys * b->d * 32 + 255) / 256, 256, 0, st>>>(b->nsys, b->d, 2 * b->w, b->k, v, y);
+  check_launch(b);
+}
+void launch_z(smpm_batch* b, const double* c, double* y, cudaStream_t st) {
+  zbroadcast_kernel<<<grid_for(b->nsys * b->k), 256, 0, st>>>(b->nsys, b->d, 2 * b->w, b->k, nullptr, c, y);
+  check_launch(b);
+}
+
+SolveCfg cfg_from(int method, const smpm_solve_options* o) {
+  SolveCfg c;
+  c.method = method;
+  c.tol = o ? o->tol : 1e-10;
+  c.max_iter = o ? o->max_iter : 100;
+  c.restart = o ? o->restart : 0;
+  c.orth = o ? o->orth : SMPM_ORTH_CGS2;
+  c.fused = o ? o->fuse_deflation != 0 : true;
+  c.final_check = o ? o->final_residual_check != 0 : true;
+  if (c.method < 0 || c.method > 3) fail(SMPM_EINVAL, "unknown method");
+  return c;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* smpm_last_error(void) { return g_last_error.c_str(); }
+
+const char* smpm_version(void) { return "smpm_b200 0.1 (sm_100a, fp64)"; }
+
+int smpm_ctx_create(int device, smpm_ctx** out) {
+  return guard([&] {
+    if (!out) fail(SMPM_EINVAL, "null out");
+    int ndev = 0;
+    CUDA_CHECK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) fail(SMPM_ECUDA, "no such CUDA device");
+    CUDA_CHECK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) fail(SMPM_ECUDA, "smpm_b200 kernels are built for sm_100a; device is sm_" +
+                                              std::to_string(prop.major) + std::to_string(prop.minor));
+    auto ctx = std::make_unique<smpm_ctx>();
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    // blocking stream: orders with the legacy default stream torch uses for handle 0
+    CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault));
+    CUSOLVER_CHECK(cusolverDnCreate(&ctx->solver));
+    CUSOLVER_CHECK(cusolverDnSetStream(ctx->solver, ctx->stream));
+    *out = ctx.release();
+  });
+}
+
+int smpm_ctx_destroy(smpm_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    if (ctx->solver) cusolverDnDestroy(ctx->solver);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+void* smpm_ctx_stream(smpm_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int smpm_batch_create(smpm_ctx* ctx, int n, int m_x, int m_z, int nsys, smpm_batch** out) {
+  return guard([&] {
+    if (!ctx || !out) fail(SMPM_EINVAL, "null argument");
+    if (n < 2 || m_x < 2 || m_z < 1 || nsys < 1) fail(SMPM_EINVAL, "smpm_batch_create: need n>=2, m_x>=2, m_z>=1, nsys>=1");
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+    auto b = std::make_unique<smpm_batch>();
+    b->ctx = ctx;
+    b->n = n;
+    b->mx = m_x;
+    b->mz = m_z;
+    b->nsys = nsys;
+    b->w = n * m_z;
+    b->d = m_x - 1;
+    b->k = 2LL * b->w * b->d;
+    b->nbf = b->d / 2;
+    b->single = (b->d % 2) == 1;
+    b->hG.assign(static_cast<size_t>(nsys) * 6 * b->w * b->w, 0.0);
+    b->have.assign(static_cast<size_t>(nsys), 0);
+    b->huS.assign(static_cast<size_t>(nsys), {});
+    *out = b.release();
+  });
+}
+
+int smpm_batch_destroy(smpm_batch* b) {
+  return guard([&] { delete b; });
+}
+
+int smpm_batch_dims(const smpm_batch* b, long long* k, int* d, int* w) {
+  return guard([&] {
+    if (!b) fail(SMPM_EINVAL, "null batch");
+    if (k) *k = b->k;
+    if (d) *d = b->d;
+    if (w) *w = b->w;
+  });
+}
+
+int smpm_batch_set_couplings(smpm_batch* b, int sys, const double* G_W, const double* G_I, const double* G_E) {
+  return guard([&] {
+    if (!b || sys < 0 || sys >= b->nsys) fail(SMPM_EINVAL, "bad system index");
+    if (b->finalized) fail(SMPM_EINVAL, "batch already finalized");
+    if (!G_W || !G_E || (b->mx >= 3 && !G_I)) fail(SMPM_EINVAL, "null coupling matrix");
+    const long long ww = 1LL * b->w * b->w;
+    double* dst = b->hG.data() + sys * 6 * ww;
+    std::memcpy(dst, G_W, sizeof(double) * ww);
+    if (G_I) std::memcpy(dst + ww, G_I, sizeof(double) * 4 * ww);
+    std::memcpy(dst + 5 * ww, G_E, sizeof(double) * ww);
+    b->have[sys] = 1;
+  });
+}
+
+int smpm_batch_set_interface_blocks(smpm_batch* b, int sys, const double* const* entries, const long long* rows,
+                                    const long long* const* seg_start, const long long* const* seg_len,
+                                    const int* nseg) {
+  return guard([&] {
+    if (!b || sys < 0 || sys >= b->nsys) fail(SMPM_EINVAL, "bad system index");
+    const int w = b->w, d = b->d;
+    const long long w2 = 2LL * w, ww = 1LL * w * w;
+    std::vector<double> GW(ww), GI(4 * ww, 0.0), GE(ww);
+    std::vector<char> seenI(4, 0);
+    // copy-and-verify helper: dst (ld) <- entries rows [r0,r0+w) x cols [c0,c0+w)
+    auto take = [&](const double* e, long long nrows, long long r0, long long c0, double* dst, long long ld,
+                    bool verify) {
+      for (long long c = 0; c < w; ++c)
+        for (long long r = 0; r < w; ++r) {
+          const double v = e[(c0 + c) * nrows + r0 + r];
+          double& t = dst[c * ld + r];
+          if (verify && t != v) fail(SMPM_EINVAL, "interface blocks are not copies of strip-kind couplings");
+          t = v;
+        }
+    };
+    for (int i = 0; i < d; ++i) {
+      const bool has_a = i >= 1, has_d = i <= d - 2;
+      const int want = 2 + (has_a ? 1 : 0) + (has_d ? 1 : 0);
+      if (nseg[i] != want || rows[i] != static_cast<long long>(want) * w)
+        fail(SMPM_EINVAL, "interface block " + std::to_string(i) + " has an unexpected segment layout");
+      long long off = 0;
+      const double* e = entries[i];
+      const long long nr = rows[i];
+      int q = 0;
+      if (has_a) {  // rows: W-readers of strip i, cols: E-own of strip i (interior)
+        if (seg_start[i][q] != (i - 1) * w2) fail(SMPM_EINVAL, "segment start mismatch");
+        take(e, nr, off, 0, GI.data() + w * w2, w2, seenI[1]);
+        seenI[1] = 1;
+        off += w;
+        ++q;
+      }
+      // seg b: W-readers of strip i+1 x W-own of strip i+1 (cols w..2w)
+      if (i + 1 == d) {
+        take(e, nr, off, w, GE.data(), w, false);
+      } else {
+        take(e, nr, off, w, GI.data(), w2, seenI[0]);
+        seenI[0] = 1;
+      }
+      off += w;
+      // seg c: E-readers of strip i x E-own of strip i (cols 0..w)
+      if (i == 0) {
+        take(e, nr, off, 0, GW.data(), w, false);
+      } else {
+        take(e, nr, off, 0, GI.data() + w * w2 + w, w2, seenI[3]);
+        seenI[3] = 1;
+      }
+      off += w;
+      if (has_d) {  // E-readers of strip i+1 x W-own of strip i+1
+        take(e, nr, off, w, GI.data() + w, w2, seenI[2]);
+        seenI[2] = 1;
+      }
+      (void)seg_len;
+    }
+    const long long ww2 = ww;
+    double* dst = b->hG.data() + sys * 6 * ww2;
+    std::memcpy(dst, GW.data(), sizeof(double) * ww);
+    std::memcpy(dst + ww, GI.data(), sizeof(double) * 4 * ww);
+    std::memcpy(dst + 5 * ww, GE.data(), sizeof(double) * ww);
+    b->have[sys] = 1;
+  });
+}
+
+int smpm_batch_set_nullspace(smpm_batch* b, int sys, const double* u_S) {
+  return guard([&] {
+    if (!b || sys < 0 || sys >= b->nsys) fail(SMPM_EINVAL, "bad system index");
+    if (b->finalized) fail(SMPM_EINVAL, "batch already finalized");
+    if (!u_S) {
+      b->huS[sys].clear();
+      return;
+    }
+    b->huS[sys].assign(u_S, u_S + b->k);
+  });
+}
+
+int smpm_batch_finalize(smpm_batch* b) {
+  return guard([&] {
+    if (!b) fail(SMPM_EINVAL, "null batch");
+    CUDA_CHECK(cudaSetDevice(b->ctx->device));
+    finalize(b);
+  });
+}
+
+int smpm_batch_coarse_info(smpm_batch* b, double* C, int* tridiagonal, int* singular) {
+  return guard([&] {
+    need_final(b);
+    if (C) std::copy(b->hC.begin(), b->hC.end(), C);
+    if (tridiagonal) std::copy(b->htri.begin(), b->htri.end(), tridiagonal);
+    if (singular) std::copy(b->hsing.begin(), b->hsing.end(), singular);
+  });
+}
+
+#define OP_ENTRY(name, body)                                                         \
+  int name(smpm_batch* b, const double* v, double* y, void* stream) {                \
+    return guard([&] {                                                               \
+      need_final(b);                                                                 \
+      if (!v || !y) fail(SMPM_EINVAL, "null vector");                                \
+      cudaStream_t st = b->st(stream);                                               \
+      body;                                                                          \
+    });                                                                              \
+  }
+OP_ENTRY(smpm_apply_S, op_S(b, v, y, nullptr, st))
+OP_ENTRY(smpm_apply_St, op_St(b, v, y, nullptr, st))
+OP_ENTRY(smpm_apply_block_jacobi_inv, op_BJ(b, v, y, nullptr, st))
+OP_ENTRY(smpm_apply_Q, op_Q(b, v, y, nullptr, st))
+OP_ENTRY(smpm_apply_Zt, launch_zt(b, v, y, st))
+OP_ENTRY(smpm_apply_Z, launch_z(b, v, y, st))
+OP_ENTRY(smpm_coarse_solve, run_deflate(b, DEFL_COARSE_DIRECT, v, nullptr, nullptr, y, nullptr, st))
+#undef OP_ENTRY
+
+int smpm_apply_P(smpm_batch* b, const double* v, double* y, int fused, void* stream) {
+  return guard([&] {
+    need_final(b);
+    op_P(b, v, y, fused != 0, nullptr, b->st(stream));
+  });
+}
+
+int smpm_project_out(smpm_batch* b, long long len, const double* v, const double* dir, double* out, void* stream) {
+  return guard([&] {
+    need_final(b);
+    if (len != b->k) fail(SMPM_EINVAL, "smpm_project_out: only interface-length vectors are supported");
+    cudaStream_t st = b->st(stream);
+    double* dots = b->dsmall.p;
+    batched_dot(b, dir, v, dots, nullptr, st);
+    project_kernel<<<grid_for(b->nsys * b->k), 256, 0, st>>>(b->nsys, b->k, dots, v, dir, out);
+    check_launch(b);
+  });
+}
+
+int smpm_solve(smpm_batch* b, int method, const double* b_S, double* x_S, const smpm_solve_options* opt,
+               smpm_report* reports, double* history, void* stream) {
+  return guard([&] {
+    need_final(b);
+    if (!b_S || !x_S) fail(SMPM_EINVAL, "null vector");
+    solve(b, cfg_from(method, opt), b_S, x_S, reports, history, b->st(stream));
+  });
+}
+
+int smpm_deflated_solve(smpm_batch* b, const double* b_S, double* x_S, const smpm_solve_options* opt,
+                        smpm_report* reports, double* history, void* stream) {
+  return smpm_solve(b, SMPM_DBJ, b_S, x_S, opt, reports, history, stream);
+}
+
+int smpm_two_level_schwarz_solve(smpm_batch* b, const double* b_S, double* x_S, const smpm_solve_options* opt,
+                                 smpm_report* reports, double* history, void* stream) {
+  return smpm_solve(b, SMPM_2LAS, b_S, x_S, opt, reports, history, stream);
+}
+
+int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x_S_host,
+                    const smpm_solve_options* opt, smpm_report* reports, double* history) {
+  return guard([&] {
+    need_final(b);
+    cudaStream_t st = b->ctx->stream;
+    const size_t bytes = sizeof(double) * b->nsys * static_cast<size_t>(b->k);
+    double* din = b->vbuf[10].p;
+    double* dout = b->vbuf[11].p;
+    CUDA_CHECK(cudaMemcpyAsync(din, b_S_host, bytes, cudaMemcpyHostToDevice, st));
+    solve(b, cfg_from(method, opt), din, dout, reports, history, st);
+    CUDA_CHECK(cudaMemcpyAsync(x_S_host, dout, bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+long long smpm_batch_launch_count(const smpm_batch* b) { return b ? b->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,596 @@
+// Bandwidth-bound kernels of the Schur-GMRES hot path (sm_100a): deflation
+// (Z^T segmented sums, coarse solve, P/Q/2LAS updates, one CTA per system so
+// the whole projection is a single launch), and the batched Arnoldi
+// orthogonalization (CGS2 and MGS) with deterministic "last CTA reduces"
+// cross-CTA reductions, device-side Givens updates and convergence flags.
+#pragma once
+
+#include "common.cuh"
+
+namespace smpm {
+
+constexpr int VEC_THREADS = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Deflation: one CTA per system.
+// ---------------------------------------------------------------------------
+struct DeflateParams {
+  int nsys, d, w;
+  long long k;
+  const int* active;        // nullable
+  const int* cmode;         // per system: 0 dense inverse (singular or general), 1 Thomas
+  const double* cinv;       // nsys x d x d (column-major)
+  const double* uc;         // nsys x d (singular systems)
+  const int* singular;      // per system
+  const double* thomas;     // nsys x 3 x d: sub, cprime, piv
+  const double* rowsum;     // nsys x 6w: rW_I(2w) rE_I(2w) rE_W(w) rW_E(w)
+  int mx;
+};
+
+enum DeflateMode : int {
+  DEFL_P_FUSED = 0,   // y = zin - S Z c(Z^T zin), S Z c via row sums (zin == y allowed? no)
+  DEFL_Q_TAIL = 1,    // y = v - Z c(Z^T zin)   (zin = S v)
+  DEFL_COARSE = 2,    // cout = c(Z^T zin)
+  DEFL_ADD_ZC = 3,    // y = v + Z c(Z^T zin)   (2LAS: zin = v, v = M^{-1} v)
+  DEFL_SUB_T = 4,     // y = v - zin            (literal P tail: zin = S Z c)
+  DEFL_COARSE_DIRECT = 5  // cout = c(zin) with zin a coarse vector (nsys x d)
+};
+
+__device__ void coarse_solve_block(const DeflateParams& P, int s, double* sums, double* c) {
+  const int d = P.d;
+  const int t = threadIdx.x;
+  if (P.singular[s]) {
+    // rhs = b - u_C (u_C . b)  (/root/reference/proj/src/deflation.cpp:73-76)
+    __shared__ double red[32];
+    const double* uc = P.uc + static_cast<long long>(s) * d;
+    double acc = 0.0;
+    for (int i = t; i < d; i += blockDim.x) acc += uc[i] * sums[i];
+    acc = warp_sum(acc);
+    if ((t & 31) == 0) red[t >> 5] = acc;
+    __syncthreads();
+    if (t < 32) {
+      double v = t < (blockDim.x >> 5) ? red[t] : 0.0;
+      v = warp_sum(v);
+      if (t == 0) red[0] = v;
+    }
+    __syncthreads();
+    const double dotv = red[0];
+    for (int i = t; i < d; i += blockDim.x) sums[i] -= uc[i] * dotv;
+    __syncthreads();
+  }
+  if (P.cmode[s] == 1) {
+    // Thomas algorithm with precomputed pivots (proj/src/deflation.cpp:77-90)
+    if (t == 0) {
+      const double* sub = P.thomas + static_cast<long long>(s) * 3 * d;
+      const double* cp = sub + d;
+      const double* piv = cp + d;
+      double yprev = sums[0] / piv[0];
+      c[0] = yprev;
+      for (int i = 1; i < d; ++i) {
+        yprev = (sums[i] - sub[i - 1] * yprev) / piv[i];
+        c[i] = yprev;
+      }
+      for (int i = d - 2; i >= 0; --i) c[i] -= cp[i] * c[i + 1];
+    }
+  } else {
+    const double* ci = P.cinv + static_cast<long long>(s) * d * d;
+    for (int i = t; i < d; i += blockDim.x) {
+      double acc = 0.0;
+      for (int j = 0; j < d; ++j) acc += ci[static_cast<long long>(j) * d + i] * sums[j];
+      c[i] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+// zin: vector whose Z^T sums feed the coarse solve; v: the vector updated.
+__global__ void __launch_bounds__(VEC_THREADS)
+deflate_kernel(DeflateParams P, int mode, const double* __restrict__ zin, const double* __restrict__ v,
+               double* __restrict__ y, double* __restrict__ cout) {
+  extern __shared__ double sm[];
+  const int s = blockIdx.x;
+  if (P.active && !P.active[s]) return;
+  const int d = P.d, w = P.w;
+  const long long k = P.k;
+  double* sums = sm;
+  double* c = sm + d;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+  const double* zs = zin + static_cast<long long>(s) * (mode == DEFL_COARSE_DIRECT ? d : k);
+  const int w2 = 2 * w;
+  if (mode == DEFL_COARSE_DIRECT) {
+    for (int i = t; i < d; i += blockDim.x) sums[i] = zin[static_cast<long long>(s) * d + i];
+    __syncthreads();
+    coarse_solve_block(P, s, sums, c);
+    for (int i = t; i < d; i += blockDim.x) cout[static_cast<long long>(s) * d + i] = c[i];
+    return;
+  }
+  if (mode != DEFL_SUB_T) {
+    // Z^T: segmented sums over the 2w slots of each interface (proj/src/deflation.cpp:16-22)
+    for (int i = warp; i < d; i += nw) {
+      const double* seg = zs + static_cast<long long>(i) * w2;
+      double acc = 0.0;
+      for (int e = lane; e < w2; e += 32) acc += seg[e];
+      acc = warp_sum(acc);
+      if (lane == 0) sums[i] = acc;
+    }
+    __syncthreads();
+    coarse_solve_block(P, s, sums, c);
+  }
+  if (mode == DEFL_COARSE) {
+    for (int i = t; i < d; i += blockDim.x) cout[static_cast<long long>(s) * d + i] = c[i];
+    return;
+  }
+  const double* vs = v + static_cast<long long>(s) * k;
+  double* ys = y + static_cast<long long>(s) * k;
+  if (mode == DEFL_SUB_T) {
+    for (long long e = t; e < k; e += blockDim.x) ys[e] = vs[e] - zs[e];
+    return;
+  }
+  if (mode == DEFL_Q_TAIL || mode == DEFL_ADD_ZC) {
+    const double sg = mode == DEFL_Q_TAIL ? -1.0 : 1.0;
+    for (long long e = t; e < k; e += blockDim.x) ys[e] = vs[e] + sg * c[e / w2];
+    return;
+  }
+  // DEFL_P_FUSED: y = v - Z c - scatter(strip row sums) ; here v == zin (t = S u)
+  const double* rs = P.rowsum + static_cast<long long>(s) * 6 * w;
+  const double* rWI = rs;           // interior strip, W-own column sums, rows [W-readers; E-readers]
+  const double* rEI = rs + w2;      // interior strip, E-own column sums
+  const double* rEW = rs + 2 * w2;  // west-boundary strip (E-readers x E-own)
+  const double* rWE = rEW + w;      // east-boundary strip (W-readers x W-own)
+  const int mx = P.mx;
+  for (long long e = t; e < k; e += blockDim.x) {
+    const int blk = static_cast<int>(e / w);
+    const int r = static_cast<int>(e - static_cast<long long>(blk) * w);
+    const int i = blk >> 1;  // interface
+    double sz;
+    if ((blk & 1) == 0) {
+      // left side of interface i = west-readers of strip i+1 (reads c_i on its W-own, c_{i+1} on E-own)
+      const int st = i + 1;
+      if (st == mx - 1)
+        sz = c[i] * rWE[r];
+      else
+        sz = c[i] * rWI[r] + c[i + 1] * rEI[r];
+    } else {
+      // right side of interface i = east-readers of strip i (c_{i-1} on W-own, c_i on E-own)
+      const int st = i;
+      if (st == 0)
+        sz = c[i] * rEW[r];
+      else
+        sz = c[i - 1] * rWI[w + r] + c[i] * rEI[w + r];
+    }
+    ys[e] = vs[e] - (c[i] + sz);
+  }
+}
+
+// y = Z c broadcast (c: nsys x d)
+__global__ void zbroadcast_kernel(int nsys, int d, int w2, long long k, const int* active, const double* __restrict__ c,
+                                  double* __restrict__ y) {
+  const long long tot = static_cast<long long>(nsys) * k;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < tot;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int s = static_cast<int>(e / k);
+    if (active && !active[s]) continue;
+    const long long r = e - static_cast<long long>(s) * k;
+    y[e] = c[static_cast<long long>(s) * d + r / w2];
+  }
+}
+
+// Z^T only (nsys x d out), one warp per interface
+__global__ void zt_kernel(int nsys, int d, int w2, long long k, const double* __restrict__ v, double* __restrict__ y) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= nsys * d) return;
+  const int s = gw / d, i = gw % d;
+  const double* seg = v + static_cast<long long>(s) * k + static_cast<long long>(i) * w2;
+  double acc = 0.0;
+  for (int e = lane; e < w2; e += 32) acc += seg[e];
+  acc = warp_sum(acc);
+  if (lane == 0) y[gw] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// Batched GMRES state (structure of arrays, one entry per system)
+// ---------------------------------------------------------------------------
+enum GmState : int { GM_RUN = 0, GM_CONV = 1, GM_BREAK = 2, GM_MAXED = 3, GM_CYCLE = 4 };
+
+struct GmState_ {
+  int* jcyc;      // Arnoldi index inside the current cycle (0-based column being built)
+  int* iters;     // total iterations
+  int* state;     // GmState
+  int* active;    // 1 while the operator/orthogonalization must run for the system
+  int* counter;   // last-CTA counters, one per system
+  int* hist_len;
+  double* bnorm;  // ||rhs of GMRES||
+  double* target; // absolute tolerance
+  double* hmax;
+  double* nrm;    // norm of the latest Arnoldi vector
+  double* R;      // nsys x (m+1) x m  (triangularized Hessenberg columns)
+  double* cs;     // nsys x m
+  double* sn;     // nsys x m
+  double* g;      // nsys x (m+1)
+  double* h1;     // nsys x (m+2)
+  double* h2;     // nsys x (m+2)
+  double* y;      // nsys x m
+  double* hist;   // nsys x histcap
+  double* part;   // nsys x nchunk x (m+2) partial sums
+  int m;          // cycle length
+  int m_total;    // max iterations
+  int histcap;
+  long long k;
+  long long vstride;  // (m+1)*k per system
+  int chunk, nchunk;
+  int nsys;
+};
+
+// partial dot products of columns [0, ncols) of V_s with x over rows [r0, r1),
+// warp per column; writes part[s][chunk][col]
+__device__ __forceinline__ void chunk_dots(const double* __restrict__ Vs, long long k, int ncols,
+                                           const double* __restrict__ xs, int r0, int r1, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < ncols; i += nw) {
+    const double* col = Vs + static_cast<long long>(i) * k;
+    double acc = 0.0;
+    for (int r = r0 + lane; r < r1; r += 32) acc = fma(col[r], xs[r], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) out[i] = acc;
+  }
+}
+
+// returns true in exactly one CTA per system once all its chunks have written partials
+__device__ __forceinline__ bool last_cta(int* counter, int nchunk) {
+  __shared__ int is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int old = atomicAdd(counter, 1);
+    is_last = (old == nchunk - 1);
+    if (is_last) *counter = 0;
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+// reduce part[s][0..nchunk)[0..ncols) in chunk order -> out[0..ncols)
+__device__ __forceinline__ void reduce_parts(const double* __restrict__ part, int nchunk, int stride, int ncols,
+                                             double* __restrict__ out) {
+  for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < nchunk; ++c) acc += part[static_cast<long long>(c) * stride + i];
+    out[i] = acc;
+  }
+}
+
+// ---- CGS2 pass 1: h1 = V^T w ----------------------------------------------
+__global__ void __launch_bounds__(VEC_THREADS) cgs_dot_kernel(GmState_ G, const double* __restrict__ V,
+                                                              const double* __restrict__ w) {
+  const int s = blockIdx.y;
+  if (!G.active[s]) return;
+  const int ncols = G.jcyc[s] + 1;
+  const int ch = blockIdx.x;
+  const int r0 = ch * G.chunk, r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
+  const int stride = G.m + 2;
+  double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
+  chunk_dots(V + s * G.vstride, G.k, ncols, w + s * G.k, r0, r1, part);
+  if (last_cta(G.counter + s, G.nchunk))
+    reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols,
+                 G.h1 + static_cast<long long>(s) * stride);
+}
+
+// ---- CGS2 pass 2/3: w -= V h; then (pass 2) h2 = V^T w or (pass 3) ||w|| ----
+template <bool NORM>
+__global__ void __launch_bounds__(VEC_THREADS) cgs_update_kernel(GmState_ G, const double* __restrict__ V,
+                                                                 double* __restrict__ w, int do_update) {
+  extern __shared__ double hs[];  // m + 2 doubles
+  __shared__ double red[32];
+  const int s = blockIdx.y;
+  if (!G.active[s]) return;
+  const int j = G.jcyc[s];
+  const int ncols = j + 1;
+  const int stride = G.m + 2;
+  const double* hin = (NORM ? G.h2 : G.h1) + static_cast<long long>(s) * stride;
+  for (int i = threadIdx.x; i < ncols; i += blockDim.x) hs[i] = hin[i];
+  __syncthreads();
+  const int ch = blockIdx.x;
+  const int r0 = ch * G.chunk, r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
+  const double* Vs = V + s * G.vstride;
+  double* ws = w + s * G.k;
+  double sq = 0.0;
+  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    double acc = ws[r];
+    if (do_update) {
+      for (int i = 0; i < ncols; ++i) acc = fma(-Vs[static_cast<long long>(i) * G.k + r], hs[i], acc);
+      ws[r] = acc;
+    }
+    sq = fma(acc, acc, sq);
+  }
+  double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
+  if (!NORM) {
+    __syncthreads();  // this CTA's rows of w are final (own rows only)
+    chunk_dots(Vs, G.k, ncols, ws, r0, r1, part);
+    if (last_cta(G.counter + s, G.nchunk))
+      reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols,
+                   G.h2 + static_cast<long long>(s) * stride);
+    return;
+  }
+  sq = warp_sum(sq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tsum = 0.0;
+    for (int i = 0; i < (blockDim.x >> 5); ++i) tsum += red[i];
+    part[0] = tsum;
+  }
+  if (!last_cta(G.counter + s, G.nchunk)) return;
+  if (threadIdx.x != 0) return;
+  // ---- last CTA, thread 0: norm + Givens + convergence (proj/src/gmres.cpp:71-99)
+  double nsq = 0.0;
+  const double* p0 = G.part + static_cast<long long>(s) * G.nchunk * stride;
+  for (int c = 0; c < G.nchunk; ++c) nsq += p0[static_cast<long long>(c) * stride];
+  const double nrm = sqrt(nsq);
+  G.nrm[s] = nrm;
+  const int m = G.m;
+  double* h1 = G.h1 + static_cast<long long>(s) * stride;
+  const double* h2 = G.h2 + static_cast<long long>(s) * stride;
+  double* cs = G.cs + static_cast<long long>(s) * m;
+  double* sn = G.sn + static_cast<long long>(s) * m;
+  double* g = G.g + static_cast<long long>(s) * (m + 1);
+  double* R = G.R + static_cast<long long>(s) * (m + 1) * m;
+  double hmax = G.hmax[s];
+  for (int i = 0; i <= j; ++i) {
+    h1[i] += h2[i];
+    hmax = fmax(hmax, fabs(h1[i]));
+  }
+  h1[j + 1] = nrm;
+  hmax = fmax(hmax, nrm);
+  G.hmax[s] = hmax;
+  for (int i = 0; i < j; ++i) {
+    const double t1 = h1[i], t2 = h1[i + 1];
+    h1[i] = cs[i] * t1 + sn[i] * t2;
+    h1[i + 1] = -sn[i] * t1 + cs[i] * t2;
+  }
+  const double rad = hypot(h1[j], h1[j + 1]);
+  cs[j] = rad > 0.0 ? h1[j] / rad : 1.0;
+  sn[j] = rad > 0.0 ? h1[j + 1] / rad : 0.0;
+  h1[j] = rad;
+  const double g1 = g[j], g2 = g[j + 1];
+  g[j] = cs[j] * g1 + sn[j] * g2;
+  g[j + 1] = -sn[j] * g1 + cs[j] * g2;
+  for (int i = 0; i <= j; ++i) R[static_cast<long long>(j) * (m + 1) + i] = h1[i];
+  const int it = G.iters[s] + 1;
+  G.iters[s] = it;
+  G.jcyc[s] = j + 1;
+  const double res = fabs(g[j + 1]);
+  const int hl = G.hist_len[s];
+  if (hl < G.histcap) {
+    G.hist[static_cast<long long>(s) * G.histcap + hl] = res / G.bnorm[s];
+    G.hist_len[s] = hl + 1;
+  }
+  int st = GM_RUN;
+  if (res <= G.target[s])
+    st = GM_CONV;
+  else if (nrm <= 1e-14 * hmax)
+    st = GM_BREAK;
+  else if (it >= G.m_total)
+    st = GM_MAXED;
+  else if (j + 1 >= m)
+    st = GM_CYCLE;
+  G.state[s] = st;
+  if (st != GM_RUN) G.active[s] = 0;
+}
+
+// v_{j+1} = w / ||w|| into V[:, jcyc] and the operator input buffer
+__global__ void gm_scale_kernel(GmState_ G, double* __restrict__ V, const double* __restrict__ w,
+                                double* __restrict__ vin) {
+  const int s = blockIdx.y;
+  if (!G.active[s]) return;
+  const double inv = 1.0 / G.nrm[s];
+  const int j = G.jcyc[s];
+  double* col = V + s * G.vstride + static_cast<long long>(j) * G.k;
+  const double* ws = w + s * G.k;
+  double* vs = vin + s * G.k;
+  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < G.k;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double v = ws[r] * inv;
+    col[r] = v;
+    vs[r] = v;
+  }
+}
+
+// ---- MGS: one fused step per basis vector: w -= h_{i-1} v_{i-1}; h_i = v_i . w
+// (i == ncols finishes with the norm + Givens via cgs_update_kernel<true> on h2 = 0)
+__global__ void __launch_bounds__(VEC_THREADS) mgs_step_kernel(GmState_ G, const double* __restrict__ V,
+                                                               double* __restrict__ w, int i) {
+  const int s = blockIdx.y;
+  if (!G.active[s]) return;
+  const int ncols = G.jcyc[s] + 1;
+  if (i > ncols) return;
+  const int stride = G.m + 2;
+  const int ch = blockIdx.x;
+  const int r0 = ch * G.chunk, r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
+  const double* Vs = V + s * G.vstride;
+  double* ws = w + s * G.k;
+  double* h1 = G.h1 + static_cast<long long>(s) * stride;
+  if (i > 0) {
+    const double hp = h1[i - 1];
+    const double* vp = Vs + static_cast<long long>(i - 1) * G.k;
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) ws[r] = fma(-hp, vp[r], ws[r]);
+    __syncthreads();
+  }
+  if (i == ncols) return;
+  double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double red[32];
+  const double* vi = Vs + static_cast<long long>(i) * G.k;
+  double acc = 0.0;
+  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) acc = fma(vi[r], ws[r], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (blockDim.x >> 5); ++q) t += red[q];
+    part[0] = t;
+  }
+  if (last_cta(G.counter + s, G.nchunk) && threadIdx.x == 0) {
+    double t = 0.0;
+    const double* p0 = G.part + static_cast<long long>(s) * G.nchunk * stride;
+    for (int c = 0; c < G.nchunk; ++c) t += p0[static_cast<long long>(c) * stride];
+    h1[i] = t;
+  }
+}
+
+// zero h2 (MGS path has no second pass)
+__global__ void gm_zero_h2_kernel(GmState_ G) {
+  const int s = blockIdx.x;
+  if (!G.active[s]) return;
+  double* h2 = G.h2 + static_cast<long long>(s) * (G.m + 2);
+  for (int i = threadIdx.x; i < G.m + 2; i += blockDim.x) h2[i] = 0.0;
+}
+
+// ---- generic batched squared norms / dots: out[s] = sum x_s . y_s --------
+__global__ void __launch_bounds__(VEC_THREADS) batched_dot_kernel(int nsys, long long k, int chunk, int nchunk,
+                                                                  const int* active, const double* __restrict__ x,
+                                                                  const double* __restrict__ y,
+                                                                  double* __restrict__ part, int* counter,
+                                                                  double* __restrict__ out) {
+  __shared__ double red[32];
+  const int s = blockIdx.y;
+  if (active && !active[s]) return;
+  const int ch = blockIdx.x;
+  const long long r0 = static_cast<long long>(ch) * chunk, r1 = min(k, r0 + chunk);
+  const double* xs = x + s * k;
+  const double* ys = y + s * k;
+  double acc = 0.0;
+  for (long long r = r0 + threadIdx.x; r < r1; r += blockDim.x) acc = fma(xs[r], ys[r], acc);
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (blockDim.x >> 5); ++q) t += red[q];
+    part[static_cast<long long>(s) * nchunk + ch] = t;
+  }
+  if (last_cta(counter + s, nchunk) && threadIdx.x == 0) {
+    double t = 0.0;
+    for (int c = 0; c < nchunk; ++c) t += part[static_cast<long long>(s) * nchunk + c];
+    out[s] = t;
+  }
+}
+
+// y = a[s]*x + b*y  per system (a from device array, optional)
+__global__ void axpby_kernel(int nsys, long long k, const int* active, const double* __restrict__ a_dev, double a,
+                             const double* __restrict__ x, double b, double* __restrict__ y) {
+  const long long tot = static_cast<long long>(nsys) * k;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < tot;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int s = static_cast<int>(e / k);
+    if (active && !active[s]) continue;
+    const double av = a_dev ? a_dev[s] : a;
+    y[e] = fma(av, x[e], b * y[e]);
+  }
+}
+
+// out = v - dir * dots[s]
+__global__ void project_kernel(int nsys, long long k, const double* __restrict__ dots, const double* __restrict__ v,
+                               const double* __restrict__ dir, double* __restrict__ out) {
+  const long long tot = static_cast<long long>(nsys) * k;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < tot;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int s = static_cast<int>(e / k);
+    out[e] = fma(-dir[e], dots[s], v[e]);
+  }
+}
+
+// ---- GMRES cycle start: bnorm/target on the first cycle, g0, v0 = r / ||r|| ----
+// nrm2sq: ||r||^2 per system; first: 1 on the first cycle.
+__global__ void gm_start_kernel(GmState_ G, const double* __restrict__ nrm2sq, const double* __restrict__ bs_nrm2sq,
+                                double tol, int first, const int* __restrict__ restart_mask) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= G.nsys) return;
+  if (!first && !(restart_mask && restart_mask[s] == GM_CYCLE)) return;
+  const double rn = sqrt(nrm2sq[s]);
+  const int m = G.m;
+  if (first) {
+    G.bnorm[s] = rn;
+    // abs target = tol * ||b_S|| (proj/src/deflation.cpp:109)
+    G.target[s] = tol * sqrt(bs_nrm2sq[s]);
+    G.hmax[s] = 0.0;
+    G.iters[s] = 0;
+    G.hist_len[s] = 1;
+    G.hist[static_cast<long long>(s) * G.histcap] = rn > 0.0 ? 1.0 : 0.0;
+  }
+  double* g = G.g + static_cast<long long>(s) * (m + 1);
+  for (int i = 0; i <= m; ++i) g[i] = 0.0;
+  g[0] = rn;
+  G.nrm[s] = rn;
+  G.jcyc[s] = 0;
+  const bool go = rn > 0.0 && G.iters[s] < G.m_total;
+  G.state[s] = go ? GM_RUN : GM_CONV;
+  G.active[s] = go ? 1 : 0;
+}
+
+// v0 = r / ||r|| into V[:,0] and vin, for systems just (re)started
+__global__ void gm_v0_kernel(GmState_ G, double* __restrict__ V, const double* __restrict__ r,
+                             double* __restrict__ vin) {
+  const int s = blockIdx.y;
+  if (!G.active[s] || G.jcyc[s] != 0) return;
+  const double inv = 1.0 / G.nrm[s];
+  double* col = V + s * G.vstride;
+  const double* rs = r + s * G.k;
+  double* vs = vin + s * G.k;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < G.k;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double v = rs[e] * inv;
+    col[e] = v;
+    vs[e] = v;
+  }
+}
+
+// back-substitution R y = g for the systems whose cycle ended (warp per system)
+// (proj/src/gmres.cpp:116-125); ncyc = columns built in this cycle
+__global__ void gm_backsolve_kernel(GmState_ G, const int* __restrict__ sel) {
+  const int s = blockIdx.x;
+  if (sel && !sel[s]) return;
+  const int lane = threadIdx.x;
+  const int n = G.jcyc[s];
+  const int m = G.m;
+  const double* R = G.R + static_cast<long long>(s) * (m + 1) * m;
+  const double* g = G.g + static_cast<long long>(s) * (m + 1);
+  double* y = G.y + static_cast<long long>(s) * m;
+  for (int i = n - 1; i >= 0; --i) {
+    double acc = 0.0;
+    for (int c = i + 1 + lane; c < n; c += 32) acc += R[static_cast<long long>(c) * (m + 1) + i] * y[c];
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const double rii = R[static_cast<long long>(i) * (m + 1) + i];
+      y[i] = fabs(rii) > 0.0 ? (g[i] - acc) / rii : 0.0;
+    }
+    __syncwarp();
+  }
+}
+
+// x (+)= V y over the columns of the finished cycle
+__global__ void gm_combine_kernel(GmState_ G, const double* __restrict__ V, double* __restrict__ x,
+                                  const int* __restrict__ sel, int accumulate) {
+  const int s = blockIdx.y;
+  if (sel && !sel[s]) return;
+  const int n = G.jcyc[s];
+  const double* y = G.y + static_cast<long long>(s) * G.m;
+  const double* Vs = V + s * G.vstride;
+  double* xs = x + s * G.k;
+  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < G.k;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double acc = accumulate ? xs[r] : 0.0;
+    for (int i = 0; i < n; ++i) acc = fma(Vs[static_cast<long long>(i) * G.k + r], y[i], acc);
+    xs[r] = acc;
+  }
+}
+
+}  // namespace smpm

@@ -1,0 +1,248 @@
+"""Host-side mirror of the reference operator/solver API over the C ABI.
+
+Names follow the reference library (``/root/reference/proj/include/smpm``):
+``apply_S``, ``apply_St``, ``apply_block_jacobi_inv``, ``apply_Z``,
+``apply_Zt``, ``coarse_solve``, ``apply_P``, ``apply_Q``, ``project_out``,
+``deflated_solve``, ``two_level_schwarz_solve``.  Vectors are torch CUDA
+tensors of shape (nsys, k) (coarse vectors (nsys, d)); matrices are host
+arrays.  Everything runs in ``lib/libsmpm_b200.so`` — there is no Python or
+CPU compute path here, only plumbing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import METHODS, ORTH, Report, SmpmError, SolveOptions, check, lib
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _dptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _hptr(a):
+    return C.c_void_p(a.ctypes.data)
+
+
+class Context:
+    """One per device (``smpm_ctx``)."""
+
+    def __init__(self, device: int = 0):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise SmpmError(5, "no CUDA device visible (the B200 path has no CPU fallback)")
+        torch.cuda.init()
+        self.device = device
+        h = C.c_void_p()
+        check(lib().smpm_ctx_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().smpm_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+@dataclass
+class SolveResult:
+    x_S: object  # torch tensor (nsys, k) or numpy for solve_host
+    iterations: list
+    converged: list
+    final_rel_residual: list
+    operator_applies: list
+    krylov_s_applies: list
+    mismatch_warning: list
+    wall_time_s: float
+    histories: list = field(repr=False, default_factory=list)
+
+
+class SchurBatch:
+    """``nsys`` Schur systems of one geometry on one device (``smpm_batch``)."""
+
+    def __init__(self, ctx: Context, n: int, m_x: int, m_z: int, nsys: int = 1):
+        self.ctx = ctx
+        h = C.c_void_p()
+        check(lib().smpm_batch_create(ctx.h, n, m_x, m_z, nsys, C.byref(h)))
+        self.h = h
+        k, d, w = C.c_longlong(), C.c_int(), C.c_int()
+        check(lib().smpm_batch_dims(h, C.byref(k), C.byref(d), C.byref(w)))
+        self.n, self.m_x, self.m_z, self.nsys = n, m_x, m_z, nsys
+        self.k, self.d, self.w = k.value, d.value, w.value
+        self._keep = []
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().smpm_batch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    # ---- setup ----------------------------------------------------------
+    def set_couplings(self, sys: int, G_W, G_I, G_E):
+        w = self.w
+        gw = np.asfortranarray(G_W, dtype=np.float64)
+        ge = np.asfortranarray(G_E, dtype=np.float64)
+        if gw.shape != (w, w) or ge.shape != (w, w):
+            raise SmpmError(1, "G_W/G_E must be w x w")
+        gi = None
+        if G_I is not None:
+            gi = np.asfortranarray(G_I, dtype=np.float64)
+            if gi.shape != (2 * w, 2 * w):
+                raise SmpmError(1, "G_I must be 2w x 2w")
+        check(lib().smpm_batch_set_couplings(self.h, sys, _hptr(gw), _hptr(gi) if gi is not None else None, _hptr(ge)))
+
+    def set_interface_blocks(self, sys: int, blocks):
+        """blocks: list of (entries[rows x 2w], [(start, len), ...]) in the
+        reference's InterfaceBlock layout (proj/include/smpm/schur.hpp:32-36)."""
+        d = len(blocks)
+        ents = [np.asfortranarray(e, dtype=np.float64) for e, _ in blocks]
+        starts = [np.array([s for s, _ in segs], dtype=np.int64) for _, segs in blocks]
+        lens = [np.array([l for _, l in segs], dtype=np.int64) for _, segs in blocks]
+        ep = (C.c_void_p * d)(*[e.ctypes.data for e in ents])
+        rows = (C.c_longlong * d)(*[e.shape[0] for e in ents])
+        sp = (C.c_void_p * d)(*[s.ctypes.data for s in starts])
+        lp = (C.c_void_p * d)(*[l.ctypes.data for l in lens])
+        ns = (C.c_int * d)(*[len(s) for s in starts])
+        check(lib().smpm_batch_set_interface_blocks(self.h, sys, ep, rows, sp, lp, ns))
+
+    def set_nullspace(self, sys: int, u_S):
+        u = np.ascontiguousarray(u_S, dtype=np.float64)
+        if u.size != self.k:
+            raise SmpmError(1, "u_S must have length k")
+        check(lib().smpm_batch_set_nullspace(self.h, sys, _hptr(u)))
+
+    def finalize(self):
+        check(lib().smpm_batch_finalize(self.h))
+        return self
+
+    def coarse_info(self):
+        Cm = np.zeros((self.nsys, self.d, self.d))
+        tri = (C.c_int * self.nsys)()
+        sing = (C.c_int * self.nsys)()
+        check(lib().smpm_batch_coarse_info(self.h, _hptr(Cm), tri, sing))
+        return np.transpose(Cm, (0, 2, 1)).copy(), list(tri), list(sing)
+
+    # ---- operators --------------------------------------------------------
+    def _stream(self):
+        torch = _torch()
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def _vec(self, v, n):
+        torch = _torch()
+        if not (isinstance(v, torch.Tensor) and v.is_cuda and v.dtype == torch.float64):
+            raise SmpmError(1, "expected a float64 CUDA tensor")
+        v = v.contiguous()
+        if v.numel() != self.nsys * n:
+            raise SmpmError(1, f"expected {self.nsys} x {n} elements, got {v.numel()}")
+        return v.view(self.nsys, n)
+
+    def _op(self, fn, v, nin, nout):
+        torch = _torch()
+        v = self._vec(v, nin)
+        y = torch.empty((self.nsys, nout), dtype=torch.float64, device=v.device)
+        check(getattr(lib(), fn)(self.h, _dptr(v), _dptr(y), self._stream()))
+        return y
+
+    def apply_S(self, v):  # proj/src/schur.cpp:143-158
+        return self._op("smpm_apply_S", v, self.k, self.k)
+
+    def apply_St(self, v):  # proj/src/schur.cpp:160-175
+        return self._op("smpm_apply_St", v, self.k, self.k)
+
+    def apply_block_jacobi_inv(self, v):  # proj/src/schur.cpp:218-225
+        return self._op("smpm_apply_block_jacobi_inv", v, self.k, self.k)
+
+    def apply_Z(self, y):  # proj/src/deflation.cpp:8-14
+        return self._op("smpm_apply_Z", y, self.d, self.k)
+
+    def apply_Zt(self, v):  # proj/src/deflation.cpp:16-22
+        return self._op("smpm_apply_Zt", v, self.k, self.d)
+
+    def coarse_solve(self, b):  # proj/src/deflation.cpp:71-92
+        return self._op("smpm_coarse_solve", b, self.d, self.d)
+
+    def apply_Q(self, v):  # proj/src/deflation.cpp:98-100
+        return self._op("smpm_apply_Q", v, self.k, self.k)
+
+    def apply_P(self, v, fused: bool = False):  # proj/src/deflation.cpp:94-96
+        torch = _torch()
+        v = self._vec(v, self.k)
+        y = torch.empty_like(v)
+        check(lib().smpm_apply_P(self.h, _dptr(v), _dptr(y), int(bool(fused)), self._stream()))
+        return y
+
+    def project_out(self, v, direction):  # proj/src/nullspace.cpp:92
+        torch = _torch()
+        v = self._vec(v, self.k)
+        dr = self._vec(direction, self.k)
+        y = torch.empty_like(v)
+        check(lib().smpm_project_out(self.h, C.c_longlong(self.k), _dptr(v), _dptr(dr), _dptr(y), self._stream()))
+        return y
+
+    # ---- solves -----------------------------------------------------------
+    @staticmethod
+    def options(tol=1e-10, max_iter=100, restart=0, orth="cgs2", fuse_deflation=True, final_residual_check=True):
+        o = SolveOptions()
+        o.tol = tol
+        o.max_iter = max_iter
+        o.restart = restart
+        o.orth = ORTH[orth]
+        o.fuse_deflation = int(bool(fuse_deflation))
+        o.final_residual_check = int(bool(final_residual_check))
+        return o
+
+    def _collect(self, x, reps, hist, cap):
+        its = [reps[i].iterations for i in range(self.nsys)]
+        hs = [hist[i, : reps[i].history_len].copy() for i in range(self.nsys)] if hist is not None else []
+        return SolveResult(
+            x, its, [bool(reps[i].converged) for i in range(self.nsys)],
+            [reps[i].final_rel_residual for i in range(self.nsys)],
+            [reps[i].operator_applies for i in range(self.nsys)],
+            [reps[i].krylov_s_applies for i in range(self.nsys)],
+            [bool(reps[i].mismatch_warning) for i in range(self.nsys)],
+            reps[0].wall_time_s if self.nsys else 0.0, hs)
+
+    def solve(self, b_S, method="dbj", tol=1e-10, max_iter=100, restart=0, orth="cgs2", fuse_deflation=True,
+              history=True):
+        torch = _torch()
+        b = self._vec(b_S, self.k)
+        x = torch.empty_like(b)
+        o = self.options(tol, max_iter, restart, orth, fuse_deflation)
+        reps = (Report * self.nsys)()
+        cap = min(max_iter, self.k) + 2
+        hist = np.zeros((self.nsys, cap)) if history else None
+        check(lib().smpm_solve(self.h, METHODS[method], _dptr(b), _dptr(x), C.byref(o), reps,
+                               _hptr(hist) if hist is not None else None, self._stream()))
+        return self._collect(x, reps, hist, cap)
+
+    def deflated_solve(self, b_S, tol=1e-10, max_iter=100, **kw):  # proj/src/deflation.cpp:102-122
+        return self.solve(b_S, "dbj", tol, max_iter, **kw)
+
+    def two_level_schwarz_solve(self, b_S, tol=1e-10, max_iter=100, **kw):  # proj/src/deflation.cpp:124-143
+        return self.solve(b_S, "2las", tol, max_iter, **kw)
+
+    def solve_host(self, b_S_host, method="dbj", tol=1e-10, max_iter=100, restart=0, orth="cgs2",
+                   fuse_deflation=True, out=None):
+        """End-to-end: host b_S in, host x_S out (copies inside the call)."""
+        b = np.ascontiguousarray(b_S_host, dtype=np.float64).reshape(self.nsys, self.k)
+        x = out if out is not None else np.empty_like(b)
+        o = self.options(tol, max_iter, restart, orth, fuse_deflation)
+        reps = (Report * self.nsys)()
+        check(lib().smpm_solve_host(self.h, METHODS[method], _hptr(b), _hptr(x), C.byref(o), reps, None))
+        return self._collect(x, reps, None, 0)
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().smpm_batch_launch_count(self.h))
