@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""Benchmark: deflated block-Jacobi Schur-GMRES solves/s (fp64) on B200.
+
+Workload (default C4, BASELINE.json configs[3]): the 3D Fourier-extended
+pressure solve, x-z plane [0,16]x[0,1], 64x16 elements, p=10 (n=11), 128
+Fourier modes; one deflated + block-Jacobi GMRES(100) Schur solve per mode
+(rtol 1e-10), seeded cosine-mode RHS.  A step = one pass of the hot path over
+one batch: every mode this rank owns, b_S -> x_S.  Modes are sharded
+round-robin across ranks (no collective inside the solve); timing is the
+device time of K steps, max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4]
+  python bench.py --impl reference ...   # the reference algorithm (CPU oracle port)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "deflated Schur-GMRES solves/s (fp64)"
+UNIT = "solves/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="C4")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--method", default="dbj")
+    p.add_argument("--orth", default="cgs2")
+    p.add_argument("--cpu-sample", type=int, default=16, help="modes in the CPU-baseline sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def solve_params(cfg):
+    # GMRES(m): restart length m = cfg.max_iter (50 / 100), total cap 10 cycles
+    return dict(tol=1e-10, restart=cfg.max_iter, max_iter=10 * cfg.max_iter)
+
+
+def sample_modes(cfg, count):
+    nm = max(cfg.modes, 1)
+    count = min(count, nm)
+    return sorted(set(int(round(i * nm / count)) % nm for i in range(count)))
+
+
+# ---------------------------------------------------------------------------
+# clocks: nvidia-smi sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        except OSError:
+            pass
+        if self.path and os.path.exists(self.path):
+            os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port of the reference algorithm)
+# ---------------------------------------------------------------------------
+def oracle_systems_from(ps, idx, threads):
+    """Oracle systems (reference per-interface layout, one LU per BJ block)
+    on the product's couplings, for the modes at positions idx of ps."""
+    from oracle import oracle as O
+
+    cfg = ps.cfg
+    O.set_threads(threads)
+    prob = O.Problem(cfg.n, cfg.m_x, cfg.m_z, cfg.l_x, cfg.l_z, cfg.c_tau)
+    systems = []
+    for i in idx:
+        s = O.System(prob, ps.mus[i], True, kinds=(ps.GW[i], ps.GI[i], ps.GE[i]))
+        s.build_bj(2)
+        s.build_coarse(ps.u_S if ps.mus[i] == 0.0 else None)
+        systems.append(s)
+    return prob, systems
+
+
+def oracle_own_setup(cfg, modes, threads):
+    """Independent oracle setup (LU / real-Schur couplings, inverse iteration,
+    seeded inputs) for the reference arm."""
+    from oracle import oracle as O
+
+    O.set_threads(threads)
+    prob = O.Problem(cfg.n, cfg.m_x, cfg.m_z, cfg.l_x, cfg.l_z, cfg.c_tau)
+    mus = cfg.mus()
+    systems, bs = [], []
+    u_S = u_L = None
+    for m in modes:
+        mu = mus[m]
+        s = O.System(prob, mu, True)
+        s.build_bj(2)
+        f, _ = prob.manufactured(cfg.kmax, cfg.decay, cfg.seed, m, mu=mu)
+        if mu == 0.0:
+            u_S, u_L, _, _ = s.nullspace()
+            s.build_coarse(u_S)
+            b = O.project_out(s.schur_rhs(O.project_out(f, u_L)), u_S)
+        else:
+            s.build_coarse(None)
+            b = prob.apply_B(prob.shifted_solve(mu, f))
+        systems.append(s)
+        bs.append(b)
+    return prob, systems, np.array(bs)
+
+
+def time_cpu(systems, b, threads, method, sp):
+    from oracle import oracle as O
+
+    t0 = time.perf_counter()
+    x, reps = O.solve_many(systems, b, method, sp["tol"], sp["max_iter"], sp["restart"], threads)
+    dt = time.perf_counter() - t0
+    return dt, [r.iterations for r in reps]
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    sp = solve_params(cfg)
+    modes = sample_modes(cfg, min(args.cpu_sample, 8) if cfg.modes else 1)
+    t0 = time.perf_counter()
+    _, systems, b = oracle_own_setup(cfg, modes, threads)
+    setup_s = time.perf_counter() - t0
+    th = min(threads, len(systems))
+    for _ in range(args.warmup):
+        time_cpu(systems, b, th, args.method, sp)
+    tot, its = 0.0, None
+    for _ in range(args.steps):
+        dt, its = time_cpu(systems, b, th, args.method, sp)
+        tot += dt
+    value = len(systems) * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "sample_modes": modes, "method": args.method, **sp},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": "port",
+                         "sample": f"{len(modes)} of {max(cfg.modes, 1)} {cfg.name} systems (modes {modes}); oracle "
+                                   f"port of the reference (per-interface block layout, LU block-Jacobi, Householder "
+                                   f"GMRES), one system per host thread; setup {setup_s:.1f}s untimed; "
+                                   f"{cpu_model()}",
+                         "iterations": its},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def algorithmic_counts(cfg):
+    """Per-system, per-application FLOPs and bytes."""
+    w, mx, k = cfg.w, cfg.m_x, cfg.k
+    d = mx - 1
+    F_S = 2 * ((2 * w) ** 2 * (mx - 2) + 2 * w * w) + k
+    B_S = 8 * ((2 * w) ** 2 + 2 * w * w + 2 * k)
+    nbf, single = d // 2, d % 2
+    # structured BJ: per two-interface block 2(2w)^2 [G'] + 2(2w)^2 [K^-1] + 2*2w^2 [Gee, Gww]
+    F_BJ = nbf * (2 * (2 * w) ** 2 * 2 + 4 * w * w) + single * (3 * 2 * w * w)
+    B_BJ = 8 * ((2 * w) ** 2 * 3 + 3 * w * w + 2 * k)
+    return dict(F_S=F_S, B_S=B_S, F_BJ=F_BJ, B_BJ=B_BJ, k=k)
+
+
+def run_ours(args, cfg):
+    import torch
+
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist_mod
+
+        dist = dist_mod
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_1512_01756_b200 import Context, lib
+    from paper_1512_01756_b200.problems import build_problem, load_batch
+
+    sp = solve_params(cfg)
+    nm = max(cfg.modes, 1)
+    modes = [m for m in range(nm) if m % ws == rank] if cfg.modes else [0]
+    if not cfg.modes and ws > 1:
+        modes = [0]  # 2D configs: replicas only
+    ps = build_problem(cfg, modes, device=f"cuda:{local}")
+    ctx = Context(local)
+    b = load_batch(ctx, ps)
+    bS = torch.tensor(ps.b_S, device=dev)
+    # measured fp64 peaks of this device
+    import ctypes as C
+
+    dfma, dmma = C.c_double(), C.c_double()
+    lib().smpm_fp64_peak(local, C.byref(dfma), C.byref(dmma))
+    peak_fp64 = max(dfma.value, dmma.value)
+
+    def step():
+        return b.solve(bS, args.method, sp["tol"], sp["max_iter"], sp["restart"], args.orth, True, history=False)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    # ---- timed region: inputs resident in HBM
+    launches0 = b.launch_count
+    b.profile(True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        its_tot = np.zeros(len(modes))
+        for _ in range(args.steps):
+            res = step()
+            its_tot += np.array(res.iterations)
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    prof = b.profile(False)
+    launches = b.launch_count - launches0
+    clocks = clk.summary()
+
+    # ---- end to end: host b_S (pinned) -> device -> solve -> host x_S
+    hb = torch.tensor(ps.b_S).pin_memory()
+    hx = torch.empty_like(hb).pin_memory()
+    hbn, hxn = hb.numpy(), hx.numpy()
+    b.solve_host(hbn, args.method, sp["tol"], sp["max_iter"], sp["restart"], args.orth, True, out=hxn)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        b.solve_host(hbn, args.method, sp["tol"], sp["max_iter"], sp["restart"], args.orth, True, out=hxn)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    barrier()
+
+    # ---- reduce timings over ranks (max)
+    t = torch.tensor([ms, e2e_s], device=dev, dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, e2e_max = float(t[0]), float(t[1])
+    total_units = (nm if cfg.modes else ws) * args.steps
+    value = total_units / (ms_max * 1e-3)
+    e2e_value = total_units / e2e_max
+
+    # gather per-mode iteration counts to rank 0 (NCCL) for the record
+    its_rank = torch.tensor(its_tot / args.steps, device=dev)
+    its_all = None
+    if dist:
+        gathered = [torch.zeros(len([m for m in range(nm) if m % ws == r]), device=dev, dtype=torch.float64)
+                    for r in range(ws)]
+        dist.all_gather(gathered, its_rank)
+        its_all = torch.cat(gathered).cpu().numpy()
+    else:
+        its_all = its_rank.cpu().numpy()
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel class (live CUDA-event timing)
+    cnt = algorithmic_counts(cfg)
+    its_local = its_tot  # summed over steps, this rank's systems
+    # S and BJ applications per system per solve: one per Arnoldi step, the
+    # final residual check and the x_S assembly (+ restart residuals)
+    applies = float((its_local + 2 * args.steps).sum())
+    classes = {}
+    peak_hbm = None
+    try:
+        peak_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        hbm_src = "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        peak_hbm, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    for name, (cms, n) in prof.items():
+        classes[name] = {"ms": cms, "launches": n, "share": cms / ms if ms else None}
+    s_ms = prof["schur_gemm"][0]
+    bj_ms = prof["bj_gemm"][0]
+    kern = {
+        "schur_gemm": {"flops": applies * cnt["F_S"], "bytes": applies * cnt["B_S"], "ms": s_ms},
+        "bj_gemm": {"flops": applies * cnt["F_BJ"], "bytes": applies * cnt["B_BJ"], "ms": bj_ms},
+    }
+    for kname, kv in kern.items():
+        if kv["ms"] > 0:
+            classes[kname]["achieved_tflops"] = kv["flops"] / (kv["ms"] * 1e-3) / 1e12
+            classes[kname]["achieved_gbs"] = kv["bytes"] / (kv["ms"] * 1e-3) / 1e9
+    dom = max(("schur_gemm", "bj_gemm"), key=lambda n: kern[n]["ms"])
+    kd = kern[dom]
+    nlaunch = max(prof[dom][1], 1)
+    achieved = kd["flops"] / (kd["ms"] * 1e-3) / 1e12 if kd["ms"] > 0 else None
+    roofline = {
+        "kernel": dom, "bound": "tensor", "pipe": "fp64 (FMA/DMMA; no tcgen05 f64 kind)",
+        "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
+        "frac": (achieved / peak_fp64) if achieved and peak_fp64 else None,
+        "peak_source": f"measured in-run fp64 microbenchmark (DFMA {dfma.value:.1f}, DMMA {dmma.value:.1f} TFLOP/s)",
+        "traffic": None,
+        "algorithmic_flops_per_launch": kd["flops"] / nlaunch,
+        "avg_launch_ms": kd["ms"] / nlaunch,
+        "hbm_peak_gbs": peak_hbm, "hbm_peak_source": hbm_src,
+    }
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong" if cfg.modes else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "grid": f"n={cfg.n} (p={cfg.n - 1}), {cfg.m_x}x{cfg.m_z} elements, "
+                                               f"[0,{cfg.l_x:g}]x[0,{cfg.l_z:g}]",
+                   "systems": nm if cfg.modes else 1, "k_per_system": cfg.k, "method": args.method,
+                   "orth": args.orth, "parallelism": f"modes sharded round-robin over {ws} GPU(s)",
+                   "l2": "inputs larger than L2 (operators + Krylov basis >> 126 MB per step)", **sp,
+                   "mean_iterations": float(np.mean(its_all)), "max_iterations": float(np.max(its_all))},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": roofline,
+        "kernels": classes,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(ps.b_S.nbytes),
+                "d2h_bytes_per_step": int(ps.b_S.nbytes)},
+    }
+
+    # ---- CPU baseline (rank 0, N = 1): oracle port on a bounded sample
+    if ws == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        idx = [modes.index(m) for m in sample_modes(cfg, args.cpu_sample) if m in modes] if cfg.modes else [0]
+        _, systems = oracle_systems_from(ps, idx, threads)
+        th = min(threads, len(systems))
+        dt, its = time_cpu(systems, ps.b_S[idx], th, args.method, sp)
+        line["cpu_baseline"] = {
+            "value": len(systems) / dt, "unit": UNIT, "cores": th, "kind": "port",
+            "sample": f"{len(systems)} of {nm} {cfg.name} systems (modes {[modes[i] for i in idx]}), oracle port of "
+                      f"the reference (per-interface blocks, LU block-Jacobi, Householder GMRES), one system per "
+                      f"thread, {dt:.1f}s; {cpu_model()}",
+        }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    from paper_1512_01756_b200.configs import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

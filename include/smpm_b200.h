@@ -161,6 +161,18 @@ int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x
  * (instrumentation for bench.py's gpu_launches). */
 long long smpm_batch_launch_count(const smpm_batch* b);
 
+/* Optional device timing of kernel classes (0 Schur GEMM, 1 block-Jacobi
+ * GEMMs, 2 deflation, 3 Arnoldi orthogonalization, 4 other), measured with
+ * CUDA events on the launching stream during solves/operators. Reads the
+ * accumulated milliseconds/launch counts (nullable), then, if enable >= 0,
+ * resets them and turns timing on (1) or off (0). */
+int smpm_batch_profile(smpm_batch* b, int enable, double* ms, long long* counts, int nclass);
+
+/* Measured fp64 throughput of the device (TFLOP/s): FP64 FMA pipe and the
+ * legacy fp64 tensor-core mma.sync (no tcgen05 f64 kind exists). Roofline
+ * denominator for the fp64 contractions. */
+int smpm_fp64_peak(int device, double* dfma_tflops, double* dmma_tflops);
+
 #ifdef __cplusplus
 }
 #endif

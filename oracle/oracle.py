@@ -161,10 +161,11 @@ class Problem:
         _chk(lib().orc_shifted_solve(C.c_void_p(self.h), C.c_double(mu), _p(b), _p(x)))
         return x
 
-    def manufactured(self, kmax, decay, seed=1234, stream=0, forcing_only=False):
+    def manufactured(self, kmax, decay, seed=1234, stream=0, forcing_only=False, mu=0.0):
+        """Seeded cosine field u and f = (Lap - mu) u (or f = u when forcing_only)."""
         f, u = np.zeros(self.r), np.zeros(self.r)
         _chk(lib().orc_manufactured(C.c_void_p(self.h), int(kmax), int(bool(decay)), C.c_ulonglong(seed),
-                                    C.c_ulonglong(stream), int(bool(forcing_only)), _p(f), _p(u)))
+                                    C.c_ulonglong(stream), int(bool(forcing_only)), C.c_double(mu), _p(f), _p(u)))
         return f, u
 
 

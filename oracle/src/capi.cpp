@@ -192,8 +192,10 @@ int orc_shifted_solve(void* vp, double mu, const double* b, double* x) {
 // (optionally / (1+k^2+l^2)), drawn k-major from Rng(seed).stream(stream).
 // forcing_only = 0: f = Lap(u) (g = 0 exactly, so the assembled rhs is f);
 // forcing_only = 1: f = the cosine series itself (per-mode Helmholtz forcing).
+// mu > 0 (with forcing_only = 0): f = (Lap - mu) u, the manufactured
+// per-mode Helmholtz right-hand side.
 int orc_manufactured(void* vp, int kmax, int decay, unsigned long long seed, unsigned long long stream,
-                     int forcing_only, double* f, double* u) {
+                     int forcing_only, double mu, double* f, double* u) {
   return guard([&] {
     const Operator& op = *static_cast<Problem*>(vp)->op;
     const Mesh& m = op.mesh;
@@ -216,7 +218,7 @@ int orc_manufactured(void* vp, int kmax, int decay, unsigned long long seed, uns
           const double ll = l * M_PI / m.l_z;
           const double mode = ck * std::cos(l * M_PI * z / m.l_z);
           us += c * mode;
-          fs += forcing_only ? c * mode : -c * (kk * kk + ll * ll) * mode;
+          fs += forcing_only ? c * mode : -c * (kk * kk + ll * ll + mu) * mode;
         }
       }
       f[g] = fs;
@@ -255,7 +257,7 @@ int orc_export_kinds(void* vs, double* GW, double* GI, double* GE) {
 }
 
 int orc_build_bj(void* vs, int dedup) {
-  return guard([&] { build_block_jacobi(static_cast<System*>(vs)->sys, dedup != 0); });
+  return guard([&] { build_block_jacobi(static_cast<System*>(vs)->sys, dedup); });
 }
 
 unsigned long long orc_applies(void* vs) { return static_cast<System*>(vs)->sys.applies->load(); }

@@ -320,7 +320,7 @@ Vec schur_rhs(const SchurSystem& sys, const Vec& f) {
 
 // proj/src/schur.cpp:188-216; identical blocks (same strip kinds and size)
 // share one factor when dedup is set — their LU factors are bitwise equal.
-void build_block_jacobi(SchurSystem& sys, bool dedup) {
+void build_block_jacobi(SchurSystem& sys, int dedup) {
   const Index w = sys.w, w2 = 2 * w;
   const Operator& op = *sys.op;
   sys.jacobi.clear();
@@ -335,7 +335,14 @@ void build_block_jacobi(SchurSystem& sys, bool dedup) {
     if (dedup) {
       auto it = seen.find(key);
       if (it != seen.end()) {
-        jb.factor = it->second;
+        if (dedup == 2) {
+          // bitwise copy of the identical factor in its own storage: the
+          // reference keeps one LU per block (memory traffic as the reference)
+          jb.factor = static_cast<int>(sys.jfactors.size());
+          sys.jfactors.push_back(sys.jfactors[it->second]);
+        } else {
+          jb.factor = it->second;
+        }
         sys.jacobi.push_back(jb);
         continue;
       }

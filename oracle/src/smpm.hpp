@@ -171,7 +171,7 @@ Vec apply_S(const SchurSystem& sys, const Vec& v);
 Vec apply_St(const SchurSystem& sys, const Vec& v);
 Vec apply_S_definition(const SchurSystem& sys, const Vec& v);
 Vec schur_rhs(const SchurSystem& sys, const Vec& f);
-void build_block_jacobi(SchurSystem& sys, bool dedup);
+void build_block_jacobi(SchurSystem& sys, int dedup);
 Vec apply_block_jacobi_inv(const SchurSystem& sys, const Vec& v);
 Vec recover_solution(const SchurSystem& sys, const Vec& f, const Vec& x_S);
 Mat dense_schur(const SchurSystem& sys);

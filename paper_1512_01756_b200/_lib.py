@@ -24,7 +24,9 @@ EXPORTS = [
     "smpm_batch_coarse_info", "smpm_apply_S", "smpm_apply_St", "smpm_apply_block_jacobi_inv", "smpm_apply_Z",
     "smpm_apply_Zt", "smpm_coarse_solve", "smpm_apply_P", "smpm_apply_Q", "smpm_project_out", "smpm_solve",
     "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_batch_launch_count",
+    "smpm_batch_profile", "smpm_fp64_peak",
 ]
+PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other"]
 
 
 class SmpmError(RuntimeError):
@@ -96,6 +98,8 @@ def lib():
     L.smpm_solve_host.argtypes = [vp, ip, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp]
     L.smpm_batch_launch_count.restype = llp
     L.smpm_batch_launch_count.argtypes = [vp]
+    L.smpm_batch_profile.argtypes = [vp, ip, C.POINTER(C.c_double), C.POINTER(C.c_longlong), ip]
+    L.smpm_fp64_peak.argtypes = [ip, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     _lib = L
     return L
 

@@ -8,7 +8,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libsmpm_b200.so")
-SOURCES = ["batch.cu"]
+SOURCES = ["batch.cu", "peak.cu"]
 HEADERS = ["common.cuh", "gemm.cuh", "vec.cuh"]
 
 NVCC_FLAGS = [

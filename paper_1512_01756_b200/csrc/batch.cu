@@ -203,6 +203,7 @@ struct smpm_batch {
   int* hcnt = nullptr;  // pinned, 4 ints (two in-flight step counters)
   ~smpm_batch() {
     if (hcnt) cudaFreeHost(hcnt);
+    for (auto e : ev_pool) cudaEventDestroy(e);
   }
   DevArray<double> dpart;
 
@@ -213,6 +214,18 @@ struct smpm_batch {
   GmState_ G{};
 
   long long launches = 0;
+
+  // optional per-class device timing (CUDA events on the launching stream)
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Span {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<Span> spans;
+  double prof_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
   cudaStream_t st(void* s) const { return s ? static_cast<cudaStream_t>(s) : ctx->stream; }
   double* GW(int s) const { return dmat.p + s * mstride + oGW; }
@@ -227,6 +240,51 @@ namespace {
 void check_launch(smpm_batch* b) {
   ++b->launches;
   CUDA_CHECK(cudaGetLastError());
+}
+
+// kernel classes for the optional timing
+enum ProfClass : int { PC_SCHUR = 0, PC_BJ = 1, PC_DEFL = 2, PC_ORTH = 3, PC_OTHER = 4 };
+
+cudaEvent_t prof_event(smpm_batch* b) {
+  if (b->ev_used == b->ev_pool.size()) {
+    cudaEvent_t e;
+    CUDA_CHECK(cudaEventCreate(&e));
+    b->ev_pool.push_back(e);
+  }
+  return b->ev_pool[b->ev_used++];
+}
+
+struct ProfScope {
+  smpm_batch* b;
+  int cls;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(smpm_batch* b_, int c, cudaStream_t s) : b(b_), cls(c), st(s) {
+    if (b->profiling) {
+      a = prof_event(b);
+      CUDA_CHECK(cudaEventRecord(a, st));
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t e = prof_event(b);
+      cudaEventRecord(e, st);
+      b->spans.push_back({cls, a, e});
+    }
+  }
+};
+
+// resolve recorded spans (call after the stream is synchronized)
+void prof_collect(smpm_batch* b) {
+  for (const auto& s : b->spans) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, s.a, s.b) == cudaSuccess) {
+      b->prof_ms[s.cls] += ms;
+      b->prof_n[s.cls] += 1;
+    }
+  }
+  b->spans.clear();
+  b->ev_used = 0;
 }
 
 void run_plan(smpm_batch* b, Plan& p, const double* in, double* out, double* tmp, const int* active,
@@ -264,6 +322,7 @@ DeflateParams deflate_params(smpm_batch* b, const int* active) {
 
 void run_deflate(smpm_batch* b, int mode, const double* zin, const double* v, double* y, double* cout,
                  const int* active, cudaStream_t st) {
+  ProfScope ps(b, PC_DEFL, st);
   const size_t shm = sizeof(double) * 2 * static_cast<size_t>(b->d);
   deflate_kernel<<<b->nsys, VEC_THREADS, shm, st>>>(deflate_params(b, active), mode, zin, v, y, cout);
   check_launch(b);
@@ -277,6 +336,7 @@ int grid_for(long long elems) {
 // Operators (device vectors nsys x k)
 // --------------------------------------------------------------------------
 void op_S(smpm_batch* b, const double* v, double* y, const int* act, cudaStream_t st) {
+  ProfScope ps(b, PC_SCHUR, st);
   run_plan(b, b->pS, v, y, nullptr, act, st);
 }
 void op_St(smpm_batch* b, const double* v, double* y, const int* act, cudaStream_t st) {
@@ -284,6 +344,7 @@ void op_St(smpm_batch* b, const double* v, double* y, const int* act, cudaStream
 }
 // structured block-Jacobi: three dependent GEMM stages
 void op_BJ(smpm_batch* b, const double* v, double* y, const int* act, cudaStream_t st) {
+  ProfScope ps(b, PC_BJ, st);
   double* tmp = b->vbuf[9].p;
   run_plan(b, b->pBJ1, v, y, tmp, act, st);
   run_plan(b, b->pBJ2, v, y, tmp, act, st);
@@ -790,6 +851,7 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, cudaStream_t st) {
   double* vin = b->vbuf[2].p;
   double* wv = b->vbuf[3].p;
   apply_op(b, c, vin, wv, G.active, st);
+  ProfScope ps(b, PC_ORTH, st);
   dim3 grid(G.nchunk, b->nsys);
   const size_t hsm = sizeof(double) * static_cast<size_t>(G.m + 2);
   if (c.orth == SMPM_ORTH_MGS) {
@@ -969,6 +1031,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   }
   CUDA_CHECK(cudaEventRecord(e1, st));
   CUDA_CHECK(cudaEventSynchronize(e1));
+  prof_collect(b);
   float ms = 0.f;
   CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
   CUDA_CHECK(cudaEventDestroy(e0));
@@ -1308,5 +1371,24 @@ int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x
 }
 
 long long smpm_batch_launch_count(const smpm_batch* b) { return b ? b->launches : 0; }
+
+int smpm_batch_profile(smpm_batch* b, int enable, double* ms, long long* counts, int nclass) {
+  return guard([&] {
+    if (!b) fail(SMPM_EINVAL, "null batch");
+    CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
+    prof_collect(b);
+    if (ms)
+      for (int i = 0; i < std::min(nclass, 8); ++i) ms[i] = b->prof_ms[i];
+    if (counts)
+      for (int i = 0; i < std::min(nclass, 8); ++i) counts[i] = b->prof_n[i];
+    if (enable >= 0) {
+      b->profiling = enable != 0;
+      for (int i = 0; i < 8; ++i) {
+        b->prof_ms[i] = 0.0;
+        b->prof_n[i] = 0;
+      }
+    }
+  });
+}
 
 }  // extern "C"

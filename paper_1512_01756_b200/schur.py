@@ -243,6 +243,17 @@ class SchurBatch:
         check(lib().smpm_solve_host(self.h, METHODS[method], _hptr(b), _hptr(x), C.byref(o), reps, None))
         return self._collect(x, reps, None, 0)
 
+    def profile(self, enable=None):
+        """Per-kernel-class device time (ms) and launch counts accumulated since
+        the last reset; enable=True/False resets and switches timing."""
+        from ._lib import PROFILE_CLASSES
+
+        ms = (C.c_double * 8)()
+        cnt = (C.c_longlong * 8)()
+        flag = -1 if enable is None else int(bool(enable))
+        check(lib().smpm_batch_profile(self.h, flag, ms, cnt, 8))
+        return {name: (ms[i], cnt[i]) for i, name in enumerate(PROFILE_CLASSES)}
+
     @property
     def launch_count(self) -> int:
         return int(lib().smpm_batch_launch_count(self.h))

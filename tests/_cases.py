@@ -25,13 +25,11 @@ def build_case(n, m_x, m_z, l_x, l_z, mus=(0.0,), kmax=4, decay=False, c_tau=2.0
     prob = O.Problem(n, m_x, m_z, l_x, l_z, c_tau)
     systems, bs, kinds = [], [], []
     u_S = u_L = None
-    if forcing_only is None:
-        forcing_only = len(mus) > 1 or mus[0] != 0.0
     streams = streams if streams is not None else list(range(len(mus)))
     for j, mu in enumerate(mus):
         s = O.System(prob, mu, layout_reference)
         s.build_bj()
-        f, _ = prob.manufactured(kmax, decay, seed, streams[j], forcing_only=forcing_only)
+        f, _ = prob.manufactured(kmax, decay, seed, streams[j], forcing_only=bool(forcing_only), mu=mu)
         if mu == 0.0:
             u_S, u_L, _, _ = s.nullspace(dense_limit)
             s.build_coarse(u_S)
