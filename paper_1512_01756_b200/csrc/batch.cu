@@ -19,7 +19,9 @@
 #include "../../include/smpm_b200.h"
 #include "common.cuh"
 #include "gemm.cuh"
+#include "gemm2.cuh"
 #include "vec.cuh"
+#include "vec2.cuh"
 
 using namespace smpm;
 
@@ -104,6 +106,61 @@ struct Plan {
   DevArray<SplitItem> ditems;
   int ntiles = 0, nitems = 0;
   long long ws_tiles = 0;
+  bool v2 = false;  // hot-path kernel (DMMA tiles + GEMV tiles)
+  DevArray<Tile2> dtiles2;
+
+  // v2 plan: N >= 2 jobs as 64x32 DMMA tiles (split-K when the plan has too
+  // few tiles for the GPU), N == 1 jobs as 32-row GEMV tiles
+  std::unique_ptr<Plan> tail;  // split-K variant for the few-systems tail (v2 only)
+
+  void build2(int num_sms, cudaStream_t st, int force_split = 0) {
+    long long tiles = 0;
+    for (const auto& j : jobs)
+      if (j.N >= 2) tiles += static_cast<long long>((j.M + G2_BM - 1) / G2_BM) * ((j.N + G2_BN - 1) / G2_BN);
+    int split = 1;
+    if (tiles > 0 && tiles < 2LL * num_sms) split = static_cast<int>((2LL * num_sms + tiles - 1) / tiles);
+    if (force_split > 0) split = std::max(split, force_split);
+    std::vector<Tile2> ht;
+    std::vector<SplitItem> hi;
+    ws_tiles = 0;
+    for (size_t ji = 0; ji < jobs.size(); ++ji) {
+      GemmJob& j = jobs[ji];
+      j.splitk = 1;
+      j.ws_off = 0;
+      if (j.N == 1) {
+        for (int m0 = 0; m0 < j.M; m0 += GV_ROWS) ht.push_back(Tile2{static_cast<int>(ji), m0, 0, -1});
+        continue;
+      }
+      const int mt = (j.M + G2_BM - 1) / G2_BM, nt = (j.N + G2_BN - 1) / G2_BN;
+      j.splitk = std::max(1, std::min(split, j.K / (4 * G2_BK)));
+      if (j.splitk > 1) {
+        j.ws_off = static_cast<int>(ws_tiles);
+        ws_tiles += static_cast<long long>(mt) * nt * j.splitk;
+      }
+      for (int a = 0; a < mt; ++a)
+        for (int b = 0; b < nt; ++b) {
+          for (int ks = 0; ks < j.splitk; ++ks) ht.push_back(Tile2{static_cast<int>(ji), a * G2_BM, b * G2_BN, ks});
+          if (j.splitk > 1) hi.push_back(SplitItem{static_cast<int>(ji), a * G2_BM, b * G2_BN});
+        }
+    }
+    // GEMM tiles first (long), GEMV tiles last
+    std::stable_sort(ht.begin(), ht.end(), [](const Tile2& x, const Tile2& y) { return (x.ks < 0) < (y.ks < 0); });
+    ntiles = static_cast<int>(ht.size());
+    nitems = static_cast<int>(hi.size());
+    v2 = true;
+    djobs.upload(jobs, st);
+    dtiles2.upload(ht, st);
+    ditems.upload(hi, st);
+  }
+
+  // the v2 kernel needs 16-byte aligned operands and unsplit B views
+  bool v2_ok() const {
+    for (const auto& j : jobs) {
+      if ((reinterpret_cast<uintptr_t>(j.A) & 15) || (j.lda & 1) || j.transA) return false;
+      if (j.b.split != INT_MAX || (j.b.off & 1) || (j.b.cs & 1)) return false;
+    }
+    return true;
+  }
 
   void add(const double* A, long long lda, bool transA, int M, int N, int K, int sys, View b, View out, View addv,
            double alpha, double beta) {
@@ -199,7 +256,9 @@ struct smpm_batch {
   // vectors (nsys x k each)
   DevArray<double> vbuf[12];
   DevArray<double> dsmall;  // nsys x (d + misc) scalars
+  DevArray<double> dcoarse;  // Z^T sums and coarse solutions, 2 x nsys x d
   DevArray<int> dones, dcount, dsel, dcnt;
+  DevArray<int> dalist;  // two compacted live lists + counts: [alist, acount, alist2, acount2]
   int* hcnt = nullptr;  // pinned, 4 ints (two in-flight step counters)
   ~smpm_batch() {
     if (hcnt) cudaFreeHost(hcnt);
@@ -287,18 +346,54 @@ void prof_collect(smpm_batch* b) {
   b->ev_used = 0;
 }
 
-void run_plan(smpm_batch* b, Plan& p, const double* in, double* out, double* tmp, const int* active,
-              cudaStream_t st) {
-  if (p.ntiles == 0) return;
+// The systems an operator application runs on: a device-compacted list of
+// live systems (alist/acount, grids sized by an upper bound nslots), or all
+// systems (alist == nullptr).  `active` is the matching per-system mask for
+// the kernels that take masks.
+struct Live {
+  const int* alist = nullptr;
+  const int* acount = nullptr;
+  int nslots = 0;
+  const int* active = nullptr;
+};
+Live all_systems(const smpm_batch* b) {
+  Live l;
+  l.nslots = b->nsys;
+  return l;
+}
+
+constexpr int kTailSystems = 8;
+
+void run_plan(smpm_batch* b, Plan& p0, const double* in, double* out, double* tmp, const Live& lv, cudaStream_t st) {
+  Plan& p = (p0.v2 && p0.tail && lv.nslots <= kTailSystems && lv.alist) ? *p0.tail : p0;
+  if (p.ntiles == 0 || lv.nslots == 0) return;
   BufTable t;
   t.p[BUF_IN] = const_cast<double*>(in);
   t.p[BUF_OUT] = out;
   t.p[BUF_TMP] = tmp;
   t.p[BUF_TMP2] = nullptr;
-  gemm_jobs_kernel<<<p.ntiles, 128, 0, st>>>(p.djobs.p, p.dtiles.p, t, active, b->dws.p);
+  if (p.v2) {
+    // per-system templates: launch only the tiles of the (bounded) live systems
+    SysMap sm;
+    sm.alist = lv.alist;
+    sm.acount = lv.acount;
+    sm.tiles_per_sys = p.ntiles;
+    sm.a_stride = b->mstride;
+    sm.v_stride = b->k;
+    sm.ws_stride = p.ws_tiles;
+    gemm2_kernel<<<p.ntiles * lv.nslots, G2_THREADS, G2_SMEM, st>>>(p.djobs.p, p.dtiles2.p, t, sm, b->dws.p);
+    check_launch(b);
+    if (p.nitems > 0) {
+      gemm2_splitk_reduce_kernel<<<p.nitems * lv.nslots * G2_RED_PARTS, 256, 0, st>>>(p.djobs.p, p.ditems.p, p.nitems, t, sm,
+                                                                       b->dws.p);
+      check_launch(b);
+    }
+    return;
+  }
+  gemm_jobs_kernel<<<p.ntiles, 128, 0, st>>>(p.djobs.p, p.dtiles.p, t, lv.active, b->dws.p);
   check_launch(b);
   if (p.nitems > 0) {
-    gemm_splitk_reduce_kernel<<<p.nitems, 256, 0, st>>>(p.djobs.p, p.ditems.p, t, active, b->dws.p);
+    gemm_splitk_reduce_kernel<<<p.nitems, 256, 0, st>>>(p.djobs.p, p.ditems.p, t, lv.active, b->dws.p);
     check_launch(b);
   }
 }
@@ -317,14 +412,36 @@ DeflateParams deflate_params(smpm_batch* b, const int* active) {
   P.thomas = b->dthomas.p;
   P.rowsum = b->drowsum.p;
   P.mx = b->mx;
+  P.alist = nullptr;
+  P.acount = nullptr;
   return P;
 }
 
 void run_deflate(smpm_batch* b, int mode, const double* zin, const double* v, double* y, double* cout,
-                 const int* active, cudaStream_t st) {
+                 const Live& lv, cudaStream_t st) {
   ProfScope ps(b, PC_DEFL, st);
+  if (lv.nslots == 0) return;
+  DeflateParams P = deflate_params(b, lv.active);
+  P.alist = lv.alist;
+  P.acount = lv.acount;
   const size_t shm = sizeof(double) * 2 * static_cast<size_t>(b->d);
-  deflate_kernel<<<b->nsys, VEC_THREADS, shm, st>>>(deflate_params(b, active), mode, zin, v, y, cout);
+  const int d = b->d, ns = lv.nslots;
+  double* sums = b->dcoarse.p;
+  double* cbuf = b->dcoarse.p + static_cast<size_t>(ns) * d;
+  if (mode == DEFL_COARSE_DIRECT) {
+    zt_coarse_kernel<<<dim3(1, ns), V2_THREADS, shm, st>>>(P, zin, sums, cout, b->dcount.p, 1);
+    check_launch(b);
+    return;
+  }
+  if (mode != DEFL_SUB_T) {
+    // Z^T + coarse solve: warp per interface, last CTA of each system solves
+    zt_coarse_kernel<<<dim3((d + DZ_IFACES - 1) / DZ_IFACES, ns), V2_THREADS, shm, st>>>(
+        P, zin, sums, mode == DEFL_COARSE ? cout : cbuf, b->dcount.p, 0);
+    check_launch(b);
+    if (mode == DEFL_COARSE) return;
+  }
+  const int gx = static_cast<int>(std::min<long long>((b->k + V2_THREADS * 4 - 1) / (V2_THREADS * 4), 256));
+  defl_update_kernel<<<dim3(gx, ns), V2_THREADS, 0, st>>>(P, mode, cbuf, zin, v, y);
   check_launch(b);
 }
 
@@ -335,41 +452,41 @@ int grid_for(long long elems) {
 // --------------------------------------------------------------------------
 // Operators (device vectors nsys x k)
 // --------------------------------------------------------------------------
-void op_S(smpm_batch* b, const double* v, double* y, const int* act, cudaStream_t st) {
+void op_S(smpm_batch* b, const double* v, double* y, const Live& lv, cudaStream_t st) {
   ProfScope ps(b, PC_SCHUR, st);
-  run_plan(b, b->pS, v, y, nullptr, act, st);
+  run_plan(b, b->pS, v, y, nullptr, lv, st);
 }
-void op_St(smpm_batch* b, const double* v, double* y, const int* act, cudaStream_t st) {
-  run_plan(b, b->pSt, v, y, nullptr, act, st);
+void op_St(smpm_batch* b, const double* v, double* y, const Live& lv, cudaStream_t st) {
+  run_plan(b, b->pSt, v, y, nullptr, lv, st);
 }
 // structured block-Jacobi: three dependent GEMM stages
-void op_BJ(smpm_batch* b, const double* v, double* y, const int* act, cudaStream_t st) {
+void op_BJ(smpm_batch* b, const double* v, double* y, const Live& lv, cudaStream_t st) {
   ProfScope ps(b, PC_BJ, st);
   double* tmp = b->vbuf[9].p;
-  run_plan(b, b->pBJ1, v, y, tmp, act, st);
-  run_plan(b, b->pBJ2, v, y, tmp, act, st);
-  run_plan(b, b->pBJ3, v, y, tmp, act, st);
+  run_plan(b, b->pBJ1, v, y, tmp, lv, st);
+  run_plan(b, b->pBJ2, v, y, tmp, lv, st);
+  run_plan(b, b->pBJ3, v, y, tmp, lv, st);
 }
 // P v = v - S Z c(Z^T v)
-void op_P(smpm_batch* b, const double* v, double* y, bool fused, const int* act, cudaStream_t st) {
+void op_P(smpm_batch* b, const double* v, double* y, bool fused, const Live& lv, cudaStream_t st) {
   if (fused) {
-    run_deflate(b, DEFL_P_FUSED, v, v, y, nullptr, act, st);
+    run_deflate(b, DEFL_P_FUSED, v, v, y, nullptr, lv, st);
     return;
   }
   double* c = b->dsmall.p;
   double* z = b->vbuf[7].p;
   double* sz = b->vbuf[8].p;
-  run_deflate(b, DEFL_COARSE, v, nullptr, nullptr, c, act, st);
-  zbroadcast_kernel<<<grid_for(b->nsys * b->k), 256, 0, st>>>(b->nsys, b->d, 2 * b->w, b->k, act, c, z);
+  run_deflate(b, DEFL_COARSE, v, nullptr, nullptr, c, lv, st);
+  zbroadcast_kernel<<<grid_for(b->nsys * b->k), 256, 0, st>>>(b->nsys, b->d, 2 * b->w, b->k, lv.active, c, z);
   check_launch(b);
-  op_S(b, z, sz, act, st);
-  run_deflate(b, DEFL_SUB_T, sz, v, y, nullptr, act, st);
+  op_S(b, z, sz, lv, st);
+  run_deflate(b, DEFL_SUB_T, sz, v, y, nullptr, lv, st);
 }
 // Q v = v - Z c(Z^T S v)
-void op_Q(smpm_batch* b, const double* v, double* y, const int* act, cudaStream_t st) {
+void op_Q(smpm_batch* b, const double* v, double* y, const Live& lv, cudaStream_t st) {
   double* t = b->vbuf[8].p;
-  op_S(b, v, t, act, st);
-  run_deflate(b, DEFL_Q_TAIL, t, v, y, nullptr, act, st);
+  op_S(b, v, t, lv, st);
+  run_deflate(b, DEFL_Q_TAIL, t, v, y, nullptr, lv, st);
 }
 
 // --------------------------------------------------------------------------
@@ -448,12 +565,34 @@ void build_plans(smpm_batch* b) {
     }
   }
   const int sms = b->ctx->num_sms;
-  b->pS.build(sms, st);
+  for (Plan* p : {&b->pS, &b->pBJ1, &b->pBJ2, &b->pBJ3}) {
+    if (!p->v2_ok()) {
+      // odd w (16-byte alignment impossible): per-system jobs on the v1 kernel
+      p->build(sms, st);
+      continue;
+    }
+    // every system's jobs are system 0's shifted by s*mstride (matrices) and
+    // s*k (vectors): keep system 0's as the per-system template
+    std::vector<GemmJob> tmpl;
+    for (const auto& j : p->jobs)
+      if (j.sys == 0) tmpl.push_back(j);
+    p->jobs.swap(tmpl);
+    // tail variant: K split 4 ways so a handful of live systems still
+    // spreads over many SMs (used when <= kTailSystems systems are live)
+    p->tail = std::make_unique<Plan>();
+    p->tail->jobs = p->jobs;
+    p->tail->build2(std::max(1, sms / b->nsys), st, 4);
+    // split-K only when even the whole batch cannot fill the GPU
+    p->build2(std::max(1, sms / b->nsys), st);
+  }
   b->pSt.build(sms, st);
-  b->pBJ1.build(sms, st);
-  b->pBJ2.build(sms, st);
-  b->pBJ3.build(sms, st);
-  long long wst = std::max({b->pS.ws_tiles, b->pSt.ws_tiles, b->pBJ1.ws_tiles, b->pBJ2.ws_tiles, b->pBJ3.ws_tiles});
+  // v2 templates hold per-system workspace counts; v1 plans hold totals
+  const long long ns = b->nsys;
+  long long wst = b->pSt.ws_tiles;
+  for (Plan* p : {&b->pS, &b->pBJ1, &b->pBJ2, &b->pBJ3}) {
+    wst = std::max(wst, p->ws_tiles * (p->v2 ? ns : 1));
+    if (p->tail) wst = std::max(wst, p->tail->ws_tiles * ns);
+  }
   b->dws.alloc(static_cast<size_t>(std::max(1LL, wst)) * GEMM_BM * GEMM_BN);
 }
 
@@ -661,8 +800,10 @@ void build_coarse(smpm_batch* b) {
         cp[i - 1] = Cat(i - 1, i) / piv[i - 1];
         piv[i] = Cat(i, i) - sub[i - 1] * cp[i - 1];
       }
-      for (int i = 0; i < d; ++i)
+      for (int i = 0; i < d; ++i) {
         if (piv[i] == 0.0) fail(SMPM_ESINGULAR, "coarse matrix is singular");
+        piv[i] = 1.0 / piv[i];  // the device multiplies by reciprocal pivots
+      }
       cmode[s] = 1;
     }
   }
@@ -709,11 +850,13 @@ void finalize(smpm_batch* b) {
   build_coarse(b);
   for (auto& v : b->vbuf) v.alloc(static_cast<size_t>(b->nsys) * b->k);
   b->dsmall.alloc(static_cast<size_t>(b->nsys) * (d + 8));
+  b->dcoarse.alloc(static_cast<size_t>(b->nsys) * 2 * d);
   std::vector<int> ones(static_cast<size_t>(b->nsys), 1);
   b->dones.upload(ones, st);
   b->dcount.alloc(static_cast<size_t>(b->nsys) + 1);
   CUDA_CHECK(cudaMemsetAsync(b->dcount.p, 0, sizeof(int) * (b->nsys + 1), st));
   b->dsel.alloc(static_cast<size_t>(b->nsys));
+  b->dalist.alloc(2 * static_cast<size_t>(b->nsys) + 2);
   b->dcnt.alloc(4);
   CUDA_CHECK(cudaMallocHost(&b->hcnt, 4 * sizeof(int)));
   CUDA_CHECK(cudaStreamSynchronize(st));
@@ -756,7 +899,9 @@ void batched_dot(smpm_batch* b, const double* x, const double* y, double* out, c
 // --------------------------------------------------------------------------
 void ensure_gmres(smpm_batch* b, int m, int mtot) {
   const int histcap = mtot + 2;
-  const Chunking c = chunking(b);
+  Chunking c;
+  c.chunk = V2_CHUNK;
+  c.nchunk = static_cast<int>((b->k + V2_CHUNK - 1) / V2_CHUNK);
   if (b->gm_m != m || b->gm_hist != histcap || b->G.nchunk != c.nchunk) {
     const size_t ns = static_cast<size_t>(b->nsys);
     b->dV.alloc(ns * (m + 1) * b->k);
@@ -768,7 +913,7 @@ void ensure_gmres(smpm_batch* b, int m, int mtot) {
     b->dh2.alloc(ns * (m + 2));
     b->dy.alloc(ns * m);
     b->dhist.alloc(ns * histcap);
-    b->dgpart.alloc(ns * c.nchunk * (m + 2));
+    b->dgpart.alloc(ns * ((b->k + 127) / 128) * (m + 2));  // adaptive chunks down to 128 rows
     b->dscal.alloc(ns * 8);
     b->dgint.alloc(ns * 8);
     b->gm_m = m;
@@ -802,9 +947,11 @@ void ensure_gmres(smpm_batch* b, int m, int mtot) {
   G.histcap = histcap;
   G.k = b->k;
   G.vstride = static_cast<long long>(m + 1) * b->k;
-  G.chunk = c.chunk;
-  G.nchunk = c.nchunk;
+  // Arnoldi passes: fixed 512-row chunks (thread-per-row kernels, vec2.cuh)
+  G.chunk = V2_CHUNK;
+  G.nchunk = static_cast<int>((b->k + V2_CHUNK - 1) / V2_CHUNK);
   G.nsys = ns;
+  (void)c;
   b->gm_mtot = mtot;
   CUDA_CHECK(cudaMemsetAsync(b->dgint.p, 0, sizeof(int) * ns * 8, b->ctx->stream));
   CUDA_CHECK(cudaMemsetAsync(b->dR.p, 0, sizeof(double) * b->dR.n, b->ctx->stream));
@@ -819,7 +966,7 @@ struct SolveCfg {
 
 // the preconditioned operator GMRES iterates on (proj/src/deflation.cpp:105-107,131; proj/src/gmres.cpp:144-150)
 // returns the number of S applications it made per system
-int apply_op(smpm_batch* b, const SolveCfg& c, const double* vin, double* wout, const int* act, cudaStream_t st) {
+int apply_op(smpm_batch* b, const SolveCfg& c, const double* vin, double* wout, const Live& act, cudaStream_t st) {
   double* u = b->vbuf[4].p;
   double* t = b->vbuf[5].p;
   switch (c.method) {
@@ -845,14 +992,15 @@ int apply_op(smpm_batch* b, const SolveCfg& c, const double* vin, double* wout, 
   fail(SMPM_EINVAL, "unknown method");
 }
 
-void arnoldi_step(smpm_batch* b, const SolveCfg& c, cudaStream_t st) {
+void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t st) {
   GmState_& G = b->G;
   double* V = b->dV.p;
   double* vin = b->vbuf[2].p;
   double* wv = b->vbuf[3].p;
-  apply_op(b, c, vin, wv, G.active, st);
+  apply_op(b, c, vin, wv, lv, st);
   ProfScope ps(b, PC_ORTH, st);
-  dim3 grid(G.nchunk, b->nsys);
+  dim3 grid(G.nchunk, b->nsys);      // system-indexed kernels (MGS, long cycles)
+  dim3 sgrid(G.nchunk, lv.nslots);   // live-slot kernels
   const size_t hsm = sizeof(double) * static_cast<size_t>(G.m + 2);
   if (c.orth == SMPM_ORTH_MGS) {
     for (int i = 0; i <= std::min(G.m, G.m_total); ++i) {
@@ -861,36 +1009,79 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, cudaStream_t st) {
     }
     gm_zero_h2_kernel<<<b->nsys, 128, 0, st>>>(G);
     check_launch(b);
-    cgs_update_kernel<true><<<grid, VEC_THREADS, hsm, st>>>(G, V, wv, 0);  // norm + Givens only
+    cgs2_update_kernel<true><<<grid, V2_THREADS, 0, st>>>(G, V, wv, 0);  // norm + Givens only
     check_launch(b);
-  } else {
+  } else if (G.m + 2 > V2_MAXCOL) {
+    // long cycles: column-count-agnostic kernels (dynamic shared memory)
     cgs_dot_kernel<<<grid, VEC_THREADS, 0, st>>>(G, V, wv);
     check_launch(b);
     cgs_update_kernel<false><<<grid, VEC_THREADS, hsm, st>>>(G, V, wv, 1);
     check_launch(b);
     cgs_update_kernel<true><<<grid, VEC_THREADS, hsm, st>>>(G, V, wv, 1);
     check_launch(b);
+  } else {
+    // chunk size adapted to the live systems so even one system spreads over
+    // ~4 CTAs per SM (the partial-sum buffer is sized for 128-row chunks)
+    GmState_ Gl = G;
+    const long long target = 4LL * b->ctx->num_sms;
+    int chunk = V2_CHUNK;
+    while (chunk > 128 && static_cast<long long>(lv.nslots) * ((b->k + chunk - 1) / chunk) < target) chunk /= 2;
+    Gl.chunk = chunk;
+    Gl.nchunk = static_cast<int>((b->k + chunk - 1) / chunk);
+    dim3 cgrid(Gl.nchunk, lv.nslots);
+    cgs2_dot_kernel<<<cgrid, V2_THREADS, 0, st>>>(Gl, V, wv);
+    check_launch(b);
+    cgs2_update_kernel<false><<<cgrid, V2_THREADS, 0, st>>>(Gl, V, wv, 1);
+    check_launch(b);
+    cgs2_update_kernel<true><<<cgrid, V2_THREADS, 0, st>>>(Gl, V, wv, 1);
+    check_launch(b);
   }
-  dim3 sg(std::max(1, std::min(G.nchunk, 64)), b->nsys);
+  (void)hsm;
+  dim3 sg(std::max(1, std::min(G.nchunk, 64)), lv.nslots);
   gm_scale_kernel<<<sg, 256, 0, st>>>(G, V, wv, vin);
   check_launch(b);
 }
 
-__global__ void count_states_kernel(const int* state, int nsys, int* out) {
-  __shared__ int run, cyc;
+// Compacted list of live systems (ascending index, so deterministic) from a
+// flag array, plus RUN / CYCLE state counts for the host; single CTA.
+__global__ void __launch_bounds__(1024) compact_kernel(const int* flags, const int* state, int nsys, int* alist,
+                                                       int* acount, int* counts) {
+  __shared__ int wsum[32];
+  __shared__ int base, run, cyc;
   if (threadIdx.x == 0) {
+    base = 0;
     run = 0;
     cyc = 0;
   }
   __syncthreads();
-  for (int s = threadIdx.x; s < nsys; s += blockDim.x) {
-    if (state[s] == GM_RUN) atomicAdd(&run, 1);
-    if (state[s] == GM_CYCLE) atomicAdd(&cyc, 1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int s0 = 0; s0 < nsys; s0 += blockDim.x) {
+    const int s = s0 + threadIdx.x;
+    const int f = (s < nsys && flags[s]) ? 1 : 0;
+    if (s < nsys && state) {
+      if (state[s] == GM_RUN) atomicAdd(&run, 1);
+      if (state[s] == GM_CYCLE) atomicAdd(&cyc, 1);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int off = base;
+    for (int q = 0; q < warp; ++q) off += wsum[q];
+    if (f) alist[off + __popc(bal & ((1u << lane) - 1u))] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int q = 0; q < nw; ++q) t += wsum[q];
+      base += t;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   if (threadIdx.x == 0) {
-    out[0] = run;
-    out[1] = cyc;
+    *acount = base;
+    if (counts) {
+      counts[0] = run;
+      counts[1] = cyc;
+    }
   }
 }
 
@@ -928,9 +1119,15 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   const long long launches0 = b->launches;
   long long s_applies = 0, op_applies = 0;
 
+  const Live all = all_systems(b);
+  int* alist = b->dalist.p;
+  int* acount = b->dalist.p + ns;
+  int* alist2 = b->dalist.p + ns + 1;
+  int* acount2 = alist2 + ns;
+
   // ---- right-hand side
   if (c.method == SMPM_DBJ) {
-    op_P(b, bS, rhs, c.fused, nullptr, st);  // pb = P b_S (proj/src/deflation.cpp:110)
+    op_P(b, bS, rhs, c.fused, all, st);  // pb = P b_S (proj/src/deflation.cpp:110)
   } else {
     CUDA_CHECK(cudaMemcpyAsync(rhs, bS, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
   }
@@ -942,16 +1139,27 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   dim3 vg(std::max(1, std::min(G.nchunk, 64)), ns);
   gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, rhs, vin);
   check_launch(b);
+  compact_kernel<<<1, 1024, 0, st>>>(G.active, nullptr, ns, alist, acount, nullptr);
+  check_launch(b);
+  G.alist = alist;
+  G.acount = acount;
 
   // ---- Arnoldi steps; device flags are polled one step behind the launches
-  // (step i+1 is queued before the host waits on step i's counters; a step
-  // issued after every system finished is a masked no-op)
+  // (step i+1 is queued before the host waits on step i's counters). Grids
+  // are sized by `bound`, the live count the host last read: systems only
+  // stop inside a cycle, so it bounds the device-compacted live list.
   int steps = 0;
+  int bound = ns;
   const int per_sys_applies = c.method == SMPM_DBJ && !c.fused ? 2 : 1;
   auto issue = [&](int slot) {
-    arnoldi_step(b, c, st);
+    Live lv;
+    lv.alist = alist;
+    lv.acount = acount;
+    lv.nslots = bound;
+    lv.active = G.active;
+    arnoldi_step(b, c, lv, st);
     ++steps;
-    count_states_kernel<<<1, 256, 0, st>>>(G.state, ns, b->dcnt.p + 2 * slot);
+    compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->dcnt.p + 2 * slot);
     check_launch(b);
     CUDA_CHECK(cudaMemcpyAsync(hcnt + 2 * slot, b->dcnt.p + 2 * slot, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaEventRecord(ev[slot], st));
@@ -963,12 +1171,14 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     if (more) issue(cur ^ 1);
     CUDA_CHECK(cudaEventSynchronize(ev[cur]));
     const int nrun = hcnt[2 * cur], ncyc = hcnt[2 * cur + 1];
+    bound = std::min(bound, nrun);
     cur ^= 1;
     if (nrun > 0 && more) continue;
     if (more) CUDA_CHECK(cudaEventSynchronize(ev[cur]));  // drain the speculative step
     const int nrun2 = more ? hcnt[2 * cur] : nrun;
     const int ncyc2 = more ? hcnt[2 * cur + 1] : ncyc;
     if (nrun2 > 0 && steps < mtot + 1) {
+      bound = std::min(bound, nrun2);
       issue(cur);
       continue;
     }
@@ -976,11 +1186,18 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       // ---- restart (GMRES(m) extension): x += V y ; r = b - op(x) ; new cycle
       select_state_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, GM_CYCLE, dsel);
       check_launch(b);
+      compact_kernel<<<1, 1024, 0, st>>>(dsel, nullptr, ns, alist2, acount2, nullptr);
+      check_launch(b);
+      Live lr;
+      lr.alist = alist2;
+      lr.acount = acount2;
+      lr.nslots = ncyc2;
+      lr.active = dsel;
       gm_backsolve_kernel<<<ns, 32, 0, st>>>(G, dsel);
       check_launch(b);
       gm_combine_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, x, dsel, 1);
       check_launch(b);
-      apply_op(b, c, x, r, dsel, st);
+      apply_op(b, c, x, r, lr, st);
       ++op_applies;
       axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, dsel, nullptr, 1.0, rhs, -1.0, r);
       check_launch(b);
@@ -989,6 +1206,9 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       check_launch(b);
       gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, r, vin);
       check_launch(b);
+      compact_kernel<<<1, 1024, 0, st>>>(G.active, nullptr, ns, alist, acount, nullptr);
+      check_launch(b);
+      bound = ncyc2;
       issue(cur);
       continue;
     }
@@ -1003,7 +1223,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   // ---- final residual check (proj/src/gmres.cpp:129-136): r = rhs - op(x')
   double* nrf = sc + 2 * ns;
   if (c.final_check) {
-    apply_op(b, c, x, r, nullptr, st);
+    apply_op(b, c, x, r, all, st);
     axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, nullptr, nullptr, 1.0, rhs, -1.0, r);
     check_launch(b);
     batched_dot(b, r, r, nrf, nullptr, st);
@@ -1015,18 +1235,18 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       CUDA_CHECK(cudaMemcpyAsync(xS, x, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
       break;
     case SMPM_BJ:
-      op_BJ(b, x, xS, nullptr, st);
+      op_BJ(b, x, xS, all, st);
       break;
     case SMPM_DBJ: {
       double* q = b->vbuf[6].p;
-      op_BJ(b, x, u, nullptr, st);
-      op_Q(b, u, q, nullptr, st);
-      run_deflate(b, DEFL_ADD_ZC, bS, q, xS, nullptr, nullptr, st);
+      op_BJ(b, x, u, all, st);
+      op_Q(b, u, q, all, st);
+      run_deflate(b, DEFL_ADD_ZC, bS, q, xS, nullptr, all, st);
       break;
     }
     case SMPM_2LAS:
-      op_BJ(b, x, u, nullptr, st);
-      run_deflate(b, DEFL_ADD_ZC, x, u, xS, nullptr, nullptr, st);
+      op_BJ(b, x, u, all, st);
+      run_deflate(b, DEFL_ADD_ZC, x, u, xS, nullptr, all, st);
       break;
   }
   CUDA_CHECK(cudaEventRecord(e1, st));
@@ -1038,6 +1258,8 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   CUDA_CHECK(cudaEventDestroy(e1));
   CUDA_CHECK(cudaEventDestroy(ev[0]));
   CUDA_CHECK(cudaEventDestroy(ev[1]));
+  G.alist = nullptr;
+  G.acount = nullptr;
   (void)launches0;
 
   // ---- reports
@@ -1138,6 +1360,7 @@ int smpm_ctx_create(int device, smpm_ctx** out) {
     CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault));
     CUSOLVER_CHECK(cusolverDnCreate(&ctx->solver));
     CUSOLVER_CHECK(cusolverDnSetStream(ctx->solver, ctx->stream));
+    CUDA_CHECK(cudaFuncSetAttribute(gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM));
     *out = ctx.release();
   });
 }
@@ -1308,19 +1531,19 @@ int smpm_batch_coarse_info(smpm_batch* b, double* C, int* tridiagonal, int* sing
       body;                                                                          \
     });                                                                              \
   }
-OP_ENTRY(smpm_apply_S, op_S(b, v, y, nullptr, st))
-OP_ENTRY(smpm_apply_St, op_St(b, v, y, nullptr, st))
-OP_ENTRY(smpm_apply_block_jacobi_inv, op_BJ(b, v, y, nullptr, st))
-OP_ENTRY(smpm_apply_Q, op_Q(b, v, y, nullptr, st))
+OP_ENTRY(smpm_apply_S, op_S(b, v, y, all_systems(b), st))
+OP_ENTRY(smpm_apply_St, op_St(b, v, y, all_systems(b), st))
+OP_ENTRY(smpm_apply_block_jacobi_inv, op_BJ(b, v, y, all_systems(b), st))
+OP_ENTRY(smpm_apply_Q, op_Q(b, v, y, all_systems(b), st))
 OP_ENTRY(smpm_apply_Zt, launch_zt(b, v, y, st))
 OP_ENTRY(smpm_apply_Z, launch_z(b, v, y, st))
-OP_ENTRY(smpm_coarse_solve, run_deflate(b, DEFL_COARSE_DIRECT, v, nullptr, nullptr, y, nullptr, st))
+OP_ENTRY(smpm_coarse_solve, run_deflate(b, DEFL_COARSE_DIRECT, v, nullptr, nullptr, y, all_systems(b), st))
 #undef OP_ENTRY
 
 int smpm_apply_P(smpm_batch* b, const double* v, double* y, int fused, void* stream) {
   return guard([&] {
     need_final(b);
-    op_P(b, v, y, fused != 0, nullptr, b->st(stream));
+    op_P(b, v, y, fused != 0, all_systems(b), b->st(stream));
   });
 }
 

@@ -31,7 +31,15 @@ struct DeflateParams {
   const double* thomas;     // nsys x 3 x d: sub, cprime, piv
   const double* rowsum;     // nsys x 6w: rW_I(2w) rE_I(2w) rE_W(w) rW_E(w)
   int mx;
+  const int* alist;         // compacted active systems for slot grids (nullable)
+  const int* acount;
 };
+
+__device__ __forceinline__ bool defl_slot(const DeflateParams& P, int slot, int& s) {
+  if (P.acount && slot >= *P.acount) return false;
+  s = P.alist ? P.alist[slot] : slot;
+  return !(P.active && !P.active[s]);
+}
 
 enum DeflateMode : int {
   DEFL_P_FUSED = 0,   // y = zin - S Z c(Z^T zin), S Z c via row sums (zin == y allowed? no)
@@ -65,15 +73,23 @@ __device__ void coarse_solve_block(const DeflateParams& P, int s, double* sums, 
     __syncthreads();
   }
   if (P.cmode[s] == 1) {
-    // Thomas algorithm with precomputed pivots (proj/src/deflation.cpp:77-90)
+    // Thomas algorithm with precomputed reciprocal pivots (proj/src/deflation.cpp:77-90);
+    // the bands are staged in shared memory so the serial recurrence never
+    // waits on global loads
+    __shared__ double band[3 * 512];
+    const double* gsrc = P.thomas + static_cast<long long>(s) * 3 * d;
+    const bool staged = d <= 512;
+    if (staged)
+      for (int i = t; i < 3 * d; i += blockDim.x) band[i] = gsrc[i];
+    __syncthreads();
     if (t == 0) {
-      const double* sub = P.thomas + static_cast<long long>(s) * 3 * d;
+      const double* sub = staged ? band : gsrc;
       const double* cp = sub + d;
-      const double* piv = cp + d;
-      double yprev = sums[0] / piv[0];
+      const double* rpiv = cp + d;
+      double yprev = sums[0] * rpiv[0];
       c[0] = yprev;
       for (int i = 1; i < d; ++i) {
-        yprev = (sums[i] - sub[i - 1] * yprev) / piv[i];
+        yprev = (sums[i] - sub[i - 1] * yprev) * rpiv[i];
         c[i] = yprev;
       }
       for (int i = d - 2; i >= 0; --i) c[i] -= cp[i] * c[i + 1];
@@ -226,7 +242,16 @@ struct GmState_ {
   long long vstride;  // (m+1)*k per system
   int chunk, nchunk;
   int nsys;
+  const int* alist;   // compacted active systems for (chunk, slot) grids
+  const int* acount;  // number of valid slots
 };
+
+// (chunk, slot) grid -> system; false when the slot is past the live count
+__device__ __forceinline__ bool gm_slot(const GmState_& G, int slot, int& s) {
+  if (G.acount && slot >= *G.acount) return false;
+  s = G.alist ? G.alist[slot] : slot;
+  return G.active[s] != 0;
+}
 
 // partial dot products of columns [0, ncols) of V_s with x over rows [r0, r1),
 // warp per column; writes part[s][chunk][col]
@@ -257,14 +282,24 @@ __device__ __forceinline__ bool last_cta(int* counter, int nchunk) {
   return is_last;
 }
 
-// reduce part[s][0..nchunk)[0..ncols) in chunk order -> out[0..ncols)
+// reduce part[s][0..nchunk)[0..ncols) -> out[0..ncols): warp per column,
+// lanes stride the chunks, fixed butterfly -> deterministic and latency-short
 __device__ __forceinline__ void reduce_parts(const double* __restrict__ part, int nchunk, int stride, int ncols,
                                              double* __restrict__ out) {
-  for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < ncols; i += nw) {
     double acc = 0.0;
-    for (int c = 0; c < nchunk; ++c) acc += part[static_cast<long long>(c) * stride + i];
-    out[i] = acc;
+    for (int c = lane; c < nchunk; c += 32) acc += part[static_cast<long long>(c) * stride + i];
+    acc = warp_sum(acc);
+    if (lane == 0) out[i] = acc;
   }
+}
+
+// sum of part[c*stride], c < nchunk, by one warp (returns the total in every lane)
+__device__ __forceinline__ double warp_reduce_strided(const double* __restrict__ part, int nchunk, int stride) {
+  double acc = 0.0;
+  for (int c = threadIdx.x & 31; c < nchunk; c += 32) acc += part[static_cast<long long>(c) * stride];
+  return warp_sum(acc);
 }
 
 // ---- CGS2 pass 1: h1 = V^T w ----------------------------------------------
@@ -282,6 +317,8 @@ __global__ void __launch_bounds__(VEC_THREADS) cgs_dot_kernel(GmState_ G, const 
     reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols,
                  G.h1 + static_cast<long long>(s) * stride);
 }
+
+__device__ void givens_step(GmState_& G, int s, int j, double nrm);
 
 // ---- CGS2 pass 2/3: w -= V h; then (pass 2) h2 = V^T w or (pass 3) ||w|| ----
 template <bool NORM>
@@ -328,13 +365,29 @@ __global__ void __launch_bounds__(VEC_THREADS) cgs_update_kernel(GmState_ G, con
     part[0] = tsum;
   }
   if (!last_cta(G.counter + s, G.nchunk)) return;
-  if (threadIdx.x != 0) return;
-  // ---- last CTA, thread 0: norm + Givens + convergence (proj/src/gmres.cpp:71-99)
-  double nsq = 0.0;
-  const double* p0 = G.part + static_cast<long long>(s) * G.nchunk * stride;
-  for (int c = 0; c < G.nchunk; ++c) nsq += p0[static_cast<long long>(c) * stride];
-  const double nrm = sqrt(nsq);
-  G.nrm[s] = nrm;
+  if (threadIdx.x >= 32) return;
+  // ---- last CTA, warp 0: norm + Givens + convergence (proj/src/gmres.cpp:71-99)
+  const double nsq = warp_reduce_strided(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride);
+  givens_step(G, s, j, sqrt(nsq));
+}
+
+// Hessenberg column j of system s from h1 + h2 (Arnoldi coefficients) and
+// nrm (subdiagonal): previous rotations, a new Givens rotation, the residual
+// estimate |g_{j+1}|, history and the stop tests (proj/src/gmres.cpp:71-99)
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Called by all 32 lanes of one warp. The column and the stored rotations
+// are staged in shared memory so the sequential rotation sweep (lane 0)
+// never waits on global loads.
+__device__ void givens_step(GmState_& G, int s, int j, double nrm) {
+  constexpr int SM = 256;
+  __shared__ double hs[SM + 1], css[SM], sns[SM];
+  const int lane = threadIdx.x & 31;
+  const int stride = G.m + 2;
   const int m = G.m;
   double* h1 = G.h1 + static_cast<long long>(s) * stride;
   const double* h2 = G.h2 + static_cast<long long>(s) * stride;
@@ -342,31 +395,53 @@ __global__ void __launch_bounds__(VEC_THREADS) cgs_update_kernel(GmState_ G, con
   double* sn = G.sn + static_cast<long long>(s) * m;
   double* g = G.g + static_cast<long long>(s) * (m + 1);
   double* R = G.R + static_cast<long long>(s) * (m + 1) * m;
-  double hmax = G.hmax[s];
-  for (int i = 0; i <= j; ++i) {
-    h1[i] += h2[i];
-    hmax = fmax(hmax, fabs(h1[i]));
+  const bool staged = j + 2 <= SM;
+  double* H = staged ? hs : h1;
+  const double* CS = staged ? css : cs;
+  const double* SN = staged ? sns : sn;
+  double hm = 0.0;
+  for (int i = lane; i <= j; i += 32) {
+    const double v = h1[i] + h2[i];
+    H[i] = v;
+    hm = fmax(hm, fabs(v));
   }
-  h1[j + 1] = nrm;
-  hmax = fmax(hmax, nrm);
-  G.hmax[s] = hmax;
-  for (int i = 0; i < j; ++i) {
-    const double t1 = h1[i], t2 = h1[i + 1];
-    h1[i] = cs[i] * t1 + sn[i] * t2;
-    h1[i + 1] = -sn[i] * t1 + cs[i] * t2;
+  if (staged)
+    for (int i = lane; i < j; i += 32) {
+      css[i] = cs[i];
+      sns[i] = sn[i];
+    }
+  hm = warp_max(hm);
+  __syncwarp();
+  __threadfence_block();
+  double hmax = 0.0, res = 0.0;
+  if (lane == 0) {
+    G.nrm[s] = nrm;
+    hmax = fmax(fmax(G.hmax[s], hm), nrm);
+    G.hmax[s] = hmax;
+    H[j + 1] = nrm;
+    for (int i = 0; i < j; ++i) {
+      const double t1 = H[i], t2 = H[i + 1];
+      H[i] = CS[i] * t1 + SN[i] * t2;
+      H[i + 1] = -SN[i] * t1 + CS[i] * t2;
+    }
+    const double rad = hypot(H[j], H[j + 1]);
+    const double c = rad > 0.0 ? H[j] / rad : 1.0;
+    const double sv = rad > 0.0 ? H[j + 1] / rad : 0.0;
+    cs[j] = c;
+    sn[j] = sv;
+    H[j] = rad;
+    const double g1 = g[j], g2 = g[j + 1];
+    g[j] = c * g1 + sv * g2;
+    g[j + 1] = -sv * g1 + c * g2;
+    res = fabs(g[j + 1]);
   }
-  const double rad = hypot(h1[j], h1[j + 1]);
-  cs[j] = rad > 0.0 ? h1[j] / rad : 1.0;
-  sn[j] = rad > 0.0 ? h1[j + 1] / rad : 0.0;
-  h1[j] = rad;
-  const double g1 = g[j], g2 = g[j + 1];
-  g[j] = cs[j] * g1 + sn[j] * g2;
-  g[j + 1] = -sn[j] * g1 + cs[j] * g2;
-  for (int i = 0; i <= j; ++i) R[static_cast<long long>(j) * (m + 1) + i] = h1[i];
+  __syncwarp();
+  __threadfence_block();
+  for (int i = lane; i <= j; i += 32) R[static_cast<long long>(j) * (m + 1) + i] = H[i];
+  if (lane != 0) return;
   const int it = G.iters[s] + 1;
   G.iters[s] = it;
   G.jcyc[s] = j + 1;
-  const double res = fabs(g[j + 1]);
   const int hl = G.hist_len[s];
   if (hl < G.histcap) {
     G.hist[static_cast<long long>(s) * G.histcap + hl] = res / G.bnorm[s];
@@ -388,8 +463,8 @@ __global__ void __launch_bounds__(VEC_THREADS) cgs_update_kernel(GmState_ G, con
 // v_{j+1} = w / ||w|| into V[:, jcyc] and the operator input buffer
 __global__ void gm_scale_kernel(GmState_ G, double* __restrict__ V, const double* __restrict__ w,
                                 double* __restrict__ vin) {
-  const int s = blockIdx.y;
-  if (!G.active[s]) return;
+  int s;
+  if (!gm_slot(G, blockIdx.y, s)) return;
   const double inv = 1.0 / G.nrm[s];
   const int j = G.jcyc[s];
   double* col = V + s * G.vstride + static_cast<long long>(j) * G.k;

@@ -1,0 +1,229 @@
+// Bandwidth/latency-oriented vector kernels, v2 (sm_100a).
+//
+// Arnoldi orthogonalization: one thread per row (R rows per thread), looping
+// over the basis columns so each thread keeps many independent coalesced
+// loads in flight; per-column sums reduce by warp shuffles, then across the
+// CTA's warps in shared memory, then across CTAs by the deterministic
+// "last CTA reduces in chunk order" pattern.
+//
+// Deflation: Z^T segmented sums by many CTAs (warp per interface), the
+// coarse solve by the last CTA of each system, and the O(k) update on a 2D
+// (chunk, system) grid with 32-bit in-system indexing.
+#pragma once
+
+#include "common.cuh"
+#include "vec.cuh"
+
+namespace smpm {
+
+constexpr int V2_THREADS = 256;
+constexpr int V2_ROWS = 2;  // rows per thread -> chunk = 512 rows
+constexpr int V2_CHUNK = V2_THREADS * V2_ROWS;
+constexpr int V2_MAXCOL = 128;
+
+// part[c] = sum over this CTA's rows of V[:, c] * x  (c < ncols); x from smem
+__device__ __forceinline__ void cta_col_dots(const double* __restrict__ Vs, long long k, int ncols, const double* xs,
+                                             int r0, int r1, double* __restrict__ part, double (*red)[V2_MAXCOL + 1]) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = V2_THREADS >> 5;
+  int rows[V2_ROWS];
+  double xv[V2_ROWS];
+#pragma unroll
+  for (int q = 0; q < V2_ROWS; ++q) {
+    rows[q] = r0 + t + q * V2_THREADS;
+    xv[q] = rows[q] < r1 ? xs[rows[q] - r0] : 0.0;
+  }
+  constexpr int GRP = 8;  // columns per group: GRP * V2_ROWS independent loads in flight
+  for (int c0 = 0; c0 < ncols; c0 += GRP) {
+    double acc[GRP];
+#pragma unroll
+    for (int u = 0; u < GRP; ++u) {
+      acc[u] = 0.0;
+      const int c = c0 + u;
+      if (c < ncols) {
+        const double* col = Vs + static_cast<long long>(c) * k;
+#pragma unroll
+        for (int q = 0; q < V2_ROWS; ++q)
+          if (rows[q] < r1) acc[u] = fma(col[rows[q]], xv[q], acc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < GRP; ++u) {
+      const double v = warp_sum(acc[u]);
+      if (lane == 0 && c0 + u < ncols) red[warp][c0 + u] = v;
+    }
+  }
+  __syncthreads();
+  for (int c = t; c < ncols; c += V2_THREADS) {
+    double s = 0.0;
+    for (int q = 0; q < nw; ++q) s += red[q][c];
+    part[c] = s;
+  }
+}
+
+// ---- CGS2 pass 1: h1 = V^T w ----------------------------------------------
+__global__ void __launch_bounds__(V2_THREADS) cgs2_dot_kernel(GmState_ G, const double* __restrict__ V,
+                                                              const double* __restrict__ w) {
+  __shared__ double xs[V2_CHUNK];
+  __shared__ double red[V2_THREADS / 32][V2_MAXCOL + 1];
+  int s;
+  if (!gm_slot(G, blockIdx.y, s)) return;
+  const int ncols = G.jcyc[s] + 1;
+  const int ch = blockIdx.x;
+  const int r0 = ch * G.chunk, r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
+  const double* ws = w + s * G.k;
+  for (int r = r0 + threadIdx.x; r < r1; r += V2_THREADS) xs[r - r0] = ws[r];
+  __syncthreads();
+  const int stride = G.m + 2;
+  double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
+  cta_col_dots(V + s * G.vstride, G.k, ncols, xs, r0, r1, part, red);
+  if (last_cta(G.counter + s, G.nchunk))
+    reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols,
+                 G.h1 + static_cast<long long>(s) * stride);
+}
+
+// ---- CGS2 pass 2 (h2 = V^T w after w -= V h1) / pass 3 (||w|| + Givens) ----
+template <bool NORM>
+__global__ void __launch_bounds__(V2_THREADS) cgs2_update_kernel(GmState_ G, const double* __restrict__ V,
+                                                                 double* __restrict__ w, int do_update) {
+  __shared__ double xs[V2_CHUNK];
+  __shared__ double hs[V2_MAXCOL];
+  __shared__ double red[V2_THREADS / 32][V2_MAXCOL + 1];
+  int s;
+  if (!gm_slot(G, blockIdx.y, s)) return;
+  const int j = G.jcyc[s];
+  const int ncols = j + 1;
+  const int stride = G.m + 2;
+  const double* hin = (NORM ? G.h2 : G.h1) + static_cast<long long>(s) * stride;
+  for (int i = threadIdx.x; i < ncols; i += V2_THREADS) hs[i] = hin[i];
+  __syncthreads();
+  const int ch = blockIdx.x;
+  const int r0 = ch * G.chunk, r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
+  const double* Vs = V + s * G.vstride;
+  double* ws = w + s * G.k;
+  double sq = 0.0;
+#pragma unroll
+  for (int q = 0; q < V2_ROWS; ++q) {
+    const int r = r0 + threadIdx.x + q * V2_THREADS;
+    if (r >= r1) continue;
+    double acc = ws[r];
+    if (do_update) {
+      double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+      int i = 0;
+      for (; i + 4 <= ncols; i += 4) {
+        a1 = fma(Vs[static_cast<long long>(i) * G.k + r], hs[i], a1);
+        a2 = fma(Vs[static_cast<long long>(i + 1) * G.k + r], hs[i + 1], a2);
+        a3 = fma(Vs[static_cast<long long>(i + 2) * G.k + r], hs[i + 2], a3);
+        a4 = fma(Vs[static_cast<long long>(i + 3) * G.k + r], hs[i + 3], a4);
+      }
+      for (; i < ncols; ++i) a1 = fma(Vs[static_cast<long long>(i) * G.k + r], hs[i], a1);
+      acc -= (a1 + a2) + (a3 + a4);
+      ws[r] = acc;
+    }
+    xs[r - r0] = acc;
+    sq = fma(acc, acc, sq);
+  }
+  double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
+  if (!NORM) {
+    __syncthreads();
+    cta_col_dots(Vs, G.k, ncols, xs, r0, r1, part, red);
+    if (last_cta(G.counter + s, G.nchunk))
+      reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols,
+                   G.h2 + static_cast<long long>(s) * stride);
+    return;
+  }
+  sq = warp_sum(sq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][0] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tsum = 0.0;
+    for (int q = 0; q < V2_THREADS / 32; ++q) tsum += red[q][0];
+    part[0] = tsum;
+  }
+  if (!last_cta(G.counter + s, G.nchunk)) return;
+  if (threadIdx.x >= 32) return;
+  const double nsq = warp_reduce_strided(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride);
+  givens_step(G, s, j, sqrt(nsq));
+}
+
+// ---------------------------------------------------------------------------
+// Deflation v2
+// ---------------------------------------------------------------------------
+constexpr int DZ_IFACES = 8;  // interfaces per CTA in the Z^T pass (warp each)
+
+// Z^T sums of zin (nsys x k) -> sums (nsys x d); last CTA per system solves
+// the coarse system and writes c (nsys x d). mode DEFL_COARSE_DIRECT takes
+// the coarse right-hand side from zin (nsys x d) directly.
+__global__ void __launch_bounds__(V2_THREADS) zt_coarse_kernel(DeflateParams P, const double* __restrict__ zin,
+                                                               double* __restrict__ sums, double* __restrict__ cout,
+                                                               int* counter, int direct) {
+  extern __shared__ double sm[];
+  int s;
+  if (!defl_slot(P, blockIdx.y, s)) return;
+  const int d = P.d, w2 = 2 * P.w;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ss = sums + static_cast<long long>(s) * d;
+  if (!direct) {
+    const double* zs = zin + static_cast<long long>(s) * P.k;
+    const int i = blockIdx.x * DZ_IFACES + warp;
+    if (warp < DZ_IFACES && i < d) {
+      const double* seg = zs + static_cast<long long>(i) * w2;
+      double a0 = 0.0, a1 = 0.0;
+      int e = lane;
+      for (; e + 32 < w2; e += 64) {
+        a0 += seg[e];
+        a1 += seg[e + 32];
+      }
+      if (e < w2) a0 += seg[e];
+      const double v = warp_sum(a0 + a1);
+      if (lane == 0) ss[i] = v;
+    }
+    if (!last_cta(counter + s, gridDim.x)) return;
+  }
+  double* bsh = sm;
+  double* csh = sm + d;
+  const double* src = direct ? zin + static_cast<long long>(s) * d : ss;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) bsh[i] = src[i];
+  __syncthreads();
+  coarse_solve_block(P, s, bsh, csh);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) cout[static_cast<long long>(s) * d + i] = csh[i];
+}
+
+// elementwise deflation updates on a (chunk, system) grid
+__global__ void __launch_bounds__(V2_THREADS) defl_update_kernel(DeflateParams P, int mode, const double* __restrict__ c,
+                                                                 const double* __restrict__ zin,
+                                                                 const double* __restrict__ v, double* __restrict__ y) {
+  int s;
+  if (!defl_slot(P, blockIdx.y, s)) return;
+  const int w = P.w, w2 = 2 * w, mx = P.mx;
+  const int k = static_cast<int>(P.k);
+  const double* cs = c + static_cast<long long>(s) * P.d;
+  const long long base = static_cast<long long>(s) * P.k;
+  const double* vs = v + base;
+  double* ys = y + base;
+  const double* rs = P.rowsum + static_cast<long long>(s) * 6 * w;
+  const double* rWI = rs;
+  const double* rEI = rs + w2;
+  const double* rEW = rs + 2 * w2;
+  const double* rWE = rEW + w;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k; e += gridDim.x * blockDim.x) {
+    const int blk = e / w;
+    const int r = e - blk * w;
+    const int i = blk >> 1;
+    if (mode == DEFL_SUB_T) {
+      ys[e] = vs[e] - zin[base + e];
+    } else if (mode == DEFL_Q_TAIL) {
+      ys[e] = vs[e] - cs[i];
+    } else if (mode == DEFL_ADD_ZC) {
+      ys[e] = vs[e] + cs[i];
+    } else {  // DEFL_P_FUSED: y = v - Z c - (S - I) Z c via strip row sums
+      double sz;
+      if ((blk & 1) == 0)
+        sz = (i + 1 == mx - 1) ? cs[i] * rWE[r] : cs[i] * rWI[r] + cs[i + 1] * rEI[r];
+      else
+        sz = (i == 0) ? cs[i] * rEW[r] : cs[i - 1] * rWI[w + r] + cs[i] * rEI[w + r];
+      ys[e] = vs[e] - (cs[i] + sz);
+    }
+  }
+}
+
+}  // namespace smpm
