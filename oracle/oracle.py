@@ -92,6 +92,13 @@ def set_threads(n: int):
     _chk(lib().orc_set_threads(int(n)))
 
 
+def rng_uniforms(seed: int, stream: int, n: int):
+    """Rng(seed).stream(stream) uniforms from the C++ engine (stream < 0: Rng(seed))."""
+    out = np.zeros(n)
+    _chk(lib().orc_rng_uniforms(C.c_ulonglong(seed), C.c_longlong(stream), int(n), _p(out)))
+    return out
+
+
 def gll(n: int):
     nodes, weights, diff = np.zeros(n), np.zeros(n), np.zeros((n, n), order="F")
     _chk(lib().orc_gll(n, _p(nodes), _p(weights), _p(diff)))

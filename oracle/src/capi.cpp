@@ -64,6 +64,14 @@ extern "C" {
 
 const char* orc_last_error() { return g_err.c_str(); }
 
+// n uniforms of Rng(seed) (stream < 0) or Rng(seed).stream(stream) (proj/include/smpm/rng.hpp)
+int orc_rng_uniforms(unsigned long long seed, long long stream, int n, double* out) {
+  return guard([&] {
+    Rng r = stream < 0 ? Rng(seed) : Rng(seed).stream(static_cast<std::uint64_t>(stream));
+    for (int i = 0; i < n; ++i) out[i] = r.uniform();
+  });
+}
+
 int orc_set_threads(int n) {
   return guard([&] { set_blas_threads(n); });
 }
