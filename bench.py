@@ -260,9 +260,10 @@ def run_ours(args, cfg):
 
     sp = solve_params(cfg)
     nm = max(cfg.modes, 1)
-    modes = [m for m in range(nm) if m % ws == rank] if cfg.modes else [0]
-    if not cfg.modes and ws > 1:
-        modes = [0]  # 2D configs: replicas only
+    from paper_1512_01756_b200.dist import gather_modes, shard_modes
+
+    # 3D configs: modes sharded round-robin; 2D configs: replicas only
+    modes = shard_modes(nm, ws, rank) if cfg.modes else [0]
     ps = build_problem(cfg, modes, device=f"cuda:{local}")
     ctx = Context(local)
     b = load_batch(ctx, ps)
@@ -328,16 +329,16 @@ def run_ours(args, cfg):
     value = total_units / (ms_max * 1e-3)
     e2e_value = total_units / e2e_max
 
-    # gather per-mode iteration counts to rank 0 (NCCL) for the record
-    its_rank = torch.tensor(its_tot / args.steps, device=dev)
-    its_all = None
-    if dist:
-        gathered = [torch.zeros(len([m for m in range(nm) if m % ws == r]), device=dev, dtype=torch.float64)
-                    for r in range(ws)]
-        dist.all_gather(gathered, its_rank)
-        its_all = torch.cat(gathered).cpu().numpy()
+    # gather the per-mode solutions and iteration counts in mode order (one
+    # NCCL all-gather over NVLink, outside the timed region)
+    its_rank = torch.tensor(its_tot / args.steps, device=dev)[:, None]
+    if dist and cfg.modes:
+        x_all = gather_modes(res.x_S, nm, ws)
+        its_all = gather_modes(its_rank, nm, ws)[:, 0].cpu().numpy()
+        gathered_bytes = int(x_all.numel() * 8)
     else:
-        its_all = its_rank.cpu().numpy()
+        its_all = its_rank[:, 0].cpu().numpy()
+        gathered_bytes = 0
 
     if rank != 0:
         if dist:
@@ -393,7 +394,8 @@ def run_ours(args, cfg):
                    "systems": nm if cfg.modes else 1, "k_per_system": cfg.k, "method": args.method,
                    "orth": args.orth, "parallelism": f"modes sharded round-robin over {ws} GPU(s)",
                    "l2": "inputs larger than L2 (operators + Krylov basis >> 126 MB per step)", **sp,
-                   "mean_iterations": float(np.mean(its_all)), "max_iterations": float(np.max(its_all))},
+                   "mean_iterations": float(np.mean(its_all)), "max_iterations": float(np.max(its_all)),
+                   "gathered_solution_bytes": gathered_bytes},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "roofline": roofline,
