@@ -26,7 +26,7 @@ EXPORTS = [
     "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_batch_launch_count",
     "smpm_batch_profile", "smpm_fp64_peak",
 ]
-PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other"]
+PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other", "cluster_arnoldi"]
 
 
 class SmpmError(RuntimeError):

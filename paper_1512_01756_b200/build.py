@@ -1,6 +1,7 @@
 """In-tree build of lib/libsmpm_b200.so for sm_100a (nvcc cross-compiles; no GPU needed)."""
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
@@ -9,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libsmpm_b200.so")
 SOURCES = ["batch.cu", "peak.cu"]
-HEADERS = ["common.cuh", "gemm.cuh", "vec.cuh"]
+HEADERS = sorted(os.path.basename(p) for p in glob.glob(os.path.join(CSRC, "*.cuh")))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -29,7 +30,7 @@ def stale() -> bool:
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps = [os.path.join(CSRC, f) for f in SOURCES] + glob.glob(os.path.join(CSRC, "*.cuh"))
     deps.append(os.path.join(HERE, "..", "include", "smpm_b200.h"))
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 

@@ -22,6 +22,7 @@
 #include "gemm2.cuh"
 #include "vec.cuh"
 #include "vec2.cuh"
+#include "cluster.cuh"
 
 using namespace smpm;
 
@@ -251,6 +252,11 @@ struct smpm_batch {
 
   // operator plans
   Plan pS, pSt, pBJ1, pBJ2, pBJ3;
+  Plan pc[4];          // unsplit per-system templates for the cluster solver (BJ1, BJ2, BJ3, S)
+  bool cluster_ok = false;
+  DevArray<double> dclpart, dclzsum;
+  DevArray<int> dclq;  // [queue, publish[kMaxClusters]]
+  int cl_size = 8, cl_max = 0;
   DevArray<double> dws;  // split-K workspace
 
   // vectors (nsys x k each)
@@ -363,6 +369,7 @@ Live all_systems(const smpm_batch* b) {
 }
 
 constexpr int kTailSystems = 8;
+constexpr int kMaxClusters = 512;
 
 void run_plan(smpm_batch* b, Plan& p0, const double* in, double* out, double* tmp, const Live& lv, cudaStream_t st) {
   Plan& p = (p0.v2 && p0.tail && lv.nslots <= kTailSystems && lv.alist) ? *p0.tail : p0;
@@ -586,6 +593,18 @@ void build_plans(smpm_batch* b) {
     p->build2(std::max(1, sms / b->nsys), st);
   }
   b->pSt.build(sms, st);
+  // cluster solver: unsplit copies of the four hot templates
+  b->cluster_ok = true;
+  Plan* src[4] = {&b->pBJ1, &b->pBJ2, &b->pBJ3, &b->pS};
+  for (int i = 0; i < 4; ++i) {
+    if (!src[i]->v2) {
+      b->cluster_ok = false;
+      break;
+    }
+    b->pc[i].jobs = src[i]->jobs;
+    for (auto& j : b->pc[i].jobs) j.splitk = 1;
+    b->pc[i].build2(0, st);
+  }
   // v2 templates hold per-system workspace counts; v1 plans hold totals
   const long long ns = b->nsys;
   long long wst = b->pSt.ws_tiles;
@@ -857,6 +876,7 @@ void finalize(smpm_batch* b) {
   CUDA_CHECK(cudaMemsetAsync(b->dcount.p, 0, sizeof(int) * (b->nsys + 1), st));
   b->dsel.alloc(static_cast<size_t>(b->nsys));
   b->dalist.alloc(2 * static_cast<size_t>(b->nsys) + 2);
+  b->dclq.alloc(1 + kMaxClusters);
   b->dcnt.alloc(4);
   CUDA_CHECK(cudaMallocHost(&b->hcnt, 4 * sizeof(int)));
   CUDA_CHECK(cudaStreamSynchronize(st));
@@ -997,7 +1017,21 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
   double* V = b->dV.p;
   double* vin = b->vbuf[2].p;
   double* wv = b->vbuf[3].p;
-  apply_op(b, c, vin, wv, lv, st);
+  // dbj with fused P on the CGS2 path: the deflation update is applied inside
+  // the first Gram-Schmidt pass (only Z^T + the coarse solve run here)
+  const bool fuse_into_cgs = c.method == SMPM_DBJ && c.fused && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= V2_MAXCOL;
+  double* cbuf = b->dcoarse.p + static_cast<size_t>(b->nsys) * b->d;
+  const double* tdefl = nullptr;
+  if (fuse_into_cgs) {
+    double* u = b->vbuf[4].p;
+    double* t = b->vbuf[5].p;
+    op_BJ(b, vin, u, lv, st);
+    op_S(b, u, t, lv, st);
+    run_deflate(b, DEFL_COARSE, t, nullptr, nullptr, cbuf, lv, st);
+    tdefl = t;
+  } else {
+    apply_op(b, c, vin, wv, lv, st);
+  }
   ProfScope ps(b, PC_ORTH, st);
   dim3 grid(G.nchunk, b->nsys);      // system-indexed kernels (MGS, long cycles)
   dim3 sgrid(G.nchunk, lv.nslots);   // live-slot kernels
@@ -1029,7 +1063,8 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
     Gl.chunk = chunk;
     Gl.nchunk = static_cast<int>((b->k + chunk - 1) / chunk);
     dim3 cgrid(Gl.nchunk, lv.nslots);
-    cgs2_dot_kernel<<<cgrid, V2_THREADS, 0, st>>>(Gl, V, wv);
+    DeflateParams P = deflate_params(b, nullptr);
+    cgs2_dot_kernel<<<cgrid, V2_THREADS, 0, st>>>(Gl, V, wv, tdefl, P, cbuf);
     check_launch(b);
     cgs2_update_kernel<false><<<cgrid, V2_THREADS, 0, st>>>(Gl, V, wv, 1);
     check_launch(b);
@@ -1090,6 +1125,85 @@ __global__ void select_state_kernel(const int* state, int nsys, int want, int* s
   if (s < nsys) sel[s] = state[s] == want ? 1 : 0;
 }
 
+// Runs the live systems' Arnoldi steps until each stops, in one
+// cluster-persistent launch (cluster.cuh).
+void arnoldi_cluster(smpm_batch* b, const SolveCfg& c, const int* alist, const int* acount, int nlive,
+                     cudaStream_t st) {
+  ProfScope ps(b, 5, st);  // class 5: cluster-persistent Arnoldi
+  GmState_& G = b->G;
+  const size_t smem = G2_SMEM + sizeof(double) * (256 + 2 * static_cast<size_t>(b->d));
+  if (const char* e = std::getenv("SMPM_CLUSTER")) b->cl_size = std::max(1, std::min(16, std::atoi(e)));
+  const int csz = b->cl_size;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csz;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(G2_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  if (b->cl_max == 0) {
+    CUDA_CHECK(cudaFuncSetAttribute(arnoldi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    if (csz > 8)
+      CUDA_CHECK(cudaFuncSetAttribute(arnoldi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cfg.gridDim = dim3(csz * 64);
+    int n = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveClusters(&n, arnoldi_cluster_kernel, &cfg));
+    b->cl_max = std::max(1, std::min(n, kMaxClusters));
+  }
+  const int ncl = std::max(1, std::min(nlive, b->cl_max));
+  const size_t stride = static_cast<size_t>(G.m + 2);
+  b->dclpart.alloc(std::max(b->dclpart.n, static_cast<size_t>(kMaxClusters) * csz * stride));
+  b->dclzsum.alloc(std::max(b->dclzsum.n, static_cast<size_t>(kMaxClusters) * b->d));
+  ClusterArgs A{};
+  for (int i = 0; i < 4; ++i) {
+    A.jobs[i] = b->pc[i].djobs.p;
+    A.tiles[i] = b->pc[i].dtiles2.p;
+    A.ntiles[i] = b->pc[i].ntiles;
+  }
+  A.a_stride = b->mstride;
+  A.vin = b->vbuf[2].p;
+  A.w = b->vbuf[3].p;
+  A.u = b->vbuf[4].p;
+  A.t = b->vbuf[5].p;
+  A.tmp = b->vbuf[9].p;
+  A.V = b->dV.p;
+  A.part = b->dclpart.p;
+  A.zsum = b->dclzsum.p;
+  A.queue = b->dclq.p;
+  A.publish = b->dclq.p + 1;
+  A.alist = alist;
+  A.acount = acount;
+  A.method = c.method;
+  A.G = G;
+  A.P = deflate_params(b, nullptr);
+  CUDA_CHECK(cudaMemsetAsync(b->dclq.p, 0, sizeof(int), st));
+  cfg.gridDim = dim3(csz * ncl);
+  // debug: SMPM_CL_TRACE=<path> dumps per-phase timestamps of every cluster's first 64 steps
+  const char* tpath = std::getenv("SMPM_CL_TRACE");
+  DevArray<unsigned long long> dtr;
+  if (tpath) {
+    dtr.alloc(static_cast<size_t>(ncl) * 64 * 12);
+    CUDA_CHECK(cudaMemsetAsync(dtr.p, 0, dtr.n * sizeof(unsigned long long), st));
+    A.trace = dtr.p;
+  }
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, arnoldi_cluster_kernel, A));
+  check_launch(b);
+  if (tpath) {
+    std::vector<unsigned long long> h(dtr.n);
+    CUDA_CHECK(cudaMemcpyAsync(h.data(), dtr.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (FILE* f = std::fopen(tpath, "ab")) {
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      std::fclose(f);
+    }
+  }
+}
+
 void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_report* reps, double* history,
            cudaStream_t st) {
   need_final(b);
@@ -1144,11 +1258,52 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   G.alist = alist;
   G.acount = acount;
 
+  const bool use_cluster = b->cluster_ok && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= 128 &&
+                           (c.method != SMPM_DBJ || c.fused) && std::getenv("SMPM_CLUSTER") != nullptr;
+  if (use_cluster) {
+    // ---- cluster-persistent Arnoldi: one launch per GMRES cycle
+    int nlive = ns;
+    for (;;) {
+      arnoldi_cluster(b, c, alist, acount, nlive, st);
+      compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist2, acount2, b->dcnt.p);
+      check_launch(b);
+      CUDA_CHECK(cudaMemcpyAsync(hcnt, b->dcnt.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      CUDA_CHECK(cudaStreamSynchronize(st));
+      const int ncyc = hcnt[1];
+      if (ncyc == 0) break;
+      // ---- restart (GMRES(m) extension): x += V y ; r = b - op(x) ; new cycle
+      select_state_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, GM_CYCLE, dsel);
+      check_launch(b);
+      compact_kernel<<<1, 1024, 0, st>>>(dsel, nullptr, ns, alist2, acount2, nullptr);
+      check_launch(b);
+      Live lr;
+      lr.alist = alist2;
+      lr.acount = acount2;
+      lr.nslots = ncyc;
+      lr.active = dsel;
+      gm_backsolve_kernel<<<ns, 32, 0, st>>>(G, dsel);
+      check_launch(b);
+      gm_combine_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, x, dsel, 1);
+      check_launch(b);
+      apply_op(b, c, x, r, lr, st);
+      ++op_applies;
+      axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, dsel, nullptr, 1.0, rhs, -1.0, r);
+      check_launch(b);
+      batched_dot(b, r, r, nr2, dsel, st);
+      gm_start_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G, nr2, nb2, c.tol, 0, G.state);
+      check_launch(b);
+      gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, r, vin);
+      check_launch(b);
+      compact_kernel<<<1, 1024, 0, st>>>(G.active, nullptr, ns, alist, acount, nullptr);
+      check_launch(b);
+      nlive = ncyc;
+    }
+  }
+  int steps = 0;
   // ---- Arnoldi steps; device flags are polled one step behind the launches
   // (step i+1 is queued before the host waits on step i's counters). Grids
   // are sized by `bound`, the live count the host last read: systems only
   // stop inside a cycle, so it bounds the device-compacted live list.
-  int steps = 0;
   int bound = ns;
   const int per_sys_applies = c.method == SMPM_DBJ && !c.fused ? 2 : 1;
   auto issue = [&](int slot) {
@@ -1165,8 +1320,8 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     CUDA_CHECK(cudaEventRecord(ev[slot], st));
   };
   int cur = 0;
-  issue(cur);
-  for (;;) {
+  if (!use_cluster) issue(cur);
+  for (; !use_cluster;) {
     const bool more = steps < mtot + 1;
     if (more) issue(cur ^ 1);
     CUDA_CHECK(cudaEventSynchronize(ev[cur]));

@@ -15,7 +15,10 @@
 
 namespace smpm {
 
-constexpr int G2_BM = 64, G2_BN = 32, G2_BK = 16, G2_STAGES = 4;
+#ifndef G2_STAGES_DEF
+#define G2_STAGES_DEF 4
+#endif
+constexpr int G2_BM = 64, G2_BN = 32, G2_BK = 16, G2_STAGES = G2_STAGES_DEF;
 constexpr int G2_APAD = 8;  // As row stride 72 doubles: 4 k-rows of 8 m's -> 2 wavefronts
 constexpr int G2_BPAD = 4;  // Bs row stride 20 doubles: 8 n-rows of 4 k's -> conflict-free
 constexpr int G2_THREADS = 128;
@@ -83,20 +86,15 @@ __device__ __forceinline__ void shift_job(GemmJob& jb, const SysMap& sm, int s) 
   jb.sys = s;
 }
 
-__global__ void __launch_bounds__(G2_THREADS, 4)
-gemm2_kernel(const GemmJob* __restrict__ jobs, const Tile2* __restrict__ tiles, BufTable bufs, SysMap smap,
-             double* __restrict__ ws) {
-  // dynamic shared memory (G2_SMEM bytes): As[STAGES][BK][BM+APAD], Bs[STAGES][BN][BK+BPAD]
-  extern __shared__ __align__(16) double g2_smem[];
-  auto As = reinterpret_cast<double(*)[G2_BK][G2_BM + G2_APAD]>(g2_smem);
-  auto Bs = reinterpret_cast<double(*)[G2_BN][G2_BK + G2_BPAD]>(g2_smem + G2_STAGES * G2_BK * (G2_BM + G2_APAD));
-
-  int sysid;
-  if (!map_system(smap, blockIdx.x / smap.tiles_per_sys, sysid)) return;
-  const Tile2 tile = tiles[blockIdx.x % smap.tiles_per_sys];
-  GemmJob jb = jobs[tile.job];
-  shift_job(jb, smap, sysid);
+// One output tile of one (system-shifted) job, computed by the calling CTA's
+// first G2_THREADS threads with G2_SMEM bytes of shared memory at `smem`.
+// Shared by the per-stage launches and the cluster-persistent solver.
+__device__ __forceinline__ void g2_run_tile(const GemmJob& jb, const Tile2& tile, const BufTable& bufs,
+                                            double* __restrict__ ws, double* smem) {
+  auto As = reinterpret_cast<double(*)[G2_BK][G2_BM + G2_APAD]>(smem);
+  auto Bs = reinterpret_cast<double(*)[G2_BN][G2_BK + G2_BPAD]>(smem + G2_STAGES * G2_BK * (G2_BM + G2_APAD));
   const int t = threadIdx.x;
+  __syncthreads();  // shared memory may still be read by this CTA's previous tile
   const int lane = t & 31, warp = t >> 5;
 
   if (tile.ks < 0) {
@@ -104,21 +102,26 @@ gemm2_kernel(const GemmJob* __restrict__ jobs, const Tile2* __restrict__ tiles, 
     const int r = t % GV_ROWS, kg = t / GV_ROWS;
     const int m = tile.m0 + r;
     const double* __restrict__ x = bufs.p[jb.b.buf] + jb.b.off;
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    // 8 independent loads in flight per thread per round
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (m < jb.M) {
       const double* __restrict__ a = jb.A + m;
       const long long lda = jb.lda;
       int k = kg;
-      for (; k + 3 * GV_KG < jb.K; k += 4 * GV_KG) {
-        acc0 = fma(__ldg(a + static_cast<long long>(k) * lda), x[k], acc0);
-        acc1 = fma(__ldg(a + static_cast<long long>(k + GV_KG) * lda), x[k + GV_KG], acc1);
-        acc2 = fma(__ldg(a + static_cast<long long>(k + 2 * GV_KG) * lda), x[k + 2 * GV_KG], acc2);
-        acc3 = fma(__ldg(a + static_cast<long long>(k + 3 * GV_KG) * lda), x[k + 3 * GV_KG], acc3);
+      for (; k + 7 * GV_KG < jb.K; k += 8 * GV_KG) {
+        double av[8], xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          av[u] = __ldg(a + static_cast<long long>(k + u * GV_KG) * lda);
+          xv[u] = x[k + u * GV_KG];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = fma(av[u], xv[u], acc[u]);
       }
-      for (; k < jb.K; k += GV_KG) acc0 = fma(__ldg(a + static_cast<long long>(k) * lda), x[k], acc0);
+      for (; k < jb.K; k += GV_KG) acc[0] = fma(__ldg(a + static_cast<long long>(k) * lda), x[k], acc[0]);
     }
     __shared__ double red[GV_KG][GV_ROWS];
-    red[kg][r] = (acc0 + acc1) + (acc2 + acc3);
+    red[kg][r] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     __syncthreads();
     if (kg == 0 && m < jb.M) {
       double s = 0.0;
@@ -230,6 +233,19 @@ gemm2_kernel(const GemmJob* __restrict__ jobs, const Tile2* __restrict__ tiles, 
         const int n = n0 + wn * 16 + j * 8 + (lane & 3) * 2 + e;
         if (m < M && n < N) store_out(jb, bufs, m, n, acc[i][j][e]);
       }
+}
+
+__global__ void __launch_bounds__(G2_THREADS, 4)
+gemm2_kernel(const GemmJob* __restrict__ jobs, const Tile2* __restrict__ tiles, BufTable bufs, SysMap smap,
+             double* __restrict__ ws) {
+  // dynamic shared memory (G2_SMEM bytes): As[STAGES][BK][BM+APAD], Bs[STAGES][BN][BK+BPAD]
+  extern __shared__ __align__(16) double g2_smem[];
+  int sysid;
+  if (!map_system(smap, blockIdx.x / smap.tiles_per_sys, sysid)) return;
+  const Tile2 tile = tiles[blockIdx.x % smap.tiles_per_sys];
+  GemmJob jb = jobs[tile.job];
+  shift_job(jb, smap, sysid);
+  g2_run_tile(jb, tile, bufs, ws, g2_smem);
 }
 
 // split-K reduction in fixed K order + epilogue (64x32 tiles)

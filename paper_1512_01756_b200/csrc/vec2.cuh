@@ -32,7 +32,7 @@ __device__ __forceinline__ void cta_col_dots(const double* __restrict__ Vs, long
     rows[q] = r0 + t + q * V2_THREADS;
     xv[q] = rows[q] < r1 ? xs[rows[q] - r0] : 0.0;
   }
-  constexpr int GRP = 8;  // columns per group: GRP * V2_ROWS independent loads in flight
+  constexpr int GRP = 16;  // columns per group: GRP * V2_ROWS independent loads in flight
   for (int c0 = 0; c0 < ncols; c0 += GRP) {
     double acc[GRP];
 #pragma unroll
@@ -61,8 +61,12 @@ __device__ __forceinline__ void cta_col_dots(const double* __restrict__ Vs, long
 }
 
 // ---- CGS2 pass 1: h1 = V^T w ----------------------------------------------
+// tdefl != nullptr: the fused deflation P of the dbj operator is applied on
+// the fly, w = t - Z c - (S - I) Z c with c = C^{-1} Z^T t precomputed per
+// system in cbuf (strip row-sum identity), and w is stored.
 __global__ void __launch_bounds__(V2_THREADS) cgs2_dot_kernel(GmState_ G, const double* __restrict__ V,
-                                                              const double* __restrict__ w) {
+                                                              double* __restrict__ w, const double* __restrict__ tdefl,
+                                                              DeflateParams P, const double* __restrict__ cbuf) {
   __shared__ double xs[V2_CHUNK];
   __shared__ double red[V2_THREADS / 32][V2_MAXCOL + 1];
   int s;
@@ -70,8 +74,27 @@ __global__ void __launch_bounds__(V2_THREADS) cgs2_dot_kernel(GmState_ G, const 
   const int ncols = G.jcyc[s] + 1;
   const int ch = blockIdx.x;
   const int r0 = ch * G.chunk, r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
-  const double* ws = w + s * G.k;
-  for (int r = r0 + threadIdx.x; r < r1; r += V2_THREADS) xs[r - r0] = ws[r];
+  double* ws = w + s * G.k;
+  if (tdefl) {
+    const int wd = P.w, w2 = 2 * wd, mx = P.mx;
+    const double* c = cbuf + static_cast<long long>(s) * P.d;
+    const double* rs = P.rowsum + static_cast<long long>(s) * 6 * wd;
+    const double *rWI = rs, *rEI = rs + w2, *rEW = rs + 2 * w2, *rWE = rEW + wd;
+    const double* ts = tdefl + s * G.k;
+    for (int e = r0 + threadIdx.x; e < r1; e += V2_THREADS) {
+      const int blk = e / wd, r = e - blk * wd, i = blk >> 1;
+      double sz;
+      if ((blk & 1) == 0)
+        sz = (i + 1 == mx - 1) ? c[i] * rWE[r] : c[i] * rWI[r] + c[i + 1] * rEI[r];
+      else
+        sz = (i == 0) ? c[i] * rEW[r] : c[i - 1] * rWI[wd + r] + c[i] * rEI[wd + r];
+      const double v = ts[e] - (c[i] + sz);
+      ws[e] = v;
+      xs[e - r0] = v;
+    }
+  } else {
+    for (int r = r0 + threadIdx.x; r < r1; r += V2_THREADS) xs[r - r0] = ws[r];
+  }
   __syncthreads();
   const int stride = G.m + 2;
   double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
@@ -107,16 +130,20 @@ __global__ void __launch_bounds__(V2_THREADS) cgs2_update_kernel(GmState_ G, con
     if (r >= r1) continue;
     double acc = ws[r];
     if (do_update) {
-      double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
-      int i = 0;
-      for (; i + 4 <= ncols; i += 4) {
-        a1 = fma(Vs[static_cast<long long>(i) * G.k + r], hs[i], a1);
-        a2 = fma(Vs[static_cast<long long>(i + 1) * G.k + r], hs[i + 1], a2);
-        a3 = fma(Vs[static_cast<long long>(i + 2) * G.k + r], hs[i + 2], a3);
-        a4 = fma(Vs[static_cast<long long>(i + 3) * G.k + r], hs[i + 3], a4);
+      // 16 independent column loads per round: the update is latency-bound
+      // when few systems are live, so the number of load rounds is what counts
+      double a1 = 0.0, a2 = 0.0;
+      for (int i0 = 0; i0 < ncols; i0 += 16) {
+        double vv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) vv[u] = i0 + u < ncols ? Vs[static_cast<long long>(i0 + u) * G.k + r] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) {
+          a1 = fma(vv[u], i0 + u < ncols ? hs[i0 + u] : 0.0, a1);
+          a2 = fma(vv[u + 1], i0 + u + 1 < ncols ? hs[i0 + u + 1] : 0.0, a2);
+        }
       }
-      for (; i < ncols; ++i) a1 = fma(Vs[static_cast<long long>(i) * G.k + r], hs[i], a1);
-      acc -= (a1 + a2) + (a3 + a4);
+      acc -= a1 + a2;
       ws[r] = acc;
     }
     xs[r - r0] = acc;
