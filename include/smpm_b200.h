@@ -122,6 +122,22 @@ int smpm_batch_set_interface_blocks(smpm_batch* b, int sys, const double* const*
  * (C + u_C u_C^T) with u_C = normalize(Z^T u_S) (proj/src/deflation.cpp:44-54). */
 int smpm_batch_set_nullspace(smpm_batch* b, int sys, const double* u_S);
 
+/* Optional spectral factors of the couplings (before finalize).  Every
+ * coupling block is G_kind[X,Y] = T diag_q(gamma_kind,XY) T^{-1} in the real
+ * eigenbasis T (w x w, column-major) of the strip operator's z factor, with
+ * the `npairs` complex-conjugate eigenpairs first (columns Re v, Im v) and the
+ * w - 2 npairs real modes after; a pair's gamma acts on z = a - i b.  gamma is
+ * nsys x 6 x nmode complex numbers (re, im interleaved; nmode = w - npairs) in
+ * kind order W_EE, I_WW, I_WE, I_EW, I_EE, E_WW (G_W = W_EE; G_I = [[I_WW,
+ * I_WE], [I_EW, I_EE]]; G_E = E_WW).  The dense couplings stay the reference
+ * data (set_couplings is still required); with factors set, the Krylov
+ * operator runs as two shared-matrix GEMMs (T^{-1}, T) around per-mode work
+ * (the fast-diagonalisation form of the A^{-1}B sweep), with identical
+ * results up to rounding.  Replaces nothing in the reference API; it is the
+ * data the reference computes in build_kind_coupling (proj/src/schur.cpp:19-69)
+ * before densifying it. */
+int smpm_batch_set_spectral(smpm_batch* b, int npairs, const double* T, const double* T_inv, const double* gamma);
+
 /* Uploads, builds the block-Jacobi inverses (proj/src/schur.cpp:188-216),
  * the coarse matrices C = Z^T S Z and their solvers (proj/src/deflation.cpp:24-69). */
 int smpm_batch_finalize(smpm_batch* b);

@@ -20,13 +20,13 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "ERUNTIME", 3: "ENONFINITE", 4: "ESINGULAR", 
 EXPORTS = [
     "smpm_last_error", "smpm_version", "smpm_ctx_create", "smpm_ctx_destroy", "smpm_ctx_stream",
     "smpm_batch_create", "smpm_batch_destroy", "smpm_batch_dims", "smpm_batch_set_couplings",
-    "smpm_batch_set_interface_blocks", "smpm_batch_set_nullspace", "smpm_batch_finalize",
+    "smpm_batch_set_interface_blocks", "smpm_batch_set_nullspace", "smpm_batch_set_spectral", "smpm_batch_finalize",
     "smpm_batch_coarse_info", "smpm_apply_S", "smpm_apply_St", "smpm_apply_block_jacobi_inv", "smpm_apply_Z",
     "smpm_apply_Zt", "smpm_coarse_solve", "smpm_apply_P", "smpm_apply_Q", "smpm_project_out", "smpm_solve",
     "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_batch_launch_count",
     "smpm_batch_profile", "smpm_fp64_peak",
 ]
-PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other", "cluster_arnoldi"]
+PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other", "cluster_arnoldi", "grid_tail", "spectral_op"]
 
 
 class SmpmError(RuntimeError):
@@ -85,6 +85,7 @@ def lib():
     L.smpm_batch_set_interface_blocks.argtypes = [vp, ip, C.POINTER(dp), C.POINTER(llp), C.POINTER(C.c_void_p),
                                                   C.POINTER(C.c_void_p), C.POINTER(ip)]
     L.smpm_batch_set_nullspace.argtypes = [vp, ip, dp]
+    L.smpm_batch_set_spectral.argtypes = [vp, ip, dp, dp, dp]
     L.smpm_batch_finalize.argtypes = [vp]
     L.smpm_batch_coarse_info.argtypes = [vp, dp, C.POINTER(ip), C.POINTER(ip)]
     for f in ("smpm_apply_S", "smpm_apply_St", "smpm_apply_block_jacobi_inv", "smpm_apply_Z", "smpm_apply_Zt",

@@ -23,6 +23,8 @@
 #include "vec.cuh"
 #include "vec2.cuh"
 #include "cluster.cuh"
+#include "grid.cuh"
+#include "spectral.cuh"
 
 using namespace smpm;
 
@@ -105,9 +107,12 @@ struct Plan {
   DevArray<GemmJob> djobs;
   DevArray<GemmTile> dtiles;
   DevArray<SplitItem> ditems;
-  int ntiles = 0, nitems = 0;
+  int ntiles = 0, nitems = 0, ngemm = 0;
   long long ws_tiles = 0;
+  DevArray<Tile2> dgv;  // GEMV jobs as GT_GVR-row cluster items (grid tail solver)
+  int ngv = 0;
   bool v2 = false;  // hot-path kernel (DMMA tiles + GEMV tiles)
+  bool shared_a = false;  // every system uses the same matrices (no per-system stride)
   DevArray<Tile2> dtiles2;
 
   // v2 plan: N >= 2 jobs as 64x32 DMMA tiles (split-K when the plan has too
@@ -147,6 +152,7 @@ struct Plan {
     // GEMM tiles first (long), GEMV tiles last
     std::stable_sort(ht.begin(), ht.end(), [](const Tile2& x, const Tile2& y) { return (x.ks < 0) < (y.ks < 0); });
     ntiles = static_cast<int>(ht.size());
+    ngemm = static_cast<int>(std::count_if(ht.begin(), ht.end(), [](const Tile2& x) { return x.ks >= 0; }));
     nitems = static_cast<int>(hi.size());
     v2 = true;
     djobs.upload(jobs, st);
@@ -252,12 +258,24 @@ struct smpm_batch {
 
   // operator plans
   Plan pS, pSt, pBJ1, pBJ2, pBJ3;
-  Plan pc[4];          // unsplit per-system templates for the cluster solver (BJ1, BJ2, BJ3, S)
+  // spectral form (spectral.cuh): T^{-1} / T transforms and per-mode factors
+  bool spectral = false;
+  int sp_npairs = 0, sp_nmode = 0;
+  std::vector<double> hT, hTi, hgam;
+  DevArray<double> dT, dTi, domega, dgam, dzpart, dvh, dth;
+  Plan pF, pB;
+  Plan pc[6];          // unsplit per-system templates (BJ1, BJ2, BJ3, S; spectral F, B) for the persistent solvers
   bool cluster_ok = false;
   DevArray<double> dclpart, dclzsum;
   DevArray<int> dclq;  // [queue, publish[kMaxClusters]]
   int cl_size = 8, cl_max = 0;
   DevArray<double> dws;  // split-K workspace
+  // grid-persistent tail solver (grid.cuh)
+  bool grid_ok = false;
+  int gt_blocks = 0;
+  bool gt_nocoop = false;  // cooperative + cluster launch rejected: plain cluster launch
+  DevArray<unsigned> dgbar;   // grid barrier counter
+  DevArray<double> dgtpart, dgtzsum, dgtzp;
 
   // vectors (nsys x k each)
   DevArray<double> vbuf[12];
@@ -385,7 +403,7 @@ void run_plan(smpm_batch* b, Plan& p0, const double* in, double* out, double* tm
     sm.alist = lv.alist;
     sm.acount = lv.acount;
     sm.tiles_per_sys = p.ntiles;
-    sm.a_stride = b->mstride;
+    sm.a_stride = p0.shared_a ? 0 : b->mstride;
     sm.v_stride = b->k;
     sm.ws_stride = p.ws_tiles;
     gemm2_kernel<<<p.ntiles * lv.nslots, G2_THREADS, G2_SMEM, st>>>(p.djobs.p, p.dtiles2.p, t, sm, b->dws.p);
@@ -509,8 +527,16 @@ void build_plans(smpm_batch* b) {
   b->pBJ1.jobs.clear();
   b->pBJ2.jobs.clear();
   b->pBJ3.jobs.clear();
+  b->pF.jobs.clear();
+  b->pB.jobs.clear();
+  b->pF.shared_a = b->pB.shared_a = true;
   for (int s = 0; s < b->nsys; ++s) {
     const long long o = s * k;
+    if (b->spectral) {
+      // every w-block through T^{-1} (forward) / T (back): w x 2d per system
+      b->pF.add(b->dTi.p, w, false, w, 2 * d, w, s, view(BUF_IN, o, w), view(BUF_OUT, o, w), kNoView, 1.0, 0.0);
+      b->pB.add(b->dT.p, w, false, w, 2 * d, w, s, view(BUF_IN, o, w), view(BUF_OUT, o, w), kNoView, 1.0, 0.0);
+    }
     // ---- S v = v + sum_s G_s [v_{2s-1}; v_{2s}] -> [y_{2s-2}; y_{2s+1}]
     if (mx >= 3)
       b->pS.add(b->GI(s), w2, false, 2 * w, mx - 2, 2 * w, s, view(BUF_IN, o + w, w2),
@@ -572,7 +598,8 @@ void build_plans(smpm_batch* b) {
     }
   }
   const int sms = b->ctx->num_sms;
-  for (Plan* p : {&b->pS, &b->pBJ1, &b->pBJ2, &b->pBJ3}) {
+  for (Plan* p : {&b->pS, &b->pBJ1, &b->pBJ2, &b->pBJ3, &b->pF, &b->pB}) {
+    if (p->jobs.empty()) continue;
     if (!p->v2_ok()) {
       // odd w (16-byte alignment impossible): per-system jobs on the v1 kernel
       p->build(sms, st);
@@ -588,6 +615,7 @@ void build_plans(smpm_batch* b) {
     // spreads over many SMs (used when <= kTailSystems systems are live)
     p->tail = std::make_unique<Plan>();
     p->tail->jobs = p->jobs;
+    p->tail->shared_a = p->shared_a;
     p->tail->build2(std::max(1, sms / b->nsys), st, 4);
     // split-K only when even the whole batch cannot fill the GPU
     p->build2(std::max(1, sms / b->nsys), st);
@@ -595,24 +623,38 @@ void build_plans(smpm_batch* b) {
   b->pSt.build(sms, st);
   // cluster solver: unsplit copies of the four hot templates
   b->cluster_ok = true;
-  Plan* src[4] = {&b->pBJ1, &b->pBJ2, &b->pBJ3, &b->pS};
-  for (int i = 0; i < 4; ++i) {
+  Plan* src[6] = {&b->pBJ1, &b->pBJ2, &b->pBJ3, &b->pS, &b->pF, &b->pB};
+  for (int i = 0; i < 6; ++i) {
+    if (i >= 4 && !b->spectral) break;
     if (!src[i]->v2) {
-      b->cluster_ok = false;
-      break;
+      if (i < 4) {
+        b->cluster_ok = false;
+        break;
+      }
+      continue;
     }
+    b->pc[i].shared_a = src[i]->shared_a;
     b->pc[i].jobs = src[i]->jobs;
     for (auto& j : b->pc[i].jobs) j.splitk = 1;
     b->pc[i].build2(0, st);
+    std::vector<Tile2> gv;
+    for (size_t ji = 0; ji < b->pc[i].jobs.size(); ++ji)
+      if (b->pc[i].jobs[ji].N == 1)
+        for (int m0 = 0; m0 < b->pc[i].jobs[ji].M; m0 += GT_GVR) gv.push_back(Tile2{static_cast<int>(ji), m0, 0, -1});
+    b->pc[i].dgv.upload(gv, st);
+    b->pc[i].ngv = static_cast<int>(gv.size());
   }
   // v2 templates hold per-system workspace counts; v1 plans hold totals
   const long long ns = b->nsys;
   long long wst = b->pSt.ws_tiles;
-  for (Plan* p : {&b->pS, &b->pBJ1, &b->pBJ2, &b->pBJ3}) {
+  for (Plan* p : {&b->pS, &b->pBJ1, &b->pBJ2, &b->pBJ3, &b->pF, &b->pB}) {
     wst = std::max(wst, p->ws_tiles * (p->v2 ? ns : 1));
     if (p->tail) wst = std::max(wst, p->tail->ws_tiles * ns);
   }
   b->dws.alloc(static_cast<size_t>(std::max(1LL, wst)) * GEMM_BM * GEMM_BN);
+  // grid tail solver: the unsplit templates of the four hot stages (pc)
+  b->grid_ok = b->cluster_ok;
+  b->dgbar.alloc(1);
 }
 
 __global__ void add_identity_kernel(double* A, long long lda, int n) {
@@ -864,7 +906,21 @@ void finalize(smpm_batch* b) {
   for (int s = 0; s < b->nsys; ++s)
     CUDA_CHECK(cudaMemcpyAsync(b->GW(s), b->hG.data() + s * 6LL * w * w, sizeof(double) * 6LL * w * w,
                                cudaMemcpyHostToDevice, st));
+  if (b->spectral) {
+    b->dT.upload(b->hT, st);
+    b->dTi.upload(b->hTi, st);
+    b->dgam.upload(b->hgam, st);
+    std::vector<double> om(static_cast<size_t>(w), 0.0);  // omega = T^T 1
+    for (int e = 0; e < w; ++e)
+      for (int r = 0; r < w; ++r) om[e] += b->hT[static_cast<size_t>(e) * w + r];
+    b->domega.upload(om, st);
+    const int nmc = (b->sp_nmode + SP_THREADS - 1) / SP_THREADS;
+    b->dzpart.alloc(static_cast<size_t>(b->nsys) * nmc * d);
+    b->dvh.alloc(static_cast<size_t>(b->nsys) * b->k);
+    b->dth.alloc(static_cast<size_t>(b->nsys) * b->k);
+  }
   build_plans(b);
+  if (b->spectral && !(b->pF.v2 && b->pB.v2)) b->spectral = false;  // odd w: dense operator path
   build_bj_inverses(b);
   build_coarse(b);
   for (auto& v : b->vbuf) v.alloc(static_cast<size_t>(b->nsys) * b->k);
@@ -984,11 +1040,71 @@ struct SolveCfg {
   bool fused, final_check;
 };
 
+// --------------------------------------------------------------------------
+// Spectral operator (spectral.cuh): T^{-1} GEMM, per-mode S^ M^^{-1}, T GEMM
+// --------------------------------------------------------------------------
+SpecParams spec_params(const smpm_batch* b) {
+  SpecParams sp;
+  sp.w = b->w;
+  sp.d = b->d;
+  sp.mx = b->mx;
+  sp.nbf = b->nbf;
+  sp.single = b->single ? 1 : 0;
+  sp.npairs = b->sp_npairs;
+  sp.nmode = b->sp_nmode;
+  sp.k = b->k;
+  sp.gam = reinterpret_cast<const double2*>(b->dgam.p);
+  sp.omega = b->domega.p;
+  sp.nmc = (b->sp_nmode + SP_THREADS - 1) / SP_THREADS;
+  sp.nseg = (b->nbf + (b->single ? 1 : 0) + SP_SEGB - 1) / SP_SEGB;
+  return sp;
+}
+
+// th = S^ M^^{-1} vh (bj) or S^ vh in T-coordinates; with cout, also
+// c = C^{-1} Z^T (T th) per system (deflation coarse solve)
+void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* cout, const Live& lv, cudaStream_t st) {
+  if (lv.nslots == 0) return;
+  const SpecParams sp = spec_params(b);
+  DeflateParams P = deflate_params(b, lv.active);
+  P.alist = lv.alist;
+  P.acount = lv.acount;
+  const dim3 grid(sp.nmc * sp.nseg, lv.nslots);
+  const size_t shm = cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0;
+  double* zp = cout ? b->dzpart.p : nullptr;
+  if (bj)
+    spec_op_kernel<true><<<grid, SP_THREADS, shm, st>>>(sp, vh, th, P, zp, b->dcount.p, cout);
+  else
+    spec_op_kernel<false><<<grid, SP_THREADS, shm, st>>>(sp, vh, th, P, zp, b->dcount.p, cout);
+  check_launch(b);
+}
+
+bool spec_ok(const smpm_batch* b, const SolveCfg& c) {
+  return b->spectral && (c.method == SMPM_SCHUR || c.method == SMPM_BJ || c.method == SMPM_DBJ) &&
+         std::getenv("SMPM_NO_SPECTRAL") == nullptr;
+}
+
+// S M^{-1} v (bj) or S v through the spectral form; out may be any buffer
+void spec_SMinv(smpm_batch* b, bool bj, const double* v, double* out, double* cout, const Live& lv, cudaStream_t st) {
+  ProfScope ps(b, 7, st);  // class 7: spectral operator
+  run_plan(b, b->pF, v, b->dvh.p, nullptr, lv, st);
+  spec_apply(b, bj, b->dvh.p, b->dth.p, cout, lv, st);
+  run_plan(b, b->pB, b->dth.p, out, nullptr, lv, st);
+}
+
 // the preconditioned operator GMRES iterates on (proj/src/deflation.cpp:105-107,131; proj/src/gmres.cpp:144-150)
 // returns the number of S applications it made per system
 int apply_op(smpm_batch* b, const SolveCfg& c, const double* vin, double* wout, const Live& act, cudaStream_t st) {
   double* u = b->vbuf[4].p;
   double* t = b->vbuf[5].p;
+  if (spec_ok(b, c)) {
+    if (c.method == SMPM_DBJ) {
+      spec_SMinv(b, true, vin, t, nullptr, act, st);
+      op_P(b, t, wout, c.fused, act, st);
+      return c.fused ? 1 : 2;
+    }
+    spec_SMinv(b, c.method == SMPM_BJ, vin, wout, nullptr, act, st);
+    return 1;
+  }
   switch (c.method) {
     case SMPM_SCHUR:
       op_S(b, vin, wout, act, st);
@@ -1022,7 +1138,12 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
   const bool fuse_into_cgs = c.method == SMPM_DBJ && c.fused && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= V2_MAXCOL;
   double* cbuf = b->dcoarse.p + static_cast<size_t>(b->nsys) * b->d;
   const double* tdefl = nullptr;
-  if (fuse_into_cgs) {
+  if (fuse_into_cgs && spec_ok(b, c)) {
+    // spectral: t = S M^{-1} v and c = C^{-1} Z^T t from the per-mode pass
+    double* t = b->vbuf[5].p;
+    spec_SMinv(b, true, vin, t, cbuf, lv, st);
+    tdefl = t;
+  } else if (fuse_into_cgs) {
     double* u = b->vbuf[4].p;
     double* t = b->vbuf[5].p;
     op_BJ(b, vin, u, lv, st);
@@ -1204,6 +1325,146 @@ void arnoldi_cluster(smpm_batch* b, const SolveCfg& c, const int* alist, const i
   }
 }
 
+// Runs the remaining Arnoldi steps of the current cycle of the (few) live
+// systems in one cooperative, grid-persistent launch (grid.cuh).
+// grid of the tail solver: as many CTAs (multiple of the cluster size) as
+// can be co-resident, up to SMPM_GRID_PER_SM (default 2) per SM
+int grid_blocks(smpm_batch* b) {
+  if (b->gt_blocks) return b->gt_blocks;
+  const size_t smem = GT_SMEM + sizeof(double) * (3 * GT_MAXCOL + 2 * static_cast<size_t>(b->d));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = GT_CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(G2_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  CUDA_CHECK(cudaFuncSetAttribute(arnoldi_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  int per = 0;
+  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, arnoldi_grid_kernel, G2_THREADS, smem));
+  int cap = 2;
+  if (const char* e = std::getenv("SMPM_GRID_PER_SM")) cap = std::max(1, std::atoi(e));
+  const int want = b->ctx->num_sms * std::max(1, std::min(per, cap));
+  // every CTA must be resident: bound by the cluster occupancy calculator
+  cfg.gridDim = dim3(want / GT_CL * GT_CL);
+  int ncl = 0;
+  CUDA_CHECK(cudaOccupancyMaxActiveClusters(&ncl, arnoldi_grid_kernel, &cfg));
+  if (ncl < 1) fail(SMPM_ECUDA, "grid tail kernel cannot be resident");
+  b->gt_blocks = std::min(want / GT_CL, ncl) * GT_CL;
+  return b->gt_blocks;
+}
+
+void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int* acount, cudaStream_t st) {
+  ProfScope ps(b, 6, st);  // class 6: grid-persistent tail
+  GmState_& G = b->G;
+  const size_t smem = GT_SMEM + sizeof(double) * (3 * GT_MAXCOL + 2 * static_cast<size_t>(b->d));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = GT_CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cfg.blockDim = dim3(G2_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  grid_blocks(b);
+  const int nb = b->gt_blocks;
+  const size_t stride = static_cast<size_t>(G.m + 2);
+  b->dgtpart.alloc(std::max(b->dgtpart.n, 3 * static_cast<size_t>(nb / GT_CL) * stride));
+  b->dgtzsum.alloc(std::max(b->dgtzsum.n, static_cast<size_t>(GT_MAXSYS) * b->d));
+  GridArgs A{};
+  const bool spec = spec_ok(b, c) && b->pc[4].v2 && b->pc[5].v2;
+  for (int i = 0; i < (spec ? 6 : 4); ++i) {
+    const Plan& p = b->pc[i];
+    A.a_stride[i] = p.shared_a ? 0 : b->mstride;
+    A.jobs[i] = p.djobs.p;
+    A.tiles[i] = p.dtiles2.p;
+    A.ntiles[i] = p.ntiles;
+    A.ngemm[i] = p.ngemm;
+    A.gv[i] = p.dgv.p;
+    A.ngv[i] = p.ngv;
+  }
+  A.vin = b->vbuf[2].p;
+  A.w = b->vbuf[3].p;
+  A.u = b->vbuf[4].p;
+  A.t = b->vbuf[5].p;
+  A.tmp = b->vbuf[9].p;
+  A.V = b->dV.p;
+  A.part = b->dgtpart.p;
+  if (spec) {
+    A.spectral = 1;
+    A.sp = spec_params(b);
+    A.sp.nseg = (b->nbf + (b->single ? 1 : 0) + GT_SEGB - 1) / GT_SEGB;
+    A.vh = b->dvh.p;
+    A.th = b->dth.p;
+    b->dgtzp.alloc(std::max(b->dgtzp.n, static_cast<size_t>(GT_MAXSYS) * A.sp.nmc * b->d));
+    A.zp = b->dgtzp.p;
+  }
+  A.zsum = b->dgtzsum.p;
+  A.bar = b->dgbar.p;
+  A.alist = alist;
+  A.acount = acount;
+  A.method = c.method;
+  A.G = G;
+  A.P = deflate_params(b, nullptr);
+  const char* tpath = std::getenv("SMPM_GT_TRACE");
+  DevArray<unsigned long long> dtr;
+  if (tpath) {
+    dtr.alloc(64 * 16);
+    CUDA_CHECK(cudaMemsetAsync(dtr.p, 0, dtr.n * sizeof(unsigned long long), st));
+    A.trace = dtr.p;
+  }
+  const char* t2path = std::getenv("SMPM_GT_TRACE2");
+  DevArray<unsigned long long> dtr2;
+  if (t2path) {
+    dtr2.alloc(static_cast<size_t>(16) * nb * 8);
+    CUDA_CHECK(cudaMemsetAsync(dtr2.p, 0, dtr2.n * sizeof(unsigned long long), st));
+    A.trace2 = dtr2.p;
+  }
+  CUDA_CHECK(cudaMemsetAsync(b->dgbar.p, 0, sizeof(unsigned), st));
+  cfg.gridDim = dim3(nb);
+  cfg.numAttrs = b->gt_nocoop ? 1 : 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, arnoldi_grid_kernel, A);
+  if (e != cudaSuccess && !b->gt_nocoop) {
+    // cooperative cluster launch rejected: the grid is already bounded by
+    // the cluster occupancy of an otherwise idle stream, launch it plainly
+    (void)cudaGetLastError();
+    b->gt_nocoop = true;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, arnoldi_grid_kernel, A);
+  }
+  CUDA_CHECK(e);
+  check_launch(b);
+  if (tpath) {
+    std::vector<unsigned long long> h(dtr.n);
+    CUDA_CHECK(cudaMemcpyAsync(h.data(), dtr.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (FILE* f = std::fopen(tpath, "ab")) {
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      std::fclose(f);
+    }
+  }
+  if (t2path) {
+    std::vector<unsigned long long> h(dtr2.n);
+    CUDA_CHECK(cudaMemcpyAsync(h.data(), dtr2.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (FILE* f = std::fopen(t2path, "ab")) {
+      const unsigned long long hdr = static_cast<unsigned long long>(nb);
+      std::fwrite(&hdr, sizeof(hdr), 1, f);
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      std::fclose(f);
+    }
+  }
+}
+
 void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_report* reps, double* history,
            cudaStream_t st) {
   need_final(b);
@@ -1319,9 +1580,65 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     CUDA_CHECK(cudaMemcpyAsync(hcnt + 2 * slot, b->dcnt.p + 2 * slot, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaEventRecord(ev[slot], st));
   };
+  // few live systems: the rest of the cycle runs grid-persistent (grid.cuh)
+  const bool use_grid = b->grid_ok && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= GT_MAXCOL &&
+                        (c.method != SMPM_DBJ || c.fused) && std::getenv("SMPM_NO_GRID") == nullptr;
+  int grid_max = 32;
+  if (const char* e = std::getenv("SMPM_GRID_MAX")) grid_max = std::max(0, std::min(GT_MAXSYS, std::atoi(e)));
+  if (use_grid) grid_max = std::min(grid_max, grid_blocks(b) / GT_CL);  // one cluster per live system at least
+  auto restart = [&](int ncycv) {
+    // ---- restart (GMRES(m) extension): x += V y ; r = b - op(x) ; new cycle
+    select_state_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, GM_CYCLE, dsel);
+    check_launch(b);
+    compact_kernel<<<1, 1024, 0, st>>>(dsel, nullptr, ns, alist2, acount2, nullptr);
+    check_launch(b);
+    Live lr;
+    lr.alist = alist2;
+    lr.acount = acount2;
+    lr.nslots = ncycv;
+    lr.active = dsel;
+    gm_backsolve_kernel<<<ns, 32, 0, st>>>(G, dsel);
+    check_launch(b);
+    gm_combine_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, x, dsel, 1);
+    check_launch(b);
+    apply_op(b, c, x, r, lr, st);
+    ++op_applies;
+    axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, dsel, nullptr, 1.0, rhs, -1.0, r);
+    check_launch(b);
+    batched_dot(b, r, r, nr2, dsel, st);
+    gm_start_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G, nr2, nb2, c.tol, 0, G.state);
+    check_launch(b);
+    gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, r, vin);
+    check_launch(b);
+    compact_kernel<<<1, 1024, 0, st>>>(G.active, nullptr, ns, alist, acount, nullptr);
+    check_launch(b);
+  };
   int cur = 0;
   if (!use_cluster) issue(cur);
   for (; !use_cluster;) {
+    // invariant here: exactly one step is in flight, in slot `cur`
+    if (use_grid && bound <= grid_max) {
+      CUDA_CHECK(cudaEventSynchronize(ev[cur]));
+      int nrun = hcnt[2 * cur], ncyc = hcnt[2 * cur + 1];
+      if (nrun > 0) {
+        arnoldi_grid(b, c, alist, acount, st);
+        ++steps;
+        compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->dcnt.p + 2 * cur);
+        check_launch(b);
+        CUDA_CHECK(cudaMemcpyAsync(hcnt + 2 * cur, b->dcnt.p + 2 * cur, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        nrun = hcnt[2 * cur];
+        ncyc = hcnt[2 * cur + 1];
+        if (nrun > 0) fail(SMPM_ERUNTIME, "grid tail launch returned with running systems");
+      }
+      if (ncyc > 0) {
+        restart(ncyc);
+        bound = ncyc;
+        issue(cur);
+        continue;
+      }
+      break;
+    }
     const bool more = steps < mtot + 1;
     if (more) issue(cur ^ 1);
     CUDA_CHECK(cudaEventSynchronize(ev[cur]));
@@ -1338,31 +1655,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       continue;
     }
     if (ncyc2 > 0) {
-      // ---- restart (GMRES(m) extension): x += V y ; r = b - op(x) ; new cycle
-      select_state_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, GM_CYCLE, dsel);
-      check_launch(b);
-      compact_kernel<<<1, 1024, 0, st>>>(dsel, nullptr, ns, alist2, acount2, nullptr);
-      check_launch(b);
-      Live lr;
-      lr.alist = alist2;
-      lr.acount = acount2;
-      lr.nslots = ncyc2;
-      lr.active = dsel;
-      gm_backsolve_kernel<<<ns, 32, 0, st>>>(G, dsel);
-      check_launch(b);
-      gm_combine_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, x, dsel, 1);
-      check_launch(b);
-      apply_op(b, c, x, r, lr, st);
-      ++op_applies;
-      axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, dsel, nullptr, 1.0, rhs, -1.0, r);
-      check_launch(b);
-      batched_dot(b, r, r, nr2, dsel, st);
-      gm_start_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G, nr2, nb2, c.tol, 0, G.state);
-      check_launch(b);
-      gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, r, vin);
-      check_launch(b);
-      compact_kernel<<<1, 1024, 0, st>>>(G.active, nullptr, ns, alist, acount, nullptr);
-      check_launch(b);
+      restart(ncyc2);
       bound = ncyc2;
       issue(cur);
       continue;
@@ -1578,6 +1871,23 @@ int smpm_batch_set_couplings(smpm_batch* b, int sys, const double* G_W, const do
     if (G_I) std::memcpy(dst + ww, G_I, sizeof(double) * 4 * ww);
     std::memcpy(dst + 5 * ww, G_E, sizeof(double) * ww);
     b->have[sys] = 1;
+  });
+}
+
+int smpm_batch_set_spectral(smpm_batch* b, int npairs, const double* T, const double* T_inv, const double* gamma) {
+  return guard([&] {
+    if (!b) fail(SMPM_EINVAL, "null batch");
+    if (b->finalized) fail(SMPM_EINVAL, "batch already finalized");
+    if (!T || !T_inv || !gamma) fail(SMPM_EINVAL, "null spectral factor");
+    if (npairs < 0 || 2 * npairs > b->w) fail(SMPM_EINVAL, "bad number of complex pairs");
+    const size_t ww = static_cast<size_t>(b->w) * b->w;
+    b->sp_npairs = npairs;
+    b->sp_nmode = b->w - npairs;
+    b->hT.assign(T, T + ww);
+    b->hTi.assign(T_inv, T_inv + ww);
+    const size_t ng = static_cast<size_t>(b->nsys) * SK_NUM * b->sp_nmode * 2;
+    b->hgam.assign(gamma, gamma + ng);
+    b->spectral = true;
   });
 }
 

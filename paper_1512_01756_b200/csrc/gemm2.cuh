@@ -54,7 +54,7 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 __device__ __forceinline__ void store_out(const GemmJob& jb, const BufTable& bufs, int m, int n, double acc) {
   double* out = bufs.p[jb.out.buf];
   double v = jb.alpha * acc;
-  if (jb.add.buf != BUF_NONE) v = fma(jb.beta, bufs.p[jb.add.buf][jb.add.at(m, n)], v);
+  if (jb.add.buf != BUF_NONE) v = fma(jb.beta, __ldcg(bufs.p[jb.add.buf] + jb.add.at(m, n)), v);
   out[jb.out.at(m, n)] = v;
 }
 
@@ -86,64 +86,80 @@ __device__ __forceinline__ void shift_job(GemmJob& jb, const SysMap& sm, int s) 
   jb.sys = s;
 }
 
-// One output tile of one (system-shifted) job, computed by the calling CTA's
-// first G2_THREADS threads with G2_SMEM bytes of shared memory at `smem`.
-// Shared by the per-stage launches and the cluster-persistent solver.
-__device__ __forceinline__ void g2_run_tile(const GemmJob& jb, const Tile2& tile, const BufTable& bufs,
-                                            double* __restrict__ ws, double* smem) {
-  auto As = reinterpret_cast<double(*)[G2_BK][G2_BM + G2_APAD]>(smem);
-  auto Bs = reinterpret_cast<double(*)[G2_BN][G2_BK + G2_BPAD]>(smem + G2_STAGES * G2_BK * (G2_BM + G2_APAD));
+// GEMV tile (N == 1): 16 rows x K, 8 interleaved k-groups, UNR independent
+// loads in flight per thread per round.
+template <int UNR = 8>
+__device__ __forceinline__ void g2_gemv_tile(const GemmJob& jb, const Tile2& tile, const BufTable& bufs) {
   const int t = threadIdx.x;
-  __syncthreads();  // shared memory may still be read by this CTA's previous tile
-  const int lane = t & 31, warp = t >> 5;
-
-  if (tile.ks < 0) {
-    // ---------------- GEMV tile: 16 rows x K, 8 interleaved k-groups ----------
-    const int r = t % GV_ROWS, kg = t / GV_ROWS;
-    const int m = tile.m0 + r;
-    const double* __restrict__ x = bufs.p[jb.b.buf] + jb.b.off;
-    // 8 independent loads in flight per thread per round
-    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    if (m < jb.M) {
-      const double* __restrict__ a = jb.A + m;
-      const long long lda = jb.lda;
-      int k = kg;
-      for (; k + 7 * GV_KG < jb.K; k += 8 * GV_KG) {
-        double av[8], xv[8];
+  const int r = t % GV_ROWS, kg = t / GV_ROWS;
+  const int m = tile.m0 + r;
+  const double* x = bufs.p[jb.b.buf] + jb.b.off;
+  double acc[UNR];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          av[u] = __ldg(a + static_cast<long long>(k + u * GV_KG) * lda);
-          xv[u] = x[k + u * GV_KG];
-        }
+  for (int u = 0; u < UNR; ++u) acc[u] = 0.0;
+  if (m < jb.M) {
+    const double* __restrict__ a = jb.A + m;
+    const long long lda = jb.lda;
+    int k = kg;
+    for (; k + (UNR - 1) * GV_KG < jb.K; k += UNR * GV_KG) {
+      double av[UNR], xv[UNR];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc[u] = fma(av[u], xv[u], acc[u]);
+      for (int u = 0; u < UNR; ++u) {
+        av[u] = __ldg(a + static_cast<long long>(k + u * GV_KG) * lda);
+        xv[u] = __ldcg(x + k + u * GV_KG);
       }
-      for (; k < jb.K; k += GV_KG) acc[0] = fma(__ldg(a + static_cast<long long>(k) * lda), x[k], acc[0]);
-    }
-    __shared__ double red[GV_KG][GV_ROWS];
-    red[kg][r] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-    __syncthreads();
-    if (kg == 0 && m < jb.M) {
-      double s = 0.0;
 #pragma unroll
-      for (int q = 0; q < GV_KG; ++q) s += red[q][r];
-      store_out(jb, bufs, m, 0, s);
+      for (int u = 0; u < UNR; ++u) acc[u] = fma(av[u], xv[u], acc[u]);
     }
-    return;
+    // remainder: still independent loads (predicated), same accumulators
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int kk = k + u * GV_KG;
+      if (kk < jb.K) acc[u] = fma(__ldg(a + static_cast<long long>(kk) * lda), __ldcg(x + kk), acc[u]);
+    }
   }
+  __shared__ double red[GV_KG][GV_ROWS];
+  double v = 0.0;
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) v += acc[u];
+  red[kg][r] = v;
+  __syncthreads();
+  if (kg == 0 && m < jb.M) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < GV_KG; ++q) s += red[q][r];
+    store_out(jb, bufs, m, 0, s);
+  }
+}
 
-  // ---------------- GEMM tile (DMMA m8n8k4) ----------------------------------
-  const int M = jb.M, N = jb.N, K = jb.K;
-  const int m0 = tile.m0, n0 = tile.n0;
-  int kb = 0, ke = K;
+// K range [kb, ke) of split `ks` of a job
+__device__ __forceinline__ void g2_krange(const GemmJob& jb, int ks, int& kb, int& ke) {
+  kb = 0;
+  ke = jb.K;
   if (jb.splitk > 1) {
-    const int kc = ((K + jb.splitk * G2_BK - 1) / (jb.splitk * G2_BK)) * G2_BK;
-    kb = tile.ks * kc;
-    ke = min(K, kb + kc);
+    const int kc = ((jb.K + jb.splitk * G2_BK - 1) / (jb.splitk * G2_BK)) * G2_BK;
+    kb = ks * kc;
+    ke = min(jb.K, kb + kc);
   }
+}
+
+// GEMM tile main loop (DMMA m8n8k4) over this split's K range; STAGES-deep
+// cp.async ring in `smem`.  acc(i, j, e) holds row wm*32+i*8+lane/4 and
+// column wn*16+j*8+(lane%4)*2+e of the 64x32 tile (warp = 2*wm + wn).
+template <int STAGES>
+__device__ __forceinline__ void g2_mainloop(const GemmJob& jb, const Tile2& tile, const BufTable& bufs, double* smem,
+                                            double (&acc)[4][2][2]) {
+  auto As = reinterpret_cast<double(*)[G2_BK][G2_BM + G2_APAD]>(smem);
+  auto Bs = reinterpret_cast<double(*)[G2_BN][G2_BK + G2_BPAD]>(smem + STAGES * G2_BK * (G2_BM + G2_APAD));
+  const int t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
+  const int M = jb.M, N = jb.N;
+  const int m0 = tile.m0, n0 = tile.n0;
+  int kb, ke;
+  g2_krange(jb, tile.ks, kb, ke);
   const double* __restrict__ A = jb.A;
   const long long lda = jb.lda;
-  const double* __restrict__ B = bufs.p[jb.b.buf] + jb.b.off;
+  const double* B = bufs.p[jb.b.buf] + jb.b.off;
   const long long ldb = jb.b.cs;
 
   auto load_stage = [&](int s, int k0) {
@@ -169,7 +185,6 @@ __device__ __forceinline__ void g2_run_tile(const GemmJob& jb, const Tile2& tile
     }
   };
 
-  double acc[4][2][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -178,17 +193,17 @@ __device__ __forceinline__ void g2_run_tile(const GemmJob& jb, const Tile2& tile
   const int wm = warp >> 1, wn = warp & 1;
   const int nk = (ke - kb + G2_BK - 1) / G2_BK;
 #pragma unroll
-  for (int s = 0; s < G2_STAGES - 1; ++s) {
+  for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk) load_stage(s, kb + s * G2_BK);
     cp_async_commit();
   }
   for (int it = 0; it < nk; ++it) {
-    cp_async_wait<G2_STAGES - 2>();
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
-    const int s = it % G2_STAGES;
-    // prefetch the stage G2_STAGES-1 ahead into the slot freed last iteration
-    const int nx = it + G2_STAGES - 1;
-    if (nx < nk) load_stage(nx % G2_STAGES, kb + nx * G2_BK);
+    const int s = it % STAGES;
+    // prefetch the stage STAGES-1 ahead into the slot freed last iteration
+    const int nx = it + STAGES - 1;
+    if (nx < nk) load_stage(nx % STAGES, kb + nx * G2_BK);
     cp_async_commit();
 #pragma unroll
     for (int kq = 0; kq < G2_BK / 4; ++kq) {
@@ -205,34 +220,60 @@ __device__ __forceinline__ void g2_run_tile(const GemmJob& jb, const Tile2& tile
     }
   }
   cp_async_wait<0>();
+}
 
-  // accumulator (i, j, e) holds row wm*32+i*8+lane/4, col wn*16+j*8+(lane%4)*2+e
-  if (jb.splitk > 1) {
-    const int ntn = (N + G2_BN - 1) / G2_BN;
-    const long long slot =
-        static_cast<long long>(jb.ws_off) + (static_cast<long long>(m0 / G2_BM) * ntn + n0 / G2_BN) * jb.splitk + tile.ks;
-    double* w = ws + slot * (G2_BM * G2_BN);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = wm * 32 + i * 8 + (lane >> 2), c = wn * 16 + j * 8 + (lane & 3) * 2 + e;
-          w[r * G2_BN + c] = acc[i][j][e];
-        }
-    return;
-  }
+// workspace slot of split `ks` of a tile (64x32 doubles each)
+__device__ __forceinline__ long long g2_ws_slot(const GemmJob& jb, const Tile2& tile, int ks) {
+  const int ntn = (jb.N + G2_BN - 1) / G2_BN;
+  return static_cast<long long>(jb.ws_off) + (static_cast<long long>(tile.m0 / G2_BM) * ntn + tile.n0 / G2_BN) * jb.splitk +
+         ks;
+}
+
+__device__ __forceinline__ void g2_store_ws(const GemmJob& jb, const Tile2& tile, double* ws, const double (&acc)[4][2][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wm = warp >> 1, wn = warp & 1;
+  double* w = ws + g2_ws_slot(jb, tile, tile.ks) * (G2_BM * G2_BN);
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
-        const int n = n0 + wn * 16 + j * 8 + (lane & 3) * 2 + e;
-        if (m < M && n < N) store_out(jb, bufs, m, n, acc[i][j][e]);
+        const int r = wm * 32 + i * 8 + (lane >> 2), c = wn * 16 + j * 8 + (lane & 3) * 2 + e;
+        w[r * G2_BN + c] = acc[i][j][e];
       }
+}
+
+__device__ __forceinline__ void g2_store_tile(const GemmJob& jb, const Tile2& tile, const BufTable& bufs,
+                                              const double (&acc)[4][2][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wm = warp >> 1, wn = warp & 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m = tile.m0 + wm * 32 + i * 8 + (lane >> 2);
+        const int n = tile.n0 + wn * 16 + j * 8 + (lane & 3) * 2 + e;
+        if (m < jb.M && n < jb.N) store_out(jb, bufs, m, n, acc[i][j][e]);
+      }
+}
+
+// One output tile of one (system-shifted) job, computed by the calling CTA's
+// first G2_THREADS threads with G2_SMEM bytes of shared memory at `smem`.
+// Shared by the per-stage launches and the cluster-persistent solver.
+__device__ __forceinline__ void g2_run_tile(const GemmJob& jb, const Tile2& tile, const BufTable& bufs,
+                                            double* __restrict__ ws, double* smem) {
+  __syncthreads();  // shared memory may still be read by this CTA's previous tile
+  if (tile.ks < 0) {
+    g2_gemv_tile(jb, tile, bufs);
+    return;
+  }
+  double acc[4][2][2];
+  g2_mainloop<G2_STAGES>(jb, tile, bufs, smem, acc);
+  if (jb.splitk > 1)
+    g2_store_ws(jb, tile, ws, acc);
+  else
+    g2_store_tile(jb, tile, bufs, acc);
 }
 
 __global__ void __launch_bounds__(G2_THREADS, 4)

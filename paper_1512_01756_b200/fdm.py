@@ -203,6 +203,40 @@ class StripFDM:
         den = lx[None, :, None] + self.tlz[None, None, :] - mu[:, None, None]  # (M, p, q)
         return -self.tau * (a[None, :, None] / den).sum(dim=1)
 
+    def real_basis(self):
+        """Real eigenbasis T of the z factor for the spectral operator form:
+        complex-conjugate pairs first (columns Re v, Im v of the member with
+        Im(lambda) > 0), then the real modes.  Returns (npairs, T, T^{-1},
+        representative eigen-indices)."""
+        if getattr(self, "_rb", None) is None:
+            lz, Vz = self.lz, np.asarray(self.Vz)
+            tol = 1e-9 * np.abs(lz).max()
+            pairs = [q for q in range(len(lz)) if lz[q].imag > tol]
+            reals = [q for q in range(len(lz)) if abs(lz[q].imag) <= tol]
+            if 2 * len(pairs) + len(reals) != len(lz):
+                raise RuntimeError("z eigenvalues are not in conjugate pairs")
+            cols = []
+            for q in pairs:
+                cols += [Vz[:, q].real, Vz[:, q].imag]
+            for q in reals:
+                cols.append(Vz[:, q].real)
+            T = np.ascontiguousarray(np.stack(cols, 1))
+            self._rb = (len(pairs), T, np.linalg.inv(T), pairs + reals)
+        return self._rb
+
+    def spectral(self, mus):
+        """(npairs, T, T^{-1}, gamma) for smpm_batch_set_spectral: gamma is
+        (len(mus), 6, nmode) complex in kind order W_EE, I_WW, I_WE, I_EW,
+        I_EE, E_WW at the representative eigen-indices (G = T diag T^{-1})."""
+        npairs, T, Ti, rep = self.real_basis()
+        mus = np.atleast_1d(np.asarray(mus, dtype=np.float64))
+        out = np.empty((len(mus), 6, len(rep)), dtype=np.complex128)
+        kinds = (((False, True), "EE"), ((True, True), "WW"), ((True, True), "WE"), ((True, True), "EW"),
+                 ((True, True), "EE"), ((True, False), "WW"))
+        for i, (key, XY) in enumerate(kinds):
+            out[:, i, :] = self.gamma(key, XY, mus).cpu().numpy()[:, rep]
+        return npairs, T, Ti, out
+
     def _block(self, gam):
         # Vz diag(gam) Vz^{-1} for a batch of diagonals -> real (M, w, w)
         t = self.torch

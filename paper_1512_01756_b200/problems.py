@@ -159,8 +159,9 @@ def build_problem(cfg: Config, modes=None, device=None) -> ProblemSet:
     return ProblemSet(cfg, list(modes), mus, GW, GI, GE, u_S, u_L, np.array(bs), F)
 
 
-def load_batch(ctx, ps: ProblemSet):
-    """SchurBatch with the couplings / null vector of a ProblemSet."""
+def load_batch(ctx, ps: ProblemSet, spectral: bool = True):
+    """SchurBatch with the couplings / null vector of a ProblemSet (and, by
+    default, the spectral factors of the couplings)."""
     from .schur import SchurBatch
 
     cfg = ps.cfg
@@ -169,4 +170,7 @@ def load_batch(ctx, ps: ProblemSet):
         b.set_couplings(i, ps.GW[i], ps.GI[i] if cfg.m_x > 2 else None, ps.GE[i])
         if ps.mus[i] == 0.0:
             b.set_nullspace(i, ps.u_S)
+    if spectral:
+        npairs, T, Ti, gam = ps.fdm.spectral(ps.mus)
+        b.set_spectral(npairs, T, Ti, gam)
     return b.finalize()

@@ -103,6 +103,20 @@ class SchurBatch:
                 raise SmpmError(1, "G_I must be 2w x 2w")
         check(lib().smpm_batch_set_couplings(self.h, sys, _hptr(gw), _hptr(gi) if gi is not None else None, _hptr(ge)))
 
+    def set_spectral(self, npairs: int, T, T_inv, gamma):
+        """Spectral factors of the couplings (smpm_batch_set_spectral): T, T_inv
+        w x w; gamma (nsys, 6, w - npairs) complex."""
+        w = self.w
+        t = np.asfortranarray(T, dtype=np.float64)
+        ti = np.asfortranarray(T_inv, dtype=np.float64)
+        g = np.ascontiguousarray(np.asarray(gamma, dtype=np.complex128))
+        if t.shape != (w, w) or ti.shape != (w, w):
+            raise SmpmError(1, "T/T_inv must be w x w")
+        if g.shape != (self.nsys, 6, w - npairs):
+            raise SmpmError(1, "gamma must be (nsys, 6, w - npairs)")
+        gv = g.view(np.float64)
+        check(lib().smpm_batch_set_spectral(self.h, int(npairs), _hptr(t), _hptr(ti), _hptr(gv)))
+
     def set_interface_blocks(self, sys: int, blocks):
         """blocks: list of (entries[rows x 2w], [(start, len), ...]) in the
         reference's InterfaceBlock layout (proj/include/smpm/schur.hpp:32-36)."""
