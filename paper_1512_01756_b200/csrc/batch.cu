@@ -262,7 +262,7 @@ struct smpm_batch {
   bool spectral = false;
   int sp_npairs = 0, sp_nmode = 0;
   std::vector<double> hT, hTi, hgam;
-  DevArray<double> dT, dTi, domega, dgam, dzpart, dvh, dth;
+  DevArray<double> dT, dTi, domega, dgam, dzpart, dvh, dth, dkinv;
   Plan pF, pB;
   Plan pc[6];          // unsplit per-system templates (BJ1, BJ2, BJ3, S; spectral F, B) for the persistent solvers
   bool cluster_ok = false;
@@ -877,6 +877,8 @@ void build_coarse(smpm_batch* b) {
   b->dsingular.upload(b->hsing, st);
 }
 
+SpecParams spec_params(const smpm_batch* b);
+
 void finalize(smpm_batch* b) {
   if (b->finalized) return;
   for (int s = 0; s < b->nsys; ++s)
@@ -914,13 +916,20 @@ void finalize(smpm_batch* b) {
     for (int e = 0; e < w; ++e)
       for (int r = 0; r < w; ++r) om[e] += b->hT[static_cast<size_t>(e) * w + r];
     b->domega.upload(om, st);
-    const int nmc = (b->sp_nmode + SP_THREADS - 1) / SP_THREADS;
+    const int nmc = (b->sp_nmode + SP_MODES - 1) / SP_MODES;
     b->dzpart.alloc(static_cast<size_t>(b->nsys) * nmc * d);
+    b->dkinv.alloc(static_cast<size_t>(b->nsys) * 20 * b->sp_nmode * 2);
     b->dvh.alloc(static_cast<size_t>(b->nsys) * b->k);
     b->dth.alloc(static_cast<size_t>(b->nsys) * b->k);
   }
   build_plans(b);
   if (b->spectral && !(b->pF.v2 && b->pB.v2)) b->spectral = false;  // odd w: dense operator path
+  if (b->spectral) {
+    const SpecParams sp = spec_params(b);
+    const long long n = 1LL * b->nsys * b->sp_nmode;
+    spec_setup_kernel<<<static_cast<int>((n + 127) / 128), 128, 0, st>>>(sp, reinterpret_cast<double2*>(b->dkinv.p), b->nsys);
+    check_launch(b);
+  }
   build_bj_inverses(b);
   build_coarse(b);
   for (auto& v : b->vbuf) v.alloc(static_cast<size_t>(b->nsys) * b->k);
@@ -1054,8 +1063,10 @@ SpecParams spec_params(const smpm_batch* b) {
   sp.nmode = b->sp_nmode;
   sp.k = b->k;
   sp.gam = reinterpret_cast<const double2*>(b->dgam.p);
+  sp.kinv = reinterpret_cast<const double2*>(b->dkinv.p);
   sp.omega = b->domega.p;
-  sp.nmc = (b->sp_nmode + SP_THREADS - 1) / SP_THREADS;
+  sp.nmc = (b->sp_nmode + SP_MODES - 1) / SP_MODES;
+  sp.segb = SP_SEGB;
   sp.nseg = (b->nbf + (b->single ? 1 : 0) + SP_SEGB - 1) / SP_SEGB;
   return sp;
 }
@@ -1068,7 +1079,7 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
   DeflateParams P = deflate_params(b, lv.active);
   P.alist = lv.alist;
   P.acount = lv.acount;
-  const dim3 grid(sp.nmc * sp.nseg, lv.nslots);
+  const dim3 grid(sp.nmc * ((sp.nseg + SP_WARPS - 1) / SP_WARPS), lv.nslots);
   const size_t shm = cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0;
   double* zp = cout ? b->dzpart.p : nullptr;
   if (bj)
@@ -1402,7 +1413,9 @@ void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
   if (spec) {
     A.spectral = 1;
     A.sp = spec_params(b);
-    A.sp.nseg = (b->nbf + (b->single ? 1 : 0) + GT_SEGB - 1) / GT_SEGB;
+    // latency-bound tail: one block per warp item (more warps, halo recomputed)
+    A.sp.segb = 1;
+    A.sp.nseg = b->nbf + (b->single ? 1 : 0);
     A.vh = b->dvh.p;
     A.th = b->dth.p;
     b->dgtzp.alloc(std::max(b->dgtzp.n, static_cast<size_t>(GT_MAXSYS) * A.sp.nmc * b->d));

@@ -40,7 +40,6 @@ constexpr int GT_MAXSYS = 32;   // live systems one tail launch may carry
 constexpr int GT_MAXCOL = 128;  // cycle length + 2
 constexpr int GT_CL = 8;        // CTAs per cluster (= K splits of a tail tile)
 constexpr int GT_GVR = 32;      // rows of a cluster GEMV item
-constexpr int GT_SEGB = 2;      // block-Jacobi blocks per spectral work item
 constexpr int GT_STAGES = 4;    // cp.async ring depth of the operator tiles
 constexpr int GT_SMEM =
     GT_STAGES * (G2_BK * (G2_BM + G2_APAD) + G2_BN * (G2_BK + G2_BPAD)) * static_cast<int>(sizeof(double));
@@ -437,44 +436,20 @@ __device__ __forceinline__ void gt_group_sum(const double* part, int stride, int
   __syncthreads();
 }
 
-// spectral per-mode pass for the live systems: items (slot, mode chunk,
-// block segment) over the grid; th = S^ M^^{-1} vh (or S^ vh) and the Z^T
-// partial sums of each (slot, mode chunk) -> zp (fixed-order CTA reductions)
+// spectral per-mode pass for the live systems: one warp per (slot, 32-mode
+// chunk, block segment) over the grid; th = S^ M^^{-1} vh (or S^ vh) and the
+// warp-reduced Z^T partials of each (slot, mode chunk) -> zp
 __device__ __forceinline__ void gt_spec(const GridArgs& a, const int* sl, int L, bool bj, bool zt_on) {
-  static_assert(SP_THREADS == G2_THREADS, "one mode per thread");
-  __shared__ double zs[G2_THREADS / 32][2 * GT_SEGB];
   const SpecParams& sp = a.sp;
   const int per = sp.nmc * sp.nseg, items = L * per;
-  const int nb = spec_nblocks(sp), lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+  const int nw = blockDim.x >> 5, gw = blockIdx.x * nw + (threadIdx.x >> 5), tw = gridDim.x * nw;
+  for (int it = gw; it < items; it += tw) {
     const int q = it / per, r = it % per, mc = r / sp.nseg, sg = r % sp.nseg;
-    const int s = sl[q], m = mc * G2_THREADS + threadIdx.x;
-    const int b0 = sg * GT_SEGB, b1 = min(nb, b0 + GT_SEGB);
-    double zt[2 * GT_SEGB];
-#pragma unroll
-    for (int i = 0; i < 2 * GT_SEGB; ++i) zt[i] = 0.0;
-    if (m < sp.nmode) {
-      const ModeRef mr = mode_ref(sp, s, m);
-      const ModeGamma g = mode_gamma(sp, s, m);
-      if (bj)
-        spec_mode_segment<true>(sp, mr, g, a.vh, a.th, b0, b1, zt_on ? zt : nullptr);
-      else
-        spec_mode_segment<false>(sp, mr, g, a.vh, a.th, b0, b1, zt_on ? zt : nullptr);
-    }
-    if (!zt_on) continue;
-    __syncthreads();  // zs may still be read for the previous item
-#pragma unroll
-    for (int i = 0; i < 2 * GT_SEGB; ++i) {
-      const double v = warp_sum(zt[i]);
-      if (lane == 0) zs[warp][i] = v;
-    }
-    __syncthreads();
-    const int i0 = 2 * b0, i1 = min(sp.d, 2 * b1);
-    for (int i = threadIdx.x; i < i1 - i0; i += blockDim.x) {
-      double v = 0.0;
-      for (int w4 = 0; w4 < G2_THREADS / 32; ++w4) v += zs[w4][i];
-      a.zp[(static_cast<long long>(q) * sp.nmc + mc) * sp.d + i0 + i] = v;
-    }
+    double* zo = zt_on ? a.zp + (static_cast<long long>(q) * sp.nmc + mc) * sp.d : nullptr;
+    if (bj)
+      spec_warp_item<true>(sp, sl[q], mc, sg, a.vh, a.th, zo);
+    else
+      spec_warp_item<false>(sp, sl[q], mc, sg, a.vh, a.th, zo);
   }
 }
 

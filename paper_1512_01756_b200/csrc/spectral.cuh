@@ -34,12 +34,15 @@ struct SpecParams {
   int npairs, nmode;           // complex-pair modes first, then real modes; nmode = w - npairs
   long long k;                 // 2 d w
   const double2* gam;          // nsys x SK_NUM x nmode
+  const double2* kinv;         // nsys x 5 x 4 x nmode: reduced block inverses (variants first|last<<1, 4 = single)
   const double* omega;         // w: column sums of T (Z^T weights)
-  int nmc, nseg;               // mode chunks, block segments (grid x = nmc * nseg)
+  int nmc, nseg, segb;         // 32-mode chunks, block segments of segb (<= SP_SEGB) blocks
 };
 
-constexpr int SP_THREADS = 128;  // modes per CTA
-constexpr int SP_SEGB = 4;       // block-Jacobi blocks per segment (8 interfaces)
+constexpr int SP_MODES = 32;               // modes per warp (one lane each)
+constexpr int SP_WARPS = 4;                // segments per CTA (one warp each)
+constexpr int SP_THREADS = 32 * SP_WARPS;
+constexpr int SP_SEGB = 4;                 // max block-Jacobi blocks per segment (8 interfaces)
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -99,35 +102,61 @@ __device__ __forceinline__ ModeGamma mode_gamma(const SpecParams& sp, int s, int
   return G;
 }
 
+// reduced-system inverses of one mode (setup): K = I - G' diag(ex, wx) with
+// G' = [[a, b], [c, e]]; variant v = first | last << 1 picks ex = W_EE | I_EE
+// and wx = E_WW | I_WW; variant 4 is the trailing single interface
+__global__ void spec_setup_kernel(SpecParams sp, double2* kinv, int nsys) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long long>(nsys) * sp.nmode) return;
+  const int s = static_cast<int>(idx / sp.nmode), m = static_cast<int>(idx % sp.nmode);
+  const double2* g = sp.gam + static_cast<long long>(s) * SK_NUM * sp.nmode + m;
+  const double2 wee = g[SK_W_EE * sp.nmode], ga = g[SK_I_WW * sp.nmode], gb = g[SK_I_WE * sp.nmode];
+  const double2 gc = g[SK_I_EW * sp.nmode], ge = g[SK_I_EE * sp.nmode], eww = g[SK_E_WW * sp.nmode];
+  const double2 one = make_double2(1.0, 0.0);
+  double2* out = kinv + static_cast<long long>(s) * 5 * 4 * sp.nmode + m;
+  for (int v = 0; v < 4; ++v) {
+    const double2 ex = (v & 1) ? wee : ge, wx = (v & 2) ? eww : ga;
+    const double2 k00 = csub(one, cmul(ga, ex)), k11 = csub(one, cmul(ge, wx));
+    const double2 k01 = cmul(gb, wx), k10 = cmul(gc, ex);  // K = [[k00, -k01], [-k10, k11]]
+    const double2 det = csub(cmul(k00, k11), cmul(k01, k10));
+    out[(v * 4 + 0) * sp.nmode] = cdiv(k11, det);
+    out[(v * 4 + 1) * sp.nmode] = cdiv(k01, det);
+    out[(v * 4 + 2) * sp.nmode] = cdiv(k10, det);
+    out[(v * 4 + 3) * sp.nmode] = cdiv(k00, det);
+  }
+  const double2 h = sp.d >= 2 ? ge : wee;
+  out[16 * sp.nmode] = cdiv(one, csub(one, cmul(eww, h)));
+  out[17 * sp.nmode] = out[18 * sp.nmode] = out[19 * sp.nmode] = make_double2(0.0, 0.0);
+}
+
 // x = M_blk^{-1} y for block blk of one mode (4 slots, or 2 for the trailing
 // single block); without BJ x = y
 template <bool BJ>
-__device__ __forceinline__ void spec_block_solve(const SpecParams& sp, const ModeGamma& g, int blk, const double2 (&y)[4],
-                                                 double2 (&x)[4]) {
+__device__ __forceinline__ void spec_block_solve(const SpecParams& sp, const ModeGamma& g, const double2* ki, int blk,
+                                                 const double2 (&y)[4], double2 (&x)[4]) {
   if (!BJ) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) x[j] = y[j];
     return;
   }
-  const double2 one = make_double2(1.0, 0.0);
+  const int nm = sp.nmode;
   if (blk == sp.nbf) {
     // trailing interface d-1 alone: y0 = x0 + G_E x1 ; y1 = Gee x0 + x1
     const double2 h = sp.d >= 2 ? g.e : g.wee;
-    x[0] = cdiv(csub(y[0], cmul(g.eww, y[1])), csub(one, cmul(g.eww, h)));
+    x[0] = cmul(csub(y[0], cmul(g.eww, y[1])), ki[16 * nm]);
     x[1] = csub(y[1], cmul(h, x[0]));
     x[2] = x[3] = make_double2(0.0, 0.0);
     return;
   }
   // y0 = x0 + a x1 + b x2 ; y1 = ex x0 + x1 ; y2 = x2 + wx x3 ; y3 = c x1 + e x2 + x3
-  const double2 ex = blk == 0 ? g.wee : g.e;
-  const double2 wx = 2 * blk + 2 <= sp.mx - 2 ? g.a : g.eww;
+  const bool first = blk == 0, last = 2 * blk + 2 > sp.mx - 2;
+  const double2 ex = first ? g.wee : g.e;
+  const double2 wx = last ? g.eww : g.a;
+  const double2* k = ki + ((first ? 1 : 0) | (last ? 2 : 0)) * 4 * nm;
   const double2 r0 = csub(csub(y[0], cmul(g.a, y[1])), cmul(g.b, y[2]));
   const double2 r3 = csub(csub(y[3], cmul(g.c, y[1])), cmul(g.e, y[2]));
-  const double2 k00 = csub(one, cmul(g.a, ex)), k11 = csub(one, cmul(g.e, wx));
-  const double2 k01 = cmul(g.b, wx), k10 = cmul(g.c, ex);  // K = [[k00, -k01], [-k10, k11]]
-  const double2 det = csub(cmul(k00, k11), cmul(k01, k10));
-  x[0] = cdiv(cfma(k01, r3, cmul(k11, r0)), det);
-  x[3] = cdiv(cfma(k10, r0, cmul(k00, r3)), det);
+  x[0] = cfma(k[nm], r3, cmul(k[0], r0));
+  x[3] = cfma(k[2 * nm], r0, cmul(k[3 * nm], r3));
   x[1] = csub(y[1], cmul(ex, x[0]));
   x[2] = csub(y[2], cmul(wx, x[3]));
 }
@@ -154,12 +183,13 @@ __device__ __forceinline__ int spec_bslots(const SpecParams& sp, int blk) { retu
 
 template <bool BJ>
 __device__ __forceinline__ void spec_load_solve(const SpecParams& sp, const ModeRef& mr, const ModeGamma& g,
-                                                const double* vh, int blk, double2 (&x)[4]) {
+                                                const double2* ki, const double* __restrict__ vh, int blk,
+                                                double2 (&x)[4]) {
   double2 y[4];
   const int ns = spec_bslots(sp, blk);
 #pragma unroll
   for (int j = 0; j < 4; ++j) y[j] = j < ns ? mr.ld(vh, 4 * blk + j) : make_double2(0.0, 0.0);
-  spec_block_solve<BJ>(sp, g, blk, y, x);
+  spec_block_solve<BJ>(sp, g, ki, blk, y, x);
 }
 
 // One mode, block-Jacobi blocks [b0, b1): th = S^ M^^{-1} vh (or S^ vh), and
@@ -167,13 +197,14 @@ __device__ __forceinline__ void spec_load_solve(const SpecParams& sp, const Mode
 // (zt indexed from interface 2*b0; nullptr: skipped)
 template <bool BJ>
 __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const ModeRef& mr, const ModeGamma& g,
-                                                  const double* vh, double* th, int b0, int b1, double* zt) {
+                                                  const double2* ki, const double* __restrict__ vh,
+                                                  double* __restrict__ th, int b0, int b1, double* zt) {
   const int nb = spec_nblocks(sp);
   double2 xp[4], xc[4], xn[4];
-  if (b0 > 0) spec_load_solve<BJ>(sp, mr, g, vh, b0 - 1, xp);
-  spec_load_solve<BJ>(sp, mr, g, vh, b0, xc);
+  if (b0 > 0) spec_load_solve<BJ>(sp, mr, g, ki, vh, b0 - 1, xp);
+  spec_load_solve<BJ>(sp, mr, g, ki, vh, b0, xc);
   for (int blk = b0; blk < b1; ++blk) {
-    if (blk + 1 < nb) spec_load_solve<BJ>(sp, mr, g, vh, blk + 1, xn);
+    if (blk + 1 < nb) spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xn);
     double2 t[4];
     spec_block_S(sp, g, blk, xc, xp[3], xn[0], t);
     const int ns = spec_bslots(sp, blk);
@@ -192,44 +223,49 @@ __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const Mo
   }
 }
 
-// th = T^-1-space operator of the live systems; with zpart, the last CTA of
-// each system also solves the coarse system for c = C^{-1} Z^T (T th) -> cout
+// One warp = one segment of 32 modes of one system: th for its blocks and,
+// with zout, the warp-reduced Z^T partials of its interfaces -> zout[i]
 template <bool BJ>
-__global__ void __launch_bounds__(SP_THREADS) spec_op_kernel(SpecParams sp, const double* vh, double* th,
-                                                             DeflateParams P, double* zpart, int* counter,
-                                                             double* cout) {
-  extern __shared__ double sm[];  // 2 d doubles (coarse solve)
-  __shared__ double zs[SP_THREADS / 32][2 * SP_SEGB];
-  int s;
-  if (!defl_slot(P, blockIdx.y, s)) return;
-  const int mc = blockIdx.x / sp.nseg, sg = blockIdx.x % sp.nseg;
-  const int m = mc * SP_THREADS + threadIdx.x;
+__device__ __forceinline__ void spec_warp_item(const SpecParams& sp, int s, int mc, int sg,
+                                               const double* __restrict__ vh, double* __restrict__ th, double* zout) {
+  const int lane = threadIdx.x & 31;
+  const int m = mc * SP_MODES + lane;
   const int nb = spec_nblocks(sp);
-  const int b0 = sg * SP_SEGB, b1 = min(nb, b0 + SP_SEGB);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b0 = sg * sp.segb, b1 = min(nb, b0 + sp.segb);
   double zt[2 * SP_SEGB];
 #pragma unroll
   for (int i = 0; i < 2 * SP_SEGB; ++i) zt[i] = 0.0;
   if (m < sp.nmode) {
     const ModeRef mr = mode_ref(sp, s, m);
     const ModeGamma g = mode_gamma(sp, s, m);
-    spec_mode_segment<BJ>(sp, mr, g, vh, th, b0, b1, zpart ? zt : nullptr);
+    const double2* ki = sp.kinv + static_cast<long long>(s) * 20 * sp.nmode + m;
+    spec_mode_segment<BJ>(sp, mr, g, ki, vh, th, b0, b1, zout ? zt : nullptr);
   }
-  if (!zpart) return;
-  // Z^T partials of this CTA's modes for its interfaces, fixed-order reductions
+  if (!zout) return;
   const int i0 = 2 * b0, i1 = min(sp.d, 2 * b1);
 #pragma unroll
   for (int i = 0; i < 2 * SP_SEGB; ++i) {
     const double v = warp_sum(zt[i]);
-    if (lane == 0) zs[warp][i] = v;
+    if (lane == 0 && i0 + i < i1) zout[i0 + i] = v;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < i1 - i0; i += blockDim.x) {
-    double v = 0.0;
-    for (int q = 0; q < SP_THREADS / 32; ++q) v += zs[q][i];
-    zpart[(static_cast<long long>(s) * sp.nmc + mc) * sp.d + i0 + i] = v;
-  }
-  if (!last_cta(counter + s, sp.nmc * sp.nseg)) return;
+}
+
+// th = T^-1-space operator of the live systems; with zpart, the last CTA of
+// each system also solves the coarse system for c = C^{-1} Z^T (T th) -> cout.
+// grid (nmc * ceil(nseg / SP_WARPS), live slots)
+template <bool BJ>
+__global__ void __launch_bounds__(SP_THREADS) spec_op_kernel(SpecParams sp, const double* __restrict__ vh,
+                                                             double* __restrict__ th, DeflateParams P, double* zpart,
+                                                             int* counter, double* cout) {
+  extern __shared__ double sm[];  // 2 d doubles (coarse solve)
+  int s;
+  if (!defl_slot(P, blockIdx.y, s)) return;
+  const int nsg = (sp.nseg + SP_WARPS - 1) / SP_WARPS;
+  const int mc = blockIdx.x / nsg, sg = (blockIdx.x % nsg) * SP_WARPS + (threadIdx.x >> 5);
+  if (sg < sp.nseg)
+    spec_warp_item<BJ>(sp, s, mc, sg, vh, th, zpart ? zpart + (static_cast<long long>(s) * sp.nmc + mc) * sp.d : nullptr);
+  if (!zpart) return;
+  if (!last_cta(counter + s, sp.nmc * nsg)) return;
   double* sums = sm;
   double* c = sm + sp.d;
   for (int i = threadIdx.x; i < sp.d; i += blockDim.x) {
