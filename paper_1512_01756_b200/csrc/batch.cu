@@ -22,6 +22,7 @@
 #include "gemm2.cuh"
 #include "vec.cuh"
 #include "vec2.cuh"
+#include "vec3.cuh"
 #include "cluster.cuh"
 #include "grid.cuh"
 #include "spectral.cuh"
@@ -1186,21 +1187,22 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
     cgs_update_kernel<true><<<grid, VEC_THREADS, hsm, st>>>(G, V, wv, 1);
     check_launch(b);
   } else {
-    // chunk size adapted to the live systems so even one system spreads over
-    // ~4 CTAs per SM (the partial-sum buffer is sized for 128-row chunks)
+    // long row chunks: (live systems x chunks) ~ 4 CTAs per SM, so a batch of
+    // live systems is one wave and per-system partial sums stay few
     GmState_ Gl = G;
     const long long target = 4LL * b->ctx->num_sms;
-    int chunk = V2_CHUNK;
-    while (chunk > 128 && static_cast<long long>(lv.nslots) * ((b->k + chunk - 1) / chunk) < target) chunk /= 2;
-    Gl.chunk = chunk;
+    const long long cps = std::max(1LL, (target + lv.nslots - 1) / lv.nslots);
+    long long chunk = (b->k + cps - 1) / cps;
+    chunk = std::max(256LL, (chunk + 255) / 256 * 256);
+    Gl.chunk = static_cast<int>(chunk);
     Gl.nchunk = static_cast<int>((b->k + chunk - 1) / chunk);
     dim3 cgrid(Gl.nchunk, lv.nslots);
     DeflateParams P = deflate_params(b, nullptr);
-    cgs2_dot_kernel<<<cgrid, V2_THREADS, 0, st>>>(Gl, V, wv, tdefl, P, cbuf);
+    cgs3_dot_kernel<<<cgrid, V3_THREADS, 0, st>>>(Gl, V, wv, tdefl, P, cbuf);
     check_launch(b);
-    cgs2_update_kernel<false><<<cgrid, V2_THREADS, 0, st>>>(Gl, V, wv, 1);
+    cgs3_update_kernel<false><<<cgrid, V3_THREADS, 0, st>>>(Gl, V, wv);
     check_launch(b);
-    cgs2_update_kernel<true><<<cgrid, V2_THREADS, 0, st>>>(Gl, V, wv, 1);
+    cgs3_update_kernel<true><<<cgrid, V3_THREADS, 0, st>>>(Gl, V, wv);
     check_launch(b);
   }
   (void)hsm;
@@ -1596,7 +1598,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   // few live systems: the rest of the cycle runs grid-persistent (grid.cuh)
   const bool use_grid = b->grid_ok && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= GT_MAXCOL &&
                         (c.method != SMPM_DBJ || c.fused) && std::getenv("SMPM_NO_GRID") == nullptr;
-  int grid_max = 32;
+  int grid_max = 16;
   if (const char* e = std::getenv("SMPM_GRID_MAX")) grid_max = std::max(0, std::min(GT_MAXSYS, std::atoi(e)));
   if (use_grid) grid_max = std::min(grid_max, grid_blocks(b) / GT_CL);  // one cluster per live system at least
   auto restart = [&](int ncycv) {
