@@ -263,7 +263,7 @@ struct smpm_batch {
   bool spectral = false;
   int sp_npairs = 0, sp_nmode = 0;
   std::vector<double> hT, hTi, hgam;
-  DevArray<double> dT, dTi, domega, dgam, dzpart, dvh, dth, dkinv;
+  DevArray<double> dT, dTi, domega, dgam, dzpart, dvh, dvh2, dth, dkinv;
   Plan pF, pB;
   Plan pc[6];          // unsplit per-system templates (BJ1, BJ2, BJ3, S; spectral F, B) for the persistent solvers
   bool cluster_ok = false;
@@ -285,8 +285,14 @@ struct smpm_batch {
   DevArray<int> dones, dcount, dsel, dcnt;
   DevArray<int> dalist;  // two compacted live lists + counts: [alist, acount, alist2, acount2]
   int* hcnt = nullptr;  // pinned, 4 ints (two in-flight step counters)
+  void* hrep = nullptr;  // pinned report staging
+  size_t hrep_bytes = 0;
+  cudaEvent_t sev[4] = {nullptr, nullptr, nullptr, nullptr};  // solve events (timing x2, step polling x2)
   ~smpm_batch() {
+    for (auto e : sev)
+      if (e) cudaEventDestroy(e);
     if (hcnt) cudaFreeHost(hcnt);
+    if (hrep) cudaFreeHost(hrep);
     for (auto e : ev_pool) cudaEventDestroy(e);
   }
   DevArray<double> dpart;
@@ -922,6 +928,7 @@ void finalize(smpm_batch* b) {
     b->dkinv.alloc(static_cast<size_t>(b->nsys) * 20 * b->sp_nmode * 2);
     b->dvh.alloc(static_cast<size_t>(b->nsys) * b->k);
     b->dth.alloc(static_cast<size_t>(b->nsys) * b->k);
+    b->dvh2.alloc(static_cast<size_t>(b->nsys) * b->k);
   }
   build_plans(b);
   if (b->spectral && !(b->pF.v2 && b->pB.v2)) b->spectral = false;  // odd w: dense operator path
@@ -1040,7 +1047,6 @@ void ensure_gmres(smpm_batch* b, int m, int mtot) {
   (void)c;
   b->gm_mtot = mtot;
   CUDA_CHECK(cudaMemsetAsync(b->dgint.p, 0, sizeof(int) * ns * 8, b->ctx->stream));
-  CUDA_CHECK(cudaMemsetAsync(b->dR.p, 0, sizeof(double) * b->dR.n, b->ctx->stream));
 }
 
 struct SolveCfg {
@@ -1074,7 +1080,8 @@ SpecParams spec_params(const smpm_batch* b) {
 
 // th = S^ M^^{-1} vh (bj) or S^ vh in T-coordinates; with cout, also
 // c = C^{-1} Z^T (T th) per system (deflation coarse solve)
-void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* cout, const Live& lv, cudaStream_t st) {
+void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* cout, const Live& lv, cudaStream_t st,
+                double* uh = nullptr) {
   if (lv.nslots == 0) return;
   const SpecParams sp = spec_params(b);
   DeflateParams P = deflate_params(b, lv.active);
@@ -1084,15 +1091,25 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
   const size_t shm = cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0;
   double* zp = cout ? b->dzpart.p : nullptr;
   if (bj)
-    spec_op_kernel<true><<<grid, SP_THREADS, shm, st>>>(sp, vh, th, P, zp, b->dcount.p, cout);
+    spec_op_kernel<true><<<grid, SP_THREADS, shm, st>>>(sp, vh, th, P, zp, b->dcount.p, cout, uh);
   else
-    spec_op_kernel<false><<<grid, SP_THREADS, shm, st>>>(sp, vh, th, P, zp, b->dcount.p, cout);
+    spec_op_kernel<false><<<grid, SP_THREADS, shm, st>>>(sp, vh, th, P, zp, b->dcount.p, cout, uh);
   check_launch(b);
 }
 
+// u = M^{-1} v through the spectral form, and (su != nullptr) S u as well
+void spec_Minv(smpm_batch* b, const double* v, double* u, double* su, const Live& lv, cudaStream_t st) {
+  ProfScope ps(b, 7, st);
+  run_plan(b, b->pF, v, b->dvh.p, nullptr, lv, st);
+  spec_apply(b, true, b->dvh.p, su ? b->dth.p : nullptr, nullptr, lv, st, b->dvh2.p);
+  run_plan(b, b->pB, b->dvh2.p, u, nullptr, lv, st);
+  if (su) run_plan(b, b->pB, b->dth.p, su, nullptr, lv, st);
+}
+
+bool spec_on(const smpm_batch* b) { return b->spectral && std::getenv("SMPM_NO_SPECTRAL") == nullptr; }
+
 bool spec_ok(const smpm_batch* b, const SolveCfg& c) {
-  return b->spectral && (c.method == SMPM_SCHUR || c.method == SMPM_BJ || c.method == SMPM_DBJ) &&
-         std::getenv("SMPM_NO_SPECTRAL") == nullptr;
+  return spec_on(b) && (c.method == SMPM_SCHUR || c.method == SMPM_BJ || c.method == SMPM_DBJ);
 }
 
 // S M^{-1} v (bj) or S v through the spectral form; out may be any buffer
@@ -1499,10 +1516,16 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   double* nb2 = sc;        // ||b_S||^2
   double* nr2 = sc + ns;   // ||rhs||^2 / ||r||^2
   cudaEvent_t e0, e1, ev[2];
-  CUDA_CHECK(cudaEventCreate(&e0));
-  CUDA_CHECK(cudaEventCreate(&e1));
-  CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-  CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  if (!b->sev[0]) {
+    CUDA_CHECK(cudaEventCreate(&b->sev[0]));
+    CUDA_CHECK(cudaEventCreate(&b->sev[1]));
+    CUDA_CHECK(cudaEventCreateWithFlags(&b->sev[2], cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&b->sev[3], cudaEventDisableTiming));
+  }
+  e0 = b->sev[0];
+  e1 = b->sev[1];
+  ev[0] = b->sev[2];
+  ev[1] = b->sev[3];
   int* dsel = b->dsel.p;
   int* hcnt = b->hcnt;
   CUDA_CHECK(cudaEventRecord(e0, st));
@@ -1698,47 +1721,69 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       CUDA_CHECK(cudaMemcpyAsync(xS, x, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
       break;
     case SMPM_BJ:
-      op_BJ(b, x, xS, all, st);
+      if (spec_on(b))
+        spec_Minv(b, x, xS, nullptr, all, st);
+      else
+        op_BJ(b, x, xS, all, st);
       break;
     case SMPM_DBJ: {
       double* q = b->vbuf[6].p;
-      op_BJ(b, x, u, all, st);
-      op_Q(b, u, q, all, st);
+      if (spec_on(b)) {
+        // u = M^{-1} x and S u from one per-mode pass, then Q u = u - Z c(Z^T S u)
+        double* su = b->vbuf[8].p;
+        spec_Minv(b, x, u, su, all, st);
+        run_deflate(b, DEFL_Q_TAIL, su, u, q, nullptr, all, st);
+      } else {
+        op_BJ(b, x, u, all, st);
+        op_Q(b, u, q, all, st);
+      }
       run_deflate(b, DEFL_ADD_ZC, bS, q, xS, nullptr, all, st);
       break;
     }
     case SMPM_2LAS:
-      op_BJ(b, x, u, all, st);
+      if (spec_on(b))
+        spec_Minv(b, x, u, nullptr, all, st);
+      else
+        op_BJ(b, x, u, all, st);
       run_deflate(b, DEFL_ADD_ZC, x, u, xS, nullptr, all, st);
       break;
+  }
+  // report data: queued on the stream into pinned staging (one host wait)
+  const size_t rep_ints = static_cast<size_t>(ns) * 8, rep_dbl = static_cast<size_t>(ns) * (8 + (m + 1) + 3);
+  const size_t rep_hist = history ? static_cast<size_t>(ns) * G.histcap : 0;
+  const size_t rep_bytes = rep_ints * sizeof(int) + (rep_dbl + rep_hist) * sizeof(double);
+  if (b->hrep_bytes < rep_bytes) {
+    if (b->hrep) cudaFreeHost(b->hrep);
+    b->hrep = nullptr;
+    CUDA_CHECK(cudaMallocHost(&b->hrep, rep_bytes));
+    b->hrep_bytes = rep_bytes;
+  }
+  double* hsc_p = reinterpret_cast<double*>(b->hrep);
+  double* hg_p = hsc_p + static_cast<size_t>(ns) * 8;
+  double* hsm_p = hg_p + static_cast<size_t>(ns) * (m + 1);
+  double* hh_p = hsm_p + static_cast<size_t>(ns) * 3;
+  int* hint_p = reinterpret_cast<int*>(hh_p + rep_hist);
+  if (reps || history) {
+    CUDA_CHECK(cudaMemcpyAsync(hint_p, b->dgint.p, sizeof(int) * ns * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaMemcpyAsync(hsc_p, b->dscal.p, sizeof(double) * ns * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaMemcpyAsync(hg_p, b->dg.p, sizeof(double) * ns * (m + 1), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaMemcpyAsync(hsm_p, sc, sizeof(double) * ns * 3, cudaMemcpyDeviceToHost, st));
+    if (history)
+      CUDA_CHECK(cudaMemcpyAsync(hh_p, b->dhist.p, sizeof(double) * rep_hist, cudaMemcpyDeviceToHost, st));
   }
   CUDA_CHECK(cudaEventRecord(e1, st));
   CUDA_CHECK(cudaEventSynchronize(e1));
   prof_collect(b);
   float ms = 0.f;
   CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
-  CUDA_CHECK(cudaEventDestroy(e0));
-  CUDA_CHECK(cudaEventDestroy(e1));
-  CUDA_CHECK(cudaEventDestroy(ev[0]));
-  CUDA_CHECK(cudaEventDestroy(ev[1]));
   G.alist = nullptr;
   G.acount = nullptr;
   (void)launches0;
 
   // ---- reports
   if (reps || history) {
-    std::vector<int> hint(static_cast<size_t>(ns) * 8);
-    std::vector<double> hsc(static_cast<size_t>(ns) * 8), hg(static_cast<size_t>(ns) * (m + 1)),
-        hsm(static_cast<size_t>(ns) * 3);
-    CUDA_CHECK(cudaMemcpy(hint.data(), b->dgint.p, sizeof(int) * ns * 8, cudaMemcpyDeviceToHost));
-    CUDA_CHECK(cudaMemcpy(hsc.data(), b->dscal.p, sizeof(double) * ns * 8, cudaMemcpyDeviceToHost));
-    CUDA_CHECK(cudaMemcpy(hg.data(), b->dg.p, sizeof(double) * ns * (m + 1), cudaMemcpyDeviceToHost));
-    CUDA_CHECK(cudaMemcpy(hsm.data(), sc, sizeof(double) * ns * 3, cudaMemcpyDeviceToHost));
-    std::vector<double> hh;
-    if (history) {
-      hh.resize(static_cast<size_t>(ns) * G.histcap);
-      CUDA_CHECK(cudaMemcpy(hh.data(), b->dhist.p, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost));
-    }
+    const int* hint = hint_p;
+    const double *hsc = hsc_p, *hg = hg_p, *hsm = hsm_p, *hh = hh_p;
     for (int s = 0; s < ns; ++s) {
       const int iters = hint[static_cast<size_t>(ns) + s];
       const int jc = hint[static_cast<size_t>(s)];

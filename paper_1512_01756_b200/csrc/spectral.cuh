@@ -194,31 +194,42 @@ __device__ __forceinline__ void spec_load_solve(const SpecParams& sp, const Mode
 
 // One mode, block-Jacobi blocks [b0, b1): th = S^ M^^{-1} vh (or S^ vh), and
 // the Z^T partial sums of th for the interfaces of those blocks -> zt[0..)
-// (zt indexed from interface 2*b0; nullptr: skipped)
+// (zt indexed from interface 2*b0; nullptr: skipped).  uh (nullable) also
+// receives M^^{-1} vh; th may be nullptr when only that is wanted.
 template <bool BJ>
 __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const ModeRef& mr, const ModeGamma& g,
                                                   const double2* ki, const double* __restrict__ vh,
-                                                  double* __restrict__ th, int b0, int b1, double* zt) {
+                                                  double* __restrict__ th, int b0, int b1, double* zt,
+                                                  double* __restrict__ uh = nullptr) {
   const int nb = spec_nblocks(sp);
   double2 xp[4], xc[4], xn[4];
-  if (b0 > 0) spec_load_solve<BJ>(sp, mr, g, ki, vh, b0 - 1, xp);
+  if (th && b0 > 0) spec_load_solve<BJ>(sp, mr, g, ki, vh, b0 - 1, xp);
   spec_load_solve<BJ>(sp, mr, g, ki, vh, b0, xc);
   for (int blk = b0; blk < b1; ++blk) {
-    if (blk + 1 < nb) spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xn);
-    double2 t[4];
-    spec_block_S(sp, g, blk, xc, xp[3], xn[0], t);
     const int ns = spec_bslots(sp, blk);
+    if (uh) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (j < ns) mr.st(th, 4 * blk + j, t[j]);
-    if (zt) {
-      zt[2 * (blk - b0)] = mr.zt(sp.omega, cadd(t[0], t[1]));
-      if (ns == 4) zt[2 * (blk - b0) + 1] = mr.zt(sp.omega, cadd(t[2], t[3]));
+      for (int j = 0; j < 4; ++j)
+        if (j < ns) mr.st(uh, 4 * blk + j, xc[j]);
     }
+    if (th) {
+      if (blk + 1 < nb) spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xn);
+      double2 t[4];
+      spec_block_S(sp, g, blk, xc, xp[3], xn[0], t);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      xp[j] = xc[j];
-      xc[j] = xn[j];
+      for (int j = 0; j < 4; ++j)
+        if (j < ns) mr.st(th, 4 * blk + j, t[j]);
+      if (zt) {
+        zt[2 * (blk - b0)] = mr.zt(sp.omega, cadd(t[0], t[1]));
+        if (ns == 4) zt[2 * (blk - b0) + 1] = mr.zt(sp.omega, cadd(t[2], t[3]));
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        xp[j] = xc[j];
+        xc[j] = xn[j];
+      }
+    } else if (blk + 1 < b1) {
+      spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xc);
     }
   }
 }
@@ -227,7 +238,8 @@ __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const Mo
 // with zout, the warp-reduced Z^T partials of its interfaces -> zout[i]
 template <bool BJ>
 __device__ __forceinline__ void spec_warp_item(const SpecParams& sp, int s, int mc, int sg,
-                                               const double* __restrict__ vh, double* __restrict__ th, double* zout) {
+                                               const double* __restrict__ vh, double* __restrict__ th, double* zout,
+                                               double* __restrict__ uh = nullptr) {
   const int lane = threadIdx.x & 31;
   const int m = mc * SP_MODES + lane;
   const int nb = spec_nblocks(sp);
@@ -239,7 +251,7 @@ __device__ __forceinline__ void spec_warp_item(const SpecParams& sp, int s, int 
     const ModeRef mr = mode_ref(sp, s, m);
     const ModeGamma g = mode_gamma(sp, s, m);
     const double2* ki = sp.kinv + static_cast<long long>(s) * 20 * sp.nmode + m;
-    spec_mode_segment<BJ>(sp, mr, g, ki, vh, th, b0, b1, zout ? zt : nullptr);
+    spec_mode_segment<BJ>(sp, mr, g, ki, vh, th, b0, b1, zout ? zt : nullptr, uh);
   }
   if (!zout) return;
   const int i0 = 2 * b0, i1 = min(sp.d, 2 * b1);
@@ -256,14 +268,15 @@ __device__ __forceinline__ void spec_warp_item(const SpecParams& sp, int s, int 
 template <bool BJ>
 __global__ void __launch_bounds__(SP_THREADS) spec_op_kernel(SpecParams sp, const double* __restrict__ vh,
                                                              double* __restrict__ th, DeflateParams P, double* zpart,
-                                                             int* counter, double* cout) {
+                                                             int* counter, double* cout, double* __restrict__ uh) {
   extern __shared__ double sm[];  // 2 d doubles (coarse solve)
   int s;
   if (!defl_slot(P, blockIdx.y, s)) return;
   const int nsg = (sp.nseg + SP_WARPS - 1) / SP_WARPS;
   const int mc = blockIdx.x / nsg, sg = (blockIdx.x % nsg) * SP_WARPS + (threadIdx.x >> 5);
   if (sg < sp.nseg)
-    spec_warp_item<BJ>(sp, s, mc, sg, vh, th, zpart ? zpart + (static_cast<long long>(s) * sp.nmc + mc) * sp.d : nullptr);
+    spec_warp_item<BJ>(sp, s, mc, sg, vh, th, zpart ? zpart + (static_cast<long long>(s) * sp.nmc + mc) * sp.d : nullptr,
+                       uh);
   if (!zpart) return;
   if (!last_cta(counter + s, sp.nmc * nsg)) return;
   double* sums = sm;

@@ -631,6 +631,11 @@ __global__ void gm_v0_kernel(GmState_ G, double* __restrict__ V, const double* _
 // back-substitution R y = g for the systems whose cycle ended (warp per system)
 // (proj/src/gmres.cpp:116-125); ncyc = columns built in this cycle
 __global__ void gm_backsolve_kernel(GmState_ G, const int* __restrict__ sel) {
+  // column-oriented back substitution: y_i = b_i / r_ii, then b_r -= r_ri y_i
+  // for r < i; the triangle is staged in shared memory for short cycles
+  constexpr int NS = 96;
+  __shared__ double tri[NS * (NS + 1) / 2];
+  __shared__ double bsh[NS];
   const int s = blockIdx.x;
   if (sel && !sel[s]) return;
   const int lane = threadIdx.x;
@@ -639,6 +644,26 @@ __global__ void gm_backsolve_kernel(GmState_ G, const int* __restrict__ sel) {
   const double* R = G.R + static_cast<long long>(s) * (m + 1) * m;
   const double* g = G.g + static_cast<long long>(s) * (m + 1);
   double* y = G.y + static_cast<long long>(s) * m;
+  if (n <= NS) {
+    // flat, independent loads of the packed triangle (column c holds rows 0..c)
+    const int nt = n * (n + 1) / 2;
+    for (int e = lane; e < nt; e += 32) {
+      int c = static_cast<int>((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      if (c * (c + 1) / 2 > e) --c;
+      if ((c + 1) * (c + 2) / 2 <= e) ++c;
+      tri[e] = R[static_cast<long long>(c) * (m + 1) + (e - c * (c + 1) / 2)];
+    }
+    for (int r = lane; r < n; r += 32) bsh[r] = g[r];
+    __syncwarp();
+    for (int i = n - 1; i >= 0; --i) {
+      const double rii = tri[i * (i + 1) / 2 + i];
+      const double yi = fabs(rii) > 0.0 ? bsh[i] / rii : 0.0;
+      if (lane == 0) y[i] = yi;
+      for (int r = lane; r < i; r += 32) bsh[r] -= tri[i * (i + 1) / 2 + r] * yi;
+      __syncwarp();
+    }
+    return;
+  }
   for (int i = n - 1; i >= 0; --i) {
     double acc = 0.0;
     for (int c = i + 1 + lane; c < n; c += 32) acc += R[static_cast<long long>(c) * (m + 1) + i] * y[c];
