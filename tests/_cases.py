@@ -44,7 +44,18 @@ def build_case(n, m_x, m_z, l_x, l_z, mus=(0.0,), kmax=4, decay=False, c_tau=2.0
     return Case(prob, systems, list(mus), np.array(bs), u_S, u_L, kinds)
 
 
-def gpu_batch(ctx, case, prob_dims=None):
+def spectral_factors(case):
+    """(npairs, T, T^-1, gamma) of the case's geometry and shifts (product FDM)."""
+    from paper_1512_01756_b200.fdm import Geometry, StripFDM
+
+    p = case.prob
+    geo = Geometry(p.n, p.m_x, p.m_z, p.l_x, p.l_z, p.c_tau)
+    return StripFDM(geo, device="cpu").spectral(case.mus)
+
+
+def gpu_batch(ctx, case, prob_dims=None, spectral=False):
+    """SchurBatch with the oracle's dense couplings (the reference data); with
+    spectral=True also the product's spectral factors of the same geometry."""
     from paper_1512_01756_b200 import SchurBatch
 
     p = case.prob
@@ -53,6 +64,8 @@ def gpu_batch(ctx, case, prob_dims=None):
         b.set_couplings(i, gw, gi if p.m_x > 2 else None, ge)
         if case.mus[i] == 0.0:
             b.set_nullspace(i, case.u_S)
+    if spectral:
+        b.set_spectral(*spectral_factors(case))
     return b.finalize()
 
 

@@ -66,6 +66,38 @@ def test_fdm_couplings_match_oracle(grid):
     assert np.linalg.norm(F.schur_rhs(f, mu) - ref) <= 1e-8 * np.linalg.norm(ref)
 
 
+def _pair_block_apply(npairs, T, Ti, gam):
+    """Dense T diag(gamma) T^-1 of the spectral form (pairs act on z = a - i b)."""
+    w = T.shape[0]
+    D = np.zeros((w, w))
+    for t in range(npairs):
+        g = gam[t]
+        D[2 * t:2 * t + 2, 2 * t:2 * t + 2] = [[g.real, g.imag], [-g.imag, g.real]]
+    for t in range(npairs, len(gam)):
+        D[npairs + t, npairs + t] = gam[t].real
+    return T @ D @ Ti
+
+
+@pytest.mark.parametrize("grid", GRIDS)
+def test_spectral_factors_reproduce_oracle_couplings(grid):
+    """smpm_batch_set_spectral data: T diag(gamma_kind) T^-1 equals the
+    reference's dense couplings G_W, G_I (four blocks), G_E."""
+    n, mx, mz, lx, lz, mu = grid
+    p = O.Problem(n, mx, mz, lx, lz, 2.0)
+    gw, gi, ge = O.System(p, mu, False).kinds()
+    F = fdm.StripFDM(fdm.Geometry(n, mx, mz, lx, lz), "cpu")
+    npairs, T, Ti, gam = F.spectral([mu])
+    w = T.shape[0]
+    assert gam.shape == (1, 6, w - npairs)
+    assert np.abs(T @ Ti - np.eye(w)).max() < 1e-10
+    blocks = {0: gw, 5: ge}
+    if mx > 2:
+        blocks.update({1: gi[:w, :w], 2: gi[:w, w:], 3: gi[w:, :w], 4: gi[w:, w:]})
+    for kind, ref in blocks.items():
+        G = _pair_block_apply(npairs, T, Ti, gam[0, kind])
+        assert np.abs(G - ref).max() <= 1e-10 * np.abs(ref).max(), kind
+
+
 @pytest.mark.parametrize("grid", [g for g in GRIDS if g[5] == 0.0])
 def test_fdm_null_vectors_match_oracle(grid):
     n, mx, mz, lx, lz, _ = grid
