@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libsmpm_b200.so")
+# SMPM_LIB: an alternative in-tree build of the same library (kernel variants for experiments)
+LIB_PATH = os.environ.get("SMPM_LIB") or os.path.join(HERE, "lib", "libsmpm_b200.so")
 
 SMPM_SCHUR, SMPM_BJ, SMPM_DBJ, SMPM_2LAS = 0, 1, 2, 3
 METHODS = {"schur": SMPM_SCHUR, "bj": SMPM_BJ, "dbj": SMPM_DBJ, "2las": SMPM_2LAS}

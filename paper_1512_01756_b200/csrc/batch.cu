@@ -1463,6 +1463,7 @@ void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
   }
   CUDA_CHECK(cudaMemsetAsync(b->dgbar.p, 0, sizeof(unsigned), st));
   cfg.gridDim = dim3(nb);
+  if (std::getenv("SMPM_GRID_NOCOOP")) b->gt_nocoop = true;  // plain cluster launch (e.g. under a profiler)
   cfg.numAttrs = b->gt_nocoop ? 1 : 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, arnoldi_grid_kernel, A);
   if (e != cudaSuccess && !b->gt_nocoop) {
