@@ -261,6 +261,26 @@ def algorithmic_counts(cfg, its, grid_max=16):
     return out
 
 
+def roofline_kernel_name(cls):
+    return {"grid_tail": "arnoldi_grid_kernel", "spectral_op": "gemm2_kernel (T^-1, full batch)",
+            "orthogonalization": "cgs3_dot_kernel (full batch, j=0)"}.get(cls, cls)
+
+
+def measured_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu summary
+    (profiles/rNN/traffic.json), or None."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
+        try:
+            v = json.load(open(path)).get(kernel)
+        except Exception:
+            v = None
+        if v is not None:
+            return {"bytes_per_launch": v, "source": os.path.relpath(path, ROOT)}
+    return None
+
+
 def run_ours(args, cfg):
     import torch
 
@@ -395,13 +415,12 @@ def run_ours(args, cfg):
     else:
         bound, achieved, peak, unit, per_launch = "hbm", by / (dms * 1e-3) / 1e9, peak_hbm, "GB/s", by / nlaunch
     roofline = {
-        "kernel": {"grid_tail": "arnoldi_grid_kernel", "spectral_op": "gemm2_kernel (T^-1, T) + spec_op_kernel",
-                   "orthogonalization": "cgs3_* + gm_scale"}.get(dom, dom),
+        "kernel": roofline_kernel_name(dom),
         "class": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
         "frac": achieved / peak if peak else None,
         "peak_source": (f"measured in-run fp64 microbenchmark (DFMA {dfma.value:.1f}, DMMA {dmma.value:.1f} TFLOP/s)"
                         if bound == "tensor" else hbm_src),
-        "traffic": None,
+        "traffic": measured_traffic(roofline_kernel_name(dom)),
         "algorithmic_per_launch": per_launch,
         "avg_launch_ms": dms / nlaunch,
         "fp64_peak_tflops": peak_fp64, "hbm_peak_gbs": peak_hbm,
