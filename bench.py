@@ -420,7 +420,9 @@ def run_ours(args, cfg):
         "frac": achieved / peak if peak else None,
         "peak_source": (f"measured in-run fp64 microbenchmark (DFMA {dfma.value:.1f}, DMMA {dmma.value:.1f} TFLOP/s)"
                         if bound == "tensor" else hbm_src),
-        "traffic": measured_traffic(roofline_kernel_name(dom)),
+        "traffic": (measured_traffic(roofline_kernel_name(dom)) or {}).get("bytes_per_launch"),
+        "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+        "traffic_source": (measured_traffic(roofline_kernel_name(dom)) or {}).get("source"),
         "algorithmic_per_launch": per_launch,
         "avg_launch_ms": dms / nlaunch,
         "fp64_peak_tflops": peak_fp64, "hbm_peak_gbs": peak_hbm,
