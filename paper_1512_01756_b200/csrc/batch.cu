@@ -276,7 +276,7 @@ struct smpm_batch {
   int gt_blocks = 0;
   bool gt_nocoop = false;  // cooperative + cluster launch rejected: plain cluster launch
   DevArray<unsigned> dgbar;   // grid barrier counter
-  DevArray<double> dgtpart, dgtzsum, dgtzp;
+  DevArray<double> dgtpart, dgtzsum, dgtzp, dgtcg;
 
   // vectors (nsys x k each)
   DevArray<double> vbuf[12];
@@ -1439,6 +1439,8 @@ void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
     A.th = b->dth.p;
     b->dgtzp.alloc(std::max(b->dgtzp.n, static_cast<size_t>(GT_MAXSYS) * A.sp.nmc * b->d));
     A.zp = b->dgtzp.p;
+    b->dgtcg.alloc(std::max(b->dgtcg.n, static_cast<size_t>(GT_MAXSYS) * b->d));
+    A.cg = b->dgtcg.p;
   }
   A.zsum = b->dgtzsum.p;
   A.bar = b->dgbar.p;

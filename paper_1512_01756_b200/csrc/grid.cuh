@@ -60,6 +60,7 @@ struct GridArgs {
   double* vh;              // T^{-1} vin
   double* th;              // S^ M^^{-1} vh
   double* zp;              // GT_MAXSYS x sp.nmc x d: Z^T partial sums per mode chunk
+  double* cg;              // GT_MAXSYS x d: coarse solutions c = C^{-1} Z^T t per live slot
   double* vin;             // v_j (operator input)
   double* w;               // Arnoldi vector under construction
   double* u;               // M^{-1} v
@@ -439,17 +440,19 @@ __device__ __forceinline__ void gt_group_sum(const double* part, int stride, int
 // spectral per-mode pass for the live systems: one warp per (slot, 32-mode
 // chunk, block segment) over the grid; th = S^ M^^{-1} vh (or S^ vh) and the
 // warp-reduced Z^T partials of each (slot, mode chunk) -> zp
-__device__ __forceinline__ void gt_spec(const GridArgs& a, const int* sl, int L, bool bj, bool zt_on) {
+// vh_from_w: vh = T^{-1} w of the previous step (unnormalised): scale by 1/||w||
+__device__ __forceinline__ void gt_spec(const GridArgs& a, const int* sl, int L, bool bj, bool zt_on, bool vh_from_w) {
   const SpecParams& sp = a.sp;
   const int per = sp.nmc * sp.nseg, items = L * per;
   const int nw = blockDim.x >> 5, gw = blockIdx.x * nw + (threadIdx.x >> 5), tw = gridDim.x * nw;
   for (int it = gw; it < items; it += tw) {
     const int q = it / per, r = it % per, mc = r / sp.nseg, sg = r % sp.nseg;
     double* zo = zt_on ? a.zp + (static_cast<long long>(q) * sp.nmc + mc) * sp.d : nullptr;
+    const double ysc = vh_from_w ? 1.0 / __ldcg(a.G.nrm + sl[q]) : 1.0;
     if (bj)
-      spec_warp_item<true>(sp, sl[q], mc, sg, a.vh, a.th, zo);
+      spec_warp_item<true>(sp, sl[q], mc, sg, a.vh, a.th, zo, nullptr, ysc);
     else
-      spec_warp_item<false>(sp, sl[q], mc, sg, a.vh, a.th, zo);
+      spec_warp_item<false>(sp, sl[q], mc, sg, a.vh, a.th, zo, nullptr, ysc);
   }
 }
 
@@ -474,6 +477,7 @@ __global__ void __launch_bounds__(G2_THREADS) arnoldi_grid_kernel(GridArgs a) {
   double* part3 = a.part + 2LL * ncl * stride;
   unsigned epoch = 0;
   int step = 0;
+  bool vh_ready = false, vh_from_w = false;
 
   for (;;) {
     // ---- live systems of this launch (identical in every CTA: state was
@@ -522,20 +526,39 @@ __global__ void __launch_bounds__(G2_THREADS) arnoldi_grid_kernel(GridArgs a) {
     bj.p[BUF_TMP] = a.tmp;
     bj.p[BUF_TMP2] = nullptr;
     if (a.spectral) {
-      // T^{-1} vin -> per-mode S^ M^^{-1} (+ Z^T partials) -> T
+      // T^{-1} v -> per-mode S^ M^^{-1} (+ Z^T partials) -> T.  The first step
+      // of the launch transforms vin; later steps find T^{-1} w of the
+      // previous step already in vh (computed with the norm, see below).
       BufTable f;
-      f.p[BUF_IN] = a.vin;
-      f.p[BUF_OUT] = a.vh;
       f.p[BUF_TMP] = f.p[BUF_TMP2] = nullptr;
-      gt_stage(a, 4, sl, L, f, gsmem, T2(0));
-      grid_sync(a.bar, epoch);
+      if (!vh_ready) {
+        f.p[BUF_IN] = a.vin;
+        f.p[BUF_OUT] = a.vh;
+        gt_stage(a, 4, sl, L, f, gsmem, T2(0));
+        grid_sync(a.bar, epoch);
+        vh_ready = true;
+      }
       mark(1);
-      gt_spec(a, sl, L, a.method != SMPM_SCHUR, a.method == SMPM_DBJ);
+      gt_spec(a, sl, L, a.method != SMPM_SCHUR, a.method == SMPM_DBJ, vh_from_w);
       grid_sync(a.bar, epoch);
       mark(2);
       f.p[BUF_IN] = a.th;
       f.p[BUF_OUT] = a.method == SMPM_DBJ ? a.t : a.w;
       gt_stage(a, 5, sl, L, f, gsmem, T2(1));
+      if (a.method == SMPM_DBJ) {
+        // coarse solves c = C^{-1} Z^T t, one idle CTA per live slot (from the end of the grid)
+        const int qc = NB - 1 - bid;
+        if (qc < L) {
+          for (int i = threadIdx.x; i < d; i += blockDim.x) {
+            double v = 0.0;
+            for (int mc = 0; mc < a.sp.nmc; ++mc) v += __ldcg(a.zp + (static_cast<long long>(qc) * a.sp.nmc + mc) * d + i);
+            cs_[i] = v;
+          }
+          __syncthreads();
+          coarse_solve_block(a.P, sl[qc], cs_, cs_ + d);
+          for (int i = threadIdx.x; i < d; i += blockDim.x) a.cg[static_cast<long long>(qc) * d + i] = cs_[d + i];
+        }
+      }
       grid_sync(a.bar, epoch);
       mark(3);
       mark(4);
@@ -585,21 +608,18 @@ __global__ void __launch_bounds__(G2_THREADS) arnoldi_grid_kernel(GridArgs a) {
     if (a.method == SMPM_DBJ) {
       // ---- fused deflation P: c = C^{-1} Z^T t ; w = t - Z c - (S - I) Z c
       if (a.spectral) {
-        // Z^T t from the per-mode pass: sum the mode chunks in fixed order
-        for (int i = threadIdx.x; i < d; i += blockDim.x) {
-          double v = 0.0;
-          for (int mc = 0; mc < a.sp.nmc; ++mc) v += __ldcg(a.zp + (static_cast<long long>(q) * a.sp.nmc + mc) * d + i);
-          cs_[i] = v;
-        }
+        // c was solved in the transform phase
+        for (int i = threadIdx.x; i < d; i += blockDim.x) cs_[d + i] = __ldcg(a.cg + static_cast<long long>(q) * d + i);
+        __syncthreads();
         mark(5);
       } else {
         gt_zt(a, a.t, sl, L);
         grid_sync(a.bar, epoch);
         mark(5);
         for (int i = threadIdx.x; i < d; i += blockDim.x) cs_[i] = __ldcg(a.zsum + static_cast<long long>(q) * d + i);
+        __syncthreads();
+        coarse_solve_block(a.P, s, cs_, cs_ + d);
       }
-      __syncthreads();
-      coarse_solve_block(a.P, s, cs_, cs_ + d);
       const double* c = cs_ + d;
       const double* rs = a.P.rowsum + static_cast<long long>(s) * 6 * w;
       const double *rWI = rs, *rEI = rs + w2, *rEW = rs + 2 * w2, *rWE = rEW + w;
@@ -666,6 +686,16 @@ __global__ void __launch_bounds__(G2_THREADS) arnoldi_grid_kernel(GridArgs a) {
         col[r] = v;
         a.vin[so + r] = v;
       }
+    if (a.spectral) {
+      // next step's T^{-1} v_{j+1} = T^{-1} w / ||w||: transform w now (the
+      // 1/||w|| is applied in the per-mode pass), saving a phase per step
+      BufTable f;
+      f.p[BUF_IN] = a.w;
+      f.p[BUF_OUT] = a.vh;
+      f.p[BUF_TMP] = f.p[BUF_TMP2] = nullptr;
+      gt_stage(a, 4, sl, L, f, gsmem, nullptr);
+      vh_from_w = true;
+    }
     grid_sync(a.bar, epoch);
     mark(10);
     if (tr && threadIdx.x == 0) tr[11] = static_cast<unsigned long long>(L);

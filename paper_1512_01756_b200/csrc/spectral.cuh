@@ -184,11 +184,15 @@ __device__ __forceinline__ int spec_bslots(const SpecParams& sp, int blk) { retu
 template <bool BJ>
 __device__ __forceinline__ void spec_load_solve(const SpecParams& sp, const ModeRef& mr, const ModeGamma& g,
                                                 const double2* ki, const double* __restrict__ vh, int blk,
-                                                double2 (&x)[4]) {
+                                                double2 (&x)[4], double ysc = 1.0) {
   double2 y[4];
   const int ns = spec_bslots(sp, blk);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) y[j] = j < ns ? mr.ld(vh, 4 * blk + j) : make_double2(0.0, 0.0);
+  for (int j = 0; j < 4; ++j) {
+    y[j] = j < ns ? mr.ld(vh, 4 * blk + j) : make_double2(0.0, 0.0);
+    y[j].x *= ysc;
+    y[j].y *= ysc;
+  }
   spec_block_solve<BJ>(sp, g, ki, blk, y, x);
 }
 
@@ -200,11 +204,11 @@ template <bool BJ>
 __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const ModeRef& mr, const ModeGamma& g,
                                                   const double2* ki, const double* __restrict__ vh,
                                                   double* __restrict__ th, int b0, int b1, double* zt,
-                                                  double* __restrict__ uh = nullptr) {
+                                                  double* __restrict__ uh = nullptr, double ysc = 1.0) {
   const int nb = spec_nblocks(sp);
   double2 xp[4], xc[4], xn[4];
-  if (th && b0 > 0) spec_load_solve<BJ>(sp, mr, g, ki, vh, b0 - 1, xp);
-  spec_load_solve<BJ>(sp, mr, g, ki, vh, b0, xc);
+  if (th && b0 > 0) spec_load_solve<BJ>(sp, mr, g, ki, vh, b0 - 1, xp, ysc);
+  spec_load_solve<BJ>(sp, mr, g, ki, vh, b0, xc, ysc);
   for (int blk = b0; blk < b1; ++blk) {
     const int ns = spec_bslots(sp, blk);
     if (uh) {
@@ -213,7 +217,7 @@ __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const Mo
         if (j < ns) mr.st(uh, 4 * blk + j, xc[j]);
     }
     if (th) {
-      if (blk + 1 < nb) spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xn);
+      if (blk + 1 < nb) spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xn, ysc);
       double2 t[4];
       spec_block_S(sp, g, blk, xc, xp[3], xn[0], t);
 #pragma unroll
@@ -229,7 +233,7 @@ __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const Mo
         xc[j] = xn[j];
       }
     } else if (blk + 1 < b1) {
-      spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xc);
+      spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xc, ysc);
     }
   }
 }
@@ -239,7 +243,7 @@ __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const Mo
 template <bool BJ>
 __device__ __forceinline__ void spec_warp_item(const SpecParams& sp, int s, int mc, int sg,
                                                const double* __restrict__ vh, double* __restrict__ th, double* zout,
-                                               double* __restrict__ uh = nullptr) {
+                                               double* __restrict__ uh = nullptr, double ysc = 1.0) {
   const int lane = threadIdx.x & 31;
   const int m = mc * SP_MODES + lane;
   const int nb = spec_nblocks(sp);
@@ -251,7 +255,7 @@ __device__ __forceinline__ void spec_warp_item(const SpecParams& sp, int s, int 
     const ModeRef mr = mode_ref(sp, s, m);
     const ModeGamma g = mode_gamma(sp, s, m);
     const double2* ki = sp.kinv + static_cast<long long>(s) * 20 * sp.nmode + m;
-    spec_mode_segment<BJ>(sp, mr, g, ki, vh, th, b0, b1, zout ? zt : nullptr, uh);
+    spec_mode_segment<BJ>(sp, mr, g, ki, vh, th, b0, b1, zout ? zt : nullptr, uh, ysc);
   }
   if (!zout) return;
   const int i0 = 2 * b0, i1 = min(sp.d, 2 * b1);
