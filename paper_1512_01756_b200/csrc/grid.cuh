@@ -258,12 +258,13 @@ __device__ __forceinline__ void gt_cluster_gemv(const GemmJob& jb, const Tile2& 
 // at a time; the round count is uniform over each cluster
 template <int SP>
 __device__ __forceinline__ void gt_stage_split(const GridArgs& a, int stage, const int* sl, int L, const BufTable& bufs,
-                                               double* smem, unsigned long long* t2) {
+                                               double* smem, unsigned long long* t2, bool rev) {
   const int ng = a.ngemm[stage], nci = ng + a.ngv[stage], items = L * nci;
   constexpr int PER = GT_CL / SP;
   const int ncl = gridDim.x / GT_CL, cid = blockIdx.x / GT_CL, nsub = ncl * PER;
   const unsigned rank = gt_rank(), sc = rank / SP, srank = rank % SP, base = sc * SP;
-  const int gsub = cid * PER + static_cast<int>(sc);
+  // rev: items from the last cluster down (keeps them off the group leaders)
+  const int gsub = (rev ? ncl - 1 - cid : cid) * PER + static_cast<int>(sc);
   const int rounds = (items + nsub - 1) / nsub;
   for (int rd = 0; rd < rounds; ++rd) {
     const int it = rd * nsub + gsub;
@@ -285,7 +286,7 @@ __device__ __forceinline__ void gt_stage_split(const GridArgs& a, int stage, con
 
 // one operator stage for the live systems sl[0..L)
 __device__ __forceinline__ void gt_stage(const GridArgs& a, int stage, const int* sl, int L, const BufTable& bufs,
-                                         double* smem, unsigned long long* t2) {
+                                         double* smem, unsigned long long* t2, bool rev = false) {
   if (t2 && threadIdx.x == 0) {
     for (int i = 1; i < 8; ++i) t2[i] = 0;
     t2[0] = gt_timer();
@@ -295,9 +296,9 @@ __device__ __forceinline__ void gt_stage(const GridArgs& a, int stage, const int
   const int NB = gridDim.x, bid = blockIdx.x, ncl = NB / GT_CL;
   // split each tile over as many CTAs as the live systems leave room for
   const int items = L * nci;
-  if (items <= ncl) return gt_stage_split<GT_CL>(a, stage, sl, L, bufs, smem, t2);
-  if (items <= 2 * ncl) return gt_stage_split<GT_CL / 2>(a, stage, sl, L, bufs, smem, t2);
-  if (items <= 4 * ncl) return gt_stage_split<GT_CL / 4>(a, stage, sl, L, bufs, smem, t2);
+  if (items <= ncl) return gt_stage_split<GT_CL>(a, stage, sl, L, bufs, smem, t2, rev);
+  if (items <= 2 * ncl) return gt_stage_split<GT_CL / 2>(a, stage, sl, L, bufs, smem, t2, rev);
+  if (items <= 4 * ncl) return gt_stage_split<GT_CL / 4>(a, stage, sl, L, bufs, smem, t2, rev);
   // many systems: whole tiles per CTA
   for (int it = bid; it < L * nt; it += NB) {
     const Tile2 tile = tiles[it % nt];
@@ -693,7 +694,7 @@ __global__ void __launch_bounds__(G2_THREADS) arnoldi_grid_kernel(GridArgs a) {
       f.p[BUF_IN] = a.w;
       f.p[BUF_OUT] = a.vh;
       f.p[BUF_TMP] = f.p[BUF_TMP2] = nullptr;
-      gt_stage(a, 4, sl, L, f, gsmem, nullptr);
+      gt_stage(a, 4, sl, L, f, gsmem, nullptr, true);
       vh_from_w = true;
     }
     grid_sync(a.bar, epoch);
