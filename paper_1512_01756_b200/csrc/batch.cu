@@ -1074,7 +1074,8 @@ SpecParams spec_params(const smpm_batch* b) {
   sp.omega = b->domega.p;
   sp.nmc = (b->sp_nmode + SP_MODES - 1) / SP_MODES;
   sp.segb = SP_SEGB;
-  sp.nseg = (b->nbf + (b->single ? 1 : 0) + SP_SEGB - 1) / SP_SEGB;
+  if (const char* e = std::getenv("SMPM_SEGB")) sp.segb = std::max(1, std::min(SP_SEGB, std::atoi(e)));
+  sp.nseg = (b->nbf + (b->single ? 1 : 0) + sp.segb - 1) / sp.segb;
   return sp;
 }
 
@@ -1710,28 +1711,49 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   check_launch(b);
 
   // ---- final residual check (proj/src/gmres.cpp:129-136): r = rhs - op(x')
+  // Spectral dbj/bj: one per-mode pass of x' gives both u = M^{-1} x' (the
+  // solution) and t = S M^{-1} x' (the residual operator), sharing T^{-1} x'.
   double* nrf = sc + 2 * ns;
+  double* u = b->vbuf[4].p;
+  double* tq = b->vbuf[5].p;
+  const bool fuse_post = spec_ok(b, c) && ((c.method == SMPM_DBJ && c.fused) || c.method == SMPM_BJ);
+  if (fuse_post) {
+    ProfScope ps7(b, 7, st);
+    run_plan(b, b->pF, x, b->dvh.p, nullptr, all, st);
+    spec_apply(b, true, b->dvh.p, b->dth.p, nullptr, all, st, b->dvh2.p);
+    run_plan(b, b->pB, b->dvh2.p, u, nullptr, all, st);
+    run_plan(b, b->pB, b->dth.p, tq, nullptr, all, st);
+  }
   if (c.final_check) {
-    apply_op(b, c, x, r, all, st);
+    if (fuse_post && c.method == SMPM_DBJ) {
+      run_deflate(b, DEFL_P_FUSED, tq, tq, r, nullptr, all, st);
+    } else if (fuse_post) {
+      CUDA_CHECK(cudaMemcpyAsync(r, tq, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
+    } else {
+      apply_op(b, c, x, r, all, st);
+    }
     axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, nullptr, nullptr, 1.0, rhs, -1.0, r);
     check_launch(b);
     batched_dot(b, r, r, nrf, nullptr, st);
   }
   // ---- solution (proj/src/deflation.cpp:118-120, :141; proj/src/gmres.cpp:148)
-  double* u = b->vbuf[4].p;
   switch (c.method) {
     case SMPM_SCHUR:
       CUDA_CHECK(cudaMemcpyAsync(xS, x, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
       break;
     case SMPM_BJ:
-      if (spec_on(b))
+      if (fuse_post)
+        CUDA_CHECK(cudaMemcpyAsync(xS, u, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
+      else if (spec_on(b))
         spec_Minv(b, x, xS, nullptr, all, st);
       else
         op_BJ(b, x, xS, all, st);
       break;
     case SMPM_DBJ: {
       double* q = b->vbuf[6].p;
-      if (spec_on(b)) {
+      if (fuse_post) {
+        run_deflate(b, DEFL_Q_TAIL, tq, u, q, nullptr, all, st);  // Q u = u - Z c(Z^T S u)
+      } else if (spec_on(b)) {
         // u = M^{-1} x and S u from one per-mode pass, then Q u = u - Z c(Z^T S u)
         double* su = b->vbuf[8].p;
         spec_Minv(b, x, u, su, all, st);
