@@ -26,6 +26,7 @@
 #include "cluster.cuh"
 #include "grid.cuh"
 #include "spectral.cuh"
+#include "xform.cuh"
 
 using namespace smpm;
 
@@ -265,6 +266,9 @@ struct smpm_batch {
   std::vector<double> hT, hTi, hgam;
   DevArray<double> dT, dTi, domega, dgam, dzpart, dvh, dvh2, dth, dkinv;
   Plan pF, pB;
+  DevArray<double> dTfrag, dTifrag;    // T, T^{-1} in the xform fragment order
+  int xf_P = 0, xf_MB = 0;  // resident-slice transform kernel (xform.cuh); 0: use pF/pB
+  size_t xf_smem = 0;
   Plan pc[6];          // unsplit per-system templates (BJ1, BJ2, BJ3, S; spectral F, B) for the persistent solvers
   bool cluster_ok = false;
   DevArray<double> dclpart, dclzsum;
@@ -381,6 +385,8 @@ void prof_collect(smpm_batch* b) {
 // live systems (alist/acount, grids sized by an upper bound nslots), or all
 // systems (alist == nullptr).  `active` is the matching per-system mask for
 // the kernels that take masks.
+void setup_xform(smpm_batch* b);
+
 struct Live {
   const int* alist = nullptr;
   const int* acount = nullptr;
@@ -932,6 +938,7 @@ void finalize(smpm_batch* b) {
   }
   build_plans(b);
   if (b->spectral && !(b->pF.v2 && b->pB.v2)) b->spectral = false;  // odd w: dense operator path
+  if (b->spectral) setup_xform(b);
   if (b->spectral) {
     const SpecParams sp = spec_params(b);
     const long long n = 1LL * b->nsys * b->sp_nmode;
@@ -1079,6 +1086,72 @@ SpecParams spec_params(const smpm_batch* b) {
   return sp;
 }
 
+// ---- shared-matrix transforms (xform.cuh): the largest row slice of T / T^{-1}
+// that fits in shared memory next to a two-deep column ring, P slices per column group
+template <int MB>
+bool xform_try(smpm_batch* b, int P) {
+  const int w = b->w;
+  const size_t smem =
+      sizeof(double) * (static_cast<size_t>(w / 8) * MB * 64 + static_cast<size_t>(XF_NS) * XF_NT * xf_bstr(w / 2));
+  if (smem > 232448 || 8 * MB * P < w || P > b->ctx->num_sms) return false;
+  CUDA_CHECK(cudaFuncSetAttribute(xform_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  std::vector<double> f(static_cast<size_t>(P) * (w / 8) * MB * 64), fi(f.size());
+  xform_frag_order(b->hT.data(), w, P, MB, f.data());
+  xform_frag_order(b->hTi.data(), w, P, MB, fi.data());
+  b->dTfrag.upload(f, b->ctx->stream);
+  b->dTifrag.upload(fi, b->ctx->stream);
+  CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
+  b->xf_P = P;
+  b->xf_MB = MB;
+  b->xf_smem = smem;
+  return true;
+}
+
+void setup_xform(smpm_batch* b) {
+  b->xf_P = 0;
+  if (b->w % 16 != 0 || std::getenv("SMPM_NO_XFORM")) return;
+  for (int P = 1; P <= 4; ++P) {
+    const int need = (b->w / 8 + P - 1) / P;
+    if (need <= 4 ? xform_try<4>(b, P) : need <= 8 ? xform_try<8>(b, P) : need <= 11 ? xform_try<11>(b, P) : false)
+      return;
+  }
+}
+
+// out = A in (and out2 = A in2) for every w-block of the live systems, A = T^{-1} (inverse) or T
+void run_xform(smpm_batch* b, bool inverse, const double* in, double* out, const Live& lv, cudaStream_t st,
+               const double* in2 = nullptr, double* out2 = nullptr) {
+  if (lv.nslots == 0) return;
+  if (b->xf_P == 0) {
+    run_plan(b, inverse ? b->pF : b->pB, in, out, nullptr, lv, st);
+    if (in2) run_plan(b, inverse ? b->pF : b->pB, in2, out2, nullptr, lv, st);
+    return;
+  }
+  XformArgs a;
+  a.Af = inverse ? b->dTifrag.p : b->dTfrag.p;
+  a.w = b->w;
+  a.ncol_sys = 2 * b->d;
+  a.k = b->k;
+  a.alist = lv.alist;
+  a.acount = lv.acount;
+  a.nslots = lv.nslots;
+  a.nv = in2 ? 2 : 1;
+  a.in[0] = in;
+  a.out[0] = out;
+  a.in[1] = in2;
+  a.out[1] = out2;
+  a.P = b->xf_P;
+  // column groups: every SM busy unless a group's share would drop below 16 columns
+  const long long nch = (static_cast<long long>(lv.nslots) * a.ncol_sys * a.nv + 15) / 16;
+  const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / a.P, nch)));
+  const dim3 grid(groups * a.P);
+  switch (b->xf_MB) {
+    case 4: xform_kernel<4><<<grid, XF_THREADS, b->xf_smem, st>>>(a); break;
+    case 8: xform_kernel<8><<<grid, XF_THREADS, b->xf_smem, st>>>(a); break;
+    default: xform_kernel<11><<<grid, XF_THREADS, b->xf_smem, st>>>(a); break;
+  }
+  check_launch(b);
+}
+
 // th = S^ M^^{-1} vh (bj) or S^ vh in T-coordinates; with cout, also
 // c = C^{-1} Z^T (T th) per system (deflation coarse solve)
 void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* cout, const Live& lv, cudaStream_t st,
@@ -1101,10 +1174,9 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
 // u = M^{-1} v through the spectral form, and (su != nullptr) S u as well
 void spec_Minv(smpm_batch* b, const double* v, double* u, double* su, const Live& lv, cudaStream_t st) {
   ProfScope ps(b, 7, st);
-  run_plan(b, b->pF, v, b->dvh.p, nullptr, lv, st);
+  run_xform(b, true, v, b->dvh.p, lv, st);
   spec_apply(b, true, b->dvh.p, su ? b->dth.p : nullptr, nullptr, lv, st, b->dvh2.p);
-  run_plan(b, b->pB, b->dvh2.p, u, nullptr, lv, st);
-  if (su) run_plan(b, b->pB, b->dth.p, su, nullptr, lv, st);
+  run_xform(b, false, b->dvh2.p, u, lv, st, su ? b->dth.p : nullptr, su);
 }
 
 bool spec_on(const smpm_batch* b) { return b->spectral && std::getenv("SMPM_NO_SPECTRAL") == nullptr; }
@@ -1116,9 +1188,9 @@ bool spec_ok(const smpm_batch* b, const SolveCfg& c) {
 // S M^{-1} v (bj) or S v through the spectral form; out may be any buffer
 void spec_SMinv(smpm_batch* b, bool bj, const double* v, double* out, double* cout, const Live& lv, cudaStream_t st) {
   ProfScope ps(b, 7, st);  // class 7: spectral operator
-  run_plan(b, b->pF, v, b->dvh.p, nullptr, lv, st);
+  run_xform(b, true, v, b->dvh.p, lv, st);
   spec_apply(b, bj, b->dvh.p, b->dth.p, cout, lv, st);
-  run_plan(b, b->pB, b->dth.p, out, nullptr, lv, st);
+  run_xform(b, false, b->dth.p, out, lv, st);
 }
 
 // the preconditioned operator GMRES iterates on (proj/src/deflation.cpp:105-107,131; proj/src/gmres.cpp:144-150)
@@ -1719,10 +1791,9 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   const bool fuse_post = spec_ok(b, c) && ((c.method == SMPM_DBJ && c.fused) || c.method == SMPM_BJ);
   if (fuse_post) {
     ProfScope ps7(b, 7, st);
-    run_plan(b, b->pF, x, b->dvh.p, nullptr, all, st);
+    run_xform(b, true, x, b->dvh.p, all, st);
     spec_apply(b, true, b->dvh.p, b->dth.p, nullptr, all, st, b->dvh2.p);
-    run_plan(b, b->pB, b->dvh2.p, u, nullptr, all, st);
-    run_plan(b, b->pB, b->dth.p, tq, nullptr, all, st);
+    run_xform(b, false, b->dvh2.p, u, all, st, b->dth.p, tq);
   }
   if (c.final_check) {
     if (fuse_post && c.method == SMPM_DBJ) {
