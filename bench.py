@@ -262,7 +262,7 @@ def algorithmic_counts(cfg, its, grid_max=16):
 
 
 def roofline_kernel_name(cls):
-    return {"grid_tail": "arnoldi_grid_kernel", "spectral_op": "gemm2_kernel (T^-1, full batch)",
+    return {"grid_tail": "arnoldi_grid_kernel", "spectral_op": "xform_kernel (T^-1 / T, full batch)",
             "orthogonalization": "cgs3_dot_kernel (full batch, j=0)"}.get(cls, cls)
 
 
@@ -305,7 +305,7 @@ def run_ours(args, cfg):
 
     # 3D configs: modes sharded round-robin; 2D configs: replicas only
     modes = shard_modes(nm, ws, rank) if cfg.modes else [0]
-    ps = build_problem(cfg, modes, device=f"cuda:{local}")
+    ps = build_problem(cfg, modes, device=f"cuda:{local}", device_rhs=True)
     ctx = Context(local)
     b = load_batch(ctx, ps)
     bS = torch.tensor(ps.b_S, device=dev)

@@ -157,6 +157,34 @@ int smpm_apply_Q(smpm_batch* b, const double* v, double* y, void* stream);      
 /* out = v - dir (dir . v) per system; dir is nsys x len (proj/src/nullspace.cpp:92) */
 int smpm_project_out(smpm_batch* b, long long len, const double* v, const double* dir, double* out, void* stream);
 
+/* ---- strip solves either side of the path --------------
+ * Fast-diagonalisation factors of the strip operator A - mu I.  The reference
+ * LU-factors every strip kind (proj/src/operator.cpp:113-124) and real-Schur
+ * factors the Helmholtz shifts (proj/src/helmholtz.cpp:58-87); every strip
+ * block is the Kronecker sum Ax_kind (x) I + I (x) Az with Az shared by all
+ * kinds and diagonalised by the spectral basis T of smpm_batch_set_spectral,
+ * so a strip solve is, per z mode, an n x n complex solve along x.  Complex
+ * numbers are (re, im) interleaved; matrices column-major. */
+typedef struct {
+  const double* Vx[3];     /* per strip kind (0: west-boundary strip, 1: interior, 2: east-boundary):
+                              eigenvectors of Ax_kind, n x n complex */
+  const double* Vx_inv[3]; /* their inverses, n x n complex */
+  const double* lx[3];     /* eigenvalues of Ax_kind, n complex */
+  const double* lz;        /* eigenvalues of Az in the spectral basis order (per complex pair the member
+                              with Im > 0, then the real modes): w - npairs complex */
+  const double* tW;        /* n: west-edge trace weights of B = -tau t_X . u (proj/src/operator.cpp:127-151) */
+  const double* tE;        /* n: east-edge trace weights */
+  double tau;              /* penalty (proj/src/operator.cpp:78-82) */
+  const double* mu;        /* nsys Helmholtz shifts k_j^2 (0: Poisson) */
+} smpm_strip_factors;
+int smpm_batch_set_strip_factors(smpm_batch* b, const smpm_strip_factors* f);
+/* b_S = B (A - mu)^{-1} f per system; f: device, nsys x r (r = m_x m_z n^2, reference node order
+ * ((ex m_z + ez) n + ix) n + iz, proj/src/mesh.cpp:27-40); b_S: device nsys x k */
+int smpm_schur_rhs(smpm_batch* b, const double* f, double* b_S, void* stream);             /* proj/src/schur.cpp:182-186 */
+/* u = (A - mu)^{-1} (f - E x_S) per system; f, u: device nsys x r; x_S: device nsys x k */
+int smpm_recover_solution(smpm_batch* b, const double* f, const double* x_S, double* u,
+                          void* stream);                                                    /* proj/src/schur.cpp:227-230 */
+
 /* ---- solves --------------------------------------------------------------- */
 /* Batched solve of S x_S = b_S for every system of the batch with `method`
  * (dbj: proj/src/deflation.cpp:102-122, 2las: :124-143, bj: proj/src/gmres.cpp:144-150,

@@ -25,7 +25,8 @@ EXPORTS = [
     "smpm_batch_coarse_info", "smpm_apply_S", "smpm_apply_St", "smpm_apply_block_jacobi_inv", "smpm_apply_Z",
     "smpm_apply_Zt", "smpm_coarse_solve", "smpm_apply_P", "smpm_apply_Q", "smpm_project_out", "smpm_solve",
     "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_batch_launch_count",
-    "smpm_batch_profile", "smpm_fp64_peak",
+    "smpm_batch_profile", "smpm_fp64_peak", "smpm_batch_set_strip_factors", "smpm_schur_rhs",
+    "smpm_recover_solution",
 ]
 PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other", "cluster_arnoldi", "grid_tail", "spectral_op"]
 
@@ -58,6 +59,20 @@ class SolveOptions(C.Structure):
         ("orth", C.c_int),
         ("fuse_deflation", C.c_int),
         ("final_residual_check", C.c_int),
+    ]
+
+
+class StripFactors(C.Structure):
+    """smpm_strip_factors (fast-diagonalisation factors of the strip operator)."""
+    _fields_ = [
+        ("Vx", C.c_void_p * 3),
+        ("Vx_inv", C.c_void_p * 3),
+        ("lx", C.c_void_p * 3),
+        ("lz", C.c_void_p),
+        ("tW", C.c_void_p),
+        ("tE", C.c_void_p),
+        ("tau", C.c_double),
+        ("mu", C.c_void_p),
     ]
 
 
@@ -102,6 +117,9 @@ def lib():
     L.smpm_batch_launch_count.argtypes = [vp]
     L.smpm_batch_profile.argtypes = [vp, ip, C.POINTER(C.c_double), C.POINTER(C.c_longlong), ip]
     L.smpm_fp64_peak.argtypes = [ip, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.smpm_batch_set_strip_factors.argtypes = [vp, C.POINTER(StripFactors)]
+    L.smpm_schur_rhs.argtypes = [vp, dp, dp, vp]
+    L.smpm_recover_solution.argtypes = [vp, dp, dp, dp, vp]
     _lib = L
     return L
 

@@ -3,6 +3,7 @@
 // plans of every operator, the batched GMRES driver and the C ABI declared in
 // include/smpm_b200.h.
 #include <cuda_runtime.h>
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -27,6 +28,7 @@
 #include "grid.cuh"
 #include "spectral.cuh"
 #include "xform.cuh"
+#include "strip.cuh"
 
 using namespace smpm;
 
@@ -231,6 +233,7 @@ struct smpm_ctx {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;
+  cublasHandle_t blas = nullptr;  // plain library GEMMs of the strip solver when the transform kernel does not apply
 };
 
 struct smpm_batch {
@@ -286,6 +289,12 @@ struct smpm_batch {
   DevArray<double> vbuf[12];
   DevArray<double> dsmall;  // nsys x (d + misc) scalars
   DevArray<double> dcoarse;  // Z^T sums and coarse solutions, 2 x nsys x d
+  DevArray<double> dczb;     // nsys x d: C^{-1} Z^T b_S of the current solve (dbj)
+  // strip solver (strip.cuh): x-factor per strip kind, z eigenvalues, shifts; scratch strip rows
+  bool strip_ok = false;
+  double strip_tau = 0.0;
+  DevArray<double> dsfac, dslz, dsmu, dsx1, dsx2, dsbh;
+  DevArray<double> dpost;    // nsys x 64: post-loop partial sums
   DevArray<int> dones, dcount, dsel, dcnt;
   DevArray<int> dalist;  // two compacted live lists + counts: [alist, acount, alist2, acount2]
   int* hcnt = nullptr;  // pinned, 4 ints (two in-flight step counters)
@@ -950,6 +959,8 @@ void finalize(smpm_batch* b) {
   for (auto& v : b->vbuf) v.alloc(static_cast<size_t>(b->nsys) * b->k);
   b->dsmall.alloc(static_cast<size_t>(b->nsys) * (d + 8));
   b->dcoarse.alloc(static_cast<size_t>(b->nsys) * 2 * d);
+  b->dczb.alloc(static_cast<size_t>(b->nsys) * d);
+  b->dpost.alloc(static_cast<size_t>(b->nsys) * 64);
   std::vector<int> ones(static_cast<size_t>(b->nsys), 1);
   b->dones.upload(ones, st);
   b->dcount.alloc(static_cast<size_t>(b->nsys) + 1);
@@ -1617,6 +1628,10 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   // ---- right-hand side
   if (c.method == SMPM_DBJ) {
     op_P(b, bS, rhs, c.fused, all, st);  // pb = P b_S (proj/src/deflation.cpp:110)
+    // keep c_b = C^{-1} Z^T b_S for the solution (proj/src/deflation.cpp:118-120)
+    if (c.fused)
+      CUDA_CHECK(cudaMemcpyAsync(b->dczb.p, b->dcoarse.p + static_cast<size_t>(ns) * b->d,
+                                 sizeof(double) * ns * b->d, cudaMemcpyDeviceToDevice, st));
   } else {
     CUDA_CHECK(cudaMemcpyAsync(rhs, bS, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
   }
@@ -1792,10 +1807,23 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   if (fuse_post) {
     ProfScope ps7(b, 7, st);
     run_xform(b, true, x, b->dvh.p, all, st);
-    spec_apply(b, true, b->dvh.p, b->dth.p, nullptr, all, st, b->dvh2.p);
+    // dbj: the per-mode pass also yields c = C^{-1} Z^T (S u) for the residual and Q
+    spec_apply(b, true, b->dvh.p, b->dth.p, c.method == SMPM_DBJ ? b->dcoarse.p + static_cast<size_t>(ns) * b->d : nullptr,
+               all, st, b->dvh2.p);
     run_xform(b, false, b->dvh2.p, u, all, st, b->dth.p, tq);
   }
-  if (c.final_check) {
+  const bool post_one_pass = fuse_post && c.method == SMPM_DBJ && std::getenv("SMPM_NO_POST_FUSE") == nullptr;
+  if (post_one_pass) {
+    // final residual + x_S = Q u + Z c_b in one pass (post_dbj_kernel)
+    ProfScope psd(b, PC_DEFL, st);
+    DeflateParams P = deflate_params(b, nullptr);
+    const int gx = static_cast<int>(std::min<long long>((b->k + V2_THREADS * 4 - 1) / (V2_THREADS * 4), 64));
+    post_dbj_kernel<<<dim3(gx, ns), V2_THREADS, 0, st>>>(P, tq, u, rhs, b->dcoarse.p + static_cast<size_t>(ns) * b->d,
+                                                           b->dczb.p, xS, b->dpost.p, b->dcount.p, nrf,
+                                                           c.final_check ? 1 : 0);
+    check_launch(b);
+  }
+  if (c.final_check && !post_one_pass) {
     if (fuse_post && c.method == SMPM_DBJ) {
       run_deflate(b, DEFL_P_FUSED, tq, tq, r, nullptr, all, st);
     } else if (fuse_post) {
@@ -1822,6 +1850,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       break;
     case SMPM_DBJ: {
       double* q = b->vbuf[6].p;
+      if (post_one_pass) break;
       if (fuse_post) {
         run_deflate(b, DEFL_Q_TAIL, tq, u, q, nullptr, all, st);  // Q u = u - Z c(Z^T S u)
       } else if (spec_on(b)) {
@@ -1940,6 +1969,96 @@ SolveCfg cfg_from(int method, const smpm_solve_options* o) {
 // ============================================================================
 // C ABI
 // ============================================================================
+// ---- strip solver ------------------------------------------
+StripParams strip_params(const smpm_batch* b) {
+  StripParams P;
+  P.n = b->n;
+  P.mx = b->mx;
+  P.mz = b->mz;
+  P.w = b->w;
+  P.nmode = b->sp_nmode;
+  P.npairs = b->sp_npairs;
+  P.nsys = b->nsys;
+  P.r = static_cast<long long>(b->mx) * b->mz * b->n * b->n;
+  P.k = b->k;
+  P.fac = reinterpret_cast<const double2*>(b->dsfac.p);
+  P.lz = reinterpret_cast<const double2*>(b->dslz.p);
+  P.mu = b->dsmu.p;
+  P.tau = b->strip_tau;
+  return P;
+}
+
+// out = A in for every w-long column of nsys x ncol_sys columns (system stride
+// sys_stride): the resident-slice transform kernel, or a plain cuBLAS GEMM
+void xf_columns(smpm_batch* b, bool inverse, const double* in, double* out, int ncol_sys, long long sys_stride,
+                cudaStream_t st) {
+  if (b->xf_P > 0) {
+    XformArgs a;
+    a.Af = inverse ? b->dTifrag.p : b->dTfrag.p;
+    a.w = b->w;
+    a.ncol_sys = ncol_sys;
+    a.k = sys_stride;
+    a.alist = nullptr;
+    a.acount = nullptr;
+    a.nslots = b->nsys;
+    a.nv = 1;
+    a.in[0] = in;
+    a.out[0] = out;
+    a.in[1] = nullptr;
+    a.out[1] = nullptr;
+    a.P = b->xf_P;
+    const long long nch = (static_cast<long long>(b->nsys) * ncol_sys + 15) / 16;
+    const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / a.P, nch)));
+    switch (b->xf_MB) {
+      case 4: xform_kernel<4><<<groups * a.P, XF_THREADS, b->xf_smem, st>>>(a); break;
+      case 8: xform_kernel<8><<<groups * a.P, XF_THREADS, b->xf_smem, st>>>(a); break;
+      default: xform_kernel<11><<<groups * a.P, XF_THREADS, b->xf_smem, st>>>(a); break;
+    }
+    check_launch(b);
+    return;
+  }
+  if (sys_stride != static_cast<long long>(ncol_sys) * b->w) fail(SMPM_EINVAL, "strip columns must be contiguous");
+  smpm_ctx* ctx = b->ctx;
+  if (!ctx->blas && cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS) fail(SMPM_ECUDA, "cublasCreate failed");
+  if (cublasSetStream(ctx->blas, st) != CUBLAS_STATUS_SUCCESS) fail(SMPM_ECUDA, "cublasSetStream failed");
+  const double one = 1.0, zero = 0.0;
+  const int w = b->w;
+  const long long ncols = static_cast<long long>(b->nsys) * ncol_sys;
+  if (ncols > INT_MAX) fail(SMPM_EINVAL, "too many strip columns");
+  if (cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, w, static_cast<int>(ncols), w, &one,
+                  inverse ? b->dTi.p : b->dT.p, w, in, w, &zero, out, w) != CUBLAS_STATUS_SUCCESS)
+    fail(SMPM_ECUDA, "cublasDgemm failed");
+}
+
+template <bool TRACES>
+void strip_modes(smpm_batch* b, const double* Xh, double* out, cudaStream_t st) {
+  const StripParams P = strip_params(b);
+  const dim3 grid((P.nmode + 127) / 128, P.mx, P.nsys);
+  switch (P.n) {
+    case 9: strip_modes_kernel<9, TRACES><<<grid, 128, 0, st>>>(P, Xh, out); break;
+    case 11: strip_modes_kernel<11, TRACES><<<grid, 128, 0, st>>>(P, Xh, out); break;
+    case 13: strip_modes_kernel<13, TRACES><<<grid, 128, 0, st>>>(P, Xh, out); break;
+    case 17: strip_modes_kernel<17, TRACES><<<grid, 128, 0, st>>>(P, Xh, out); break;
+    default: fail(SMPM_EINVAL, "strip solver: n must be 9, 11, 13 or 17");
+  }
+  check_launch(b);
+}
+
+void strip_scratch(smpm_batch* b) {
+  const size_t r = static_cast<size_t>(b->mx) * b->mz * b->n * b->n;
+  if (b->dsx1.n < b->nsys * r) {
+    b->dsx1.alloc(b->nsys * r);
+    b->dsx2.alloc(b->nsys * r);
+  }
+  if (b->dsbh.n < static_cast<size_t>(b->nsys) * b->k) b->dsbh.alloc(static_cast<size_t>(b->nsys) * b->k);
+}
+
+void need_strip(smpm_batch* b) {
+  need_final(b);
+  if (!b->strip_ok) fail(SMPM_EINVAL, "strip factors not set (smpm_batch_set_strip_factors)");
+  strip_scratch(b);
+}
+
 extern "C" {
 
 const char* smpm_last_error(void) { return g_last_error.c_str(); }
@@ -1973,6 +2092,7 @@ int smpm_ctx_destroy(smpm_ctx* ctx) {
   return guard([&] {
     if (!ctx) return;
     if (ctx->solver) cusolverDnDestroy(ctx->solver);
+    if (ctx->blas) cublasDestroy(ctx->blas);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -2165,6 +2285,80 @@ int smpm_apply_P(smpm_batch* b, const double* v, double* y, int fused, void* str
   return guard([&] {
     need_final(b);
     op_P(b, v, y, fused != 0, all_systems(b), b->st(stream));
+  });
+}
+
+int smpm_batch_set_strip_factors(smpm_batch* b, const smpm_strip_factors* f) {
+  return guard([&] {
+    if (!b || !f) fail(SMPM_EINVAL, "null argument");
+    if (!b->spectral || b->hT.empty()) fail(SMPM_EINVAL, "strip factors need the spectral basis (smpm_batch_set_spectral)");
+    if (b->mx < 3) fail(SMPM_EINVAL, "strip solver needs m_x >= 3");
+    const int n = b->n;
+    for (int kd = 0; kd < 3; ++kd)
+      if (!f->Vx[kd] || !f->Vx_inv[kd] || !f->lx[kd]) fail(SMPM_EINVAL, "null x factor");
+    if (!f->lz || !f->tW || !f->tE || !f->mu) fail(SMPM_EINVAL, "null strip factor");
+    const int L = strip_fac_len(n);
+    std::vector<double> fac(static_cast<size_t>(3) * L * 2);
+    for (int kd = 0; kd < 3; ++kd) {
+      double* o = fac.data() + static_cast<size_t>(kd) * L * 2;
+      std::copy(f->Vx[kd], f->Vx[kd] + 2 * n * n, o);
+      std::copy(f->Vx_inv[kd], f->Vx_inv[kd] + 2 * n * n, o + 2 * n * n);
+      std::copy(f->lx[kd], f->lx[kd] + 2 * n, o + 4 * n * n);
+      // tW Vx, tE Vx (row vector times the complex eigenvector matrix)
+      for (int p = 0; p < n; ++p) {
+        double wr = 0, wi = 0, er = 0, ei = 0;
+        for (int ix = 0; ix < n; ++ix) {
+          const double vr = f->Vx[kd][2 * (ix + p * n)], vi = f->Vx[kd][2 * (ix + p * n) + 1];
+          wr += f->tW[ix] * vr;
+          wi += f->tW[ix] * vi;
+          er += f->tE[ix] * vr;
+          ei += f->tE[ix] * vi;
+        }
+        o[4 * n * n + 2 * n + 2 * p] = wr;
+        o[4 * n * n + 2 * n + 2 * p + 1] = wi;
+        o[4 * n * n + 4 * n + 2 * p] = er;
+        o[4 * n * n + 4 * n + 2 * p + 1] = ei;
+      }
+    }
+    cudaStream_t st = b->ctx->stream;
+    b->dsfac.upload(fac, st);
+    b->dslz.upload(std::vector<double>(f->lz, f->lz + 2 * static_cast<size_t>(b->sp_nmode)), st);
+    b->dsmu.upload(std::vector<double>(f->mu, f->mu + b->nsys), st);
+    b->strip_tau = f->tau;
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    b->strip_ok = true;
+  });
+}
+
+int smpm_schur_rhs(smpm_batch* b, const double* f, double* b_S, void* stream) {
+  return guard([&] {
+    need_strip(b);
+    if (!f || !b_S) fail(SMPM_EINVAL, "null vector");
+    cudaStream_t st = b->st(stream);
+    const StripParams P = strip_params(b);
+    const long long tot = static_cast<long long>(b->nsys) * P.r;
+    strip_gather_kernel<<<grid_for(tot), 256, 0, st>>>(P, f, nullptr, b->dsx1.p);
+    check_launch(b);
+    xf_columns(b, true, b->dsx1.p, b->dsx2.p, b->mx * b->n, P.r, st);
+    strip_modes<true>(b, b->dsx2.p, b->dsbh.p, st);
+    xf_columns(b, false, b->dsbh.p, b_S, 2 * b->d, b->k, st);
+  });
+}
+
+int smpm_recover_solution(smpm_batch* b, const double* f, const double* x_S, double* u, void* stream) {
+  return guard([&] {
+    need_strip(b);
+    if (!f || !x_S || !u) fail(SMPM_EINVAL, "null vector");
+    cudaStream_t st = b->st(stream);
+    const StripParams P = strip_params(b);
+    const long long tot = static_cast<long long>(b->nsys) * P.r;
+    strip_gather_kernel<<<grid_for(tot), 256, 0, st>>>(P, f, x_S, b->dsx1.p);
+    check_launch(b);
+    xf_columns(b, true, b->dsx1.p, b->dsx2.p, b->mx * b->n, P.r, st);
+    strip_modes<false>(b, b->dsx2.p, b->dsx1.p, st);
+    xf_columns(b, false, b->dsx1.p, b->dsx2.p, b->mx * b->n, P.r, st);
+    strip_scatter_kernel<<<grid_for(tot), 256, 0, st>>>(P, b->dsx2.p, u);
+    check_launch(b);
   });
 }
 

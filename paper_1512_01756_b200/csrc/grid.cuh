@@ -422,16 +422,17 @@ __device__ __forceinline__ void gt_cluster_sum(const double* pin, int n, double*
 }
 
 // every CTA of a group: sum of the group's cluster partials (fixed order,
-// 8 independent loads per round) -> dst[0..n)
+// 16 independent loads per round: one or two L2 round trips for any group) -> dst[0..n)
 __device__ __forceinline__ void gt_group_sum(const double* part, int stride, int c0, int c1, int n, double* dst) {
+  constexpr int R = 16;
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
     double s = 0.0;
-    for (int g0 = c0; g0 < c1; g0 += 8) {
-      double v[8];
+    for (int g0 = c0; g0 < c1; g0 += R) {
+      double v[R];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = g0 + u < c1 ? __ldcg(part + static_cast<long long>(g0 + u) * stride + c) : 0.0;
+      for (int u = 0; u < R; ++u) v[u] = g0 + u < c1 ? __ldcg(part + static_cast<long long>(g0 + u) * stride + c) : 0.0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) s += v[u];
+      for (int u = 0; u < R; ++u) s += v[u];
     }
     dst[c] = s;
   }

@@ -253,4 +253,55 @@ __global__ void __launch_bounds__(V2_THREADS) defl_update_kernel(DeflateParams P
   }
 }
 
+// dbj epilogue in one pass over the batch (spectral fused path):
+//   final residual (proj/src/gmres.cpp:129-136): r = rhs - P t with t = S M^{-1} x',
+//     P t = t - Z c - (S - I) Z c, c = C^{-1} Z^T t (from the per-mode pass); ||r||^2 -> nrf
+//   solution (proj/src/deflation.cpp:118-120): x_S = Q u + Z c_b with u = M^{-1} x',
+//     Q u = u - Z C^{-1} Z^T S u = u - Z c (S u = t: the same coarse solution), c_b = C^{-1} Z^T b_S
+// Per-system ||r||^2: CTA partials summed by the last CTA in chunk order (deterministic).
+__global__ void __launch_bounds__(V2_THREADS)
+post_dbj_kernel(DeflateParams P, const double* __restrict__ t, const double* __restrict__ u,
+                const double* __restrict__ rhs, const double* __restrict__ ct, const double* __restrict__ cb,
+                double* __restrict__ xS, double* __restrict__ part, int* counter, double* __restrict__ nrf, int check) {
+  __shared__ double red[V2_THREADS / 32];
+  int s;
+  if (!defl_slot(P, blockIdx.y, s)) return;
+  const int w = P.w, w2 = 2 * w, mx = P.mx;
+  const int k = static_cast<int>(P.k);
+  const double* c = ct + static_cast<long long>(s) * P.d;
+  const double* c2 = cb + static_cast<long long>(s) * P.d;
+  const long long base = static_cast<long long>(s) * P.k;
+  const double* rs = P.rowsum + static_cast<long long>(s) * 6 * w;
+  const double *rWI = rs, *rEI = rs + w2, *rEW = rs + 2 * w2, *rWE = rEW + w;
+  double sq = 0.0;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k; e += gridDim.x * blockDim.x) {
+    const int blk = e / w, r = e - blk * w, i = blk >> 1;
+    xS[base + e] = (u[base + e] - c[i]) + c2[i];
+    if (check) {
+      double sz;
+      if ((blk & 1) == 0)
+        sz = (i + 1 == mx - 1) ? c[i] * rWE[r] : c[i] * rWI[r] + c[i + 1] * rEI[r];
+      else
+        sz = (i == 0) ? c[i] * rEW[r] : c[i - 1] * rWI[w + r] + c[i] * rEI[w + r];
+      const double rr = rhs[base + e] - (t[base + e] - (c[i] + sz));
+      sq = fma(rr, rr, sq);
+    }
+  }
+  if (!check) return;
+  sq = warp_sum(sq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int q = 0; q < V2_THREADS / 32; ++q) a += red[q];
+    part[static_cast<long long>(s) * gridDim.x + blockIdx.x] = a;
+  }
+  if (!last_cta(counter + s, gridDim.x)) return;
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int q = 0; q < static_cast<int>(gridDim.x); ++q) a += __ldcg(part + static_cast<long long>(s) * gridDim.x + q);
+    nrf[s] = a;
+  }
+}
+
 }  // namespace smpm

@@ -237,6 +237,18 @@ class StripFDM:
             out[:, i, :] = self.gamma(key, XY, mus).cpu().numpy()[:, rep]
         return npairs, T, Ti, out
 
+    def strip_factors(self, mus):
+        """smpm_strip_factors of this geometry for shifts `mus`: x factors per strip
+        kind (west-boundary, interior, east-boundary), z eigenvalues in the
+        spectral basis order, trace weights, tau."""
+        _, _, _, rep = self.real_basis()
+        keys = ((False, True), (True, True), (True, False))
+        kd = [self.kinds[k] for k in keys]
+        return dict(Vx=[k["Vx"] for k in kd], Vx_inv=[k["Vxi"] for k in kd], lx=[k["lx"] for k in kd],
+                    lz=np.asarray(self.lz)[rep], tW=self.kinds[(True, True)]["tW"],
+                    tE=self.kinds[(True, True)]["tE"], tau=self.tau,
+                    mu=np.atleast_1d(np.asarray(mus, dtype=np.float64)))
+
     def _block(self, gam):
         # Vz diag(gam) Vz^{-1} for a batch of diagonals -> real (M, w, w)
         t = self.torch

@@ -119,6 +119,31 @@ def manufactured(geo: Geometry, kmax: int, decay: bool, seed: int = 1234, stream
     return f, u
 
 
+def manufactured_batch(geo: Geometry, kmax: int, decay: bool, seed: int, streams, mus, device):
+    """f = (Lap - mu) u of `manufactured` for several (stream, mu) at once, on
+    `device` (torch, nsys x r): the same seeded coefficients and formula."""
+    import torch
+
+    x, z = node_coords(geo)
+    kk = np.arange(kmax + 1) * math.pi / geo.l_x
+    ll = np.arange(kmax + 1) * math.pi / geo.l_z
+    cx = torch.cos(torch.outer(torch.tensor(x, device=device), torch.tensor(kk, device=device)))  # (r, K)
+    cz = torch.cos(torch.outer(torch.tensor(z, device=device), torch.tensor(ll, device=device)))
+    out = torch.empty((len(streams), x.size), dtype=torch.float64, device=device)
+    for i, (st, mu) in enumerate(zip(streams, mus)):
+        rng = Rng(seed).stream(st)
+        a = np.zeros((kmax + 1, kmax + 1))
+        for k in range(kmax + 1):
+            for l in range(kmax + 1):
+                c = rng.normal()
+                if decay:
+                    c /= 1.0 + k * k + l * l
+                a[k, l] = c
+        lap = -(kk[:, None] ** 2 + ll[None, :] ** 2 + mu) * a
+        out[i] = ((cx @ torch.tensor(lap, device=device)) * cz).sum(dim=1)
+    return out
+
+
 @dataclass
 class ProblemSet:
     """Everything a SchurBatch needs for a set of systems of one config."""
@@ -130,13 +155,16 @@ class ProblemSet:
     GE: np.ndarray
     u_S: np.ndarray | None
     u_L: np.ndarray | None
-    b_S: np.ndarray  # (nsys, k)
+    b_S: np.ndarray  # (nsys, k); None until load_batch computes it on the device (device_rhs)
     fdm: StripFDM
+    f: object = None  # device_rhs: torch (nsys, r) forcing (mode 0 already projected with u_L)
 
 
-def build_problem(cfg: Config, modes=None, device=None) -> ProblemSet:
+def build_problem(cfg: Config, modes=None, device=None, device_rhs=False) -> ProblemSet:
     """Product setup for `modes` of a 3D config (all modes by default) or the
-    single system of a 2D config."""
+    single system of a 2D config.  device_rhs: the seeded forcings are built on
+    the device and b_S = B (A - mu)^{-1} f is left to load_batch, which runs it
+    through the C ABI's schur_rhs (strip.cuh) instead of the host FDM."""
     geo = Geometry(cfg.n, cfg.m_x, cfg.m_z, cfg.l_x, cfg.l_z, cfg.c_tau)
     F = StripFDM(geo, device)
     mus_all = cfg.mus()
@@ -147,6 +175,16 @@ def build_problem(cfg: Config, modes=None, device=None) -> ProblemSet:
     u_S = u_L = None
     if any(mu == 0.0 for mu in mus):
         u_S, u_L = F.nullspace()
+    if device_rhs:
+        import torch
+
+        f = manufactured_batch(geo, cfg.kmax, cfg.decay, cfg.seed, modes, mus, device)
+        if u_L is not None:
+            uL = torch.tensor(u_L, device=device)
+            for i, mu in enumerate(mus):
+                if mu == 0.0:
+                    f[i] -= uL * torch.dot(uL, f[i])
+        return ProblemSet(cfg, list(modes), mus, GW, GI, GE, u_S, u_L, None, F, f)
     bs = []
     for m, mu in zip(modes, mus):
         f, _ = manufactured(geo, cfg.kmax, cfg.decay, cfg.seed, m, mu=mu)
@@ -173,4 +211,20 @@ def load_batch(ctx, ps: ProblemSet, spectral: bool = True):
     if spectral:
         npairs, T, Ti, gam = ps.fdm.spectral(ps.mus)
         b.set_spectral(npairs, T, Ti, gam)
-    return b.finalize()
+    b.finalize()
+    if spectral and b.m_x >= 3 and b.n in (9, 11, 13, 17):
+        b.set_strip_factors(ps.fdm.strip_factors(ps.mus))
+    if ps.b_S is None:
+        # device b_S = B (A - mu)^{-1} f, then the mode-0 projection with u_S
+        # (proj/src/helmholtz.cpp:159-176)
+        import torch
+
+        bS = b.schur_rhs(ps.f)
+        if ps.u_S is not None:
+            sing = torch.tensor([mu == 0.0 for mu in ps.mus], device=bS.device)
+            uS = torch.tensor(ps.u_S, device=bS.device)
+            dirs = torch.where(sing[:, None], uS[None, :], torch.zeros_like(uS)[None, :]).contiguous()
+            bS = b.project_out(bS, dirs)
+        torch.cuda.synchronize()
+        ps.b_S = bS.cpu().numpy()
+    return b

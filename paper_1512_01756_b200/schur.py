@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import METHODS, ORTH, Report, SmpmError, SolveOptions, check, lib
+from ._lib import METHODS, ORTH, Report, SmpmError, SolveOptions, StripFactors, check, lib
 
 
 def _torch():
@@ -137,6 +137,37 @@ class SchurBatch:
             raise SmpmError(1, "u_S must have length k")
         check(lib().smpm_batch_set_nullspace(self.h, sys, _hptr(u)))
 
+    def set_strip_factors(self, fac: dict):
+        """Fast-diagonalisation factors of the strip operator (smpm_batch_set_strip_factors):
+        fac from StripFDM.strip_factors(mus) — Vx, Vx_inv, lx (3 kinds each, complex),
+        lz (nmode complex), tW, tE (n), tau, mu (nsys)."""
+        keep = []
+
+        def cplx(a):
+            a = np.ascontiguousarray(np.asarray(a, dtype=np.complex128).reshape(-1, order="F"))
+            keep.append(a)
+            return a.ctypes.data
+
+        def real(a):
+            a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+            keep.append(a)
+            return a.ctypes.data
+
+        sf = StripFactors()
+        for i in range(3):
+            sf.Vx[i] = cplx(fac["Vx"][i])
+            sf.Vx_inv[i] = cplx(fac["Vx_inv"][i])
+            sf.lx[i] = cplx(fac["lx"][i])
+        sf.lz = cplx(fac["lz"])
+        sf.tW = real(fac["tW"])
+        sf.tE = real(fac["tE"])
+        sf.tau = float(fac["tau"])
+        mu = np.asarray(fac["mu"], dtype=np.float64)
+        if mu.size != self.nsys:
+            raise SmpmError(1, "mu must have one shift per system")
+        sf.mu = real(mu)
+        check(lib().smpm_batch_set_strip_factors(self.h, C.byref(sf)))
+
     def finalize(self):
         check(lib().smpm_batch_finalize(self.h))
         return self
@@ -204,6 +235,26 @@ class SchurBatch:
         y = torch.empty_like(v)
         check(lib().smpm_project_out(self.h, C.c_longlong(self.k), _dptr(v), _dptr(dr), _dptr(y), self._stream()))
         return y
+
+    # ---- strip solves -------------------------------------
+    @property
+    def r(self):
+        return self.m_x * self.m_z * self.n * self.n
+
+    def schur_rhs(self, f):  # proj/src/schur.cpp:182-186
+        torch = _torch()
+        f = self._vec(f, self.r)
+        y = torch.empty((self.nsys, self.k), dtype=torch.float64, device=f.device)
+        check(lib().smpm_schur_rhs(self.h, _dptr(f), _dptr(y), self._stream()))
+        return y
+
+    def recover_solution(self, f, x_S):  # proj/src/schur.cpp:227-230
+        torch = _torch()
+        f = self._vec(f, self.r)
+        x = self._vec(x_S, self.k)
+        u = torch.empty((self.nsys, self.r), dtype=torch.float64, device=f.device)
+        check(lib().smpm_recover_solution(self.h, _dptr(f), _dptr(x), _dptr(u), self._stream()))
+        return u
 
     # ---- solves -----------------------------------------------------------
     @staticmethod
