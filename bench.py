@@ -305,7 +305,11 @@ def run_ours(args, cfg):
 
     # 3D configs: modes sharded round-robin; 2D configs: replicas only
     modes = shard_modes(nm, ws, rank) if cfg.modes else [0]
-    ps = build_problem(cfg, modes, device=f"cuda:{local}", device_rhs=True)
+    # b_S from the host FDM setup (the workload's definition since round 1): the
+    # device schur_rhs agrees to ~1e-13, but 17 of the 128 C4 modes stagnate near
+    # the 1e-10 target and their iteration counts move with O(1e-13) changes of
+    # b_S, so the measured workload keeps one fixed b_S
+    ps = build_problem(cfg, modes, device=f"cuda:{local}")
     ctx = Context(local)
     b = load_batch(ctx, ps)
     bS = torch.tensor(ps.b_S, device=dev)

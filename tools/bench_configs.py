@@ -108,7 +108,7 @@ def main():
             continue
         sp = bench.solve_params(cfg)
         t0 = time.perf_counter()
-        ps = build_problem(cfg, device="cuda", device_rhs=True)
+        ps = build_problem(cfg, device="cuda")  # host FDM b_S, as bench.py
         b = load_batch(ctx, ps)
         setup_s = time.perf_counter() - t0
         bS = torch.tensor(ps.b_S, device="cuda")
