@@ -297,7 +297,8 @@ struct smpm_batch {
   DevArray<double> dpost;    // nsys x 64: post-loop partial sums
   DevArray<int> dones, dcount, dsel, dcnt;
   DevArray<int> dalist;  // two compacted live lists + counts: [alist, acount, alist2, acount2]
-  int* hcnt = nullptr;  // pinned, 4 ints (two in-flight step counters)
+  int* hcnt = nullptr;      // pinned + mapped, 4 ints (two in-flight step counters)
+  int* hcnt_dev = nullptr;  // device alias of hcnt: compact_kernel writes the counters straight to the host
   void* hrep = nullptr;  // pinned report staging
   size_t hrep_bytes = 0;
   cudaEvent_t sev[4] = {nullptr, nullptr, nullptr, nullptr};  // solve events (timing x2, step polling x2)
@@ -969,7 +970,8 @@ void finalize(smpm_batch* b) {
   b->dalist.alloc(2 * static_cast<size_t>(b->nsys) + 2);
   b->dclq.alloc(1 + kMaxClusters);
   b->dcnt.alloc(4);
-  CUDA_CHECK(cudaMallocHost(&b->hcnt, 4 * sizeof(int)));
+  CUDA_CHECK(cudaHostAlloc(&b->hcnt, 4 * sizeof(int), cudaHostAllocMapped));
+  CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&b->hcnt_dev), b->hcnt, 0));
   CUDA_CHECK(cudaStreamSynchronize(st));
   b->finalized = true;
 }
@@ -1704,9 +1706,9 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     lv.active = G.active;
     arnoldi_step(b, c, lv, st);
     ++steps;
-    compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->dcnt.p + 2 * slot);
+    // live / cycle-end counts go straight into mapped host memory (no copy in the stream)
+    compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->hcnt_dev + 2 * slot);
     check_launch(b);
-    CUDA_CHECK(cudaMemcpyAsync(hcnt + 2 * slot, b->dcnt.p + 2 * slot, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaEventRecord(ev[slot], st));
   };
   // few live systems: the rest of the cycle runs grid-persistent (grid.cuh)
@@ -1752,9 +1754,8 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       if (nrun > 0) {
         arnoldi_grid(b, c, alist, acount, st);
         ++steps;
-        compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->dcnt.p + 2 * cur);
+        compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->hcnt_dev + 2 * cur);
         check_launch(b);
-        CUDA_CHECK(cudaMemcpyAsync(hcnt + 2 * cur, b->dcnt.p + 2 * cur, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
         CUDA_CHECK(cudaStreamSynchronize(st));
         nrun = hcnt[2 * cur];
         ncyc = hcnt[2 * cur + 1];

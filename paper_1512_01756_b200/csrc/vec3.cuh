@@ -17,28 +17,36 @@ namespace smpm {
 constexpr int V3_THREADS = 256;
 constexpr int V3_GRP = 8;  // columns per register group
 
-// partial dots over rows [r0, r1) of V_s[:, 0..ncols) with x -> out[0..ncols)
+constexpr int V3_NR = 2;   // rows per thread per round (stride V3_THREADS)
+
+// partial dots over rows [r0, r1) of V_s[:, 0..ncols) with x -> out[0..ncols).
+// Thread t accumulates rows r0 + t, r0 + t + 256, ... in that order, V3_NR rows
+// per round with every load of the round independent; columns past ncols are
+// not loaded.
 __device__ __forceinline__ void cta_dots_long(const double* __restrict__ Vs, long long k, int ncols,
                                               const double* x, int r0, int r1, double* __restrict__ out,
                                               double (*red)[V3_GRP]) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int c0 = 0; c0 < ncols; c0 += V3_GRP) {
+    const int nc = min(V3_GRP, ncols - c0);
     double acc[V3_GRP];
 #pragma unroll
     for (int u = 0; u < V3_GRP; ++u) acc[u] = 0.0;
-    for (int r = r0 + t; r < r1; r += 2 * V3_THREADS) {
-      const int r2 = r + V3_THREADS;
-      const bool two = r2 < r1;
-      const double x0 = __ldcg(x + r), x1 = two ? __ldcg(x + r2) : 0.0;
-      double v0[V3_GRP], v1[V3_GRP];
+    for (int r = r0 + t; r < r1; r += V3_NR * V3_THREADS) {
+      double xv[V3_NR], v[V3_NR][V3_GRP];
 #pragma unroll
-      for (int u = 0; u < V3_GRP; ++u) {
-        const double* col = Vs + static_cast<long long>(min(c0 + u, ncols - 1)) * k;
-        v0[u] = __ldcg(col + r);
-        v1[u] = two ? __ldcg(col + r2) : 0.0;
+      for (int q = 0; q < V3_NR; ++q) {
+        const int rq = r + q * V3_THREADS;
+        const bool ok = rq < r1;
+        xv[q] = ok ? __ldcg(x + rq) : 0.0;
+#pragma unroll
+        for (int u = 0; u < V3_GRP; ++u)
+          v[q][u] = (ok && u < nc) ? __ldcg(Vs + static_cast<long long>(c0 + u) * k + rq) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < V3_GRP; ++u) acc[u] = fma(v1[u], x1, fma(v0[u], x0, acc[u]));
+      for (int q = 0; q < V3_NR; ++q)
+#pragma unroll
+        for (int u = 0; u < V3_GRP; ++u) acc[u] = fma(v[q][u], xv[q], acc[u]);
     }
 #pragma unroll
     for (int u = 0; u < V3_GRP; ++u) {
@@ -57,6 +65,8 @@ __device__ __forceinline__ void cta_dots_long(const double* __restrict__ Vs, lon
 }
 
 // w[r] -= sum_c V[r, c] h[c] over rows [r0, r1); returns sum of squares of the new rows
+// (two rows per thread and round; per row, even / odd columns accumulate
+// separately in column order; columns past ncols are not loaded)
 __device__ __forceinline__ double rows_update_long(const double* __restrict__ Vs, long long k, int ncols,
                                                    const double* h, double* ws, int r0, int r1) {
   double sq = 0.0;
@@ -65,16 +75,17 @@ __device__ __forceinline__ double rows_update_long(const double* __restrict__ Vs
     const bool two = r2 < r1;
     double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
     for (int c0 = 0; c0 < ncols; c0 += V3_GRP) {
+      const int nc = min(V3_GRP, ncols - c0);
       double v0[V3_GRP], v1[V3_GRP];
 #pragma unroll
       for (int u = 0; u < V3_GRP; ++u) {
-        const double* col = Vs + static_cast<long long>(min(c0 + u, ncols - 1)) * k;
-        v0[u] = __ldcg(col + r);
-        v1[u] = two ? __ldcg(col + r2) : 0.0;
+        const double* col = Vs + static_cast<long long>(c0 + u) * k;
+        v0[u] = u < nc ? __ldcg(col + r) : 0.0;
+        v1[u] = (two && u < nc) ? __ldcg(col + r2) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < V3_GRP; u += 2) {
-        const double h0 = c0 + u < ncols ? h[c0 + u] : 0.0, h1 = c0 + u + 1 < ncols ? h[c0 + u + 1] : 0.0;
+        const double h0 = u < nc ? h[c0 + u] : 0.0, h1 = u + 1 < nc ? h[c0 + u + 1] : 0.0;
         a0 = fma(v0[u], h0, a0);
         a1 = fma(v0[u + 1], h1, a1);
         b0 = fma(v1[u], h0, b0);
