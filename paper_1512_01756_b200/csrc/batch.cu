@@ -270,7 +270,8 @@ struct smpm_batch {
   DevArray<double> dT, dTi, domega, dgam, dzpart, dvh, dvh2, dth, dkinv;
   Plan pF, pB;
   DevArray<double> dTfrag, dTifrag;    // T, T^{-1} in the xform fragment order
-  int xf_P = 0, xf_MB = 0;  // resident-slice transform kernel (xform.cuh); 0: use pF/pB
+  int xf_P = 0, xf_MB = 0;
+  bool pdl = true;  // programmatic dependent launch for the Arnoldi step chain (SMPM_NO_PDL=1: off)  // resident-slice transform kernel (xform.cuh); 0: use pF/pB
   size_t xf_smem = 0;
   Plan pc[6];          // unsplit per-system templates (BJ1, BJ2, BJ3, S; spectral F, B) for the persistent solvers
   bool cluster_ok = false;
@@ -344,6 +345,25 @@ namespace {
 void check_launch(smpm_batch* b) {
   ++b->launches;
   CUDA_CHECK(cudaGetLastError());
+}
+
+// launch `kern` with programmatic stream serialization (common.cuh pdl_wait /
+// pdl_launch): used for the kernel chain of an Arnoldi step
+template <typename... KArgs, typename... Args>
+void launch_pdl(smpm_batch* b, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = b->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+  check_launch(b);
 }
 
 // kernel classes for the optional timing
@@ -1158,11 +1178,10 @@ void run_xform(smpm_batch* b, bool inverse, const double* in, double* out, const
   const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / a.P, nch)));
   const dim3 grid(groups * a.P);
   switch (b->xf_MB) {
-    case 4: xform_kernel<4><<<grid, XF_THREADS, b->xf_smem, st>>>(a); break;
-    case 8: xform_kernel<8><<<grid, XF_THREADS, b->xf_smem, st>>>(a); break;
-    default: xform_kernel<11><<<grid, XF_THREADS, b->xf_smem, st>>>(a); break;
+    case 4: launch_pdl(b, xform_kernel<4>, grid, dim3(XF_THREADS), b->xf_smem, st, a); break;
+    case 8: launch_pdl(b, xform_kernel<8>, grid, dim3(XF_THREADS), b->xf_smem, st, a); break;
+    default: launch_pdl(b, xform_kernel<11>, grid, dim3(XF_THREADS), b->xf_smem, st, a); break;
   }
-  check_launch(b);
 }
 
 // th = S^ M^^{-1} vh (bj) or S^ vh in T-coordinates; with cout, also
@@ -1178,10 +1197,9 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
   const size_t shm = cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0;
   double* zp = cout ? b->dzpart.p : nullptr;
   if (bj)
-    spec_op_kernel<true><<<grid, SP_THREADS, shm, st>>>(sp, vh, th, P, zp, b->dcount.p, cout, uh);
+    launch_pdl(b, spec_op_kernel<true>, grid, dim3(SP_THREADS), shm, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);
   else
-    spec_op_kernel<false><<<grid, SP_THREADS, shm, st>>>(sp, vh, th, P, zp, b->dcount.p, cout, uh);
-  check_launch(b);
+    launch_pdl(b, spec_op_kernel<false>, grid, dim3(SP_THREADS), shm, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);
 }
 
 // u = M^{-1} v through the spectral form, and (su != nullptr) S u as well
@@ -1301,23 +1319,21 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
     Gl.nchunk = static_cast<int>((b->k + chunk - 1) / chunk);
     dim3 cgrid(Gl.nchunk, lv.nslots);
     DeflateParams P = deflate_params(b, nullptr);
-    cgs3_dot_kernel<<<cgrid, V3_THREADS, 0, st>>>(Gl, V, wv, tdefl, P, cbuf);
-    check_launch(b);
-    cgs3_update_kernel<false><<<cgrid, V3_THREADS, 0, st>>>(Gl, V, wv);
-    check_launch(b);
-    cgs3_update_kernel<true><<<cgrid, V3_THREADS, 0, st>>>(Gl, V, wv);
-    check_launch(b);
+    launch_pdl(b, cgs3_dot_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, tdefl, P, cbuf);
+    launch_pdl(b, cgs3_update_kernel<false>, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv);
+    launch_pdl(b, cgs3_update_kernel<true>, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv);
   }
   (void)hsm;
   dim3 sg(std::max(1, std::min(G.nchunk, 64)), lv.nslots);
-  gm_scale_kernel<<<sg, 256, 0, st>>>(G, V, wv, vin);
-  check_launch(b);
+  launch_pdl(b, gm_scale_kernel, sg, dim3(256), 0, st, G, V, wv, vin);
 }
 
 // Compacted list of live systems (ascending index, so deterministic) from a
 // flag array, plus RUN / CYCLE state counts for the host; single CTA.
 __global__ void __launch_bounds__(1024) compact_kernel(const int* flags, const int* state, int nsys, int* alist,
                                                        int* acount, int* counts) {
+  pdl_wait();
+  pdl_launch();
   __shared__ int wsum[32];
   __shared__ int base, run, cyc;
   if (threadIdx.x == 0) {
@@ -1589,6 +1605,7 @@ void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
 void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_report* reps, double* history,
            cudaStream_t st) {
   need_final(b);
+  b->pdl = std::getenv("SMPM_NO_PDL") == nullptr;
   if (c.max_iter < 1) fail(SMPM_EINVAL, "max_iter must be >= 1");
   const int mtot = static_cast<int>(std::min<long long>(c.max_iter, b->k));
   int m = c.restart > 0 ? std::min(c.restart, mtot) : mtot;
@@ -1707,8 +1724,8 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     arnoldi_step(b, c, lv, st);
     ++steps;
     // live / cycle-end counts go straight into mapped host memory (no copy in the stream)
-    compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->hcnt_dev + 2 * slot);
-    check_launch(b);
+    launch_pdl(b, compact_kernel, dim3(1), dim3(1024), 0, st, static_cast<const int*>(G.active),
+               static_cast<const int*>(G.state), ns, alist, acount, b->hcnt_dev + 2 * slot);
     CUDA_CHECK(cudaEventRecord(ev[slot], st));
   };
   // few live systems: the rest of the cycle runs grid-persistent (grid.cuh)

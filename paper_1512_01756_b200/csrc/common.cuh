@@ -48,6 +48,14 @@ struct GemmTile {
   int ks;  // K-split index
 };
 
+// Programmatic dependent launch (kernels of one Arnoldi step are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel first waits for
+// the grid before it (all of its memory operations visible), then lets the next
+// kernel of the stream start launching so its CTAs are resident when this one
+// drains. Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BN = 32;
 constexpr int GEMM_BK = 16;

@@ -273,6 +273,8 @@ template <bool BJ>
 __global__ void __launch_bounds__(SP_THREADS) spec_op_kernel(SpecParams sp, const double* __restrict__ vh,
                                                              double* __restrict__ th, DeflateParams P, double* zpart,
                                                              int* counter, double* cout, double* __restrict__ uh) {
+  pdl_wait();
+  pdl_launch();
   extern __shared__ double sm[];  // 2 d doubles (coarse solve)
   int s;
   if (!defl_slot(P, blockIdx.y, s)) return;

@@ -463,6 +463,8 @@ __device__ void givens_step(GmState_& G, int s, int j, double nrm) {
 // v_{j+1} = w / ||w|| into V[:, jcyc] and the operator input buffer
 __global__ void gm_scale_kernel(GmState_ G, double* __restrict__ V, const double* __restrict__ w,
                                 double* __restrict__ vin) {
+  pdl_wait();
+  pdl_launch();
   int s;
   if (!gm_slot(G, blockIdx.y, s)) return;
   const double inv = 1.0 / G.nrm[s];

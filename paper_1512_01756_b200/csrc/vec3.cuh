@@ -108,6 +108,8 @@ __device__ __forceinline__ double rows_update_long(const double* __restrict__ Vs
 __global__ void __launch_bounds__(V3_THREADS) cgs3_dot_kernel(GmState_ G, const double* __restrict__ V, double* w,
                                                               const double* __restrict__ tdefl, DeflateParams P,
                                                               const double* __restrict__ cbuf) {
+  pdl_wait();
+  pdl_launch();
   __shared__ double red[V3_THREADS / 32][V3_GRP];
   int s;
   if (!gm_slot(G, blockIdx.y, s)) return;
@@ -145,6 +147,8 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_dot_kernel(GmState_ G, const 
 // ---- pass 2 (w -= V h1 ; h2 = V^T w) / pass 3 (w -= V h2 ; ||w|| + Givens) ----
 template <bool NORM>
 __global__ void __launch_bounds__(V3_THREADS) cgs3_update_kernel(GmState_ G, const double* __restrict__ V, double* w) {
+  pdl_wait();
+  pdl_launch();
   __shared__ double hs[V2_MAXCOL];
   __shared__ double red[V3_THREADS / 32][V3_GRP];
   int s;

@@ -203,6 +203,8 @@ __device__ __forceinline__ void xf_warp(const XformArgs& a, const double* Af, do
 // smem: Af[w/8][MB][32] double2 (A slice, fragment order) | ring[XF_NS][XF_NT][xf_bstr(w/2)]
 template <int MB>
 __global__ void __launch_bounds__(XF_THREADS, 1) xform_kernel(XformArgs a) {
+  pdl_wait();
+  pdl_launch();
   extern __shared__ __align__(16) double xf_smem[];
   const int t = threadIdx.x, warp = t >> 5;
   const int K8 = a.w >> 3;
