@@ -227,7 +227,7 @@ def run_reference(args, cfg):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-def algorithmic_counts(cfg, its, grid_max=16):
+def algorithmic_counts(cfg, its, grid_max=8):
     """Algorithmic FLOPs and HBM bytes of one batched solve,
     from the per-system iteration counts `its` of that solve.
 

@@ -1487,6 +1487,8 @@ int grid_blocks(smpm_batch* b) {
   CUDA_CHECK(cudaOccupancyMaxActiveClusters(&ncl, arnoldi_grid_kernel, &cfg));
   if (ncl < 1) fail(SMPM_ECUDA, "grid tail kernel cannot be resident");
   b->gt_blocks = std::min(want / GT_CL, ncl) * GT_CL;
+  if (const char* e = std::getenv("SMPM_GT_CTAS"))  // experiment: cap the tail grid (multiple of the cluster size)
+    b->gt_blocks = std::max(GT_CL, std::min(b->gt_blocks, std::atoi(e) / GT_CL * GT_CL));
   return b->gt_blocks;
 }
 
@@ -1731,7 +1733,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   // few live systems: the rest of the cycle runs grid-persistent (grid.cuh)
   const bool use_grid = b->grid_ok && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= GT_MAXCOL &&
                         (c.method != SMPM_DBJ || c.fused) && std::getenv("SMPM_NO_GRID") == nullptr;
-  int grid_max = 16;
+  int grid_max = 8;  // measured on C4 with the PDL step chain: 8-10 live systems is the crossover
   if (const char* e = std::getenv("SMPM_GRID_MAX")) grid_max = std::max(0, std::min(GT_MAXSYS, std::atoi(e)));
   if (use_grid) grid_max = std::min(grid_max, grid_blocks(b) / GT_CL);  // one cluster per live system at least
   auto restart = [&](int ncycv) {

@@ -40,7 +40,13 @@ constexpr int GT_MAXSYS = 32;   // live systems one tail launch may carry
 constexpr int GT_MAXCOL = 128;  // cycle length + 2
 constexpr int GT_CL = 8;        // CTAs per cluster (= K splits of a tail tile)
 constexpr int GT_GVR = 32;      // rows of a cluster GEMV item
-constexpr int GT_STAGES = 4;    // cp.async ring depth of the operator tiles
+#ifndef GT_STAGES_DEF
+#define GT_STAGES_DEF 4
+#endif
+#ifndef GT_MINB
+#define GT_MINB 1
+#endif
+constexpr int GT_STAGES = GT_STAGES_DEF;  // cp.async ring depth of the operator tiles
 constexpr int GT_SMEM =
     GT_STAGES * (G2_BK * (G2_BM + G2_APAD) + G2_BN * (G2_BK + G2_BPAD)) * static_cast<int>(sizeof(double));
 static_assert(GT_SMEM >= G2_BM * G2_BN * static_cast<int>(sizeof(double)), "tile partial must fit the ring");
@@ -458,7 +464,7 @@ __device__ __forceinline__ void gt_spec(const GridArgs& a, const int* sl, int L,
   }
 }
 
-__global__ void __launch_bounds__(G2_THREADS) arnoldi_grid_kernel(GridArgs a) {
+__global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridArgs a) {
   extern __shared__ __align__(16) double gt_smem[];
   double* gsmem = gt_smem;                // GT_SMEM bytes: tile pipeline / tile partial
   double* hs = gt_smem + GT_SMEM / 8;     // GT_MAXCOL: h1 of this CTA's system
