@@ -206,7 +206,9 @@ int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x
 long long smpm_batch_launch_count(const smpm_batch* b);
 
 /* Optional device timing of kernel classes (0 Schur GEMM, 1 block-Jacobi
- * GEMMs, 2 deflation, 3 Arnoldi orthogonalization, 4 other), measured with
+ * GEMMs, 2 deflation, 3 Arnoldi orthogonalization, 4 other, 5 cluster-persistent
+ * Arnoldi, 6 grid-persistent tail, 7 spectral per-mode pass, 8 shared-matrix
+ * transforms, 9 reserved; nclass <= 10), measured with
  * CUDA events on the launching stream during solves/operators. Reads the
  * accumulated milliseconds/launch counts (nullable), then, if enable >= 0,
  * resets them and turns timing on (1) or off (0). */

@@ -28,7 +28,8 @@ EXPORTS = [
     "smpm_batch_profile", "smpm_fp64_peak", "smpm_batch_set_strip_factors", "smpm_schur_rhs",
     "smpm_recover_solution",
 ]
-PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other", "cluster_arnoldi", "grid_tail", "spectral_op"]
+PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other", "cluster_arnoldi", "grid_tail",
+                   "spectral_op", "transform", "reserved"]
 
 
 class SmpmError(RuntimeError):

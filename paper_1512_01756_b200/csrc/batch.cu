@@ -329,8 +329,8 @@ struct smpm_batch {
     cudaEvent_t a, b;
   };
   std::vector<Span> spans;
-  double prof_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long prof_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double prof_ms[10] = {};  // per kernel class (see PROFILE_CLASSES in _lib.py)
+  long long prof_n[10] = {};
 
   cudaStream_t st(void* s) const { return s ? static_cast<cudaStream_t>(s) : ctx->stream; }
   double* GW(int s) const { return dmat.p + s * mstride + oGW; }
@@ -1154,6 +1154,7 @@ void setup_xform(smpm_batch* b) {
 void run_xform(smpm_batch* b, bool inverse, const double* in, double* out, const Live& lv, cudaStream_t st,
                const double* in2 = nullptr, double* out2 = nullptr) {
   if (lv.nslots == 0) return;
+  ProfScope psx(b, 8, st);  // class 8: shared-matrix transforms
   if (b->xf_P == 0) {
     run_plan(b, inverse ? b->pF : b->pB, in, out, nullptr, lv, st);
     if (in2) run_plan(b, inverse ? b->pF : b->pB, in2, out2, nullptr, lv, st);
@@ -1189,6 +1190,7 @@ void run_xform(smpm_batch* b, bool inverse, const double* in, double* out, const
 void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* cout, const Live& lv, cudaStream_t st,
                 double* uh = nullptr) {
   if (lv.nslots == 0) return;
+  ProfScope ps(b, 7, st);  // class 7: per-mode pass
   const SpecParams sp = spec_params(b);
   DeflateParams P = deflate_params(b, lv.active);
   P.alist = lv.alist;
@@ -1204,7 +1206,6 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
 
 // u = M^{-1} v through the spectral form, and (su != nullptr) S u as well
 void spec_Minv(smpm_batch* b, const double* v, double* u, double* su, const Live& lv, cudaStream_t st) {
-  ProfScope ps(b, 7, st);
   run_xform(b, true, v, b->dvh.p, lv, st);
   spec_apply(b, true, b->dvh.p, su ? b->dth.p : nullptr, nullptr, lv, st, b->dvh2.p);
   run_xform(b, false, b->dvh2.p, u, lv, st, su ? b->dth.p : nullptr, su);
@@ -1218,7 +1219,6 @@ bool spec_ok(const smpm_batch* b, const SolveCfg& c) {
 
 // S M^{-1} v (bj) or S v through the spectral form; out may be any buffer
 void spec_SMinv(smpm_batch* b, bool bj, const double* v, double* out, double* cout, const Live& lv, cudaStream_t st) {
-  ProfScope ps(b, 7, st);  // class 7: spectral operator
   run_xform(b, true, v, b->dvh.p, lv, st);
   spec_apply(b, bj, b->dvh.p, b->dth.p, cout, lv, st);
   run_xform(b, false, b->dth.p, out, lv, st);
@@ -1825,7 +1825,6 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   double* tq = b->vbuf[5].p;
   const bool fuse_post = spec_ok(b, c) && ((c.method == SMPM_DBJ && c.fused) || c.method == SMPM_BJ);
   if (fuse_post) {
-    ProfScope ps7(b, 7, st);
     run_xform(b, true, x, b->dvh.p, all, st);
     // dbj: the per-mode pass also yields c = C^{-1} Z^T (S u) for the residual and Q
     spec_apply(b, true, b->dvh.p, b->dth.p, c.method == SMPM_DBJ ? b->dcoarse.p + static_cast<size_t>(ns) * b->d : nullptr,
@@ -2436,12 +2435,12 @@ int smpm_batch_profile(smpm_batch* b, int enable, double* ms, long long* counts,
     CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
     prof_collect(b);
     if (ms)
-      for (int i = 0; i < std::min(nclass, 8); ++i) ms[i] = b->prof_ms[i];
+      for (int i = 0; i < std::min(nclass, 10); ++i) ms[i] = b->prof_ms[i];
     if (counts)
-      for (int i = 0; i < std::min(nclass, 8); ++i) counts[i] = b->prof_n[i];
+      for (int i = 0; i < std::min(nclass, 10); ++i) counts[i] = b->prof_n[i];
     if (enable >= 0) {
       b->profiling = enable != 0;
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 10; ++i) {
         b->prof_ms[i] = 0.0;
         b->prof_n[i] = 0;
       }

@@ -313,10 +313,11 @@ class SchurBatch:
         the last reset; enable=True/False resets and switches timing."""
         from ._lib import PROFILE_CLASSES
 
-        ms = (C.c_double * 8)()
-        cnt = (C.c_longlong * 8)()
+        n = len(PROFILE_CLASSES)
+        ms = (C.c_double * n)()
+        cnt = (C.c_longlong * n)()
         flag = -1 if enable is None else int(bool(enable))
-        check(lib().smpm_batch_profile(self.h, flag, ms, cnt, 8))
+        check(lib().smpm_batch_profile(self.h, flag, ms, cnt, n))
         return {name: (ms[i], cnt[i]) for i, name in enumerate(PROFILE_CLASSES)}
 
     @property
