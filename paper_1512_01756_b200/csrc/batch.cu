@@ -271,6 +271,7 @@ struct smpm_batch {
   Plan pF, pB;
   DevArray<double> dTfrag, dTifrag;    // T, T^{-1} in the xform fragment order
   int xf_P = 0, xf_MB = 0;
+  long long cgs3_res = 0;  // resident CTAs of the CGS2 pass kernels (device)
   bool pdl = true;  // programmatic dependent launch for the Arnoldi step chain (SMPM_NO_PDL=1: off)  // resident-slice transform kernel (xform.cuh); 0: use pF/pB
   size_t xf_smem = 0;
   Plan pc[6];          // unsplit per-system templates (BJ1, BJ2, BJ3, S; spectral F, B) for the persistent solvers
@@ -1308,11 +1309,19 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
     cgs_update_kernel<true><<<grid, VEC_THREADS, hsm, st>>>(G, V, wv, 1);
     check_launch(b);
   } else {
-    // long row chunks: (live systems x chunks) ~ 4 CTAs per SM, so a batch of
-    // live systems is one wave and per-system partial sums stay few
+    // long row chunks: (live systems x chunks) <= the resident CTA count of the
+    // passes, so a batch of live systems is one wave (a 5 % second wave would
+    // double the pass) and per-system partial sums stay few
     GmState_ Gl = G;
-    const long long target = 4LL * b->ctx->num_sms;
-    const long long cps = std::max(1LL, (target + lv.nslots - 1) / lv.nslots);
+    if (b->cgs3_res == 0) {
+      int o1 = 0, o2 = 0, o3 = 0;
+      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, cgs3_dot_kernel, V3_THREADS, 0));
+      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, cgs3_update_kernel<false>, V3_THREADS, 0));
+      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, cgs3_update_kernel<true>, V3_THREADS, 0));
+      b->cgs3_res = std::max(1, std::min(o1, std::min(o2, o3))) * b->ctx->num_sms;
+    }
+    const long long target = b->cgs3_res;
+    const long long cps = std::max(1LL, target / lv.nslots);
     long long chunk = (b->k + cps - 1) / cps;
     chunk = std::max(256LL, (chunk + 255) / 256 * 256);
     Gl.chunk = static_cast<int>(chunk);

@@ -17,12 +17,36 @@ namespace smpm {
 constexpr int V3_THREADS = 256;
 constexpr int V3_GRP = 8;  // columns per register group
 
-constexpr int V3_NR = 2;   // rows per thread per round (stride V3_THREADS)
+// Row-major work of one thread: rows r0 + t, r0 + t + 256, ... in that order.
+// NR rows per round and NG columns per register group, all loads of a round
+// independent; few columns (early Arnoldi steps) take more rows per round so
+// the memory-level parallelism stays ~16-20 loads per thread.  The per-column
+// (dots) and per-row (update) accumulation sequences do not depend on NR / NG,
+// so every instance gives bit-identical results.
 
-// partial dots over rows [r0, r1) of V_s[:, 0..ncols) with x -> out[0..ncols).
-// Thread t accumulates rows r0 + t, r0 + t + 256, ... in that order, V3_NR rows
-// per round with every load of the round independent; columns past ncols are
-// not loaded.
+// acc[u] += sum over this thread's rows of V[r, c0 + u] x[r], u < nc <= NG
+template <int NR, int NG>
+__device__ __forceinline__ void dots_rows(const double* __restrict__ Vs, long long k, int c0, int nc,
+                                          const double* x, int r0, int r1, double (&acc)[V3_GRP]) {
+  for (int r = r0 + static_cast<int>(threadIdx.x); r < r1; r += NR * V3_THREADS) {
+    double xv[NR], v[NR][NG];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int rq = r + q * V3_THREADS;
+      const bool ok = rq < r1;
+      xv[q] = ok ? __ldcg(x + rq) : 0.0;
+#pragma unroll
+      for (int u = 0; u < NG; ++u)
+        v[q][u] = (ok && u < nc) ? __ldcg(Vs + static_cast<long long>(c0 + u) * k + rq) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+#pragma unroll
+      for (int u = 0; u < NG; ++u) acc[u] = fma(v[q][u], xv[q], acc[u]);
+  }
+}
+
+// partial dots over rows [r0, r1) of V_s[:, 0..ncols) with x -> out[0..ncols)
 __device__ __forceinline__ void cta_dots_long(const double* __restrict__ Vs, long long k, int ncols,
                                               const double* x, int r0, int r1, double* __restrict__ out,
                                               double (*red)[V3_GRP]) {
@@ -32,22 +56,14 @@ __device__ __forceinline__ void cta_dots_long(const double* __restrict__ Vs, lon
     double acc[V3_GRP];
 #pragma unroll
     for (int u = 0; u < V3_GRP; ++u) acc[u] = 0.0;
-    for (int r = r0 + t; r < r1; r += V3_NR * V3_THREADS) {
-      double xv[V3_NR], v[V3_NR][V3_GRP];
-#pragma unroll
-      for (int q = 0; q < V3_NR; ++q) {
-        const int rq = r + q * V3_THREADS;
-        const bool ok = rq < r1;
-        xv[q] = ok ? __ldcg(x + rq) : 0.0;
-#pragma unroll
-        for (int u = 0; u < V3_GRP; ++u)
-          v[q][u] = (ok && u < nc) ? __ldcg(Vs + static_cast<long long>(c0 + u) * k + rq) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < V3_NR; ++q)
-#pragma unroll
-        for (int u = 0; u < V3_GRP; ++u) acc[u] = fma(v[q][u], xv[q], acc[u]);
-    }
+    if (nc <= 1)
+      dots_rows<8, 1>(Vs, k, c0, nc, x, r0, r1, acc);
+    else if (nc <= 2)
+      dots_rows<8, 2>(Vs, k, c0, nc, x, r0, r1, acc);
+    else if (nc <= 4)
+      dots_rows<4, 4>(Vs, k, c0, nc, x, r0, r1, acc);
+    else
+      dots_rows<2, V3_GRP>(Vs, k, c0, nc, x, r0, r1, acc);
 #pragma unroll
     for (int u = 0; u < V3_GRP; ++u) {
       const double v = warp_sum(acc[u]);
@@ -64,44 +80,55 @@ __device__ __forceinline__ void cta_dots_long(const double* __restrict__ Vs, lon
   }
 }
 
-// w[r] -= sum_c V[r, c] h[c] over rows [r0, r1); returns sum of squares of the new rows
-// (two rows per thread and round; per row, even / odd columns accumulate
-// separately in column order; columns past ncols are not loaded)
-__device__ __forceinline__ double rows_update_long(const double* __restrict__ Vs, long long k, int ncols,
-                                                   const double* h, double* ws, int r0, int r1) {
+// w[r] -= sum_c V[r, c] h[c] for this thread's rows, NR rows per round; per row
+// the even / odd columns (within each group of 8) accumulate separately in column
+// order; returns the sum of squares of the new rows (in row order)
+template <int NR, int NG>
+__device__ __forceinline__ double rows_update_nr(const double* __restrict__ Vs, long long k, int ncols,
+                                                 const double* h, double* ws, int r0, int r1) {
   double sq = 0.0;
-  for (int r = r0 + static_cast<int>(threadIdx.x); r < r1; r += 2 * V3_THREADS) {
-    const int r2 = r + V3_THREADS;
-    const bool two = r2 < r1;
-    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-    for (int c0 = 0; c0 < ncols; c0 += V3_GRP) {
-      const int nc = min(V3_GRP, ncols - c0);
-      double v0[V3_GRP], v1[V3_GRP];
+  for (int r = r0 + static_cast<int>(threadIdx.x); r < r1; r += NR * V3_THREADS) {
+    double a[NR][2];
 #pragma unroll
-      for (int u = 0; u < V3_GRP; ++u) {
-        const double* col = Vs + static_cast<long long>(c0 + u) * k;
-        v0[u] = u < nc ? __ldcg(col + r) : 0.0;
-        v1[u] = (two && u < nc) ? __ldcg(col + r2) : 0.0;
+    for (int q = 0; q < NR; ++q) a[q][0] = a[q][1] = 0.0;
+    for (int c0 = 0; c0 < ncols; c0 += NG) {
+      const int nc = min(NG, ncols - c0);
+      double v[NR][NG];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const int rq = r + q * V3_THREADS;
+#pragma unroll
+        for (int u = 0; u < NG; ++u)
+          v[q][u] = (rq < r1 && u < nc) ? __ldcg(Vs + static_cast<long long>(c0 + u) * k + rq) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < V3_GRP; u += 2) {
+      for (int u = 0; u < NG; u += 2) {
         const double h0 = u < nc ? h[c0 + u] : 0.0, h1 = u + 1 < nc ? h[c0 + u + 1] : 0.0;
-        a0 = fma(v0[u], h0, a0);
-        a1 = fma(v0[u + 1], h1, a1);
-        b0 = fma(v1[u], h0, b0);
-        b1 = fma(v1[u + 1], h1, b1);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          a[q][0] = fma(v[q][u], h0, a[q][0]);
+          if (u + 1 < NG) a[q][1] = fma(v[q][u + 1], h1, a[q][1]);
+        }
       }
     }
-    const double n0 = __ldcg(ws + r) - (a0 + a1);
-    ws[r] = n0;
-    sq = fma(n0, n0, sq);
-    if (two) {
-      const double n1 = __ldcg(ws + r2) - (b0 + b1);
-      ws[r2] = n1;
-      sq = fma(n1, n1, sq);
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int rq = r + q * V3_THREADS;
+      if (rq < r1) {
+        const double nv = __ldcg(ws + rq) - (a[q][0] + a[q][1]);
+        ws[rq] = nv;
+        sq = fma(nv, nv, sq);
+      }
     }
   }
   return sq;
+}
+
+__device__ __forceinline__ double rows_update_long(const double* __restrict__ Vs, long long k, int ncols,
+                                                   const double* h, double* ws, int r0, int r1) {
+  if (ncols <= 2) return rows_update_nr<8, 2>(Vs, k, ncols, h, ws, r0, r1);
+  if (ncols <= 4) return rows_update_nr<4, 4>(Vs, k, ncols, h, ws, r0, r1);
+  return rows_update_nr<2, V3_GRP>(Vs, k, ncols, h, ws, r0, r1);
 }
 
 // ---- pass 1: h1 = V^T w (with the fused deflation P when tdefl != nullptr) ----
