@@ -504,14 +504,13 @@ void run_deflate(smpm_batch* b, int mode, const double* zin, const double* v, do
   }
   if (mode != DEFL_SUB_T) {
     // Z^T + coarse solve: warp per interface, last CTA of each system solves
-    zt_coarse_kernel<<<dim3((d + DZ_IFACES - 1) / DZ_IFACES, ns), V2_THREADS, shm, st>>>(
-        P, zin, sums, mode == DEFL_COARSE ? cout : cbuf, b->dcount.p, 0);
-    check_launch(b);
+    launch_pdl(b, zt_coarse_kernel, dim3((d + DZ_IFACES - 1) / DZ_IFACES, ns), dim3(V2_THREADS), shm, st, P, zin, sums,
+               mode == DEFL_COARSE ? cout : cbuf, b->dcount.p, 0);
     if (mode == DEFL_COARSE) return;
   }
   const int gx = static_cast<int>(std::min<long long>((b->k + V2_THREADS * 4 - 1) / (V2_THREADS * 4), 256));
-  defl_update_kernel<<<dim3(gx, ns), V2_THREADS, 0, st>>>(P, mode, cbuf, zin, v, y);
-  check_launch(b);
+  launch_pdl(b, defl_update_kernel, dim3(gx, ns), dim3(V2_THREADS), 0, st, P, mode, static_cast<const double*>(cbuf),
+             zin, v, y);
 }
 
 int grid_for(long long elems) {
@@ -1668,13 +1667,12 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   batched_dot(b, bS, bS, nb2, nullptr, st);
   batched_dot(b, rhs, rhs, nr2, nullptr, st);
   CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double) * nk, st));
-  gm_start_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G, nr2, nb2, c.tol, 1, nullptr);
-  check_launch(b);
+  launch_pdl(b, gm_start_kernel, dim3((ns + 127) / 128), dim3(128), 0, st, G, static_cast<const double*>(nr2),
+             static_cast<const double*>(nb2), c.tol, 1, static_cast<const int*>(nullptr));
   dim3 vg(std::max(1, std::min(G.nchunk, 64)), ns);
-  gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, rhs, vin);
-  check_launch(b);
-  compact_kernel<<<1, 1024, 0, st>>>(G.active, nullptr, ns, alist, acount, nullptr);
-  check_launch(b);
+  launch_pdl(b, gm_v0_kernel, vg, dim3(256), 0, st, G, b->dV.p, static_cast<const double*>(rhs), vin);
+  launch_pdl(b, compact_kernel, dim3(1), dim3(1024), 0, st, static_cast<const int*>(G.active),
+             static_cast<const int*>(nullptr), ns, alist, acount, static_cast<int*>(nullptr));
   G.alist = alist;
   G.acount = acount;
 
@@ -1821,10 +1819,9 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     break;
   }
   // ---- assemble x' = V y for the last cycle of every system
-  gm_backsolve_kernel<<<ns, 32, 0, st>>>(G, nullptr);
-  check_launch(b);
-  gm_combine_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, x, nullptr, 1);
-  check_launch(b);
+  launch_pdl(b, gm_backsolve_kernel, dim3(ns), dim3(32), 0, st, G, static_cast<const int*>(nullptr));
+  launch_pdl(b, gm_combine_kernel, vg, dim3(256), 0, st, G, static_cast<const double*>(b->dV.p), x,
+             static_cast<const int*>(nullptr), 1);
 
   // ---- final residual check (proj/src/gmres.cpp:129-136): r = rhs - op(x')
   // Spectral dbj/bj: one per-mode pass of x' gives both u = M^{-1} x' (the
@@ -1846,10 +1843,10 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     ProfScope psd(b, PC_DEFL, st);
     DeflateParams P = deflate_params(b, nullptr);
     const int gx = static_cast<int>(std::min<long long>((b->k + V2_THREADS * 4 - 1) / (V2_THREADS * 4), 64));
-    post_dbj_kernel<<<dim3(gx, ns), V2_THREADS, 0, st>>>(P, tq, u, rhs, b->dcoarse.p + static_cast<size_t>(ns) * b->d,
-                                                           b->dczb.p, xS, b->dpost.p, b->dcount.p, nrf,
-                                                           c.final_check ? 1 : 0);
-    check_launch(b);
+    launch_pdl(b, post_dbj_kernel, dim3(gx, ns), dim3(V2_THREADS), 0, st, P, static_cast<const double*>(tq),
+               static_cast<const double*>(u), static_cast<const double*>(rhs),
+               static_cast<const double*>(b->dcoarse.p + static_cast<size_t>(ns) * b->d),
+               static_cast<const double*>(b->dczb.p), xS, b->dpost.p, b->dcount.p, nrf, c.final_check ? 1 : 0);
   }
   if (c.final_check && !post_one_pass) {
     if (fuse_post && c.method == SMPM_DBJ) {

@@ -589,6 +589,8 @@ __global__ void project_kernel(int nsys, long long k, const double* __restrict__
 // nrm2sq: ||r||^2 per system; first: 1 on the first cycle.
 __global__ void gm_start_kernel(GmState_ G, const double* __restrict__ nrm2sq, const double* __restrict__ bs_nrm2sq,
                                 double tol, int first, const int* __restrict__ restart_mask) {
+  pdl_wait();
+  pdl_launch();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= G.nsys) return;
   if (!first && !(restart_mask && restart_mask[s] == GM_CYCLE)) return;
@@ -616,6 +618,8 @@ __global__ void gm_start_kernel(GmState_ G, const double* __restrict__ nrm2sq, c
 // v0 = r / ||r|| into V[:,0] and vin, for systems just (re)started
 __global__ void gm_v0_kernel(GmState_ G, double* __restrict__ V, const double* __restrict__ r,
                              double* __restrict__ vin) {
+  pdl_wait();
+  pdl_launch();
   const int s = blockIdx.y;
   if (!G.active[s] || G.jcyc[s] != 0) return;
   const double inv = 1.0 / G.nrm[s];
@@ -633,6 +637,8 @@ __global__ void gm_v0_kernel(GmState_ G, double* __restrict__ V, const double* _
 // back-substitution R y = g for the systems whose cycle ended (warp per system)
 // (proj/src/gmres.cpp:116-125); ncyc = columns built in this cycle
 __global__ void gm_backsolve_kernel(GmState_ G, const int* __restrict__ sel) {
+  pdl_wait();
+  pdl_launch();
   // column-oriented back substitution: y_i = b_i / r_ii, then b_r -= r_ri y_i
   // for r < i; the triangle is staged in shared memory for short cycles
   constexpr int NS = 96;
@@ -681,6 +687,8 @@ __global__ void gm_backsolve_kernel(GmState_ G, const int* __restrict__ sel) {
 // x (+)= V y over the columns of the finished cycle
 __global__ void gm_combine_kernel(GmState_ G, const double* __restrict__ V, double* __restrict__ x,
                                   const int* __restrict__ sel, int accumulate) {
+  pdl_wait();
+  pdl_launch();
   const int s = blockIdx.y;
   if (sel && !sel[s]) return;
   const int n = G.jcyc[s];

@@ -183,6 +183,8 @@ constexpr int DZ_IFACES = 8;  // interfaces per CTA in the Z^T pass (warp each)
 __global__ void __launch_bounds__(V2_THREADS) zt_coarse_kernel(DeflateParams P, const double* __restrict__ zin,
                                                                double* __restrict__ sums, double* __restrict__ cout,
                                                                int* counter, int direct) {
+  pdl_wait();
+  pdl_launch();
   extern __shared__ double sm[];
   int s;
   if (!defl_slot(P, blockIdx.y, s)) return;
@@ -219,6 +221,8 @@ __global__ void __launch_bounds__(V2_THREADS) zt_coarse_kernel(DeflateParams P, 
 __global__ void __launch_bounds__(V2_THREADS) defl_update_kernel(DeflateParams P, int mode, const double* __restrict__ c,
                                                                  const double* __restrict__ zin,
                                                                  const double* __restrict__ v, double* __restrict__ y) {
+  pdl_wait();
+  pdl_launch();
   int s;
   if (!defl_slot(P, blockIdx.y, s)) return;
   const int w = P.w, w2 = 2 * w, mx = P.mx;
@@ -263,6 +267,8 @@ __global__ void __launch_bounds__(V2_THREADS)
 post_dbj_kernel(DeflateParams P, const double* __restrict__ t, const double* __restrict__ u,
                 const double* __restrict__ rhs, const double* __restrict__ ct, const double* __restrict__ cb,
                 double* __restrict__ xS, double* __restrict__ part, int* counter, double* __restrict__ nrf, int check) {
+  pdl_wait();
+  pdl_launch();
   __shared__ double red[V2_THREADS / 32];
   int s;
   if (!defl_slot(P, blockIdx.y, s)) return;
