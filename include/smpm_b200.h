@@ -196,6 +196,14 @@ int smpm_deflated_solve(smpm_batch* b, const double* b_S, double* x_S, const smp
                         smpm_report* reports, double* history, void* stream);
 int smpm_two_level_schwarz_solve(smpm_batch* b, const double* b_S, double* x_S, const smpm_solve_options* opt,
                                  smpm_report* reports, double* history, void* stream);
+/* Stacked solve (proj/src/helmholtz.cpp:187-246, the reference bench's 3D
+ * default): ONE GMRES whose Krylov vectors are the concatenation of the nsys
+ * systems (dbj: right-hand side P_j b_j, operator block-diagonal P_j S_j M_j^{-1};
+ * 2las: S_j (M_j^{-1} + Z C_j^{-1} Z^T)), abs tolerance tol * sqrt(sum_j ||b_j||^2);
+ * x_S per system as in smpm_solve.  One report (shared by all systems); history:
+ * host, max_iter + 2 (nullable).  CGS2, fused deflation, restart <= 126. */
+int smpm_solve_stacked(smpm_batch* b, int method, const double* b_S, double* x_S, const smpm_solve_options* opt,
+                       smpm_report* report, double* history, void* stream);
 /* Same as smpm_solve with HOST b_S / x_S: the H2D and D2H copies are inside
  * the call (the reference-facing end-to-end path). */
 int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x_S_host,

@@ -347,6 +347,23 @@ def solve_many(systems, b, method="dbj", tol=1e-10, max_iter=100, restart=0, thr
     return x, [reps[i] for i in range(n)]
 
 
+def solve_stacked(systems, b, method="dbj", tol=1e-10, max_iter=100, restart=0):
+    """Stacked solve of proj/src/helmholtz.cpp:187-246: one GMRES over every
+    system's (deflated) right-hand side with the block-diagonal operator."""
+    n = len(systems)
+    k = systems[0].k
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(n, k)
+    x = np.zeros((n, k))
+    rep = Report()
+    cap = max_iter + 2
+    hist = np.zeros(cap)
+    sys_arr = (C.c_void_p * n)(*[s.h for s in systems])
+    cs_arr = (C.c_void_p * n)(*[s.coarse.h for s in systems])
+    _chk(lib().orc_solve_stacked(sys_arr, cs_arr, n, METHODS[method], _p(b), C.c_double(tol), int(max_iter),
+                                 int(restart), _p(x), C.byref(rep), _p(hist), cap))
+    return _result(x, rep, hist)
+
+
 def gmres_dense(A, b, tol=1e-10, max_iter=200, restart=0):
     A = np.asfortranarray(A, dtype=np.float64)
     b = _vec(b, A.shape[0])

@@ -388,6 +388,80 @@ int orc_solve(void* vs, void* vc, int method, const double* b, double tol, int m
   });
 }
 
+// Stacked solve (proj/src/helmholtz.cpp:187-246, the reference bench's 3D
+// default, proj/src/bench.cpp:129): ONE GMRES over the concatenation of every
+// system's right-hand side (dbj: P_j b_j) with the block-diagonal operator
+// (dbj: P_j S_j M_j^{-1}; 2las: S_j (M_j^{-1} + Z c_j Z^T)), abs_tol = tol *
+// sqrt(sum_j ||b_j||^2); then per system x_j = Q_j M_j^{-1} x'_j + Z c_j(Z^T b_j)
+// (dbj) or M_j^{-1} x'_j + Z c_j(Z^T x'_j) (2las). One report.
+int orc_solve_stacked(void** systems, void** coarse, int nsys, int method, const double* b, double tol, int max_iter,
+                      int restart, double* x, Report* rep, double* hist, int cap) {
+  return guard([&] {
+    if (nsys < 1) invalid("no systems");
+    if (method != 2 && method != 3) invalid("stacked solve: dbj or 2las");
+    std::vector<const SchurSystem*> S(static_cast<std::size_t>(nsys));
+    std::vector<const CoarseSpace*> CS(static_cast<std::size_t>(nsys));
+    for (int j = 0; j < nsys; ++j) {
+      S[j] = &static_cast<System*>(systems[j])->sys;
+      CS[j] = static_cast<CoarseSpace*>(coarse[j]);
+      if (!CS[j]) invalid("stacked solve needs coarse spaces");
+    }
+    const Index k = S[0]->k;
+    const Index total = static_cast<Index>(nsys) * k;
+    Vec rhs(static_cast<std::size_t>(total));
+    double bnorm2 = 0.0;
+    for (int j = 0; j < nsys; ++j) {
+      const Vec bj = vin(b + static_cast<Index>(j) * k, k);
+      for (double v : bj) bnorm2 += v * v;
+      const Vec pj = method == 2 ? apply_P(*CS[j], *S[j], bj) : bj;
+      std::copy(pj.begin(), pj.end(), rhs.begin() + static_cast<Index>(j) * k);
+    }
+    auto seg = [&](const Vec& v, int j) { return Vec(v.begin() + static_cast<Index>(j) * k, v.begin() + static_cast<Index>(j + 1) * k); };
+    LinOp op = [&](const Vec& v) {
+      Vec y(static_cast<std::size_t>(total));
+      for (int j = 0; j < nsys; ++j) {
+        const Vec vj = seg(v, j);
+        const SchurSystem& sj = *S[j];
+        const Decomposition& dec = sj.op->dec;
+        Vec w;
+        if (method == 2) {
+          w = apply_P(*CS[j], sj, apply_S(sj, apply_block_jacobi_inv(sj, vj)));
+        } else {
+          Vec m = apply_block_jacobi_inv(sj, vj);
+          const Vec zc = apply_Z(dec, coarse_solve(*CS[j], apply_Zt(dec, vj)));
+          for (std::size_t i = 0; i < m.size(); ++i) m[i] += zc[i];
+          w = apply_S(sj, m);
+        }
+        std::copy(w.begin(), w.end(), y.begin() + static_cast<Index>(j) * k);
+      }
+      return y;
+    };
+    GmresOptions opt;
+    opt.abs_tol = tol * std::sqrt(bnorm2);
+    opt.max_iter = max_iter;
+    opt.restart = restart;
+    SchurSolveResult r;
+    const Vec xp = gmres(op, rhs, opt, r.report);
+    for (int j = 0; j < nsys; ++j) {
+      const SchurSystem& sj = *S[j];
+      const Decomposition& dec = sj.op->dec;
+      const Vec xj = seg(xp, j);
+      Vec out;
+      if (method == 2) {
+        out = apply_Q(*CS[j], sj, apply_block_jacobi_inv(sj, xj));
+        const Vec zc = apply_Z(dec, coarse_solve(*CS[j], apply_Zt(dec, vin(b + static_cast<Index>(j) * k, k))));
+        for (std::size_t i = 0; i < out.size(); ++i) out[i] += zc[i];
+      } else {
+        out = apply_block_jacobi_inv(sj, xj);
+        const Vec zc = apply_Z(dec, coarse_solve(*CS[j], apply_Zt(dec, xj)));
+        for (std::size_t i = 0; i < out.size(); ++i) out[i] += zc[i];
+      }
+      vout(out, x + static_cast<Index>(j) * k);
+    }
+    fill_report(r, rep, hist, cap);
+  });
+}
+
 // Independent per-system deflated solves across host threads (the
 // `parallel_trials` analogue, proj/src/bench.cpp:79-84). systems[i] and
 // coarse[i] pair up; b and x are nsys x k, system-major.

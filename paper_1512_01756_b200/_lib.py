@@ -26,7 +26,7 @@ EXPORTS = [
     "smpm_apply_Zt", "smpm_coarse_solve", "smpm_apply_P", "smpm_apply_Q", "smpm_project_out", "smpm_solve",
     "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_batch_launch_count",
     "smpm_batch_profile", "smpm_fp64_peak", "smpm_batch_set_strip_factors", "smpm_schur_rhs",
-    "smpm_recover_solution",
+    "smpm_recover_solution", "smpm_solve_stacked",
 ]
 PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other", "cluster_arnoldi", "grid_tail",
                    "spectral_op", "transform", "reserved"]
@@ -114,6 +114,7 @@ def lib():
     L.smpm_deflated_solve.argtypes = [vp, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp, vp]
     L.smpm_two_level_schwarz_solve.argtypes = [vp, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp, vp]
     L.smpm_solve_host.argtypes = [vp, ip, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp]
+    L.smpm_solve_stacked.argtypes = [vp, ip, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp, vp]
     L.smpm_batch_launch_count.restype = llp
     L.smpm_batch_launch_count.argtypes = [vp]
     L.smpm_batch_profile.argtypes = [vp, ip, C.POINTER(C.c_double), C.POINTER(C.c_longlong), ip]

@@ -292,6 +292,7 @@ struct smpm_batch {
   DevArray<double> dsmall;  // nsys x (d + misc) scalars
   DevArray<double> dcoarse;  // Z^T sums and coarse solutions, 2 x nsys x d
   DevArray<double> dczb;     // nsys x d: C^{-1} Z^T b_S of the current solve (dbj)
+  DevArray<double> dsnsq;    // nsys: per-system ||w||^2 of the stacked solve's norm pass
   // strip solver (strip.cuh): x-factor per strip kind, z eigenvalues, shifts; scratch strip rows
   bool strip_ok = false;
   double strip_tau = 0.0;
@@ -1084,6 +1085,9 @@ void ensure_gmres(smpm_batch* b, int m, int mtot) {
   G.chunk = V2_CHUNK;
   G.nchunk = static_cast<int>((b->k + V2_CHUNK - 1) / V2_CHUNK);
   G.nsys = ns;
+  b->dsnsq.alloc(static_cast<size_t>(ns));
+  G.snsq = b->dsnsq.p;
+  G.stacked = 0;
   (void)c;
   b->gm_mtot = mtot;
   CUDA_CHECK(cudaMemsetAsync(b->dgint.p, 0, sizeof(int) * ns * 8, b->ctx->stream));
@@ -1094,6 +1098,7 @@ struct SolveCfg {
   double tol;
   int max_iter, restart, orth;
   bool fused, final_check;
+  bool stacked = false;  // one GMRES over all systems (proj/src/helmholtz.cpp:187-246)
 };
 
 // --------------------------------------------------------------------------
@@ -1328,8 +1333,11 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
     dim3 cgrid(Gl.nchunk, lv.nslots);
     DeflateParams P = deflate_params(b, nullptr);
     launch_pdl(b, cgs3_dot_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, tdefl, P, cbuf);
+    if (G.stacked) launch_pdl(b, stack_h_kernel, dim3(1), dim3(128), 0, st, G, G.h1);
     launch_pdl(b, cgs3_update_kernel<false>, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv);
+    if (G.stacked) launch_pdl(b, stack_h_kernel, dim3(1), dim3(128), 0, st, G, G.h2);
     launch_pdl(b, cgs3_update_kernel<true>, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv);
+    if (G.stacked) launch_pdl(b, stack_givens_kernel, dim3(b->nsys), dim3(32), 0, st, G);
   }
   (void)hsm;
   dim3 sg(std::max(1, std::min(G.nchunk, 64)), lv.nslots);
@@ -1612,6 +1620,10 @@ void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
   }
 }
 
+void stack_sum(smpm_batch* b, double* v, cudaStream_t st) {
+  launch_pdl(b, stack_sum_kernel, dim3(1), dim3(128), 0, st, b->nsys, v);
+}
+
 void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_report* reps, double* history,
            cudaStream_t st) {
   need_final(b);
@@ -1622,6 +1634,12 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   if (m > 4000) fail(SMPM_EINVAL, "Krylov cycle length above 4000 is not supported (use restart)");
   ensure_gmres(b, m, mtot);
   GmState_& G = b->G;
+  G.stacked = c.stacked ? 1 : 0;
+  if (c.stacked) {
+    if (c.orth != SMPM_ORTH_CGS2) fail(SMPM_EINVAL, "stacked solve: CGS2 orthogonalization only");
+    if (m + 2 > V2_MAXCOL) fail(SMPM_EINVAL, "stacked solve: cycle length above 126 (use restart)");
+    if (c.method == SMPM_DBJ && !c.fused) fail(SMPM_EINVAL, "stacked solve: fused deflation only");
+  }
   const int ns = b->nsys;
   const long long nk = static_cast<long long>(ns) * b->k;
   double* rhs = b->vbuf[0].p;  // GMRES right-hand side (P b_S for dbj)
@@ -1666,6 +1684,10 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   }
   batched_dot(b, bS, bS, nb2, nullptr, st);
   batched_dot(b, rhs, rhs, nr2, nullptr, st);
+  if (c.stacked) {  // ||b|| and ||rhs|| of the stacked vector (proj/src/helmholtz.cpp:193-201)
+    stack_sum(b, nb2, st);
+    stack_sum(b, nr2, st);
+  }
   CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double) * nk, st));
   launch_pdl(b, gm_start_kernel, dim3((ns + 127) / 128), dim3(128), 0, st, G, static_cast<const double*>(nr2),
              static_cast<const double*>(nb2), c.tol, 1, static_cast<const int*>(nullptr));
@@ -1676,7 +1698,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   G.alist = alist;
   G.acount = acount;
 
-  const bool use_cluster = b->cluster_ok && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= 128 &&
+  const bool use_cluster = b->cluster_ok && !c.stacked && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= 128 &&
                            (c.method != SMPM_DBJ || c.fused) && std::getenv("SMPM_CLUSTER") != nullptr;
   if (use_cluster) {
     // ---- cluster-persistent Arnoldi: one launch per GMRES cycle
@@ -1708,6 +1730,8 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, dsel, nullptr, 1.0, rhs, -1.0, r);
       check_launch(b);
       batched_dot(b, r, r, nr2, dsel, st);
+    if (c.stacked) stack_sum(b, nr2, st);
+      if (c.stacked) stack_sum(b, nr2, st);
       gm_start_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G, nr2, nb2, c.tol, 0, G.state);
       check_launch(b);
       gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, r, vin);
@@ -1738,7 +1762,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     CUDA_CHECK(cudaEventRecord(ev[slot], st));
   };
   // few live systems: the rest of the cycle runs grid-persistent (grid.cuh)
-  const bool use_grid = b->grid_ok && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= GT_MAXCOL &&
+  const bool use_grid = b->grid_ok && !c.stacked && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= GT_MAXCOL &&
                         (c.method != SMPM_DBJ || c.fused) && std::getenv("SMPM_NO_GRID") == nullptr;
   int grid_max = 8;  // measured on C4 with the PDL step chain: 8-10 live systems is the crossover
   if (const char* e = std::getenv("SMPM_GRID_MAX")) grid_max = std::max(0, std::min(GT_MAXSYS, std::atoi(e)));
@@ -1943,7 +1967,13 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       double frel = bn > 0 ? std::fabs(hg[static_cast<size_t>(s) * (m + 1) + jc]) / bn : 0.0;
       bool mismatch = false;
       if (c.final_check && bn > 0) {
-        const double true_rel = std::sqrt(hsm[static_cast<size_t>(2 * ns) + s]) / bn;
+        // stacked: the true residual of the stacked vector (proj/src/gmres.cpp:129-136)
+        double r2 = hsm[static_cast<size_t>(2 * ns) + s];
+        if (c.stacked) {
+          r2 = 0.0;
+          for (int t = 0; t < ns; ++t) r2 += hsm[static_cast<size_t>(2 * ns) + t];
+        }
+        const double true_rel = std::sqrt(r2) / bn;
         if (true_rel * bn > 10.0 * std::max(tgt, frel * bn)) mismatch = true;
         frel = true_rel;
       }
@@ -2416,6 +2446,24 @@ int smpm_deflated_solve(smpm_batch* b, const double* b_S, double* x_S, const smp
 int smpm_two_level_schwarz_solve(smpm_batch* b, const double* b_S, double* x_S, const smpm_solve_options* opt,
                                  smpm_report* reports, double* history, void* stream) {
   return smpm_solve(b, SMPM_2LAS, b_S, x_S, opt, reports, history, stream);
+}
+
+int smpm_solve_stacked(smpm_batch* b, int method, const double* b_S, double* x_S, const smpm_solve_options* opt,
+                       smpm_report* report, double* history, void* stream) {
+  return guard([&] {
+    need_final(b);
+    if (!b_S || !x_S) fail(SMPM_EINVAL, "null vector");
+    if (method != SMPM_DBJ && method != SMPM_2LAS) fail(SMPM_EINVAL, "stacked solve: dbj or 2las");
+    SolveCfg c = cfg_from(method, opt);
+    c.stacked = true;
+    // every system carries the same (global) report and history: keep one
+    std::vector<smpm_report> reps(static_cast<size_t>(b->nsys));
+    const int cap = static_cast<int>(std::min<long long>(c.max_iter, b->k)) + 2;  // solve's history stride
+    std::vector<double> hist(history ? static_cast<size_t>(b->nsys) * cap : 0);
+    solve(b, c, b_S, x_S, reps.data(), history ? hist.data() : nullptr, b->st(stream));
+    if (report) *report = reps[0];
+    if (history) std::copy(hist.begin(), hist.begin() + cap, history);
+  });
 }
 
 int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x_S_host,

@@ -244,6 +244,8 @@ struct GmState_ {
   int nsys;
   const int* alist;   // compacted active systems for (chunk, slot) grids
   const int* acount;  // number of valid slots
+  int stacked;        // one GMRES over all systems stacked (proj/src/helmholtz.cpp:187-246)
+  double* snsq;       // stacked: per-system ||w||^2 of the norm pass
 };
 
 // (chunk, slot) grid -> system; false when the slot is past the live count
@@ -701,6 +703,51 @@ __global__ void gm_combine_kernel(GmState_ G, const double* __restrict__ V, doub
     for (int i = 0; i < n; ++i) acc = fma(Vs[static_cast<long long>(i) * G.k + r], y[i], acc);
     xs[r] = acc;
   }
+}
+
+// ---- stacked GMRES (proj/src/helmholtz.cpp:187-246): the systems of the batch are
+// the segments of ONE Krylov vector, so every inner product is the sum of the
+// per-system ones.  The per-system reductions of the passes run unchanged; these
+// kernels then sum them over the systems in a fixed order (deterministic) and
+// hand every system the same global value, so all systems carry an identical
+// Hessenberg / Givens state and stop together.
+
+// v[s] = sum_t v[t] for every system (one CTA)
+__global__ void stack_sum_kernel(int nsys, double* __restrict__ v) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ double tot;
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int t = 0; t < nsys; ++t) a += v[t];
+    tot = a;
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < nsys; s += blockDim.x) v[s] = tot;
+}
+
+// h[s][c] = sum_t h[t][c] for the current Arnoldi column count (one CTA, thread per column)
+__global__ void stack_h_kernel(GmState_ G, double* __restrict__ h) {
+  pdl_wait();
+  pdl_launch();
+  const int stride = G.m + 2;
+  const int ncols = G.jcyc[0] + 1;
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+    double a = 0.0;
+    for (int t = 0; t < G.nsys; ++t) a += h[static_cast<long long>(t) * stride + c];
+    for (int t = 0; t < G.nsys; ++t) h[static_cast<long long>(t) * stride + c] = a;
+  }
+}
+
+// global ||w|| from the per-system squares, then the Givens step of every system (warp each)
+__global__ void stack_givens_kernel(GmState_ G) {
+  pdl_wait();
+  pdl_launch();
+  const int s = blockIdx.x;
+  if (!G.active[s]) return;
+  double a = 0.0;
+  for (int t = 0; t < G.nsys; ++t) a += G.snsq[t];
+  givens_step(G, s, G.jcyc[s], sqrt(a));
 }
 
 }  // namespace smpm

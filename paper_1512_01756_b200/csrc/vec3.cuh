@@ -212,6 +212,10 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_update_kernel(GmState_ G, con
   if (!last_cta(G.counter + s, G.nchunk)) return;
   if (threadIdx.x >= 32) return;
   const double nsq = warp_reduce_strided(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride);
+  if (G.stacked) {
+    if (threadIdx.x == 0) G.snsq[s] = nsq;  // stack_givens_kernel sums over the systems
+    return;
+  }
   givens_step(G, s, j, sqrt(nsq));
 }
 

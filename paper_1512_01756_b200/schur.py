@@ -292,6 +292,21 @@ class SchurBatch:
                                _hptr(hist) if hist is not None else None, self._stream()))
         return self._collect(x, reps, hist, cap)
 
+    def solve_stacked(self, b_S, method="dbj", tol=1e-10, max_iter=100, restart=0, history=True):
+        """One GMRES over all systems stacked (proj/src/helmholtz.cpp:187-246); one report."""
+        torch = _torch()
+        b = self._vec(b_S, self.k)
+        x = torch.empty_like(b)
+        o = self.options(tol, max_iter, restart, "cgs2", True)
+        rep = Report()
+        cap = min(max_iter, self.k) + 2
+        hist = np.zeros(cap) if history else None
+        check(lib().smpm_solve_stacked(self.h, METHODS[method], _dptr(b), _dptr(x), C.byref(o), C.byref(rep),
+                                       _hptr(hist) if hist is not None else None, self._stream()))
+        return SolveResult(x, [rep.iterations], [bool(rep.converged)], [rep.final_rel_residual],
+                           [rep.operator_applies], [rep.krylov_s_applies], [bool(rep.mismatch_warning)],
+                           rep.wall_time_s, [hist[: rep.history_len].copy()] if hist is not None else [])
+
     def deflated_solve(self, b_S, tol=1e-10, max_iter=100, **kw):  # proj/src/deflation.cpp:102-122
         return self.solve(b_S, "dbj", tol, max_iter, **kw)
 

@@ -246,3 +246,16 @@ def neumann_rows(prob, x, z, lx, lz):
             b = node(ex, mz - 1, ix, n - 1)
             g[b] += prob.tau * uz(x[b], z[b])
     return g
+
+
+def test_oracle_stacked_reduces_to_independent_solve():
+    """The stacked restatement (proj/src/helmholtz.cpp:187-246) with one system is
+    the deflated solve of that system: same iterations, same solution."""
+    from tests._cases import build_case
+
+    case = build_case(9, 4, 4, 1.0, 1.0, (0.0,), kmax=4, decay=False)
+    s = case.systems[0]
+    a = O.solve_stacked([s], case.b_S, "dbj", 1e-10, 50)
+    c = s.solve(case.b_S[0], "dbj", 1e-10, 50)
+    assert a.iterations == c.iterations
+    assert np.linalg.norm(a.x_S[0] - c.x_S) <= 1e-12 * np.linalg.norm(c.x_S)
