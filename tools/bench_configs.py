@@ -96,6 +96,7 @@ def main():
     ap.add_argument("--cpu-max-s", type=float, default=60.0, help="skip the CPU leg when one solve would exceed this")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--c5-chunk", type=int, default=64, help="C5 modes per batch")
+    ap.add_argument("--no-stacked", action="store_true")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     ctx = Context(0)
@@ -133,6 +134,29 @@ def main():
                 elif not cfg.modes:
                     row["cpu_allcores_note"] = "one system: the reference has no intra-solve threading"
                 row["cpu_threads"] = threads
+            rows.append(row)
+            print(json.dumps(row), flush=True)
+        if cfg.modes and not a.no_stacked:
+            # the reference bench's 3D default: one stacked GMRES over all modes
+            # (proj/src/helmholtz.cpp:187-246, proj/src/bench.cpp:129), max_iter = 100, no restart
+            def st():
+                return b.solve_stacked(bS, "dbj", 1e-10, 100, 0, history=False)
+
+            for _ in range(3):
+                r = st()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            nrep = 5
+            for _ in range(nrep):
+                r = st()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / nrep
+            row = {"config": name, "method": "dbj", "regime": "stacked (one GMRES over all modes)", "systems": b.nsys,
+                   "k_per_system": b.k, "gpu_solves_per_s": b.nsys / (ms * 1e-3), "gpu_ms_per_batch": ms,
+                   "iterations": int(r.iterations[0]), "converged": bool(r.converged[0]),
+                   "final_rel_residual": float(r.final_rel_residual[0])}
             rows.append(row)
             print(json.dumps(row), flush=True)
         b.close()
