@@ -99,6 +99,12 @@ class System {
     if (static_cast<long long>(u_S.size()) != k_) throw std::invalid_argument("u_S has wrong length");
     check(smpm_batch_set_nullspace(b_, 0, u_S.data()));
   }
+  // optional spectral factors (before finalize) and strip factors (after): the
+  // fast-diagonalisation operator form and the device strip solves
+  void set_spectral(int npairs, const double* T, const double* T_inv, const double* gamma) {
+    check(smpm_batch_set_spectral(b_, npairs, T, T_inv, gamma));
+  }
+  void set_strip_factors(const smpm_strip_factors& f) { check(smpm_batch_set_strip_factors(b_, &f)); }
   void finalize() { check(smpm_batch_finalize(b_)); }
 
   long long k() const { return k_; }
@@ -163,6 +169,37 @@ inline Vector project_out(const System& s, const Vector& v, const Vector& dir) {
   return s.run(v, s.k(), s.k(), [&](double* i, double* o) {
     return smpm_project_out(s.batch(), s.k(), i, s.scratch(2), o, nullptr);
   });
+}
+
+// proj/src/schur.cpp:182-186 (mu = 0) / proj/src/helmholtz.cpp:172-176 (mode shift mu):
+// b_S = B (A - mu)^{-1} f; needs set_strip_factors. f has r = m_x m_z n^2 entries.
+inline Vector schur_rhs(const System& s, const Vector& f) {
+  double* df = nullptr;
+  if (cudaMalloc(&df, sizeof(double) * f.size()) != cudaSuccess) throw std::runtime_error("smpm_b200: cudaMalloc failed");
+  s.up(df, f);
+  const int rc = smpm_schur_rhs(s.batch(), df, s.scratch(1), nullptr);
+  cudaFree(df);
+  check(rc);
+  return s.down(s.scratch(1), s.k());
+}
+// proj/src/schur.cpp:227-230 / proj/src/helmholtz.cpp:282-292: u = (A - mu)^{-1} (f - E x_S)
+inline Vector recover_solution(const System& s, const Vector& f, const Vector& x_S) {
+  if (static_cast<long long>(x_S.size()) != s.k()) throw std::invalid_argument("x_S has wrong length");
+  double *df = nullptr, *du = nullptr;
+  if (cudaMalloc(&df, sizeof(double) * f.size()) != cudaSuccess ||
+      cudaMalloc(&du, sizeof(double) * f.size()) != cudaSuccess) {
+    cudaFree(df);
+    throw std::runtime_error("smpm_b200: cudaMalloc failed");
+  }
+  s.up(df, f);
+  s.up(s.scratch(0), x_S);
+  const int rc = smpm_recover_solution(s.batch(), df, s.scratch(0), du, nullptr);
+  Vector u;
+  if (rc == SMPM_OK) u = s.down(du, static_cast<long long>(f.size()));
+  cudaFree(df);
+  cudaFree(du);
+  check(rc);
+  return u;
 }
 
 namespace detail {
