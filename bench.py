@@ -446,6 +446,9 @@ def run_ours(args, cfg):
         "traffic": (measured_traffic(roofline_kernel_name(dom)) or {}).get("bytes_per_launch"),
         "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
         "traffic_source": (measured_traffic(roofline_kernel_name(dom)) or {}).get("source"),
+        "traffic_note": "ncu DRAM bytes of one launch of the named kernel(s) on the first full-batch Arnoldi step "
+                        "(for the CGS2 class: the three passes of that step); algorithmic_per_launch is the class "
+                        "average per timed span (one span = one step's launches of the class)",
         "algorithmic_per_launch": per_launch,
         "avg_launch_ms": dms / nlaunch,
         "fp64_peak_tflops": peak_fp64, "hbm_peak_gbs": peak_hbm,
