@@ -185,6 +185,13 @@ int smpm_schur_rhs(smpm_batch* b, const double* f, double* b_S, void* stream);  
 int smpm_recover_solution(smpm_batch* b, const double* f, const double* x_S, double* u,
                           void* stream);                                                    /* proj/src/schur.cpp:227-230 */
 
+/* ---- transverse Fourier transforms of the 3D extension ----
+ * field: device, r x m_y column-major (plane y = field + y r); coeff: device,
+ * m_y x r = (m_y / 2) modes x (real, imaginary) as Schur-batch systems 2 j + part.
+ * m_y a power of two in [2, 4096]. */
+int smpm_fourier_y(long long r, int m_y, const double* field, double* coeff, void* stream);         /* proj/src/fourier.cpp:47-62 */
+int smpm_inverse_fourier_y(long long r, int m_y, const double* coeff, double* field, void* stream); /* proj/src/fourier.cpp:64-86 */
+
 /* ---- solves --------------------------------------------------------------- */
 /* Batched solve of S x_S = b_S for every system of the batch with `method`
  * (dbj: proj/src/deflation.cpp:102-122, 2las: :124-143, bj: proj/src/gmres.cpp:144-150,

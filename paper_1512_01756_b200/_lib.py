@@ -26,7 +26,7 @@ EXPORTS = [
     "smpm_apply_Zt", "smpm_coarse_solve", "smpm_apply_P", "smpm_apply_Q", "smpm_project_out", "smpm_solve",
     "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_batch_launch_count",
     "smpm_batch_profile", "smpm_fp64_peak", "smpm_batch_set_strip_factors", "smpm_schur_rhs",
-    "smpm_recover_solution", "smpm_solve_stacked",
+    "smpm_recover_solution", "smpm_solve_stacked", "smpm_fourier_y", "smpm_inverse_fourier_y",
 ]
 PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other", "cluster_arnoldi", "grid_tail",
                    "spectral_op", "transform", "reserved"]
@@ -121,6 +121,8 @@ def lib():
     L.smpm_fp64_peak.argtypes = [ip, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.smpm_batch_set_strip_factors.argtypes = [vp, C.POINTER(StripFactors)]
     L.smpm_schur_rhs.argtypes = [vp, dp, dp, vp]
+    L.smpm_fourier_y.argtypes = [llp, ip, dp, dp, vp]
+    L.smpm_inverse_fourier_y.argtypes = [llp, ip, dp, dp, vp]
     L.smpm_recover_solution.argtypes = [vp, dp, dp, dp, vp]
     _lib = L
     return L

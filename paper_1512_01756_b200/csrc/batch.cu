@@ -29,6 +29,7 @@
 #include "spectral.cuh"
 #include "xform.cuh"
 #include "strip.cuh"
+#include "fourier.cuh"
 
 using namespace smpm;
 
@@ -2090,11 +2091,13 @@ void strip_modes(smpm_batch* b, const double* Xh, double* out, cudaStream_t st) 
   const StripParams P = strip_params(b);
   const dim3 grid((P.nmode + 127) / 128, P.mx, P.nsys);
   switch (P.n) {
-    case 9: strip_modes_kernel<9, TRACES><<<grid, 128, 0, st>>>(P, Xh, out); break;
-    case 11: strip_modes_kernel<11, TRACES><<<grid, 128, 0, st>>>(P, Xh, out); break;
-    case 13: strip_modes_kernel<13, TRACES><<<grid, 128, 0, st>>>(P, Xh, out); break;
-    case 17: strip_modes_kernel<17, TRACES><<<grid, 128, 0, st>>>(P, Xh, out); break;
-    default: fail(SMPM_EINVAL, "strip solver: n must be 9, 11, 13 or 17");
+#define SMPM_STRIP_CASE(N) \
+  case N: strip_modes_kernel<N, TRACES><<<grid, 128, 0, st>>>(P, Xh, out); break;
+    SMPM_STRIP_CASE(4) SMPM_STRIP_CASE(5) SMPM_STRIP_CASE(6) SMPM_STRIP_CASE(7) SMPM_STRIP_CASE(8)
+    SMPM_STRIP_CASE(9) SMPM_STRIP_CASE(10) SMPM_STRIP_CASE(11) SMPM_STRIP_CASE(12) SMPM_STRIP_CASE(13)
+    SMPM_STRIP_CASE(14) SMPM_STRIP_CASE(15) SMPM_STRIP_CASE(16) SMPM_STRIP_CASE(17)
+#undef SMPM_STRIP_CASE
+    default: fail(SMPM_EINVAL, "strip solver: n must be in [4, 17]");
   }
   check_launch(b);
 }
@@ -2112,6 +2115,50 @@ void need_strip(smpm_batch* b) {
   need_final(b);
   if (!b->strip_ok) fail(SMPM_EINVAL, "strip factors not set (smpm_batch_set_strip_factors)");
   strip_scratch(b);
+}
+
+// ---- transverse Fourier transforms (fourier.cuh) ----------------------------
+// twiddle tables exp(sign 2 pi i k / m), k < m / 2, per (device, m, sign), kept for the process
+const double2* fy_twiddles(int m, int sign) {
+  static std::vector<std::pair<long long, double*>> cache;
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  const long long key = (static_cast<long long>(dev) << 32) | (static_cast<long long>(m) << 1) | (sign > 0 ? 1 : 0);
+  for (auto& e : cache)
+    if (e.first == key) return reinterpret_cast<const double2*>(e.second);
+  std::vector<double> h(static_cast<size_t>(m));
+  for (int k = 0; k < m / 2; ++k) {
+    const double ang = sign * 2.0 * M_PI * k / m;
+    h[2 * k] = std::cos(ang);
+    h[2 * k + 1] = std::sin(ang);
+  }
+  double* d = nullptr;
+  CUDA_CHECK(cudaMalloc(&d, sizeof(double) * h.size()));
+  CUDA_CHECK(cudaMemcpy(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+  cache.emplace_back(key, d);
+  return reinterpret_cast<const double2*>(d);
+}
+
+void fourier_launch(long long r, int m_y, const double* in, double* out, int sign, cudaStream_t st) {
+  if (r < 1 || m_y < 2 || m_y > 4096 || (m_y & (m_y - 1)) != 0)
+    fail(SMPM_EINVAL, "fourier_y: m_y must be a power of two in [2, 4096] and r >= 1");
+  if (!in || !out) fail(SMPM_EINVAL, "null vector");
+  FourierArgs a;
+  a.r = r;
+  a.m_y = m_y;
+  a.tile = std::max(1, std::min(32, 6144 / (m_y + 1)));
+  a.tw = fy_twiddles(m_y, sign);
+  const size_t smem = sizeof(double2) * static_cast<size_t>(a.tile) * (m_y + 1);
+  const unsigned grid = static_cast<unsigned>((r + a.tile - 1) / a.tile);
+  if (sign < 0) {
+    CUDA_CHECK(cudaFuncSetAttribute(fourier_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    fourier_y_kernel<<<grid, FY_THREADS, smem, st>>>(a, in, out);
+  } else {
+    CUDA_CHECK(cudaFuncSetAttribute(inverse_fourier_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    inverse_fourier_y_kernel<<<grid, FY_THREADS, smem, st>>>(a, in, out);
+  }
+  CUDA_CHECK(cudaGetLastError());
 }
 
 extern "C" {
@@ -2415,6 +2462,14 @@ int smpm_recover_solution(smpm_batch* b, const double* f, const double* x_S, dou
     strip_scatter_kernel<<<grid_for(tot), 256, 0, st>>>(P, b->dsx2.p, u);
     check_launch(b);
   });
+}
+
+int smpm_fourier_y(long long r, int m_y, const double* field, double* coeff, void* stream) {
+  return guard([&] { fourier_launch(r, m_y, field, coeff, -1, static_cast<cudaStream_t>(stream)); });
+}
+
+int smpm_inverse_fourier_y(long long r, int m_y, const double* coeff, double* field, void* stream) {
+  return guard([&] { fourier_launch(r, m_y, coeff, field, +1, static_cast<cudaStream_t>(stream)); });
 }
 
 int smpm_project_out(smpm_batch* b, long long len, const double* v, const double* dir, double* out, void* stream) {

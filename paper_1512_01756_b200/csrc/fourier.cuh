@@ -1,0 +1,111 @@
+// Transverse Fourier transforms of the 3D extension, sm_100a:
+//   fourier_transform_y  (/root/reference/proj/src/fourier.cpp:47-62): per node row of an
+//     r x m_y field (column-major: plane y is a contiguous r-vector), the first m_y / 2
+//     coefficients of the forward DFT, scaled by 1 / m_y;
+//   inverse_fourier_y    (:64-86): the Hermitian extension of those coefficients
+//     (Nyquist term zero) transformed back, real part.
+// Coefficients are laid out as Schur-batch systems: system 2 j + part (part 0 = real,
+// 1 = imaginary) is the r-vector of mode j, so the per-mode real / imaginary right-hand
+// sides of proj/src/helmholtz.cpp:162-178 feed smpm_schur_rhs directly.
+// One CTA per tile of consecutive nodes: coalesced loads along the nodes of each plane
+// into shared memory (node rows padded to m_y + 1), one radix-2 FFT per node by a warp (bit reversal, log2 m_y
+// butterfly stages, twiddles from a table), coalesced stores per mode.
+#pragma once
+
+#include "common.cuh"
+
+namespace smpm {
+
+constexpr int FY_THREADS = 256;
+
+struct FourierArgs {
+  long long r;            // nodes (rows)
+  int m_y;                // planes (power of two)
+  int tile;               // nodes per CTA
+  const double2* tw;      // m_y / 2 twiddles exp(sign 2 pi i k / m_y) for the direction used
+};
+
+// in-place radix-2 FFT of x[0..m) (shared memory) by one warp; tw[k] = exp(sign 2 pi i k / m)
+__device__ __forceinline__ void warp_fft(double2* x, int m, const double2* __restrict__ tw) {
+  const int lane = threadIdx.x & 31;
+  int lg = 0;
+  while ((1 << lg) < m) ++lg;
+  for (int i = lane; i < m; i += 32) {
+    const int j = static_cast<int>(__brev(static_cast<unsigned>(i)) >> (32 - lg));
+    if (i < j) {
+      const double2 t = x[i];
+      x[i] = x[j];
+      x[j] = t;
+    }
+  }
+  __syncwarp();
+  for (int len = 2; len <= m; len <<= 1) {
+    const int h = len >> 1, step = m / len;
+    for (int b = lane; b < m / 2; b += 32) {
+      const int grp = b / h, jj = b - grp * h;
+      const int i0 = grp * len + jj, i1 = i0 + h;
+      const double2 w = tw[jj * step];
+      const double2 v = x[i1];
+      const double2 vw = make_double2(fma(v.x, w.x, -v.y * w.y), fma(v.x, w.y, v.y * w.x));
+      const double2 u = x[i0];
+      x[i0] = make_double2(u.x + vw.x, u.y + vw.y);
+      x[i1] = make_double2(u.x - vw.x, u.y - vw.y);
+    }
+    __syncwarp();
+  }
+}
+
+// field (r x m_y, plane-major) -> coeff (2 (m_y/2) systems x r)
+__global__ void __launch_bounds__(FY_THREADS) fourier_y_kernel(FourierArgs a, const double* __restrict__ field,
+                                                               double* __restrict__ coeff) {
+  extern __shared__ double2 fy_smem[];
+  const int m = a.m_y, half = m / 2, T = a.tile;
+  const long long i0 = static_cast<long long>(blockIdx.x) * T;
+  const int nt = static_cast<int>(min(static_cast<long long>(T), a.r - i0));
+  for (int e = threadIdx.x; e < T * m; e += FY_THREADS) {
+    const int y = e / T, n = e - y * T;
+    fy_smem[n * (m + 1) + y] = make_double2(n < nt ? field[static_cast<long long>(y) * a.r + i0 + n] : 0.0, 0.0);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, nw = FY_THREADS / 32;
+  for (int n = warp; n < nt; n += nw) warp_fft(fy_smem + n * (m + 1), m, a.tw);
+  __syncthreads();
+  const double inv = 1.0 / m;
+  for (int e = threadIdx.x; e < 2 * half * T; e += FY_THREADS) {
+    const int s = e / T, n = e - s * T, j = s >> 1;
+    if (n < nt) {
+      const double2 c = fy_smem[n * (m + 1) + j];
+      coeff[static_cast<long long>(s) * a.r + i0 + n] = ((s & 1) ? c.y : c.x) * inv;
+    }
+  }
+}
+
+// coeff (2 (m_y/2) systems x r) -> field (r x m_y): Hermitian extension, Nyquist zero
+__global__ void __launch_bounds__(FY_THREADS) inverse_fourier_y_kernel(FourierArgs a, const double* __restrict__ coeff,
+                                                                       double* __restrict__ field) {
+  extern __shared__ double2 fy_smem[];
+  const int m = a.m_y, half = m / 2, T = a.tile;
+  const long long i0 = static_cast<long long>(blockIdx.x) * T;
+  const int nt = static_cast<int>(min(static_cast<long long>(T), a.r - i0));
+  for (int e = threadIdx.x; e < T * m; e += FY_THREADS) {
+    const int y = e / T, n = e - y * T;
+    double2 v = make_double2(0.0, 0.0);
+    if (n < nt && y != half) {
+      const int j = y < half ? y : m - y;  // row(m - j) = conj(coeff_j)
+      const double re = coeff[static_cast<long long>(2 * j) * a.r + i0 + n];
+      const double im = coeff[static_cast<long long>(2 * j + 1) * a.r + i0 + n];
+      v = make_double2(re, y < half ? im : -im);
+    }
+    fy_smem[n * (m + 1) + y] = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, nw = FY_THREADS / 32;
+  for (int n = warp; n < nt; n += nw) warp_fft(fy_smem + n * (m + 1), m, a.tw);
+  __syncthreads();
+  for (int e = threadIdx.x; e < T * m; e += FY_THREADS) {
+    const int y = e / T, n = e - y * T;
+    if (n < nt) field[static_cast<long long>(y) * a.r + i0 + n] = fy_smem[n * (m + 1) + y].x;
+  }
+}
+
+}  // namespace smpm

@@ -269,8 +269,11 @@ __device__ __forceinline__ void spec_warp_item(const SpecParams& sp, int s, int 
 // th = T^-1-space operator of the live systems; with zpart, the last CTA of
 // each system also solves the coarse system for c = C^{-1} Z^T (T th) -> cout.
 // grid (nmc * ceil(nseg / SP_WARPS), live slots)
+#ifndef SP_MINB
+#define SP_MINB 1
+#endif
 template <bool BJ>
-__global__ void __launch_bounds__(SP_THREADS) spec_op_kernel(SpecParams sp, const double* __restrict__ vh,
+__global__ void __launch_bounds__(SP_THREADS, SP_MINB) spec_op_kernel(SpecParams sp, const double* __restrict__ vh,
                                                              double* __restrict__ th, DeflateParams P, double* zpart,
                                                              int* counter, double* cout, double* __restrict__ uh) {
   pdl_wait();

@@ -212,7 +212,7 @@ def load_batch(ctx, ps: ProblemSet, spectral: bool = True):
         npairs, T, Ti, gam = ps.fdm.spectral(ps.mus)
         b.set_spectral(npairs, T, Ti, gam)
     b.finalize()
-    if spectral and b.m_x >= 3 and b.n in (9, 11, 13, 17):
+    if spectral and b.m_x >= 3 and 4 <= b.n <= 17:
         b.set_strip_factors(ps.fdm.strip_factors(ps.mus))
     if ps.b_S is None:
         # device b_S = B (A - mu)^{-1} f, then the mode-0 projection with u_S
