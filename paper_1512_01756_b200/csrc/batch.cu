@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -2121,6 +2122,8 @@ void need_strip(smpm_batch* b) {
 // twiddle tables exp(sign 2 pi i k / m), k < m / 2, per (device, m, sign), kept for the process
 const double2* fy_twiddles(int m, int sign) {
   static std::vector<std::pair<long long, double*>> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   int dev = 0;
   CUDA_CHECK(cudaGetDevice(&dev));
   const long long key = (static_cast<long long>(dev) << 32) | (static_cast<long long>(m) << 1) | (sign > 0 ? 1 : 0);
