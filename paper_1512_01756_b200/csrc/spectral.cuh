@@ -36,6 +36,8 @@ struct SpecParams {
   const double2* gam;          // nsys x SK_NUM x nmode
   const double2* kinv;         // nsys x 5 x 4 x nmode: reduced block inverses (variants first|last<<1, 4 = single)
   const double* omega;         // w: column sums of T (Z^T weights)
+  const double* nu;            // w: T^{-1} 1, a constant w-block in spectral coordinates
+  const double* cadd;          // nullable, nsys x d: 2LAS coarse solutions c added as Z c before S^
   int nmc, nseg, segb;         // 32-mode chunks, block segments of segb (<= SP_SEGB) blocks
 };
 
@@ -61,7 +63,7 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 // base + beta*w + e0 (and e0 + 1 for the second coordinate of a pair)
 struct ModeRef {
   long long base;
-  int w, e0;
+  int sys, w, e0;
   bool pair;
   __device__ __forceinline__ double2 ld(const double* v, int beta) const {
     const double* p = v + base + static_cast<long long>(beta) * w + e0;
@@ -79,6 +81,7 @@ struct ModeRef {
 
 __device__ __forceinline__ ModeRef mode_ref(const SpecParams& sp, int s, int m) {
   ModeRef r;
+  r.sys = s;
   r.base = s * sp.k;
   r.w = sp.w;
   r.pair = m < sp.npairs;
@@ -194,6 +197,18 @@ __device__ __forceinline__ void spec_load_solve(const SpecParams& sp, const Mode
     y[j].y *= ysc;
   }
   spec_block_solve<BJ>(sp, g, ki, blk, y, x);
+  if (sp.cadd) {
+    // 2LAS: (M^{-1} + Z C^{-1} Z^T) v in spectral coordinates: slot 4 blk + j of
+    // interface 2 blk + j / 2 gains c_i T^{-1} 1 (proj/src/deflation.cpp:127-130)
+    const double* c = sp.cadd + static_cast<long long>(mr.sys) * sp.d;
+    const double2 nu = make_double2(sp.nu[mr.e0], mr.pair ? -sp.nu[mr.e0 + 1] : 0.0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < ns) {
+        const double ci = c[2 * blk + (j >> 1)];
+        x[j] = make_double2(fma(ci, nu.x, x[j].x), fma(ci, nu.y, x[j].y));
+      }
+  }
 }
 
 // One mode, block-Jacobi blocks [b0, b1): th = S^ M^^{-1} vh (or S^ vh), and
