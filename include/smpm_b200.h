@@ -117,6 +117,11 @@ int smpm_batch_set_interface_blocks(smpm_batch* b, int sys, const double* const*
                                     const long long* const* seg_start, const long long* const* seg_len,
                                     const int* nseg);
 
+/* Reads the reference's binary block file (dump_schur_blocks, proj/src/schur.cpp:246-297:
+ * int64 n, m_x, m_z, k; per interface block rows, cols, nseg, (start, len) x nseg,
+ * column-major entries) for system `sys` and imports it as set_interface_blocks does. */
+int smpm_batch_load_schur_blocks(smpm_batch* b, int sys, const char* path);
+
 /* Left null vector u_S of a singular system (the j = 0 / Poisson system):
  * marks the system singular; the coarse solve uses the rank-one shift
  * (C + u_C u_C^T) with u_C = normalize(Z^T u_S) (proj/src/deflation.cpp:44-54). */

@@ -255,6 +255,10 @@ class System:
         _chk(lib().orc_recover(C.c_void_p(self.h), _p(f), _p(x_S), _p(u)))
         return u
 
+    def dump_blocks(self, path):
+        """The reference's binary block file (proj/src/schur.cpp:246-264); needs layout_reference."""
+        _chk(lib().orc_dump_schur_blocks(C.c_void_p(self.h), str(path).encode()))
+
     def dense_S(self):
         out = np.zeros((self.k, self.k), order="F")
         _chk(lib().orc_dense_S(C.c_void_p(self.h), _p(out)))

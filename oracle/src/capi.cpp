@@ -2,6 +2,8 @@
 // __graft_entry__.smoke() and bench.py's CPU-baseline legs. Not the product.
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -385,6 +387,34 @@ int orc_solve(void* vs, void* vc, int method, const double* b, double tol, int m
     }
     vout(r.x_S, x);
     fill_report(r, rep, hist, cap);
+  });
+}
+
+// proj/src/schur.cpp:246-264 (dump_schur_blocks): the reference's binary block file
+// (int64 n, m_x, m_z, k; per interface block: rows, cols, nseg, (start, len) x nseg,
+// then the column-major entries). Needs the materialized reference layout.
+int orc_dump_schur_blocks(void* vs, const char* path) {
+  return guard([&] {
+    const SchurSystem& sys = static_cast<System*>(vs)->sys;
+    if (!sys.materialized) invalid("dump_schur_blocks: needs the reference per-interface layout");
+    std::FILE* fp = std::fopen(path, "wb");
+    if (!fp) runtime(std::string("dump_schur_blocks: cannot open ") + path);
+    auto put = [&](std::int64_t v) { std::fwrite(&v, sizeof v, 1, fp); };
+    put(sys.op->mesh.n);
+    put(sys.op->mesh.m_x);
+    put(sys.op->mesh.m_z);
+    put(sys.k);
+    for (const auto& blk : sys.blocks) {
+      put(blk.entries.rows);
+      put(blk.entries.cols);
+      put(static_cast<std::int64_t>(blk.segs.size()));
+      for (const auto& sg : blk.segs) {
+        put(sg.first);
+        put(sg.second);
+      }
+      std::fwrite(blk.entries.data(), sizeof(double), blk.entries.a.size(), fp);
+    }
+    std::fclose(fp);
   });
 }
 

@@ -27,6 +27,7 @@ EXPORTS = [
     "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_batch_launch_count",
     "smpm_batch_profile", "smpm_fp64_peak", "smpm_batch_set_strip_factors", "smpm_schur_rhs",
     "smpm_recover_solution", "smpm_solve_stacked", "smpm_fourier_y", "smpm_inverse_fourier_y",
+    "smpm_batch_load_schur_blocks",
 ]
 PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other", "cluster_arnoldi", "grid_tail",
                    "spectral_op", "transform", "reserved"]
@@ -102,6 +103,7 @@ def lib():
     L.smpm_batch_set_interface_blocks.argtypes = [vp, ip, C.POINTER(dp), C.POINTER(llp), C.POINTER(C.c_void_p),
                                                   C.POINTER(C.c_void_p), C.POINTER(ip)]
     L.smpm_batch_set_nullspace.argtypes = [vp, ip, dp]
+    L.smpm_batch_load_schur_blocks.argtypes = [vp, ip, C.c_char_p]
     L.smpm_batch_set_spectral.argtypes = [vp, ip, dp, dp, dp]
     L.smpm_batch_finalize.argtypes = [vp]
     L.smpm_batch_coarse_info.argtypes = [vp, dp, C.POINTER(ip), C.POINTER(ip)]

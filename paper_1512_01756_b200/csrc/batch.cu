@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <cstdint>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -2293,6 +2294,51 @@ int smpm_batch_set_spectral(smpm_batch* b, int npairs, const double* T, const do
     const size_t ng = static_cast<size_t>(b->nsys) * SK_NUM * b->sp_nmode * 2;
     b->hgam.assign(gamma, gamma + ng);
     b->spectral = true;
+  });
+}
+
+int smpm_batch_load_schur_blocks(smpm_batch* b, int sys, const char* path) {
+  return guard([&] {
+    if (!b || !path) fail(SMPM_EINVAL, "null argument");
+    std::FILE* fp = std::fopen(path, "rb");
+    if (!fp) fail(SMPM_EINVAL, std::string("load_schur_blocks: cannot open ") + path);
+    std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard_fp(fp, std::fclose);
+    auto get = [&]() {
+      std::int64_t v = 0;
+      if (std::fread(&v, sizeof v, 1, fp) != 1) fail(SMPM_EINVAL, "load_schur_blocks: truncated file");
+      return static_cast<long long>(v);
+    };
+    const long long n = get(), mx = get(), mz = get(), k = get();
+    if (n != b->n || mx != b->mx || mz != b->mz || k != b->k)
+      fail(SMPM_EINVAL, "load_schur_blocks: file geometry differs from the batch");
+    const int d = b->d;
+    std::vector<std::vector<double>> ent(d);
+    std::vector<std::vector<long long>> st(d), ln(d);
+    std::vector<long long> rows(d);
+    std::vector<int> nseg(d);
+    for (int i = 0; i < d; ++i) {
+      rows[i] = get();
+      const long long cols = get(), ns = get();
+      if (cols != 2LL * b->w || rows[i] <= 0 || rows[i] > 4LL * b->w || ns < 1 || ns > 4)
+        fail(SMPM_EINVAL, "load_schur_blocks: unexpected block shape");
+      nseg[i] = static_cast<int>(ns);
+      for (long long q = 0; q < ns; ++q) {
+        st[i].push_back(get());
+        ln[i].push_back(get());
+      }
+      ent[i].resize(static_cast<size_t>(rows[i] * cols));
+      if (std::fread(ent[i].data(), sizeof(double), ent[i].size(), fp) != ent[i].size())
+        fail(SMPM_EINVAL, "load_schur_blocks: truncated file");
+    }
+    std::vector<const double*> ep(d);
+    std::vector<const long long*> sp(d), lp(d);
+    for (int i = 0; i < d; ++i) {
+      ep[i] = ent[i].data();
+      sp[i] = st[i].data();
+      lp[i] = ln[i].data();
+    }
+    const int rc = smpm_batch_set_interface_blocks(b, sys, ep.data(), rows.data(), sp.data(), lp.data(), nseg.data());
+    if (rc != SMPM_OK) fail(rc, smpm_last_error());
   });
 }
 

@@ -131,6 +131,10 @@ class SchurBatch:
         ns = (C.c_int * d)(*[len(s) for s in starts])
         check(lib().smpm_batch_set_interface_blocks(self.h, sys, ep, rows, sp, lp, ns))
 
+    def load_schur_blocks(self, sys: int, path):
+        """The reference's dump_schur_blocks file (proj/src/schur.cpp:246-297) for system `sys`."""
+        check(lib().smpm_batch_load_schur_blocks(self.h, sys, str(path).encode()))
+
     def set_nullspace(self, sys: int, u_S):
         u = np.ascontiguousarray(u_S, dtype=np.float64)
         if u.size != self.k:
