@@ -2174,7 +2174,10 @@ void fourier_launch(long long r, int m_y, const double* in, double* out, int sig
   FourierArgs a;
   a.r = r;
   a.m_y = m_y;
-  a.tile = std::max(1, std::min(32, 6144 / (m_y + 1)));
+  // nodes per CTA: 16 (128-byte coalesced runs per plane) while the padded complex
+  // tile stays <= 66 KB (3 CTAs per SM), fewer for long transforms
+  a.tile = std::max(1, std::min(16, 4224 / (m_y + 1)));
+  if (const char* e = std::getenv("SMPM_FY_TILE")) a.tile = std::max(1, std::min(64, std::atoi(e)));
   a.tw = fy_twiddles(m_y, sign);
   const size_t smem = sizeof(double2) * static_cast<size_t>(a.tile) * (m_y + 1);
   const unsigned grid = static_cast<unsigned>((r + a.tile - 1) / a.tile);

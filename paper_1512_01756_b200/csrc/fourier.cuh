@@ -39,12 +39,12 @@ __device__ __forceinline__ void warp_fft(double2* x, int m, const double2* __res
     }
   }
   __syncwarp();
-  for (int len = 2; len <= m; len <<= 1) {
-    const int h = len >> 1, step = m / len;
+  for (int ls = 0; ls < lg; ++ls) {
+    const int h = 1 << ls, sshift = lg - 1 - ls;  // half length, log2(m / len)
     for (int b = lane; b < m / 2; b += 32) {
-      const int grp = b / h, jj = b - grp * h;
-      const int i0 = grp * len + jj, i1 = i0 + h;
-      const double2 w = tw[jj * step];
+      const int grp = b >> ls, jj = b & (h - 1);
+      const int i0 = (grp << (ls + 1)) + jj, i1 = i0 + h;
+      const double2 w = __ldg(tw + (jj << sshift));
       const double2 v = x[i1];
       const double2 vw = make_double2(fma(v.x, w.x, -v.y * w.y), fma(v.x, w.y, v.y * w.x));
       const double2 u = x[i0];
@@ -62,9 +62,10 @@ __global__ void __launch_bounds__(FY_THREADS) fourier_y_kernel(FourierArgs a, co
   const int m = a.m_y, half = m / 2, T = a.tile;
   const long long i0 = static_cast<long long>(blockIdx.x) * T;
   const int nt = static_cast<int>(min(static_cast<long long>(T), a.r - i0));
+#pragma unroll 8
   for (int e = threadIdx.x; e < T * m; e += FY_THREADS) {
     const int y = e / T, n = e - y * T;
-    fy_smem[n * (m + 1) + y] = make_double2(n < nt ? field[static_cast<long long>(y) * a.r + i0 + n] : 0.0, 0.0);
+    fy_smem[n * (m + 1) + y] = make_double2(n < nt ? __ldcs(field + static_cast<long long>(y) * a.r + i0 + n) : 0.0, 0.0);
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, nw = FY_THREADS / 32;
@@ -87,13 +88,14 @@ __global__ void __launch_bounds__(FY_THREADS) inverse_fourier_y_kernel(FourierAr
   const int m = a.m_y, half = m / 2, T = a.tile;
   const long long i0 = static_cast<long long>(blockIdx.x) * T;
   const int nt = static_cast<int>(min(static_cast<long long>(T), a.r - i0));
+#pragma unroll 4
   for (int e = threadIdx.x; e < T * m; e += FY_THREADS) {
     const int y = e / T, n = e - y * T;
     double2 v = make_double2(0.0, 0.0);
     if (n < nt && y != half) {
       const int j = y < half ? y : m - y;  // row(m - j) = conj(coeff_j)
-      const double re = coeff[static_cast<long long>(2 * j) * a.r + i0 + n];
-      const double im = coeff[static_cast<long long>(2 * j + 1) * a.r + i0 + n];
+      const double re = __ldcs(coeff + static_cast<long long>(2 * j) * a.r + i0 + n);
+      const double im = __ldcs(coeff + static_cast<long long>(2 * j + 1) * a.r + i0 + n);
       v = make_double2(re, y < half ? im : -im);
     }
     fy_smem[n * (m + 1) + y] = v;
