@@ -2181,13 +2181,17 @@ void fourier_launch(long long r, int m_y, const double* in, double* out, int sig
   a.tw = fy_twiddles(m_y, sign);
   const size_t smem = sizeof(double2) * static_cast<size_t>(a.tile) * (m_y + 1);
   const unsigned grid = static_cast<unsigned>((r + a.tile - 1) / a.tile);
-  if (sign < 0) {
-    CUDA_CHECK(cudaFuncSetAttribute(fourier_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    fourier_y_kernel<<<grid, FY_THREADS, smem, st>>>(a, in, out);
-  } else {
-    CUDA_CHECK(cudaFuncSetAttribute(inverse_fourier_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    inverse_fourier_y_kernel<<<grid, FY_THREADS, smem, st>>>(a, in, out);
+  auto go = [&](auto kfwd, auto kinv) {
+    auto k = sign < 0 ? kfwd : kinv;
+    CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k<<<grid, FY_THREADS, smem, st>>>(a, in, out);
+  };
+  switch (m_y) {  // register FFT for 64 <= m_y <= 512 (R = m_y / 32 per lane)
+    case 64: go(fourier_y_kernel<2>, inverse_fourier_y_kernel<2>); break;
+    case 128: go(fourier_y_kernel<4>, inverse_fourier_y_kernel<4>); break;
+    case 256: go(fourier_y_kernel<8>, inverse_fourier_y_kernel<8>); break;
+    case 512: go(fourier_y_kernel<16>, inverse_fourier_y_kernel<16>); break;
+    default: go(fourier_y_kernel<0>, inverse_fourier_y_kernel<0>); break;
   }
   CUDA_CHECK(cudaGetLastError());
 }

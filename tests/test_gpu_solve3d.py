@@ -32,7 +32,7 @@ def np_inverse_fourier_y(coeff, m):
     return (np.fft.ifft(row, axis=0) * m).real
 
 
-@pytest.mark.parametrize("m_y", [2, 8, 64, 256])
+@pytest.mark.parametrize("m_y", [2, 8, 32, 64, 128, 256, 512, 1024])
 def test_fourier_transforms(ctx, m_y):
     import torch
 
