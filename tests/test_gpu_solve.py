@@ -66,3 +66,18 @@ def test_restart(ctx):
     case = build_case(6, 6, 4, 24.0, 4.0, (0.0,))
     b = gpu_batch(ctx, case)
     check_solve(case, b, "schur", max_iter=60, restart=8)
+
+
+def test_long_cycle_unrestarted(ctx):
+    """Unrestarted GMRES with a cycle longer than the grid tail and the long-chunk
+    CGS2 kernels carry (m + 2 > 128): the column-count-agnostic passes of vec.cuh."""
+    case = build_case(6, 6, 4, 24.0, 4.0, (0.0,))
+    b = gpu_batch(ctx, case)
+    check_solve(case, b, "schur", max_iter=200, restart=0)
+
+
+def test_long_cycle_batched_helmholtz(ctx):
+    mus = [(2 * np.pi * j / 6.0) ** 2 for j in range(6)]
+    case = build_case(7, 6, 4, 6.0, 1.0, mus, kmax=4, decay=True)
+    b = gpu_batch(ctx, case)
+    check_solve(case, b, "dbj", max_iter=150, restart=0)
