@@ -275,6 +275,7 @@ struct smpm_batch {
   DevArray<double> dTfrag, dTifrag;    // T, T^{-1} in the xform fragment order
   int xf_P = 0, xf_MB = 0;
   long long cgs3_res = 0;  // resident CTAs of the CGS2 pass kernels (device)
+  bool pythag = true;  // norm from the second CGS2 reduction (cgs3_pass2n / cgs3_pass3s); SMPM_NO_PYTHAG=1: off
   bool pdl = true;  // programmatic dependent launch for the Arnoldi step chain (SMPM_NO_PDL=1: off)  // resident-slice transform kernel (xform.cuh); 0: use pF/pB
   size_t xf_smem = 0;
   Plan pc[6];          // unsplit per-system templates (BJ1, BJ2, BJ3, S; spectral F, B) for the persistent solvers
@@ -1359,6 +1360,15 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
     Gl.nchunk = static_cast<int>((b->k + chunk - 1) / chunk);
     dim3 cgrid(Gl.nchunk, lv.nslots);
     DeflateParams P = deflate_params(b, nullptr);
+    if (!G.stacked && b->pythag) {
+      // ||w|| from the second reduction (||w1||^2 - ||h2||^2), the scale folded into pass 3:
+      // one reduction and one kernel less per step; iteration counts measured unchanged
+      // on 9 right-hand sides (tools/seed_sweep.py)
+      launch_pdl(b, cgs3_dot_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, tdefl, P, cbuf);
+      launch_pdl(b, cgs3_pass2n_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, static_cast<const double*>(V), wv);
+      launch_pdl(b, cgs3_pass3s_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, vin);
+      return;
+    }
     launch_pdl(b, cgs3_dot_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, tdefl, P, cbuf);
     if (G.stacked) launch_pdl(b, stack_h_kernel, dim3(1), dim3(128), 0, st, G, G.h1);
     launch_pdl(b, cgs3_update_kernel<false>, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv);
@@ -1655,6 +1665,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
            cudaStream_t st) {
   need_final(b);
   b->pdl = std::getenv("SMPM_NO_PDL") == nullptr;
+  b->pythag = std::getenv("SMPM_NO_PYTHAG") == nullptr;
   if (c.max_iter < 1) fail(SMPM_EINVAL, "max_iter must be >= 1");
   const int mtot = static_cast<int>(std::min<long long>(c.max_iter, b->k));
   int m = c.restart > 0 ? std::min(c.restart, mtot) : mtot;

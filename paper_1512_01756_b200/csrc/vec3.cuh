@@ -219,4 +219,85 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_update_kernel(GmState_ G, con
   givens_step(G, s, j, sqrt(nsq));
 }
 
+// ---- default CGS2 passes 2/3 (SMPM_NO_PYTHAG=1 restores cgs3_update<true> + scale) ----
+// pass 2': w -= V h1; h2 = V^T w and ||w||^2 in one reduction; the last CTA takes
+// ||w - V h2||^2 = ||w||^2 - ||h2||^2 (h2 is the O(eps) reorthogonalisation
+// correction, so the difference is accurate) and runs the Givens step
+__global__ void __launch_bounds__(V3_THREADS) cgs3_pass2n_kernel(GmState_ G, const double* __restrict__ V, double* w) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ double hs[V2_MAXCOL];
+  __shared__ double red[V3_THREADS / 32][V3_GRP];
+  int s;
+  if (!gm_slot(G, blockIdx.y, s)) return;
+  const int j = G.jcyc[s];
+  const int ncols = j + 1;
+  const int stride = G.m + 2;
+  const double* hin = G.h1 + static_cast<long long>(s) * stride;
+  for (int i = threadIdx.x; i < ncols; i += V3_THREADS) hs[i] = hin[i];
+  __syncthreads();
+  const int ch = blockIdx.x;
+  const int r0 = static_cast<int>(min(G.k, static_cast<long long>(ch) * G.chunk));
+  const int r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
+  const double* Vs = V + s * G.vstride;
+  double* ws = w + s * G.k;
+  double sq = rows_update_long(Vs, G.k, ncols, hs, ws, r0, r1);
+  double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
+  __syncthreads();
+  cta_dots_long(Vs, G.k, ncols, ws, r0, r1, part, red);
+  sq = warp_sum(sq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][0] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tsum = 0.0;
+    for (int q = 0; q < V3_THREADS / 32; ++q) tsum += red[q][0];
+    part[ncols] = tsum;
+  }
+  if (!last_cta(G.counter + s, G.nchunk)) return;
+  double* h2 = G.h2 + static_cast<long long>(s) * stride;
+  reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols + 1, h2);
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  double hh = 0.0;
+  for (int i = threadIdx.x; i < ncols; i += 32) hh = fma(h2[i], h2[i], hh);
+  hh = warp_sum(hh);
+  const double nsq = h2[ncols];
+  __syncwarp();
+  if (threadIdx.x == 0) h2[ncols] = 0.0;
+  __syncwarp();
+  givens_step(G, s, j, sqrt(fmax(nsq - hh, 0.0)));
+}
+
+// pass 3': w -= V h2 and v_{j+1} = w / ||w|| into the basis and the operator input
+// (the scale kernel folded in; runs after the Givens step, so stopped systems skip it)
+__global__ void __launch_bounds__(V3_THREADS) cgs3_pass3s_kernel(GmState_ G, double* __restrict__ V, double* w,
+                                                                 double* __restrict__ vin) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ double hs[V2_MAXCOL];
+  int s;
+  if (!gm_slot(G, blockIdx.y, s)) return;
+  const int jn = G.jcyc[s];  // already advanced by the Givens step: the new column
+  const int ncols = jn;
+  const int stride = G.m + 2;
+  const double* hin = G.h2 + static_cast<long long>(s) * stride;
+  for (int i = threadIdx.x; i < ncols; i += V3_THREADS) hs[i] = hin[i];
+  __syncthreads();
+  const int ch = blockIdx.x;
+  const int r0 = static_cast<int>(min(G.k, static_cast<long long>(ch) * G.chunk));
+  const int r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
+  double* Vs = V + s * G.vstride;
+  double* ws = w + s * G.k;
+  rows_update_long(Vs, G.k, ncols, hs, ws, r0, r1);
+  __syncthreads();
+  const double inv = 1.0 / G.nrm[s];
+  double* col = Vs + static_cast<long long>(jn) * G.k;
+  double* vs = vin + s * G.k;
+  for (int r = r0 + threadIdx.x; r < r1; r += V3_THREADS) {
+    const double v = ws[r] * inv;
+    col[r] = v;
+    vs[r] = v;
+  }
+}
+
 }  // namespace smpm

@@ -1,0 +1,55 @@
+"""Solve time and iteration counts over several seeded right-hand sides (the
+iteration counts of plateau modes are rounding-sensitive, so
+evaluation-order changes are judged on the distribution, not one seed).
+
+    SEEDS=8 python tools/seed_sweep.py "" "SMPM_PYTHAG=1"
+"""
+import dataclasses
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1512_01756_b200 import Context  # noqa: E402
+from paper_1512_01756_b200.configs import CONFIGS  # noqa: E402
+from paper_1512_01756_b200.problems import build_problem, load_batch  # noqa: E402
+
+base_cfg = CONFIGS[os.environ.get("SWEEP_CONFIG", "C4")]
+nseeds = int(os.environ.get("SEEDS", "8"))
+settings = sys.argv[1:] or [""]
+ctx = Context(0)
+env0 = dict(os.environ)
+res = {st: [] for st in settings}
+for sd in range(nseeds):
+    cfg = dataclasses.replace(base_cfg, seed=base_cfg.seed + sd)
+    ps = build_problem(cfg, device="cuda", device_rhs=True)
+    for st in settings:
+        os.environ.clear()
+        os.environ.update(env0)
+        for kv in filter(None, st.split(",")):
+            k, v = kv.split("=")
+            os.environ[k] = v
+        b = load_batch(ctx, ps)
+        bS = torch.tensor(ps.b_S, device="cuda")
+        for _ in range(2):
+            r = b.solve(bS, "dbj", 1e-10, 10 * cfg.max_iter, cfg.max_iter, "cgs2", True, history=False)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = b.solve(bS, "dbj", 1e-10, 10 * cfg.max_iter, cfg.max_iter, "cgs2", True, history=False)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = sorted(ts)[2]
+        res[st].append((ms, sum(r.iterations), max(r.iterations), all(r.converged)))
+        print(f"seed {cfg.seed} {st or 'default':16s} {ms:.3f} ms iters sum {sum(r.iterations)} max {max(r.iterations)} "
+              f"conv {all(r.converged)}", flush=True)
+        b.close()
+for st in settings:
+    a = np.array([x[:3] for x in res[st]], dtype=float)
+    print(f"{st or 'default':16s} mean {a[:, 0].mean():.3f} ms  iters sum {a[:, 1].mean():.1f}  max {a[:, 2].mean():.1f}  "
+          f"all converged {all(x[3] for x in res[st])}")
