@@ -1604,6 +1604,7 @@ void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
   A.alist = alist;
   A.acount = acount;
   A.method = c.method;
+  A.pythag = b->pythag ? 1 : 0;
   A.G = G;
   A.P = deflate_params(b, nullptr);
   const char* tpath = std::getenv("SMPM_GT_TRACE");

@@ -79,6 +79,7 @@ struct GridArgs {
   const int* alist;        // candidate systems (compacted live list)
   const int* acount;
   int method;              // smpm_method
+  int pythag;              // ||w|| from the second CGS2 reduction (as cgs3_pass2n)
   unsigned long long* trace;  // debug: 64 steps x 16 phase timestamps of CTA 0 (nullable)
   unsigned long long* trace2; // debug: 4 steps x 4 stages x gridDim.x x 8 per-CTA timestamps (nullable)
   GmState_ G;
@@ -414,6 +415,28 @@ __device__ __forceinline__ double gt_update(const double* Vs, long long k, int n
   return sq;
 }
 
+// pass 3 with the norm known: w -= V h for this CTA's rows, then
+// v_{j+1} = w * inv into the basis column and the operator input (when col != nullptr)
+__device__ __forceinline__ void gt_update_scale(const double* Vs, long long k, int ncols, const double* h, double* ws,
+                                                int r0, int r1, double inv, double* col, double* vin) {
+  for (int r = r0 + static_cast<int>(threadIdx.x); r < r1; r += blockDim.x) {
+    double a4[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i0 = 0; i0 < ncols; i0 += 16) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = i0 + u < ncols ? __ldcg(Vs + static_cast<long long>(i0 + u) * k + r) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) a4[u & 3] = fma(v[u], i0 + u < ncols ? h[i0 + u] : 0.0, a4[u & 3]);
+    }
+    const double nv = __ldcg(ws + r) - ((a4[0] + a4[1]) + (a4[2] + a4[3]));
+    ws[r] = nv;
+    if (col) {
+      col[r] = nv * inv;
+      vin[r] = nv * inv;
+    }
+  }
+}
+
 // sum of the cluster's CTA partials pin[0..n) (rank order, through DSMEM) ->
 // gout[0..n) (this cluster's slot of a global partial buffer); ranks split the entries
 __device__ __forceinline__ void gt_cluster_sum(const double* pin, int n, double* gout) {
@@ -650,14 +673,67 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
     grid_sync(a.bar, epoch);
     gt_group_sum(part1, stride, gc0, gc1, ncols, hs);
     mark(7);
-    // ---- pass 2: w -= V h1 ; h2 = V^T w
-    gt_update(Vs, k, ncols, hs, ws, r0, r1);
+    // ---- pass 2: w -= V h1 ; h2 = V^T w (and ||w||^2 of the updated w)
+    const double sq1 = gt_update(Vs, k, ncols, hs, ws, r0, r1);
     __syncthreads();
     gt_col_dots(Vs, k, ncols, ws, r0, r1, pdot);
-    gt_cluster_sum(pdot, ncols, part2 + static_cast<long long>(cid) * stride);
+    const int n2 = a.pythag ? ncols + 1 : ncols;
+    if (a.pythag) {
+      const double q1 = warp_sum(sq1);
+      if ((threadIdx.x & 31) == 0) bred[threadIdx.x >> 5] = q1;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double tsum = 0.0;
+        for (int i = 0; i < G2_THREADS / 32; ++i) tsum += bred[i];
+        pdot[ncols] = tsum;
+      }
+    }
+    gt_cluster_sum(pdot, n2, part2 + static_cast<long long>(cid) * stride);
     grid_sync(a.bar, epoch);
-    gt_group_sum(part2, stride, gc0, gc1, ncols, h2s);
+    gt_group_sum(part2, stride, gc0, gc1, n2, h2s);
     mark(8);
+    if (a.pythag) {
+      // ||w - V h2||^2 = ||w||^2 - ||h2||^2 (h2 is the O(eps) reorthogonalisation
+      // correction); every CTA of the group computes it in the same order
+      if (threadIdx.x < 32) {
+        double hh = 0.0;
+        for (int i = threadIdx.x; i < ncols; i += 32) hh = fma(h2s[i], h2s[i], hh);
+        hh = warp_sum(hh);
+        if (threadIdx.x == 0) bred[0] = sqrt(fmax(h2s[ncols] - hh, 0.0));
+      }
+      __syncthreads();
+      const double nrm = bred[0];
+      if (idx == 0) {
+        double* gh1 = G.h1 + static_cast<long long>(s) * stride;
+        double* gh2 = G.h2 + static_cast<long long>(s) * stride;
+        for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
+          gh1[i] = hs[i];
+          gh2[i] = h2s[i];
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) givens_step(G, s, j, nrm);
+      }
+      // ---- pass 3: w -= V h2 ; v_{j+1} = w / ||w|| (own rows; unused if the system stops)
+      double* col = a.V + s * G.vstride + static_cast<long long>(j + 1) * k;
+      const bool wr = j + 1 <= G.m;
+      gt_update_scale(Vs, k, ncols, h2s, ws, r0, r1, 1.0 / nrm, wr ? col : nullptr, a.vin + so);
+      mark(9);
+      if (a.spectral) {
+        // next step's T^{-1} v_{j+1} = T^{-1} w / ||w|| (1/||w|| applied in the per-mode pass)
+        grid_sync(a.bar, epoch);
+        BufTable f;
+        f.p[BUF_IN] = a.w;
+        f.p[BUF_OUT] = a.vh;
+        f.p[BUF_TMP] = f.p[BUF_TMP2] = nullptr;
+        gt_stage(a, 4, sl, L, f, gsmem, nullptr, true);
+        vh_from_w = true;
+      }
+      grid_sync(a.bar, epoch);
+      mark(10);
+      if (tr && threadIdx.x == 0) tr[11] = static_cast<unsigned long long>(L);
+      ++step;
+      continue;
+    }
     // ---- pass 3: w -= V h2 ; ||w||
     double sq = gt_update(Vs, k, ncols, h2s, ws, r0, r1);
     sq = warp_sum(sq);

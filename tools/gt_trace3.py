@@ -6,7 +6,7 @@ import sys
 import numpy as np
 
 a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 64, 16).astype(np.int64)
-names = ["T^-1", "spec", "T+coarse", "-", "P", "pass1", "pass2", "pass3", "next-T^-1"]
+names = ["T^-1", "spec", "T+coarse", "-", "coarse read", "P", "pass1", "pass2", "pass3", "next-T^-1"]
 for li, launch in enumerate(a):
     st = launch[(launch[:, 0] > 0) & (launch[:, 10] > 0)]
     if not len(st):
