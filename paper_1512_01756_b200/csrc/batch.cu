@@ -309,9 +309,20 @@ struct smpm_batch {
   void* hrep = nullptr;  // pinned report staging
   size_t hrep_bytes = 0;
   cudaEvent_t sev[4] = {nullptr, nullptr, nullptr, nullptr};  // solve events (timing x2, step polling x2)
+  // early epilogue: the systems already stopped when the grid tail starts are finished
+  // (x' = V y, M^{-1}, residual, x_S) on a side stream while the tail runs
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t eev[3] = {nullptr, nullptr, nullptr};  // early list ready, early epilogue done, host copy done
+  int* hearly = nullptr;      // pinned + mapped: nsys flags of the early set (read by solve_host)
+  int* hearly_dev = nullptr;
+  DevArray<int> dearly;       // [early flags, early list, count, late flags, late list, count]
   ~smpm_batch() {
     for (auto e : sev)
       if (e) cudaEventDestroy(e);
+    for (auto e : eev)
+      if (e) cudaEventDestroy(e);
+    if (st2) cudaStreamDestroy(st2);
+    if (hearly) cudaFreeHost(hearly);
     if (hcnt) cudaFreeHost(hcnt);
     if (hrep) cudaFreeHost(hrep);
     for (auto e : ev_pool) cudaEventDestroy(e);
@@ -1001,6 +1012,9 @@ void finalize(smpm_batch* b) {
   b->dcnt.alloc(4);
   CUDA_CHECK(cudaHostAlloc(&b->hcnt, 4 * sizeof(int), cudaHostAllocMapped));
   CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&b->hcnt_dev), b->hcnt, 0));
+  b->dearly.alloc(4 * static_cast<size_t>(b->nsys) + 2);
+  CUDA_CHECK(cudaHostAlloc(&b->hearly, sizeof(int) * b->nsys, cudaHostAllocMapped));
+  CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&b->hearly_dev), b->hearly, 0));
   CUDA_CHECK(cudaStreamSynchronize(st));
   b->finalized = true;
 }
@@ -1426,6 +1440,17 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int* flags, const i
   }
 }
 
+// early / late split of the epilogue: systems in a final state (converged, breakdown,
+// iteration cap) when the grid tail starts, and the rest
+__global__ void early_select_kernel(const int* state, int nsys, int* early, int* late, int* hearly) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nsys) return;
+  const int f = (state[s] != GM_RUN && state[s] != GM_CYCLE) ? 1 : 0;
+  early[s] = f;
+  late[s] = 1 - f;
+  hearly[s] = f;
+}
+
 __global__ void select_state_kernel(const int* state, int nsys, int want, int* sel) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s < nsys) sel[s] = state[s] == want ? 1 : 0;
@@ -1662,8 +1687,10 @@ void stack_sum(smpm_batch* b, double* v, cudaStream_t st) {
   launch_pdl(b, stack_sum_kernel, dim3(1), dim3(128), 0, st, b->nsys, v);
 }
 
+// xS_host (optional, pinned): also deliver x_S to the host; with the early epilogue the
+// rows of the early systems are copied while the grid tail runs
 void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_report* reps, double* history,
-           cudaStream_t st) {
+           cudaStream_t st, double* xS_host = nullptr) {
   need_final(b);
   b->pdl = std::getenv("SMPM_NO_PDL") == nullptr;
   b->pythag = std::getenv("SMPM_NO_PYTHAG") == nullptr;
@@ -1833,6 +1860,72 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     compact_kernel<<<1, 1024, 0, st>>>(G.active, nullptr, ns, alist, acount, nullptr);
     check_launch(b);
   };
+  // ---- epilogue (spectral dbj): x' = V y, then one per-mode pass of x' gives both
+  // u = M^{-1} x' (the solution) and t = S M^{-1} x' (the final residual, proj/src/gmres.cpp:129-136),
+  // sharing T^{-1} x'; post_dbj_kernel forms x_S = Q u + Z c_b and ||r||^2
+  // (proj/src/deflation.cpp:118-120) in one pass
+  double* nrf = sc + 2 * ns;
+  double* u = b->vbuf[4].p;
+  double* tq = b->vbuf[5].p;
+  const bool fuse_post = spec_ok(b, c) && ((c.method == SMPM_DBJ && c.fused) || c.method == SMPM_BJ);
+  const bool post_one_pass = fuse_post && c.method == SMPM_DBJ && std::getenv("SMPM_NO_POST_FUSE") == nullptr;
+  auto epilogue_dbj = [&](const Live& lv, const int* sel, cudaStream_t s2) {
+    launch_pdl(b, gm_backsolve_kernel, dim3(ns), dim3(32), 0, s2, G, sel);
+    launch_pdl(b, gm_combine_kernel, vg, dim3(256), 0, s2, G, static_cast<const double*>(b->dV.p), x, sel, 1);
+    run_xform(b, true, x, b->dvh.p, lv, s2);
+    spec_apply(b, true, b->dvh.p, b->dth.p, b->dcoarse.p + static_cast<size_t>(ns) * b->d, lv, s2, b->dvh2.p);
+    run_xform(b, false, b->dvh2.p, u, lv, s2, b->dth.p, tq);
+    ProfScope psd(b, PC_DEFL, s2);
+    DeflateParams P = deflate_params(b, sel);
+    P.alist = lv.alist;
+    P.acount = lv.acount;
+    const int gx = static_cast<int>(std::min<long long>((b->k + V2_THREADS * 4 - 1) / (V2_THREADS * 4), 64));
+    launch_pdl(b, post_dbj_kernel, dim3(gx, lv.nslots), dim3(V2_THREADS), 0, s2, P, static_cast<const double*>(tq),
+               static_cast<const double*>(u), static_cast<const double*>(rhs),
+               static_cast<const double*>(b->dcoarse.p + static_cast<size_t>(ns) * b->d),
+               static_cast<const double*>(b->dczb.p), xS, b->dpost.p, b->dcount.p, nrf, c.final_check ? 1 : 0);
+  };
+  // early epilogue: the systems that have stopped when the grid tail starts are
+  // finished before it (same total work), so that their rows of x_S can travel to
+  // the host (solve_host) on a side stream while the tail runs. Running the epilogue
+  // itself beside the tail was measured slower: its kernels compete with the
+  // latency-bound tail for the SMs. SMPM_NO_EARLY=1: off.
+  const bool early_ok = post_one_pass && xS_host && std::getenv("SMPM_NO_EARLY") == nullptr;
+  bool early_done = false;
+  int* eflag = b->dearly.p;
+  int* elist = eflag + ns;
+  int* ecount = elist + ns;
+  int* lflag = ecount + 1;
+  int* llist = lflag + ns;
+  int* lcount = llist + ns;
+  auto launch_tail = [&](int nrun) {
+    const bool early = early_ok && !early_done && nrun < ns;
+    if (early) {
+      if (!b->st2) {
+        int lo = 0, hi = 0;
+        CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CUDA_CHECK(cudaStreamCreateWithPriority(&b->st2, cudaStreamNonBlocking, lo));
+        for (auto& e : b->eev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      early_select_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, eflag, lflag, b->hearly_dev);
+      check_launch(b);
+      compact_kernel<<<1, 1024, 0, st>>>(eflag, nullptr, ns, elist, ecount, nullptr);
+      check_launch(b);
+      Live le;
+      le.alist = elist;
+      le.acount = ecount;
+      le.nslots = ns - nrun;
+      le.active = eflag;
+      epilogue_dbj(le, eflag, st);
+      CUDA_CHECK(cudaEventRecord(b->eev[1], st));
+      // every row (the late systems' rows are copied again at the end)
+      CUDA_CHECK(cudaStreamWaitEvent(b->st2, b->eev[1], 0));
+      CUDA_CHECK(cudaMemcpyAsync(xS_host, xS, sizeof(double) * nk, cudaMemcpyDeviceToHost, b->st2));
+      CUDA_CHECK(cudaEventRecord(b->eev[2], b->st2));
+      early_done = true;
+    }
+    arnoldi_grid(b, c, alist, acount, st);
+  };
   int cur = 0;
   if (!use_cluster) issue(cur);
   for (; !use_cluster;) {
@@ -1841,7 +1934,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       CUDA_CHECK(cudaEventSynchronize(ev[cur]));
       int nrun = hcnt[2 * cur], ncyc = hcnt[2 * cur + 1];
       if (nrun > 0) {
-        arnoldi_grid(b, c, alist, acount, st);
+        launch_tail(nrun);
         ++steps;
         compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->hcnt_dev + 2 * cur);
         check_launch(b);
@@ -1881,35 +1974,35 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     }
     break;
   }
-  // ---- assemble x' = V y for the last cycle of every system
-  launch_pdl(b, gm_backsolve_kernel, dim3(ns), dim3(32), 0, st, G, static_cast<const int*>(nullptr));
-  launch_pdl(b, gm_combine_kernel, vg, dim3(256), 0, st, G, static_cast<const double*>(b->dV.p), x,
-             static_cast<const int*>(nullptr), 1);
-
-  // ---- final residual check (proj/src/gmres.cpp:129-136): r = rhs - op(x')
-  // Spectral dbj/bj: one per-mode pass of x' gives both u = M^{-1} x' (the
-  // solution) and t = S M^{-1} x' (the residual operator), sharing T^{-1} x'.
-  double* nrf = sc + 2 * ns;
-  double* u = b->vbuf[4].p;
-  double* tq = b->vbuf[5].p;
-  const bool fuse_post = spec_ok(b, c) && ((c.method == SMPM_DBJ && c.fused) || c.method == SMPM_BJ);
-  if (fuse_post) {
-    run_xform(b, true, x, b->dvh.p, all, st);
-    // dbj: the per-mode pass also yields c = C^{-1} Z^T (S u) for the residual and Q
-    spec_apply(b, true, b->dvh.p, b->dth.p, c.method == SMPM_DBJ ? b->dcoarse.p + static_cast<size_t>(ns) * b->d : nullptr,
-               all, st, b->dvh2.p);
-    run_xform(b, false, b->dvh2.p, u, all, st, b->dth.p, tq);
-  }
-  const bool post_one_pass = fuse_post && c.method == SMPM_DBJ && std::getenv("SMPM_NO_POST_FUSE") == nullptr;
   if (post_one_pass) {
-    // final residual + x_S = Q u + Z c_b in one pass (post_dbj_kernel)
-    ProfScope psd(b, PC_DEFL, st);
-    DeflateParams P = deflate_params(b, nullptr);
-    const int gx = static_cast<int>(std::min<long long>((b->k + V2_THREADS * 4 - 1) / (V2_THREADS * 4), 64));
-    launch_pdl(b, post_dbj_kernel, dim3(gx, ns), dim3(V2_THREADS), 0, st, P, static_cast<const double*>(tq),
-               static_cast<const double*>(u), static_cast<const double*>(rhs),
-               static_cast<const double*>(b->dcoarse.p + static_cast<size_t>(ns) * b->d),
-               static_cast<const double*>(b->dczb.p), xS, b->dpost.p, b->dcount.p, nrf, c.final_check ? 1 : 0);
+    if (early_done) {
+      // the systems not finished by the early epilogue
+      compact_kernel<<<1, 1024, 0, st>>>(lflag, nullptr, ns, llist, lcount, nullptr);
+      check_launch(b);
+      Live ll;
+      ll.alist = llist;
+      ll.acount = lcount;
+      ll.nslots = ns;
+      ll.active = lflag;
+      epilogue_dbj(ll, lflag, st);
+    } else {
+      epilogue_dbj(all, nullptr, st);
+    }
+  } else {
+    // ---- assemble x' = V y for the last cycle of every system
+    launch_pdl(b, gm_backsolve_kernel, dim3(ns), dim3(32), 0, st, G, static_cast<const int*>(nullptr));
+    launch_pdl(b, gm_combine_kernel, vg, dim3(256), 0, st, G, static_cast<const double*>(b->dV.p), x,
+               static_cast<const int*>(nullptr), 1);
+    // ---- final residual check (proj/src/gmres.cpp:129-136): r = rhs - op(x')
+    // Spectral dbj/bj: one per-mode pass of x' gives both u = M^{-1} x' (the
+    // solution) and t = S M^{-1} x' (the residual operator), sharing T^{-1} x'.
+    if (fuse_post) {
+      run_xform(b, true, x, b->dvh.p, all, st);
+      // dbj: the per-mode pass also yields c = C^{-1} Z^T (S u) for the residual and Q
+      spec_apply(b, true, b->dvh.p, b->dth.p, c.method == SMPM_DBJ ? b->dcoarse.p + static_cast<size_t>(ns) * b->d : nullptr,
+                 all, st, b->dvh2.p);
+      run_xform(b, false, b->dvh2.p, u, all, st, b->dth.p, tq);
+    }
   }
   if (c.final_check && !post_one_pass) {
     if (fuse_post && c.method == SMPM_DBJ) {
@@ -1960,6 +2053,25 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
         op_BJ(b, x, u, all, st);
       run_deflate(b, DEFL_ADD_ZC, x, u, xS, nullptr, all, st);
       break;
+  }
+  if (xS_host) {
+    if (early_done) {
+      // the full copy of the early epilogue first, then the late systems' rows
+      CUDA_CHECK(cudaStreamWaitEvent(st, b->eev[2], 0));
+      for (int q = 0; q < ns;) {
+        if (b->hearly[q]) {
+          ++q;
+          continue;
+        }
+        int q1 = q + 1;
+        while (q1 < ns && !b->hearly[q1]) ++q1;  // one copy per run of late rows
+        CUDA_CHECK(cudaMemcpyAsync(xS_host + static_cast<size_t>(q) * b->k, xS + static_cast<size_t>(q) * b->k,
+                                   sizeof(double) * b->k * (q1 - q), cudaMemcpyDeviceToHost, st));
+        q = q1;
+      }
+    } else {
+      CUDA_CHECK(cudaMemcpyAsync(xS_host, xS, sizeof(double) * nk, cudaMemcpyDeviceToHost, st));
+    }
   }
   // report data: queued on the stream into pinned staging (one host wait)
   const size_t rep_ints = static_cast<size_t>(ns) * 8, rep_dbl = static_cast<size_t>(ns) * (8 + (m + 1) + 3);
@@ -2622,8 +2734,7 @@ int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x
     double* din = b->vbuf[10].p;
     double* dout = b->vbuf[11].p;
     CUDA_CHECK(cudaMemcpyAsync(din, b_S_host, bytes, cudaMemcpyHostToDevice, st));
-    solve(b, cfg_from(method, opt), din, dout, reports, history, st);
-    CUDA_CHECK(cudaMemcpyAsync(x_S_host, dout, bytes, cudaMemcpyDeviceToHost, st));
+    solve(b, cfg_from(method, opt), din, dout, reports, history, st, x_S_host);
     CUDA_CHECK(cudaStreamSynchronize(st));
   });
 }
