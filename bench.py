@@ -270,7 +270,7 @@ def algorithmic_counts(cfg, its, grid_max=8):
 def roofline_kernel_name(cls):
     return {"grid_tail": "arnoldi_grid_kernel", "transform": "xform_kernel (T^-1 / T)",
             "spectral_op": "spec_op_kernel (per-mode pass)",
-            "orthogonalization": "cgs3_dot_kernel + cgs3_update_kernel (CGS2 passes)"}.get(cls, cls)
+            "orthogonalization": "cgs3_dot_kernel + cgs3_pass2n_kernel + cgs3_pass3s_kernel (CGS2 passes)"}.get(cls, cls)
 
 
 def measured_traffic(kernel):

@@ -287,6 +287,8 @@ struct smpm_batch {
   // grid-persistent tail solver (grid.cuh)
   bool grid_ok = false;
   int gt_blocks = 0;
+  size_t gt_smem = 0;  // tail dynamic shared memory (tile ring / V-row block region + vectors)
+  int gt_vcap = 0;     // doubles of the ring / V-row block region
   bool gt_nocoop = false;  // cooperative + cluster launch rejected: plain cluster launch
   DevArray<unsigned> dgbar;   // grid barrier counter
   DevArray<double> dgtpart, dgtzsum, dgtzp, dgtcg;
@@ -1541,7 +1543,26 @@ void arnoldi_cluster(smpm_batch* b, const SolveCfg& c, const int* alist, const i
 // can be co-resident, up to SMPM_GRID_PER_SM (default 2) per SM
 int grid_blocks(smpm_batch* b) {
   if (b->gt_blocks) return b->gt_blocks;
-  const size_t smem = GT_SMEM + sizeof(double) * (3 * GT_MAXCOL + 2 * static_cast<size_t>(b->d));
+  // the tile-ring region doubles as the per-step V-row block of the CGS2 passes
+  // (SMPM_GT_VBLOCK: 0 off, 1 ring size, 2 as large as two CTAs per SM allow)
+  const size_t rest = sizeof(double) * (3 * GT_MAXCOL + 2 * static_cast<size_t>(b->d));
+  size_t region = GT_SMEM;
+  int vmode = 2;  // 0: no V-row block, 1: within the ring region, 2: as large as 2 CTAs / SM allow (measured best)
+  if (const char* e = std::getenv("SMPM_GT_VBLOCK")) vmode = std::atoi(e);
+  if (vmode >= 2) {
+    cudaFuncAttributes fa{};
+    CUDA_CHECK(cudaFuncGetAttributes(&fa, arnoldi_grid_kernel));
+    int dev = 0, per_sm = 0, resv = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    CUDA_CHECK(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    CUDA_CHECK(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev));
+    const long long avail = static_cast<long long>(per_sm) / 2 - resv - static_cast<long long>(fa.sharedSizeBytes) -
+                            static_cast<long long>(rest);
+    region = std::max<size_t>(GT_SMEM, static_cast<size_t>(std::max(0LL, avail)) / 1024 * 1024);
+  }
+  b->gt_vcap = vmode > 0 ? static_cast<int>(region / sizeof(double)) : 0;
+  b->gt_smem = region + rest;
+  const size_t smem = b->gt_smem;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1573,7 +1594,8 @@ int grid_blocks(smpm_batch* b) {
 void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int* acount, cudaStream_t st) {
   ProfScope ps(b, 6, st);  // class 6: grid-persistent tail
   GmState_& G = b->G;
-  const size_t smem = GT_SMEM + sizeof(double) * (3 * GT_MAXCOL + 2 * static_cast<size_t>(b->d));
+  grid_blocks(b);
+  const size_t smem = b->gt_smem;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1630,6 +1652,7 @@ void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
   A.acount = acount;
   A.method = c.method;
   A.pythag = b->pythag ? 1 : 0;
+  A.vcap = b->gt_vcap;
   A.G = G;
   A.P = deflate_params(b, nullptr);
   const char* tpath = std::getenv("SMPM_GT_TRACE");

@@ -80,6 +80,8 @@ struct GridArgs {
   const int* acount;
   int method;              // smpm_method
   int pythag;              // ||w|| from the second CGS2 reduction (as cgs3_pass2n)
+  int vcap;                // doubles of the tile-ring region (>= GT_SMEM / 8); with pythag, a CTA whose
+                           // V rows (ncols x rows) fit there stages them once per step (gt_vblock)
   unsigned long long* trace;  // debug: 64 steps x 16 phase timestamps of CTA 0 (nullable)
   unsigned long long* trace2; // debug: 4 steps x 4 stages x gridDim.x x 8 per-CTA timestamps (nullable)
   GmState_ G;
@@ -437,6 +439,54 @@ __device__ __forceinline__ void gt_update_scale(const double* Vs, long long k, i
   }
 }
 
+// ---- CGS2 on a shared-memory copy of this CTA's rows of V (one async load per step) ----
+// vb: ncols x nr column-major (rows r0.., nr even), wb: nr rows of w
+
+// issue the 16-byte async copies of V[r0:r0+nr, 0:ncols) (k and r0 even: aligned pairs)
+__device__ __forceinline__ void gt_vblock_load(const double* Vs, long long k, int ncols, int r0, int nr, double* vb) {
+  const int np = nr >> 1;
+  for (int e = threadIdx.x; e < ncols * np; e += blockDim.x) {
+    const int c = e / np, p = e - c * np;
+    cp_async16(vb + c * nr + 2 * p, Vs + static_cast<long long>(c) * k + r0 + 2 * p, true);
+  }
+  cp_async_commit();
+}
+
+// out[c] = sum_r vb[c, r] wb[r]: each warp takes groups of 4 columns, lanes run over rows
+__device__ __forceinline__ void gt_vblock_dots(const double* vb, const double* wb, int nr, int ncols, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c0 = warp * 4; c0 < ncols; c0 += nw * 4) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const int nc = min(4, ncols - c0);
+    for (int r = lane; r < nr; r += 32) {
+      const double x = wb[r];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (u < nc) acc[u] = fma(vb[(c0 + u) * nr + r], x, acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = warp_sum(acc[u]);
+    if (lane < nc) {
+      const double v = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
+      out[c0 + lane] = v;
+    }
+  }
+}
+
+// (V h)[r] for row r of the block (4 independent chains)
+__device__ __forceinline__ double gt_vblock_row(const double* vb, int nr, int ncols, const double* h, int r) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int c = 0;
+  for (; c + 4 <= ncols; c += 4) {
+    a0 = fma(vb[c * nr + r], h[c], a0);
+    a1 = fma(vb[(c + 1) * nr + r], h[c + 1], a1);
+    a2 = fma(vb[(c + 2) * nr + r], h[c + 2], a2);
+    a3 = fma(vb[(c + 3) * nr + r], h[c + 3], a3);
+  }
+  for (; c < ncols; ++c) a0 = fma(vb[c * nr + r], h[c], a0);
+  return (a0 + a1) + (a2 + a3);
+}
+
 // sum of the cluster's CTA partials pin[0..n) (rank order, through DSMEM) ->
 // gout[0..n) (this cluster's slot of a global partial buffer); ranks split the entries
 __device__ __forceinline__ void gt_cluster_sum(const double* pin, int n, double* gout) {
@@ -490,7 +540,7 @@ __device__ __forceinline__ void gt_spec(const GridArgs& a, const int* sl, int L,
 __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridArgs a) {
   extern __shared__ __align__(16) double gt_smem[];
   double* gsmem = gt_smem;                // GT_SMEM bytes: tile pipeline / tile partial
-  double* hs = gt_smem + GT_SMEM / 8;     // GT_MAXCOL: h1 of this CTA's system
+  double* hs = gt_smem + max(a.vcap, GT_SMEM / 8);  // GT_MAXCOL: h1 of this CTA's system
   double* h2s = hs + GT_MAXCOL;           // GT_MAXCOL: h2
   double* pdot = h2s + GT_MAXCOL;         // GT_MAXCOL: this CTA's partial dots (read by the cluster)
   double* cs_ = pdot + GT_MAXCOL;         // 2 d: coarse rhs / solution
@@ -605,12 +655,17 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
     while (q + 1 < L && c0s[q + 1] <= cid) ++q;
     const int gc0 = c0s[q], gc1 = c0s[q + 1];
     const int s = sl[q], nper = (gc1 - gc0) * GT_CL, idx = bid - gc0 * GT_CL;
-    const long long rows_per = (k + nper - 1) / nper;
+    // even row ranges (k = 2 w (m_x - 1) is even): 16-byte aligned row pairs for gt_vblock_load
+    const long long rows_per = ((k + nper - 1) / nper + 1) & ~1LL;
     const int r0 = static_cast<int>(min(k, idx * rows_per)), r1 = static_cast<int>(min(k, (idx + 1) * rows_per));
     const long long so = s * k;
     const int j = ncol[q] - 1, ncols = ncol[q];
     const double* Vs = a.V + s * G.vstride;
     double* ws = a.w + so;
+    const int nr = r1 - r0;
+    const bool vc = a.pythag && static_cast<long long>(ncols + 1) * nr <= a.vcap && (k & 1) == 0;
+    double* vb = gsmem;
+    double* wb = gsmem + ncols * nr;
 
     const double* sin = a.method == SMPM_SCHUR ? a.vin : a.u;
     if (a.method == SMPM_2LAS) {
@@ -635,6 +690,10 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
       gt_stage(a, 3, sl, L, sb, gsmem, T2(3));
       grid_sync(a.bar, epoch);
       mark(4);
+    }
+    if (vc) {
+      __syncthreads();  // the tile ring (same region) is free from here to the next operator stage
+      gt_vblock_load(Vs, k, ncols, r0, nr, vb);
     }
     if (a.method == SMPM_DBJ) {
       // ---- fused deflation P: c = C^{-1} Z^T t ; w = t - Z c - (S - I) Z c
@@ -662,21 +721,46 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
           sz = (i + 1 == mx - 1) ? c[i] * rWE[r] : c[i] * rWI[r] + c[i + 1] * rEI[r];
         else
           sz = (i == 0) ? c[i] * rEW[r] : c[i - 1] * rWI[w + r] + c[i] * rEI[w + r];
-        ws[e] = __ldcg(ts + e) - (c[i] + sz);
+        const double wv = __ldcg(ts + e) - (c[i] + sz);
+        ws[e] = wv;
+        if (vc) wb[e - r0] = wv;
       }
       __syncthreads();
       mark(6);
+    } else if (vc) {
+      for (int r = threadIdx.x; r < nr; r += blockDim.x) wb[r] = __ldcg(ws + r0 + r);
+    }
+    if (vc) {
+      cp_async_wait<0>();
+      __syncthreads();
     }
     // ---- CGS2 pass 1: h1 = V^T w
-    gt_col_dots(Vs, k, ncols, ws, r0, r1, pdot);
+    if (vc) {
+      gt_vblock_dots(vb, wb, nr, ncols, pdot);
+      __syncthreads();
+    } else {
+      gt_col_dots(Vs, k, ncols, ws, r0, r1, pdot);
+    }
     gt_cluster_sum(pdot, ncols, part1 + static_cast<long long>(cid) * stride);
     grid_sync(a.bar, epoch);
     gt_group_sum(part1, stride, gc0, gc1, ncols, hs);
     mark(7);
     // ---- pass 2: w -= V h1 ; h2 = V^T w (and ||w||^2 of the updated w)
-    const double sq1 = gt_update(Vs, k, ncols, hs, ws, r0, r1);
-    __syncthreads();
-    gt_col_dots(Vs, k, ncols, ws, r0, r1, pdot);
+    double sq1 = 0.0;
+    if (vc) {
+      for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+        const double nv = wb[r] - gt_vblock_row(vb, nr, ncols, hs, r);
+        wb[r] = nv;
+        sq1 = fma(nv, nv, sq1);
+      }
+      __syncthreads();
+      gt_vblock_dots(vb, wb, nr, ncols, pdot);
+      __syncthreads();
+    } else {
+      sq1 = gt_update(Vs, k, ncols, hs, ws, r0, r1);
+      __syncthreads();
+      gt_col_dots(Vs, k, ncols, ws, r0, r1, pdot);
+    }
     const int n2 = a.pythag ? ncols + 1 : ncols;
     if (a.pythag) {
       const double q1 = warp_sum(sq1);
@@ -716,7 +800,20 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
       // ---- pass 3: w -= V h2 ; v_{j+1} = w / ||w|| (own rows; unused if the system stops)
       double* col = a.V + s * G.vstride + static_cast<long long>(j + 1) * k;
       const bool wr = j + 1 <= G.m;
-      gt_update_scale(Vs, k, ncols, h2s, ws, r0, r1, 1.0 / nrm, wr ? col : nullptr, a.vin + so);
+      if (vc) {
+        const double inv = 1.0 / nrm;
+        double* vs = a.vin + so;
+        for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+          const double nv = wb[r] - gt_vblock_row(vb, nr, ncols, h2s, r);
+          ws[r0 + r] = nv;
+          if (wr) {
+            col[r0 + r] = nv * inv;
+            vs[r0 + r] = nv * inv;
+          }
+        }
+      } else {
+        gt_update_scale(Vs, k, ncols, h2s, ws, r0, r1, 1.0 / nrm, wr ? col : nullptr, a.vin + so);
+      }
       mark(9);
       if (a.spectral) {
         // next step's T^{-1} v_{j+1} = T^{-1} w / ||w|| (1/||w|| applied in the per-mode pass)

@@ -17,3 +17,9 @@ for li, launch in enumerate(a):
     print(f"launch {li}: steps {len(st)} live {live.tolist()} mean step us {float((st[:, 10] - st[:, 0]).mean() / 1e3):.1f}")
     print("   mean us per phase:", {"T^-1": round(float(d0.mean()), 2),
                                     **{n: round(float(v), 2) for n, v in zip(names[1:], d.mean(axis=0))}})
+    for Lv in sorted(set(live.tolist())):
+        sel = live == Lv
+        dd = d[sel].mean(axis=0)
+        print(f"   L={Lv}: steps {int(sel.sum())} step us {float(((st[sel, 10] - st[sel, 0]) / 1e3).mean()):.1f}",
+              {n: round(float(v), 2) for n, v in zip(names[1:], dd)})
+
