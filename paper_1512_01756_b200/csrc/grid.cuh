@@ -41,7 +41,7 @@ constexpr int GT_MAXCOL = 128;  // cycle length + 2
 constexpr int GT_CL = 8;        // CTAs per cluster (= K splits of a tail tile)
 constexpr int GT_GVR = 32;      // rows of a cluster GEMV item
 #ifndef GT_STAGES_DEF
-#define GT_STAGES_DEF 4
+#define GT_STAGES_DEF 2
 #endif
 #ifndef GT_MINB
 #define GT_MINB 1
@@ -444,10 +444,19 @@ __device__ __forceinline__ void gt_update_scale(const double* Vs, long long k, i
 
 // issue the 16-byte async copies of V[r0:r0+nr, 0:ncols) (k and r0 even: aligned pairs)
 __device__ __forceinline__ void gt_vblock_load(const double* Vs, long long k, int ncols, int r0, int nr, double* vb) {
-  const int np = nr >> 1;
-  for (int e = threadIdx.x; e < ncols * np; e += blockDim.x) {
-    const int c = e / np, p = e - c * np;
-    cp_async16(vb + c * nr + 2 * p, Vs + static_cast<long long>(c) * k + r0 + 2 * p, true);
+  const int np = nr >> 1, tot = ncols * np;
+  if (np > 0) {
+    int c = static_cast<int>(threadIdx.x) / np, p = static_cast<int>(threadIdx.x) - c * np;
+    const int dc = static_cast<int>(blockDim.x) / np, dp = static_cast<int>(blockDim.x) - dc * np;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+      cp_async16(vb + c * nr + 2 * p, Vs + static_cast<long long>(c) * k + r0 + 2 * p, true);
+      c += dc;
+      p += dp;
+      if (p >= np) {
+        p -= np;
+        ++c;
+      }
+    }
   }
   cp_async_commit();
 }
@@ -504,6 +513,33 @@ __device__ __forceinline__ void gt_cluster_sum(const double* pin, int n, double*
 // 16 independent loads per round: one or two L2 round trips for any group) -> dst[0..n)
 __device__ __forceinline__ void gt_group_sum(const double* part, int stride, int c0, int c1, int n, double* dst) {
   constexpr int R = 16;
+  if (2 * n <= static_cast<int>(blockDim.x)) {
+    // T threads per entry, each summing a contiguous subset of the clusters (one
+    // round of loads for up to 16 T clusters), then the T subsets in order
+    __shared__ double gsp[G2_THREADS];
+    const int T = static_cast<int>(blockDim.x) / n, t = threadIdx.x, col = t % n, q = t / n;
+    const int sub = (c1 - c0 + T - 1) / T;
+    double s = 0.0;
+    if (q < T) {
+      const int g0 = c0 + q * sub, g1 = min(c1, g0 + sub);
+      for (int gb = g0; gb < g1; gb += R) {
+        double v[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) v[u] = gb + u < g1 ? __ldcg(part + static_cast<long long>(gb + u) * stride + col) : 0.0;
+#pragma unroll
+        for (int u = 0; u < R; ++u) s += v[u];
+      }
+    }
+    gsp[t] = s;
+    __syncthreads();
+    if (t < n) {
+      double r = 0.0;
+      for (int qq = 0; qq < T; ++qq) r += gsp[qq * n + t];
+      dst[t] = r;
+    }
+    __syncthreads();
+    return;
+  }
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
     double s = 0.0;
     for (int g0 = c0; g0 < c1; g0 += R) {
@@ -600,6 +636,28 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
       return a.trace2 ? a.trace2 + ((static_cast<long long>(step % 4) * 4 + stg) * NB + bid) * 8 : nullptr;
     };
 
+    // this CTA's system and rows for the vector phases (groups of whole clusters)
+    int q = 0;
+    while (q + 1 < L && c0s[q + 1] <= cid) ++q;
+    const int gc0 = c0s[q], gc1 = c0s[q + 1];
+    const int s = sl[q], nper = (gc1 - gc0) * GT_CL, idx = bid - gc0 * GT_CL;
+    // even row ranges (k = 2 w (m_x - 1) is even): 16-byte aligned row pairs for gt_vblock_load
+    const long long rows_per = ((k + nper - 1) / nper + 1) & ~1LL;
+    const int r0 = static_cast<int>(min(k, idx * rows_per)), r1 = static_cast<int>(min(k, (idx + 1) * rows_per));
+    const long long so = s * k;
+    const int j = ncol[q] - 1, ncols = ncol[q];
+    const double* Vs = a.V + s * G.vstride;
+    double* ws = a.w + so;
+    const int nr = r1 - r0;
+    // V-row block: beyond the tile ring (loaded at the step start, under the operator
+    // phases) when it fits there, else over the ring after the operator stages
+    const long long vneed = static_cast<long long>(ncols + 1) * nr;
+    const bool vc_early = a.pythag && (k & 1) == 0 && vneed <= a.vcap - GT_SMEM / 8;
+    const bool vc = vc_early || (a.pythag && (k & 1) == 0 && vneed <= a.vcap);
+    double* vb = vc_early ? gsmem + GT_SMEM / 8 : gsmem;
+    double* wb = vb + ncols * nr;
+    if (vc_early) gt_vblock_load(Vs, k, ncols, r0, nr, vb);
+
     // ---- operator: u = M^{-1} vin (block-Jacobi stages), then S
     BufTable bj;
     bj.p[BUF_IN] = a.vin;
@@ -650,23 +708,6 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
         mark(1 + stg);
       }
     }
-    // this CTA's system and rows for the vector phases (groups of whole clusters)
-    int q = 0;
-    while (q + 1 < L && c0s[q + 1] <= cid) ++q;
-    const int gc0 = c0s[q], gc1 = c0s[q + 1];
-    const int s = sl[q], nper = (gc1 - gc0) * GT_CL, idx = bid - gc0 * GT_CL;
-    // even row ranges (k = 2 w (m_x - 1) is even): 16-byte aligned row pairs for gt_vblock_load
-    const long long rows_per = ((k + nper - 1) / nper + 1) & ~1LL;
-    const int r0 = static_cast<int>(min(k, idx * rows_per)), r1 = static_cast<int>(min(k, (idx + 1) * rows_per));
-    const long long so = s * k;
-    const int j = ncol[q] - 1, ncols = ncol[q];
-    const double* Vs = a.V + s * G.vstride;
-    double* ws = a.w + so;
-    const int nr = r1 - r0;
-    const bool vc = a.pythag && static_cast<long long>(ncols + 1) * nr <= a.vcap && (k & 1) == 0;
-    double* vb = gsmem;
-    double* wb = gsmem + ncols * nr;
-
     const double* sin = a.method == SMPM_SCHUR ? a.vin : a.u;
     if (a.method == SMPM_2LAS) {
       // minv = M^{-1} v + Z C^{-1} Z^T v : t = u + Z c(Z^T vin)
@@ -691,7 +732,7 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
       grid_sync(a.bar, epoch);
       mark(4);
     }
-    if (vc) {
+    if (vc && !vc_early) {
       __syncthreads();  // the tile ring (same region) is free from here to the next operator stage
       gt_vblock_load(Vs, k, ncols, r0, nr, vb);
     }
