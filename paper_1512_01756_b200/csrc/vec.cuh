@@ -398,6 +398,18 @@ __device__ void givens_step(GmState_& G, int s, int j, double nrm) {
   double* g = G.g + static_cast<long long>(s) * (m + 1);
   double* R = G.R + static_cast<long long>(s) * (m + 1) * m;
   const bool staged = j + 2 <= SM;
+  // lane 0's scalars, loaded up front (independent loads: one round trip under the column loads)
+  double p_hmax = 0.0, p_g1 = 0.0, p_g2 = 0.0, p_target = 0.0, p_bnorm = 1.0;
+  int p_it = 0, p_hl = 0;
+  if (lane == 0) {
+    p_hmax = G.hmax[s];
+    p_g1 = g[j];
+    p_g2 = g[j + 1];
+    p_target = G.target[s];
+    p_bnorm = G.bnorm[s];
+    p_it = G.iters[s];
+    p_hl = G.hist_len[s];
+  }
   double* H = staged ? hs : h1;
   const double* CS = staged ? css : cs;
   const double* SN = staged ? sns : sn;
@@ -418,7 +430,7 @@ __device__ void givens_step(GmState_& G, int s, int j, double nrm) {
   double hmax = 0.0, res = 0.0;
   if (lane == 0) {
     G.nrm[s] = nrm;
-    hmax = fmax(fmax(G.hmax[s], hm), nrm);
+    hmax = fmax(fmax(p_hmax, hm), nrm);
     G.hmax[s] = hmax;
     H[j + 1] = nrm;
     for (int i = 0; i < j; ++i) {
@@ -432,25 +444,26 @@ __device__ void givens_step(GmState_& G, int s, int j, double nrm) {
     cs[j] = c;
     sn[j] = sv;
     H[j] = rad;
-    const double g1 = g[j], g2 = g[j + 1];
+    const double g1 = p_g1, g2 = p_g2;
+    const double gj1 = -sv * g1 + c * g2;
     g[j] = c * g1 + sv * g2;
-    g[j + 1] = -sv * g1 + c * g2;
-    res = fabs(g[j + 1]);
+    g[j + 1] = gj1;
+    res = fabs(gj1);
   }
   __syncwarp();
   __threadfence_block();
   for (int i = lane; i <= j; i += 32) R[static_cast<long long>(j) * (m + 1) + i] = H[i];
   if (lane != 0) return;
-  const int it = G.iters[s] + 1;
+  const int it = p_it + 1;
   G.iters[s] = it;
   G.jcyc[s] = j + 1;
-  const int hl = G.hist_len[s];
+  const int hl = p_hl;
   if (hl < G.histcap) {
-    G.hist[static_cast<long long>(s) * G.histcap + hl] = res / G.bnorm[s];
+    G.hist[static_cast<long long>(s) * G.histcap + hl] = res / p_bnorm;
     G.hist_len[s] = hl + 1;
   }
   int st = GM_RUN;
-  if (res <= G.target[s])
+  if (res <= p_target)
     st = GM_CONV;
   else if (nrm <= 1e-14 * hmax)
     st = GM_BREAK;
