@@ -1625,6 +1625,7 @@ void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
     A.ngemm[i] = p.ngemm;
     A.gv[i] = p.dgv.p;
     A.ngv[i] = p.ngv;
+    A.njobs[i] = static_cast<int>(p.jobs.size());
   }
   A.vin = b->vbuf[2].p;
   A.w = b->vbuf[3].p;

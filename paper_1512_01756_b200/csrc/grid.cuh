@@ -55,6 +55,7 @@ struct GridArgs {
   // unsplit per-system templates of the operator stages: BJ1 BJ2 BJ3 S, and
   // the spectral transforms F (T^{-1}) and B (T) (tiles sorted GEMM first, then GEMV)
   const GemmJob* jobs[6];
+  int njobs[6];
   const Tile2* tiles[6];
   int ntiles[6];
   int ngemm[6];            // GEMM tiles (the rest are GEMV tiles)
@@ -188,8 +189,46 @@ __device__ __forceinline__ void gt_cluster_tile(GemmJob jb, Tile2 tile, const Bu
   if (valid && t2 && threadIdx.x == 0) t2[3] = gt_timer();
 }
 
-__device__ __forceinline__ GemmJob gt_job(const GridArgs& a, int stage, const Tile2& tile, int s) {
-  GemmJob jb = a.jobs[stage][tile.job];
+// stage descriptors (tiles, jobs, GEMV items): copied to shared memory at the kernel
+// start when they are few (the spectral transforms: one job, 12 tiles), so a stage's
+// data loads are not behind two dependent L2 round trips for its descriptors
+constexpr int GT_TC = 96, GT_JC = 8, GT_GC = 32;
+struct GtDesc {
+  const Tile2* tiles[6];
+  const GemmJob* jobs[6];
+  const Tile2* gv[6];
+};
+
+__device__ __forceinline__ void gt_desc_init(const GridArgs& a, GtDesc& D, Tile2* tc, GemmJob* jc, Tile2* gc) {
+  if (threadIdx.x == 0) {
+    int nt = 0, nj = 0, ng = 0;
+    for (int st = 0; st < 6; ++st) {
+      D.tiles[st] = a.tiles[st];
+      D.jobs[st] = a.jobs[st];
+      D.gv[st] = a.gv[st];
+      if (!a.jobs[st]) continue;
+      if (a.njobs[st] > 0 && nt + a.ntiles[st] <= GT_TC && nj + a.njobs[st] <= GT_JC && ng + a.ngv[st] <= GT_GC) {
+        D.tiles[st] = tc + nt;
+        D.jobs[st] = jc + nj;
+        D.gv[st] = gc + ng;
+        nt += a.ntiles[st];
+        nj += a.njobs[st];
+        ng += a.ngv[st];
+      }
+    }
+  }
+  __syncthreads();
+  for (int st = 0; st < 6; ++st) {
+    if (!a.jobs[st] || D.jobs[st] == a.jobs[st]) continue;
+    for (int i = threadIdx.x; i < a.ntiles[st]; i += blockDim.x) const_cast<Tile2*>(D.tiles[st])[i] = a.tiles[st][i];
+    for (int i = threadIdx.x; i < a.ngv[st]; i += blockDim.x) const_cast<Tile2*>(D.gv[st])[i] = a.gv[st][i];
+    for (int i = threadIdx.x; i < a.njobs[st]; i += blockDim.x) const_cast<GemmJob*>(D.jobs[st])[i] = a.jobs[st][i];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ GemmJob gt_job(const GridArgs& a, const GtDesc& D, int stage, const Tile2& tile, int s) {
+  GemmJob jb = D.jobs[stage][tile.job];
   jb.A += s * a.a_stride[stage];
   const long long vo = s * a.G.k;
   jb.b.off += vo;
@@ -266,8 +305,8 @@ __device__ __forceinline__ void gt_cluster_gemv(const GemmJob& jb, const Tile2& 
 // cluster items of one stage, SP CTAs per item, GT_CL / SP items per cluster
 // at a time; the round count is uniform over each cluster
 template <int SP>
-__device__ __forceinline__ void gt_stage_split(const GridArgs& a, int stage, const int* sl, int L, const BufTable& bufs,
-                                               double* smem, unsigned long long* t2, bool rev) {
+__device__ __forceinline__ void gt_stage_split(const GridArgs& a, const GtDesc& D, int stage, const int* sl, int L,
+                                               const BufTable& bufs, double* smem, unsigned long long* t2, bool rev) {
   const int ng = a.ngemm[stage], nci = ng + a.ngv[stage], items = L * nci;
   constexpr int PER = GT_CL / SP;
   const int ncl = gridDim.x / GT_CL, cid = blockIdx.x / GT_CL, nsub = ncl * PER;
@@ -282,36 +321,36 @@ __device__ __forceinline__ void gt_stage_split(const GridArgs& a, int stage, con
     // the item kind may differ between the sub-clusters of one cluster: both
     // kinds pass exactly two cluster barriers
     if (r < ng) {
-      const Tile2 tile = a.tiles[stage][r];
-      gt_cluster_tile<SP>(gt_job(a, stage, tile, s), tile, bufs, smem, base, srank, valid, t2);
+      const Tile2 tile = D.tiles[stage][r];
+      gt_cluster_tile<SP>(gt_job(a, D, stage, tile, s), tile, bufs, smem, base, srank, valid, t2);
     } else {
-      const Tile2 tile = a.gv[stage][r - ng];
+      const Tile2 tile = D.gv[stage][r - ng];
       if (valid && t2 && threadIdx.x == 0) t2[4] = gt_timer();
-      gt_cluster_gemv<SP>(gt_job(a, stage, tile, s), tile, bufs, smem, base, srank, valid);
+      gt_cluster_gemv<SP>(gt_job(a, D, stage, tile, s), tile, bufs, smem, base, srank, valid);
       if (valid && t2 && threadIdx.x == 0) t2[5] = gt_timer();
     }
   }
 }
 
 // one operator stage for the live systems sl[0..L)
-__device__ __forceinline__ void gt_stage(const GridArgs& a, int stage, const int* sl, int L, const BufTable& bufs,
+__device__ __forceinline__ void gt_stage(const GridArgs& a, const GtDesc& D, int stage, const int* sl, int L, const BufTable& bufs,
                                          double* smem, unsigned long long* t2, bool rev = false) {
   if (t2 && threadIdx.x == 0) {
     for (int i = 1; i < 8; ++i) t2[i] = 0;
     t2[0] = gt_timer();
   }
   const int nt = a.ntiles[stage], nci = a.ngemm[stage] + a.ngv[stage];
-  const Tile2* tiles = a.tiles[stage];
+  const Tile2* tiles = D.tiles[stage];
   const int NB = gridDim.x, bid = blockIdx.x, ncl = NB / GT_CL;
   // split each tile over as many CTAs as the live systems leave room for
   const int items = L * nci;
-  if (items <= ncl) return gt_stage_split<GT_CL>(a, stage, sl, L, bufs, smem, t2, rev);
-  if (items <= 2 * ncl) return gt_stage_split<GT_CL / 2>(a, stage, sl, L, bufs, smem, t2, rev);
-  if (items <= 4 * ncl) return gt_stage_split<GT_CL / 4>(a, stage, sl, L, bufs, smem, t2, rev);
+  if (items <= ncl) return gt_stage_split<GT_CL>(a, D, stage, sl, L, bufs, smem, t2, rev);
+  if (items <= 2 * ncl) return gt_stage_split<GT_CL / 2>(a, D, stage, sl, L, bufs, smem, t2, rev);
+  if (items <= 4 * ncl) return gt_stage_split<GT_CL / 4>(a, D, stage, sl, L, bufs, smem, t2, rev);
   // many systems: whole tiles per CTA
   for (int it = bid; it < L * nt; it += NB) {
     const Tile2 tile = tiles[it % nt];
-    const GemmJob jb = gt_job(a, stage, tile, sl[it / nt]);
+    const GemmJob jb = gt_job(a, D, stage, tile, sl[it / nt]);
     __syncthreads();
     if (tile.ks < 0) {
       g2_gemv_tile<16>(jb, tile, bufs);
@@ -583,6 +622,10 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
   __shared__ int sl[GT_MAXSYS], ncol[GT_MAXSYS], c0s[GT_MAXSYS + 1];
   __shared__ int s_L;
   __shared__ double bred[G2_THREADS / 32];
+  __shared__ GtDesc gd;
+  __shared__ Tile2 gd_tiles[GT_TC], gd_gv[GT_GC];
+  __shared__ GemmJob gd_jobs[GT_JC];
+  gt_desc_init(a, gd, gd_tiles, gd_jobs, gd_gv);
 
   GmState_& G = a.G;
   const long long k = G.k;
@@ -673,7 +716,7 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
       if (!vh_ready) {
         f.p[BUF_IN] = a.vin;
         f.p[BUF_OUT] = a.vh;
-        gt_stage(a, 4, sl, L, f, gsmem, T2(0));
+        gt_stage(a, gd, 4, sl, L, f, gsmem, T2(0));
         grid_sync(a.bar, epoch);
         vh_ready = true;
       }
@@ -683,7 +726,7 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
       mark(2);
       f.p[BUF_IN] = a.th;
       f.p[BUF_OUT] = a.method == SMPM_DBJ ? a.t : a.w;
-      gt_stage(a, 5, sl, L, f, gsmem, T2(1));
+      gt_stage(a, gd, 5, sl, L, f, gsmem, T2(1));
       if (a.method == SMPM_DBJ) {
         // coarse solves c = C^{-1} Z^T t, one idle CTA per live slot (from the end of the grid)
         const int qc = NB - 1 - bid;
@@ -703,7 +746,7 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
       mark(4);
     } else if (a.method != SMPM_SCHUR) {
       for (int stg = 0; stg < 3; ++stg) {
-        gt_stage(a, stg, sl, L, bj, gsmem, T2(stg));
+        gt_stage(a, gd, stg, sl, L, bj, gsmem, T2(stg));
         grid_sync(a.bar, epoch);
         mark(1 + stg);
       }
@@ -728,7 +771,7 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
       sb.p[BUF_OUT] = a.method == SMPM_DBJ ? a.t : a.w;
       sb.p[BUF_TMP] = nullptr;
       sb.p[BUF_TMP2] = nullptr;
-      gt_stage(a, 3, sl, L, sb, gsmem, T2(3));
+      gt_stage(a, gd, 3, sl, L, sb, gsmem, T2(3));
       grid_sync(a.bar, epoch);
       mark(4);
     }
@@ -863,7 +906,7 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
         f.p[BUF_IN] = a.w;
         f.p[BUF_OUT] = a.vh;
         f.p[BUF_TMP] = f.p[BUF_TMP2] = nullptr;
-        gt_stage(a, 4, sl, L, f, gsmem, nullptr, true);
+        gt_stage(a, gd, 4, sl, L, f, gsmem, nullptr, true);
         vh_from_w = true;
       }
       grid_sync(a.bar, epoch);
@@ -915,7 +958,7 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
       f.p[BUF_IN] = a.w;
       f.p[BUF_OUT] = a.vh;
       f.p[BUF_TMP] = f.p[BUF_TMP2] = nullptr;
-      gt_stage(a, 4, sl, L, f, gsmem, nullptr, true);
+      gt_stage(a, gd, 4, sl, L, f, gsmem, nullptr, true);
       vh_from_w = true;
     }
     grid_sync(a.bar, epoch);
