@@ -151,8 +151,12 @@ __device__ __forceinline__ void gt_frag_rc(int q, int& r, int& c) {
 // [r*64/SP, (r+1)*64/SP) in sub-rank order.  Every CTA of the cluster calls
 // this the same number of times (valid = false: barriers only).
 template <int SP>
+// tail_sync = false skips the trailing cluster barrier: allowed for a stage's last
+// round, because every caller passes a grid barrier before the ring is reused (and a
+// rank's DSMEM reads have completed before it arrives there)
 __device__ __forceinline__ void gt_cluster_tile(GemmJob jb, Tile2 tile, const BufTable& bufs, double* smem,
-                                                unsigned base, unsigned srank, bool valid, unsigned long long* t2) {
+                                                unsigned base, unsigned srank, bool valid, unsigned long long* t2,
+                                                bool tail_sync) {
   __syncthreads();  // ring may still be read by this CTA's previous tile
   if (valid) {
     jb.splitk = SP;
@@ -185,7 +189,7 @@ __device__ __forceinline__ void gt_cluster_tile(GemmJob jb, Tile2 tile, const Bu
     }
     if (t2 && threadIdx.x == 0) t2[2] = gt_timer();
   }
-  gt_cl_sync();  // partials consumed before any rank reuses its ring
+  if (tail_sync) gt_cl_sync();  // partials consumed before any rank reuses its ring
   if (valid && t2 && threadIdx.x == 0) t2[3] = gt_timer();
 }
 
@@ -244,7 +248,7 @@ __device__ __forceinline__ GemmJob gt_job(const GridArgs& a, const GtDesc& D, in
 // DSMEM, sub-rank r finishes rows [r*GT_GVR/SP, (r+1)*GT_GVR/SP) in order.
 template <int SP>
 __device__ __forceinline__ void gt_cluster_gemv(const GemmJob& jb, const Tile2& tile, const BufTable& bufs,
-                                                double* smem, unsigned base, unsigned srank, bool valid) {
+                                                double* smem, unsigned base, unsigned srank, bool valid, bool tail_sync) {
   constexpr int KG = G2_THREADS / GT_GVR;  // 4 k-groups
   constexpr int UNR = 16;
   const int t = threadIdx.x, r = t % GT_GVR, kg = t / GT_GVR;
@@ -299,7 +303,7 @@ __device__ __forceinline__ void gt_cluster_gemv(const GemmJob& jb, const Tile2& 
       store_out(jb, bufs, mm, 0, sum);
     }
   }
-  gt_cl_sync();
+  if (tail_sync) gt_cl_sync();
 }
 
 // cluster items of one stage, SP CTAs per item, GT_CL / SP items per cluster
@@ -319,14 +323,15 @@ __device__ __forceinline__ void gt_stage_split(const GridArgs& a, const GtDesc& 
     const bool valid = it < items;
     const int s = valid ? sl[it / nci] : sl[0], r = valid ? it % nci : 0;
     // the item kind may differ between the sub-clusters of one cluster: both
-    // kinds pass exactly two cluster barriers
+    // kinds pass the same cluster barriers (two, one in the last round)
+    const bool more = rd + 1 < rounds;
     if (r < ng) {
       const Tile2 tile = D.tiles[stage][r];
-      gt_cluster_tile<SP>(gt_job(a, D, stage, tile, s), tile, bufs, smem, base, srank, valid, t2);
+      gt_cluster_tile<SP>(gt_job(a, D, stage, tile, s), tile, bufs, smem, base, srank, valid, t2, more);
     } else {
       const Tile2 tile = D.gv[stage][r - ng];
       if (valid && t2 && threadIdx.x == 0) t2[4] = gt_timer();
-      gt_cluster_gemv<SP>(gt_job(a, D, stage, tile, s), tile, bufs, smem, base, srank, valid);
+      gt_cluster_gemv<SP>(gt_job(a, D, stage, tile, s), tile, bufs, smem, base, srank, valid, more);
       if (valid && t2 && threadIdx.x == 0) t2[5] = gt_timer();
     }
   }
