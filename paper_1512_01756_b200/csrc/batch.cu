@@ -287,6 +287,7 @@ struct smpm_batch {
   // grid-persistent tail solver (grid.cuh)
   bool grid_ok = false;
   int gt_blocks = 0;
+  bool sp_smem_set = false;
   size_t gt_smem = 0;  // tail dynamic shared memory (tile ring / V-row block region + vectors)
   int gt_vcap = 0;     // doubles of the ring / V-row block region
   bool gt_nocoop = false;  // cooperative + cluster launch rejected: plain cluster launch
@@ -1129,7 +1130,7 @@ struct SolveCfg {
 // Spectral operator (spectral.cuh): T^{-1} GEMM, per-mode S^ M^^{-1}, T GEMM
 // --------------------------------------------------------------------------
 SpecParams spec_params(const smpm_batch* b) {
-  SpecParams sp;
+  SpecParams sp{};
   sp.w = b->w;
   sp.d = b->d;
   sp.mx = b->mx;
@@ -1228,7 +1229,16 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
   P.alist = lv.alist;
   P.acount = lv.acount;
   const dim3 grid(sp.nmc * ((sp.nseg + SP_WARPS - 1) / SP_WARPS), lv.nslots);
-  const size_t shm = cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0;
+  // staged slot rows (SMPM_SP_NO_STAGE=1: direct loads)
+  sp.stage = sp.segb <= SP_SEGB && std::getenv("SMPM_SP_NO_STAGE") == nullptr ? 1 : 0;
+  const size_t shm = (cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0) +
+                     (sp.stage ? sizeof(double) * SP_STAGE_DOUBLES : 0);
+  if (sp.stage && !b->sp_smem_set) {
+    const int mx = static_cast<int>(sizeof(double) * (SP_STAGE_DOUBLES + 2 * 256));
+    CUDA_CHECK(cudaFuncSetAttribute(spec_op_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CUDA_CHECK(cudaFuncSetAttribute(spec_op_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    b->sp_smem_set = true;
+  }
   double* zp = cout ? b->dzpart.p : nullptr;
   if (bj)
     launch_pdl(b, spec_op_kernel<true>, grid, dim3(SP_THREADS), shm, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);

@@ -39,12 +39,16 @@ struct SpecParams {
   const double* nu;            // w: T^{-1} 1, a constant w-block in spectral coordinates
   const double* cadd;          // nullable, nsys x d: 2LAS coarse solutions c added as Z c before S^
   int nmc, nseg, segb;         // 32-mode chunks, block segments of segb (<= SP_SEGB) blocks
+  int stage;                   // spec_op_kernel: stage each warp's vh rows in shared memory first
 };
 
 constexpr int SP_MODES = 32;               // modes per warp (one lane each)
 constexpr int SP_WARPS = 4;                // segments per CTA (one warp each)
 constexpr int SP_THREADS = 32 * SP_WARPS;
 constexpr int SP_SEGB = 4;                 // max block-Jacobi blocks per segment (8 interfaces)
+constexpr int SP_SROW = 66;                // staged doubles per slot row (32 modes, pairs take 2; 16-byte aligned start)
+constexpr int SP_SSLOTS = 4 * (SP_SEGB + 2);  // slot rows per warp: the segment and its two halo blocks
+constexpr int SP_STAGE_DOUBLES = SP_WARPS * SP_SSLOTS * SP_SROW;  // 48 KB per CTA
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -78,6 +82,19 @@ struct ModeRef {
     return pair ? fma(omega[e0], z.x, -omega[e0 + 1] * z.y) : omega[e0] * z.x;
   }
 };
+
+// shared-memory copy of one warp's slot rows: slot row (blk - bs) * 4 + j holds
+// coordinates [elo, elo + SP_SROW) of slot 4 blk + j
+struct SpecStage {
+  const double* buf;  // nullptr: read vh directly
+  int bs, elo;
+};
+
+__device__ __forceinline__ double2 spec_ld(const ModeRef& mr, const SpecStage& sg, const double* vh, int beta) {
+  if (!sg.buf) return mr.ld(vh, beta);
+  const double* p = sg.buf + ((beta >> 2) - sg.bs) * 4 * SP_SROW + (beta & 3) * SP_SROW + (mr.e0 - sg.elo);
+  return make_double2(p[0], mr.pair ? -p[1] : 0.0);
+}
 
 __device__ __forceinline__ ModeRef mode_ref(const SpecParams& sp, int s, int m) {
   ModeRef r;
@@ -187,12 +204,12 @@ __device__ __forceinline__ int spec_bslots(const SpecParams& sp, int blk) { retu
 template <bool BJ>
 __device__ __forceinline__ void spec_load_solve(const SpecParams& sp, const ModeRef& mr, const ModeGamma& g,
                                                 const double2* ki, const double* __restrict__ vh, int blk,
-                                                double2 (&x)[4], double ysc = 1.0) {
+                                                double2 (&x)[4], double ysc, const SpecStage& stg) {
   double2 y[4];
   const int ns = spec_bslots(sp, blk);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    y[j] = j < ns ? mr.ld(vh, 4 * blk + j) : make_double2(0.0, 0.0);
+    y[j] = j < ns ? spec_ld(mr, stg, vh, 4 * blk + j) : make_double2(0.0, 0.0);
     y[j].x *= ysc;
     y[j].y *= ysc;
   }
@@ -219,11 +236,11 @@ template <bool BJ>
 __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const ModeRef& mr, const ModeGamma& g,
                                                   const double2* ki, const double* __restrict__ vh,
                                                   double* __restrict__ th, int b0, int b1, double* zt,
-                                                  double* __restrict__ uh = nullptr, double ysc = 1.0) {
+                                                  double* __restrict__ uh, double ysc, const SpecStage& stg) {
   const int nb = spec_nblocks(sp);
   double2 xp[4], xc[4], xn[4];
-  if (th && b0 > 0) spec_load_solve<BJ>(sp, mr, g, ki, vh, b0 - 1, xp, ysc);
-  spec_load_solve<BJ>(sp, mr, g, ki, vh, b0, xc, ysc);
+  if (th && b0 > 0) spec_load_solve<BJ>(sp, mr, g, ki, vh, b0 - 1, xp, ysc, stg);
+  spec_load_solve<BJ>(sp, mr, g, ki, vh, b0, xc, ysc, stg);
   for (int blk = b0; blk < b1; ++blk) {
     const int ns = spec_bslots(sp, blk);
     if (uh) {
@@ -232,7 +249,7 @@ __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const Mo
         if (j < ns) mr.st(uh, 4 * blk + j, xc[j]);
     }
     if (th) {
-      if (blk + 1 < nb) spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xn, ysc);
+      if (blk + 1 < nb) spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xn, ysc, stg);
       double2 t[4];
       spec_block_S(sp, g, blk, xc, xp[3], xn[0], t);
 #pragma unroll
@@ -248,7 +265,7 @@ __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const Mo
         xc[j] = xn[j];
       }
     } else if (blk + 1 < b1) {
-      spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xc, ysc);
+      spec_load_solve<BJ>(sp, mr, g, ki, vh, blk + 1, xc, ysc, stg);
     }
   }
 }
@@ -258,11 +275,42 @@ __device__ __forceinline__ void spec_mode_segment(const SpecParams& sp, const Mo
 template <bool BJ>
 __device__ __forceinline__ void spec_warp_item(const SpecParams& sp, int s, int mc, int sg,
                                                const double* __restrict__ vh, double* __restrict__ th, double* zout,
-                                               double* __restrict__ uh = nullptr, double ysc = 1.0) {
+                                               double* __restrict__ uh = nullptr, double ysc = 1.0,
+                                               double* sbuf = nullptr) {
   const int lane = threadIdx.x & 31;
   const int m = mc * SP_MODES + lane;
   const int nb = spec_nblocks(sp);
   const int b0 = sg * sp.segb, b1 = min(nb, b0 + sp.segb);
+  SpecStage stg{nullptr, 0, 0};
+  if (sbuf) {
+    // the warp's slot rows (segment + halo blocks) into shared memory with 8-byte async
+    // copies issued together, so the per-block chain below reads shared memory only
+    const int bs = (th && b0 > 0) ? b0 - 1 : b0, be = th ? min(nb, b1 + 1) : b1;
+    const int mf = mc * SP_MODES, ml = min(sp.nmode, mf + SP_MODES) - 1;
+    // 16-byte copies of the even-aligned range (k and w even), through L2 (.cg)
+    const int elo = (mf < sp.npairs ? 2 * mf : sp.npairs + mf) & ~1;
+    const int ehi = ml < sp.npairs ? 2 * ml + 2 : sp.npairs + ml + 1;
+    const int npr = (ehi - elo + 1) >> 1;  // <= 33 pairs
+    const double* src0 = vh + s * sp.k + elo;
+    for (int bl = bs; bl < be; ++bl) {
+      const int ns = spec_bslots(sp, bl);
+      for (int jj = 0; jj < ns; ++jj) {
+        const double* src = src0 + static_cast<long long>(4 * bl + jj) * sp.w;
+        double* dst = sbuf + ((bl - bs) * 4 + jj) * SP_SROW;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = lane + 32 * h;
+          if (e < npr) {
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + 2 * e));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 2 * e));
+          }
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+    stg = SpecStage{sbuf, bs, elo};
+  }
   double zt[2 * SP_SEGB];
 #pragma unroll
   for (int i = 0; i < 2 * SP_SEGB; ++i) zt[i] = 0.0;
@@ -270,7 +318,7 @@ __device__ __forceinline__ void spec_warp_item(const SpecParams& sp, int s, int 
     const ModeRef mr = mode_ref(sp, s, m);
     const ModeGamma g = mode_gamma(sp, s, m);
     const double2* ki = sp.kinv + static_cast<long long>(s) * 20 * sp.nmode + m;
-    spec_mode_segment<BJ>(sp, mr, g, ki, vh, th, b0, b1, zout ? zt : nullptr, uh, ysc);
+    spec_mode_segment<BJ>(sp, mr, g, ki, vh, th, b0, b1, zout ? zt : nullptr, uh, ysc, stg);
   }
   if (!zout) return;
   const int i0 = 2 * b0, i1 = min(sp.d, 2 * b1);
@@ -293,17 +341,18 @@ __global__ void __launch_bounds__(SP_THREADS, SP_MINB) spec_op_kernel(SpecParams
                                                              int* counter, double* cout, double* __restrict__ uh) {
   pdl_wait();
   pdl_launch();
-  extern __shared__ double sm[];  // 2 d doubles (coarse solve)
+  extern __shared__ double sm[];  // [stage: SP_STAGE_DOUBLES] 2 d doubles (coarse solve)
   int s;
   if (!defl_slot(P, blockIdx.y, s)) return;
   const int nsg = (sp.nseg + SP_WARPS - 1) / SP_WARPS;
   const int mc = blockIdx.x / nsg, sg = (blockIdx.x % nsg) * SP_WARPS + (threadIdx.x >> 5);
+  double* sbuf = sp.stage ? sm + (threadIdx.x >> 5) * SP_SSLOTS * SP_SROW : nullptr;
   if (sg < sp.nseg)
     spec_warp_item<BJ>(sp, s, mc, sg, vh, th, zpart ? zpart + (static_cast<long long>(s) * sp.nmc + mc) * sp.d : nullptr,
-                       uh);
+                       uh, 1.0, sbuf);
   if (!zpart) return;
   if (!last_cta(counter + s, sp.nmc * nsg)) return;
-  double* sums = sm;
+  double* sums = sm + (sp.stage ? SP_STAGE_DOUBLES : 0);
   double* c = sm + sp.d;
   for (int i = threadIdx.x; i < sp.d; i += blockDim.x) {
     double v = 0.0;
