@@ -1391,7 +1391,9 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
       // one reduction and one kernel less per step; iteration counts measured unchanged
       // on 9 right-hand sides (tools/seed_sweep.py)
       launch_pdl(b, cgs3_dot_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, tdefl, P, cbuf);
-      launch_pdl(b, cgs3_pass2n_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, static_cast<const double*>(V), wv);
+      // ncols <= 8: update and dots in one read of V (SMPM_NO_P2FUSE=1: two reads)
+      launch_pdl(b, cgs3_pass2n_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, static_cast<const double*>(V), wv,
+                 std::getenv("SMPM_NO_P2FUSE") ? 0 : 1);
       launch_pdl(b, cgs3_pass3s_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, vin);
       return;
     }

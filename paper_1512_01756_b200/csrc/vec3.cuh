@@ -131,6 +131,48 @@ __device__ __forceinline__ double rows_update_long(const double* __restrict__ Vs
   return rows_update_nr<2, V3_GRP>(Vs, k, ncols, h, ws, r0, r1);
 }
 
+// Pass 2 for ncols <= 8 in one traversal of V: each round's V values stay in
+// registers for both the update w -= V h and the reorthogonalisation dots
+// acc[u] += V[r, u] w_new[r]; same accumulation orders as rows_update_nr and
+// dots_rows (bit-identical), one read of V instead of two. Returns ||w_new||^2
+// of this thread's rows.
+template <int NR, int NG>
+__device__ __forceinline__ double pass2_fused_rows(const double* __restrict__ Vs, long long k, int ncols,
+                                                   const double* h, double* ws, int r0, int r1,
+                                                   double (&acc)[V3_GRP]) {
+  double sq = 0.0;
+  for (int r = r0 + static_cast<int>(threadIdx.x); r < r1; r += NR * V3_THREADS) {
+    double v[NR][NG], wv[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int rq = r + q * V3_THREADS;
+      const bool ok = rq < r1;
+      wv[q] = ok ? __ldcg(ws + rq) : 0.0;
+#pragma unroll
+      for (int u = 0; u < NG; ++u) v[q][u] = (ok && u < ncols) ? __ldcg(Vs + static_cast<long long>(u) * k + rq) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int rq = r + q * V3_THREADS;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int u = 0; u < NG; u += 2) {
+        const double h0 = u < ncols ? h[u] : 0.0, h1 = u + 1 < ncols ? h[u + 1] : 0.0;
+        a0 = fma(v[q][u], h0, a0);
+        a1 = fma(v[q][u + 1], h1, a1);
+      }
+      const double nv = rq < r1 ? wv[q] - (a0 + a1) : 0.0;
+      if (rq < r1) {
+        ws[rq] = nv;
+        sq = fma(nv, nv, sq);
+      }
+#pragma unroll
+      for (int u = 0; u < NG; ++u) acc[u] = fma(v[q][u], nv, acc[u]);
+    }
+  }
+  return sq;
+}
+
 // ---- pass 1: h1 = V^T w (with the fused deflation P when tdefl != nullptr) ----
 __global__ void __launch_bounds__(V3_THREADS) cgs3_dot_kernel(GmState_ G, const double* __restrict__ V, double* w,
                                                               const double* __restrict__ tdefl, DeflateParams P,
@@ -223,7 +265,8 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_update_kernel(GmState_ G, con
 // pass 2': w -= V h1; h2 = V^T w and ||w||^2 in one reduction; the last CTA takes
 // ||w - V h2||^2 = ||w||^2 - ||h2||^2 (h2 is the O(eps) reorthogonalisation
 // correction, so the difference is accurate) and runs the Givens step
-__global__ void __launch_bounds__(V3_THREADS) cgs3_pass2n_kernel(GmState_ G, const double* __restrict__ V, double* w) {
+__global__ void __launch_bounds__(V3_THREADS) cgs3_pass2n_kernel(GmState_ G, const double* __restrict__ V, double* w,
+                                                                 int fuse) {
   pdl_wait();
   pdl_launch();
   __shared__ double hs[V2_MAXCOL];
@@ -241,10 +284,37 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_pass2n_kernel(GmState_ G, con
   const int r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
   const double* Vs = V + s * G.vstride;
   double* ws = w + s * G.k;
-  double sq = rows_update_long(Vs, G.k, ncols, hs, ws, r0, r1);
   double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
-  __syncthreads();
-  cta_dots_long(Vs, G.k, ncols, ws, r0, r1, part, red);
+  double sq;
+  if (fuse && ncols <= V3_GRP) {
+    double acc[V3_GRP];
+#pragma unroll
+    for (int u = 0; u < V3_GRP; ++u) acc[u] = 0.0;
+    if (ncols <= 2)
+      sq = pass2_fused_rows<8, 2>(Vs, G.k, ncols, hs, ws, r0, r1, acc);
+    else if (ncols <= 4)
+      sq = pass2_fused_rows<4, 4>(Vs, G.k, ncols, hs, ws, r0, r1, acc);
+    else
+      sq = pass2_fused_rows<2, V3_GRP>(Vs, G.k, ncols, hs, ws, r0, r1, acc);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int u = 0; u < V3_GRP; ++u) {
+      const double v = warp_sum(acc[u]);
+      if (lane == 0) red[warp][u] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < V3_GRP && static_cast<int>(threadIdx.x) < ncols) {
+      double a = 0.0;
+#pragma unroll
+      for (int q = 0; q < V3_THREADS / 32; ++q) a += red[q][threadIdx.x];
+      part[threadIdx.x] = a;
+    }
+    __syncthreads();
+  } else {
+    sq = rows_update_long(Vs, G.k, ncols, hs, ws, r0, r1);
+    __syncthreads();
+    cta_dots_long(Vs, G.k, ncols, ws, r0, r1, part, red);
+  }
   sq = warp_sum(sq);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][0] = sq;
   __syncthreads();
