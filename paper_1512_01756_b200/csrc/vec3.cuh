@@ -139,7 +139,7 @@ __device__ __forceinline__ double rows_update_long(const double* __restrict__ Vs
 template <int NR, int NG>
 __device__ __forceinline__ double pass2_fused_rows(const double* __restrict__ Vs, long long k, int ncols,
                                                    const double* h, double* ws, int r0, int r1,
-                                                   double (&acc)[V3_GRP]) {
+                                                   double (&acc)[2 * V3_GRP]) {
   double sq = 0.0;
   for (int r = r0 + static_cast<int>(threadIdx.x); r < r1; r += NR * V3_THREADS) {
     double v[NR][NG], wv[NR];
@@ -156,7 +156,7 @@ __device__ __forceinline__ double pass2_fused_rows(const double* __restrict__ Vs
       const int rq = r + q * V3_THREADS;
       double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-      for (int u = 0; u < NG; u += 2) {
+      for (int u = 0; u < NG; u += 2) {  // groups of 8 in order: the same sequence as rows_update_nr<2, 8>
         const double h0 = u < ncols ? h[u] : 0.0, h1 = u + 1 < ncols ? h[u + 1] : 0.0;
         a0 = fma(v[q][u], h0, a0);
         a1 = fma(v[q][u + 1], h1, a1);
@@ -286,30 +286,36 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_pass2n_kernel(GmState_ G, con
   double* ws = w + s * G.k;
   double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
   double sq;
-  if (fuse && ncols <= V3_GRP) {
-    double acc[V3_GRP];
+  if (fuse && ncols <= 2 * V3_GRP) {
+    double acc[2 * V3_GRP];
 #pragma unroll
-    for (int u = 0; u < V3_GRP; ++u) acc[u] = 0.0;
+    for (int u = 0; u < 2 * V3_GRP; ++u) acc[u] = 0.0;
     if (ncols <= 2)
       sq = pass2_fused_rows<8, 2>(Vs, G.k, ncols, hs, ws, r0, r1, acc);
     else if (ncols <= 4)
       sq = pass2_fused_rows<4, 4>(Vs, G.k, ncols, hs, ws, r0, r1, acc);
-    else
+    else if (ncols <= V3_GRP)
       sq = pass2_fused_rows<2, V3_GRP>(Vs, G.k, ncols, hs, ws, r0, r1, acc);
+    else
+      sq = pass2_fused_rows<1, 2 * V3_GRP>(Vs, G.k, ncols, hs, ws, r0, r1, acc);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int u = 0; u < V3_GRP; ++u) {
-      const double v = warp_sum(acc[u]);
-      if (lane == 0) red[warp][u] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < V3_GRP && static_cast<int>(threadIdx.x) < ncols) {
-      double a = 0.0;
+    for (int g = 0; g < 2; ++g) {
+      if (g * V3_GRP >= ncols) break;
 #pragma unroll
-      for (int q = 0; q < V3_THREADS / 32; ++q) a += red[q][threadIdx.x];
-      part[threadIdx.x] = a;
+      for (int u = 0; u < V3_GRP; ++u) {
+        const double v = warp_sum(acc[g * V3_GRP + u]);
+        if (lane == 0) red[warp][u] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x < V3_GRP && g * V3_GRP + static_cast<int>(threadIdx.x) < ncols) {
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q < V3_THREADS / 32; ++q) a += red[q][threadIdx.x];
+        part[g * V3_GRP + threadIdx.x] = a;
+      }
+      __syncthreads();
     }
-    __syncthreads();
   } else {
     sq = rows_update_long(Vs, G.k, ncols, hs, ws, r0, r1);
     __syncthreads();
