@@ -39,7 +39,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [nvcc(), *NVCC_FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", OUT, "-lcusolver", "-lcublas"]
+    extra = os.environ.get("SMPM_NVCC_EXTRA", "").split()  # tuning experiments, e.g. -DCGS3_MINB=3
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, *[os.path.join(CSRC, s) for s in SOURCES], "-o", OUT, "-lcusolver",
+           "-lcublas"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)

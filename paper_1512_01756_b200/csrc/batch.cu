@@ -275,6 +275,7 @@ struct smpm_batch {
   DevArray<double> dTfrag, dTifrag;    // T, T^{-1} in the xform fragment order
   int xf_P = 0, xf_MB = 0;
   long long cgs3_res = 0;  // resident CTAs of the CGS2 pass kernels (device)
+  long long cgs3_kres[3] = {0, 0, 0};  // per kernel: pass 1, pass 2', pass 3' (norm-from-h2 path)
   bool pythag = true;  // norm from the second CGS2 reduction (cgs3_pass2n / cgs3_pass3s); SMPM_NO_PYTHAG=1: off
   bool pdl = true;  // programmatic dependent launch for the Arnoldi step chain (SMPM_NO_PDL=1: off)  // resident-slice transform kernel (xform.cuh); 0: use pF/pB
   size_t xf_smem = 0;
@@ -1389,12 +1390,35 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
     if (!G.stacked && b->pythag) {
       // ||w|| from the second reduction (||w1||^2 - ||h2||^2), the scale folded into pass 3:
       // one reduction and one kernel less per step; iteration counts measured unchanged
-      // on 9 right-hand sides (tools/seed_sweep.py)
-      launch_pdl(b, cgs3_dot_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, tdefl, P, cbuf);
-      // ncols <= 8: update and dots in one read of V (SMPM_NO_P2FUSE=1: two reads)
-      launch_pdl(b, cgs3_pass2n_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, static_cast<const double*>(V), wv,
+      // on 9 right-hand sides (tools/seed_sweep.py).
+      // Each pass gets its own row chunking sized to ITS resident CTA count (the
+      // passes differ in registers: one wave each; partials and counters are per
+      // kernel, the work vector is exchanged only between kernels)
+      if (b->cgs3_kres[0] == 0) {
+        int o[3] = {0, 0, 0};
+        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[0], cgs3_dot_kernel, V3_THREADS, 0));
+        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[1], cgs3_pass2n_kernel, V3_THREADS, 0));
+        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[2], cgs3_pass3s_kernel, V3_THREADS, 0));
+        for (int i = 0; i < 3; ++i) b->cgs3_kres[i] = std::max(1, std::min(o[i], 3)) * b->ctx->num_sms;
+      }
+      auto chunked = [&](long long res, dim3& g) {
+        GmState_ Gk = G;
+        const long long kc = std::max(1LL, res / lv.nslots);
+        long long ck = (b->k + kc - 1) / kc;
+        ck = std::max(256LL, (ck + 255) / 256 * 256);
+        Gk.chunk = static_cast<int>(ck);
+        Gk.nchunk = static_cast<int>((b->k + ck - 1) / ck);
+        g = dim3(Gk.nchunk, lv.nslots);
+        return Gk;
+      };
+      dim3 g1, g2, g3;
+      const GmState_ G1 = chunked(b->cgs3_kres[0], g1), G2 = chunked(b->cgs3_kres[1], g2),
+                     G3 = chunked(b->cgs3_kres[2], g3);
+      launch_pdl(b, cgs3_dot_kernel, g1, dim3(V3_THREADS), 0, st, G1, V, wv, tdefl, P, cbuf);
+      // ncols <= 16: update and dots in one read of V (SMPM_NO_P2FUSE=1: two reads)
+      launch_pdl(b, cgs3_pass2n_kernel, g2, dim3(V3_THREADS), 0, st, G2, static_cast<const double*>(V), wv,
                  std::getenv("SMPM_NO_P2FUSE") ? 0 : 1);
-      launch_pdl(b, cgs3_pass3s_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, vin);
+      launch_pdl(b, cgs3_pass3s_kernel, g3, dim3(V3_THREADS), 0, st, G3, V, wv, vin);
       return;
     }
     launch_pdl(b, cgs3_dot_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, tdefl, P, cbuf);

@@ -16,6 +16,9 @@ namespace smpm {
 
 constexpr int V3_THREADS = 256;
 constexpr int V3_GRP = 8;  // columns per register group
+#ifndef CGS3_MINB
+#define CGS3_MINB 2  // minimum resident CTAs per SM requested for pass 2'
+#endif
 
 // Row-major work of one thread: rows r0 + t, r0 + t + 256, ... in that order.
 // NR rows per round and NG columns per register group, all loads of a round
@@ -24,17 +27,46 @@ constexpr int V3_GRP = 8;  // columns per register group
 // (dots) and per-row (update) accumulation sequences do not depend on NR / NG,
 // so every instance gives bit-identical results.
 
+// x[r] read from memory (the default source of dots_rows)
+struct XLoad {
+  const double* x;
+  __device__ __forceinline__ double operator()(int r) const { return __ldcg(x + r); }
+  __device__ __forceinline__ bool first() const { return false; }
+};
+
+// pass 1's fused deflation: x[r] = t[r] - (Z c)[r] - ((S - I) Z c)[r] (strip
+// row-sum identity), stored to w[r] as it is produced
+struct XDeflate {
+  const double *c, *rWI, *rEI, *rEW, *rWE, *ts;
+  double* ws;
+  int wd, mx;
+  __device__ __forceinline__ bool first() const { return true; }
+  __device__ __forceinline__ double operator()(int e) const {
+    const int blk = e / wd, r = e - blk * wd, i = blk >> 1;
+    double sz;
+    if ((blk & 1) == 0)
+      sz = (i + 1 == mx - 1) ? c[i] * rWE[r] : c[i] * rWI[r] + c[i + 1] * rEI[r];
+    else
+      sz = (i == 0) ? c[i] * rEW[r] : c[i - 1] * rWI[wd + r] + c[i] * rEI[wd + r];
+    const double v = ts[e] - (c[i] + sz);
+    ws[e] = v;
+    return v;
+  }
+};
+
 // acc[u] += sum over this thread's rows of V[r, c0 + u] x[r], u < nc <= NG
-template <int NR, int NG>
+// (x[r] = xs(r); a thread visits rows r0 + t + i * 256, the same rows every pass
+// owns, so a source that computes and stores x[r] needs no barrier)
+template <int NR, int NG, class XS = XLoad>
 __device__ __forceinline__ void dots_rows(const double* __restrict__ Vs, long long k, int c0, int nc,
-                                          const double* x, int r0, int r1, double (&acc)[V3_GRP]) {
+                                          XS xs, int r0, int r1, double (&acc)[V3_GRP]) {
   for (int r = r0 + static_cast<int>(threadIdx.x); r < r1; r += NR * V3_THREADS) {
     double xv[NR], v[NR][NG];
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
       const int rq = r + q * V3_THREADS;
       const bool ok = rq < r1;
-      xv[q] = ok ? __ldcg(x + rq) : 0.0;
+      xv[q] = ok ? xs(rq) : 0.0;
 #pragma unroll
       for (int u = 0; u < NG; ++u)
         v[q][u] = (ok && u < nc) ? __ldcg(Vs + static_cast<long long>(c0 + u) * k + rq) : 0.0;
@@ -46,24 +78,36 @@ __device__ __forceinline__ void dots_rows(const double* __restrict__ Vs, long lo
   }
 }
 
-// partial dots over rows [r0, r1) of V_s[:, 0..ncols) with x -> out[0..ncols)
+template <class XS>
+__device__ __forceinline__ void dots_rows_any(const double* __restrict__ Vs, long long k, int c0, int nc, XS xs,
+                                              int r0, int r1, double (&acc)[V3_GRP]) {
+  if (nc <= 1)
+    dots_rows<8, 1>(Vs, k, c0, nc, xs, r0, r1, acc);
+  else if (nc <= 2)
+    dots_rows<8, 2>(Vs, k, c0, nc, xs, r0, r1, acc);
+  else if (nc <= 4)
+    dots_rows<4, 4>(Vs, k, c0, nc, xs, r0, r1, acc);
+  else
+    dots_rows<2, V3_GRP>(Vs, k, c0, nc, xs, r0, r1, acc);
+}
+
+// partial dots over rows [r0, r1) of V_s[:, 0..ncols) with x -> out[0..ncols);
+// the first column group takes x from xs0 (which may compute and store x), the
+// rest re-read the stored x
+template <class XS = XLoad>
 __device__ __forceinline__ void cta_dots_long(const double* __restrict__ Vs, long long k, int ncols,
                                               const double* x, int r0, int r1, double* __restrict__ out,
-                                              double (*red)[V3_GRP]) {
+                                              double (*red)[V3_GRP], XS xs0 = XS{}) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int c0 = 0; c0 < ncols; c0 += V3_GRP) {
     const int nc = min(V3_GRP, ncols - c0);
     double acc[V3_GRP];
 #pragma unroll
     for (int u = 0; u < V3_GRP; ++u) acc[u] = 0.0;
-    if (nc <= 1)
-      dots_rows<8, 1>(Vs, k, c0, nc, x, r0, r1, acc);
-    else if (nc <= 2)
-      dots_rows<8, 2>(Vs, k, c0, nc, x, r0, r1, acc);
-    else if (nc <= 4)
-      dots_rows<4, 4>(Vs, k, c0, nc, x, r0, r1, acc);
+    if (c0 == 0 && xs0.first())
+      dots_rows_any(Vs, k, c0, nc, xs0, r0, r1, acc);
     else
-      dots_rows<2, V3_GRP>(Vs, k, c0, nc, x, r0, r1, acc);
+      dots_rows_any(Vs, k, c0, nc, XLoad{x}, r0, r1, acc);
 #pragma unroll
     for (int u = 0; u < V3_GRP; ++u) {
       const double v = warp_sum(acc[u]);
@@ -83,9 +127,12 @@ __device__ __forceinline__ void cta_dots_long(const double* __restrict__ Vs, lon
 // w[r] -= sum_c V[r, c] h[c] for this thread's rows, NR rows per round; per row
 // the even / odd columns (within each group of 8) accumulate separately in column
 // order; returns the sum of squares of the new rows (in row order)
-template <int NR, int NG>
+// SCALE: also v = w_new * inv into col and vs (pass 3', the same rows this thread
+// owns, so the new basis vector comes from registers instead of a re-read of w)
+template <int NR, int NG, bool SCALE = false>
 __device__ __forceinline__ double rows_update_nr(const double* __restrict__ Vs, long long k, int ncols,
-                                                 const double* h, double* ws, int r0, int r1) {
+                                                 const double* h, double* ws, int r0, int r1,
+                                                 double inv = 0.0, double* col = nullptr, double* vs = nullptr) {
   double sq = 0.0;
   for (int r = r0 + static_cast<int>(threadIdx.x); r < r1; r += NR * V3_THREADS) {
     double a[NR][2];
@@ -118,6 +165,11 @@ __device__ __forceinline__ double rows_update_nr(const double* __restrict__ Vs, 
         const double nv = __ldcg(ws + rq) - (a[q][0] + a[q][1]);
         ws[rq] = nv;
         sq = fma(nv, nv, sq);
+        if (SCALE) {
+          const double v = nv * inv;
+          col[rq] = v;
+          vs[rq] = v;
+        }
       }
     }
   }
@@ -174,7 +226,7 @@ __device__ __forceinline__ double pass2_fused_rows(const double* __restrict__ Vs
 }
 
 // ---- pass 1: h1 = V^T w (with the fused deflation P when tdefl != nullptr) ----
-__global__ void __launch_bounds__(V3_THREADS) cgs3_dot_kernel(GmState_ G, const double* __restrict__ V, double* w,
+__global__ void __launch_bounds__(V3_THREADS, 3) cgs3_dot_kernel(GmState_ G, const double* __restrict__ V, double* w,
                                                               const double* __restrict__ tdefl, DeflateParams P,
                                                               const double* __restrict__ cbuf) {
   pdl_wait();
@@ -187,27 +239,19 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_dot_kernel(GmState_ G, const 
   const int r0 = static_cast<int>(min(G.k, static_cast<long long>(ch) * G.chunk));
   const int r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
   double* ws = w + s * G.k;
-  if (tdefl) {
-    // w = t - Z c - (S - I) Z c (strip row-sum identity)
-    const int wd = P.w, w2 = 2 * wd, mx = P.mx;
-    const double* c = cbuf + static_cast<long long>(s) * P.d;
-    const double* rs = P.rowsum + static_cast<long long>(s) * 6 * wd;
-    const double *rWI = rs, *rEI = rs + w2, *rEW = rs + 2 * w2, *rWE = rEW + wd;
-    const double* ts = tdefl + s * G.k;
-    for (int e = r0 + threadIdx.x; e < r1; e += V3_THREADS) {
-      const int blk = e / wd, r = e - blk * wd, i = blk >> 1;
-      double sz;
-      if ((blk & 1) == 0)
-        sz = (i + 1 == mx - 1) ? c[i] * rWE[r] : c[i] * rWI[r] + c[i + 1] * rEI[r];
-      else
-        sz = (i == 0) ? c[i] * rEW[r] : c[i - 1] * rWI[wd + r] + c[i] * rEI[wd + r];
-      ws[e] = ts[e] - (c[i] + sz);
-    }
-    __syncthreads();
-  }
   const int stride = G.m + 2;
   double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
-  cta_dots_long(V + s * G.vstride, G.k, ncols, ws, r0, r1, part, red);
+  if (tdefl) {
+    // w = t - Z c - (S - I) Z c computed row by row inside the first column
+    // group's dots (the thread's own rows: no barrier, no re-read of w)
+    const int wd = P.w, w2 = 2 * wd;
+    const double* rs = P.rowsum + static_cast<long long>(s) * 6 * wd;
+    XDeflate xd{cbuf + static_cast<long long>(s) * P.d, rs, rs + w2, rs + 2 * w2, rs + 2 * w2 + wd,
+                tdefl + s * G.k, ws, wd, P.mx};
+    cta_dots_long(V + s * G.vstride, G.k, ncols, ws, r0, r1, part, red, xd);
+  } else {
+    cta_dots_long(V + s * G.vstride, G.k, ncols, ws, r0, r1, part, red);
+  }
   if (last_cta(G.counter + s, G.nchunk))
     reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols,
                  G.h1 + static_cast<long long>(s) * stride);
@@ -265,7 +309,7 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_update_kernel(GmState_ G, con
 // pass 2': w -= V h1; h2 = V^T w and ||w||^2 in one reduction; the last CTA takes
 // ||w - V h2||^2 = ||w||^2 - ||h2||^2 (h2 is the O(eps) reorthogonalisation
 // correction, so the difference is accurate) and runs the Givens step
-__global__ void __launch_bounds__(V3_THREADS) cgs3_pass2n_kernel(GmState_ G, const double* __restrict__ V, double* w,
+__global__ void __launch_bounds__(V3_THREADS, CGS3_MINB) cgs3_pass2n_kernel(GmState_ G, const double* __restrict__ V, double* w,
                                                                  int fuse) {
   pdl_wait();
   pdl_launch();
@@ -364,16 +408,15 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_pass3s_kernel(GmState_ G, dou
   const int r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
   double* Vs = V + s * G.vstride;
   double* ws = w + s * G.k;
-  rows_update_long(Vs, G.k, ncols, hs, ws, r0, r1);
-  __syncthreads();
   const double inv = 1.0 / G.nrm[s];
   double* col = Vs + static_cast<long long>(jn) * G.k;
   double* vs = vin + s * G.k;
-  for (int r = r0 + threadIdx.x; r < r1; r += V3_THREADS) {
-    const double v = ws[r] * inv;
-    col[r] = v;
-    vs[r] = v;
-  }
+  if (ncols <= 2)
+    rows_update_nr<8, 2, true>(Vs, G.k, ncols, hs, ws, r0, r1, inv, col, vs);
+  else if (ncols <= 4)
+    rows_update_nr<4, 4, true>(Vs, G.k, ncols, hs, ws, r0, r1, inv, col, vs);
+  else
+    rows_update_nr<2, V3_GRP, true>(Vs, G.k, ncols, hs, ws, r0, r1, inv, col, vs);
 }
 
 }  // namespace smpm
