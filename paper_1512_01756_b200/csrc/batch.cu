@@ -1399,7 +1399,7 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
         CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[0], cgs3_dot_kernel, V3_THREADS, 0));
         CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[1], cgs3_pass2n_kernel, V3_THREADS, 0));
         CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[2], cgs3_pass3s_kernel, V3_THREADS, 0));
-        for (int i = 0; i < 3; ++i) b->cgs3_kres[i] = std::max(1, std::min(o[i], 3)) * b->ctx->num_sms;
+        for (int i = 0; i < 3; ++i) b->cgs3_kres[i] = std::max(1, o[i]) * b->ctx->num_sms;
       }
       auto chunked = [&](long long res, dim3& g) {
         GmState_ Gk = G;
