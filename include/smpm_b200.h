@@ -159,7 +159,8 @@ int smpm_apply_Zt(smpm_batch* b, const double* v, double* y_d, void* stream);   
 int smpm_coarse_solve(smpm_batch* b, const double* b_d, double* x_d, void* stream);        /* proj/src/deflation.cpp:71-92 */
 int smpm_apply_P(smpm_batch* b, const double* v, double* y, int fused, void* stream);      /* proj/src/deflation.cpp:94-96 */
 int smpm_apply_Q(smpm_batch* b, const double* v, double* y, void* stream);                 /* proj/src/deflation.cpp:98-100 */
-/* out = v - dir (dir . v) per system; dir is nsys x len (proj/src/nullspace.cpp:92) */
+/* out = v - dir (dir . v) per system; v, dir, out are nsys x len, any len >= 1:
+ * u_S on b_S (len = k) or u_L on f (len = r) (proj/src/nullspace.cpp:92). */
 int smpm_project_out(smpm_batch* b, long long len, const double* v, const double* dir, double* out, void* stream);
 
 /* ---- strip solves either side of the path --------------
@@ -226,13 +227,25 @@ int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x
 long long smpm_batch_launch_count(const smpm_batch* b);
 
 /* Optional device timing of kernel classes (0 Schur GEMM, 1 block-Jacobi
- * GEMMs, 2 deflation, 3 Arnoldi orthogonalization, 4 other, 5 cluster-persistent
- * Arnoldi, 6 grid-persistent tail, 7 spectral per-mode pass, 8 shared-matrix
+ * GEMMs, 2 deflation, 3 Arnoldi orthogonalization, 4 other, 5 reserved,
+ * 6 grid-persistent tail, 7 spectral per-mode pass, 8 shared-matrix
  * transforms, 9 reserved; nclass <= 10), measured with
  * CUDA events on the launching stream during solves/operators. Reads the
  * accumulated milliseconds/launch counts (nullable), then, if enable >= 0,
  * resets them and turns timing on (1) or off (0). */
 int smpm_batch_profile(smpm_batch* b, int enable, double* ms, long long* counts, int nclass);
+
+/* Performance knobs of a batch (no reference counterpart; defaults are the
+ * measured-best settings). Keys: segb, xform, sp_stage, spectral, spec_2las,
+ * p2fuse, gt_vblock, grid_per_sm, gt_ctas, grid_nocoop (profilers only: the
+ * tail then launches without the co-residency guarantee of a cooperative
+ * launch), pdl, pythag, grid, grid_max, post_fuse, early; with b = NULL:
+ * fy_tile (transverse FFT). SMPM_EINVAL for an unknown key. The library reads
+ * no environment variables. */
+int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value);
+/* Phase-trace dump of the grid-persistent tail into `path` (appended; NULL or
+ * "" off): which = 0 per-step phase timestamps, 1 per-CTA timestamps. */
+int smpm_batch_set_trace(smpm_batch* b, int which, const char* path);
 
 /* Measured fp64 throughput of the device (TFLOP/s): FP64 FMA pipe and the
  * legacy fp64 tensor-core mma.sync (no tcgen05 f64 kind exists). Roofline

@@ -26,7 +26,6 @@
 #include "vec.cuh"
 #include "vec2.cuh"
 #include "vec3.cuh"
-#include "cluster.cuh"
 #include "grid.cuh"
 #include "spectral.cuh"
 #include "xform.cuh"
@@ -239,8 +238,32 @@ struct smpm_ctx {
   cublasHandle_t blas = nullptr;  // plain library GEMMs of the strip solver when the transform kernel does not apply
 };
 
+// Performance knobs and diagnostics of one batch (smpm_batch_set_tuning). The
+// defaults are the measured-best settings; nothing here changes results except
+// the switches documented as evaluation-order changes (pythag, p2fuse).
+struct Tuning {
+  int segb = 0;          // per-mode pass: blocks per warp item (0: SP_SEGB)
+  int xform = 1;         // resident-slice transform kernel (xform.cuh) where it applies
+  int sp_stage = 1;      // per-mode pass stages slot rows in shared memory
+  int spectral = 1;      // spectral operator when its factors are set
+  int spec_2las = 1;     // spectral operator for 2LAS
+  int p2fuse = 1;        // CGS2 pass 2 single-read fusion
+  int gt_vblock = 2;     // grid tail V-row block: 0 off, 1 ring size, 2 as large as 2 CTAs/SM allow
+  int grid_per_sm = 2;   // grid tail CTAs per SM (cap)
+  int gt_ctas = 0;       // grid tail CTA cap (0: none)
+  int grid_nocoop = 0;   // opt-in: plain (non-cooperative) cluster launch of the tail, for profilers only
+  int pdl = 1;           // programmatic dependent launch of the step chain
+  int pythag = 1;        // norm from the second CGS2 reduction
+  int grid = 1;          // grid-persistent tail
+  int grid_max = 8;      // live systems at which the tail takes over
+  int post_fuse = 1;     // one-pass dbj epilogue
+  int early = 1;         // early epilogue + x_S copy during the tail (solve_host)
+  std::string gt_trace, gt_trace2;  // phase-trace dump files of the grid tail
+};
+
 struct smpm_batch {
   smpm_ctx* ctx = nullptr;
+  Tuning tune;
   int n = 0, mx = 0, mz = 0, nsys = 0, w = 0, d = 0;
   long long k = 0;
   int nbf = 0;       // block-Jacobi blocks covering two interfaces
@@ -276,14 +299,11 @@ struct smpm_batch {
   int xf_P = 0, xf_MB = 0;
   long long cgs3_res = 0;  // resident CTAs of the CGS2 pass kernels (device)
   long long cgs3_kres[3] = {0, 0, 0};  // per kernel: pass 1, pass 2', pass 3' (norm-from-h2 path)
-  bool pythag = true;  // norm from the second CGS2 reduction (cgs3_pass2n / cgs3_pass3s); SMPM_NO_PYTHAG=1: off
-  bool pdl = true;  // programmatic dependent launch for the Arnoldi step chain (SMPM_NO_PDL=1: off)  // resident-slice transform kernel (xform.cuh); 0: use pF/pB
+  bool pythag = true;  // norm from the second CGS2 reduction (cgs3_pass2n / cgs3_pass3s); tuning pythag
+  bool pdl = true;  // programmatic dependent launch for the Arnoldi step chain (tuning pdl)
   size_t xf_smem = 0;
   Plan pc[6];          // unsplit per-system templates (BJ1, BJ2, BJ3, S; spectral F, B) for the persistent solvers
-  bool cluster_ok = false;
-  DevArray<double> dclpart, dclzsum;
-  DevArray<int> dclq;  // [queue, publish[kMaxClusters]]
-  int cl_size = 8, cl_max = 0;
+  bool tmpl_ok = false;  // unsplit per-system templates of the hot stages exist (grid tail)
   DevArray<double> dws;  // split-K workspace
   // grid-persistent tail solver (grid.cuh)
   bool grid_ok = false;
@@ -291,7 +311,6 @@ struct smpm_batch {
   bool sp_smem_set = false;
   size_t gt_smem = 0;  // tail dynamic shared memory (tile ring / V-row block region + vectors)
   int gt_vcap = 0;     // doubles of the ring / V-row block region
-  bool gt_nocoop = false;  // cooperative + cluster launch rejected: plain cluster launch
   DevArray<unsigned> dgbar;   // grid barrier counter
   DevArray<double> dgtpart, dgtzsum, dgtzp, dgtcg;
 
@@ -451,7 +470,6 @@ Live all_systems(const smpm_batch* b) {
 }
 
 constexpr int kTailSystems = 8;
-constexpr int kMaxClusters = 512;
 
 void run_plan(smpm_batch* b, Plan& p0, const double* in, double* out, double* tmp, const Live& lv, cudaStream_t st) {
   Plan& p = (p0.v2 && p0.tail && lv.nslots <= kTailSystems && lv.alist) ? *p0.tail : p0;
@@ -684,14 +702,14 @@ void build_plans(smpm_batch* b) {
     p->build2(std::max(1, sms / b->nsys), st);
   }
   b->pSt.build(sms, st);
-  // cluster solver: unsplit copies of the four hot templates
-  b->cluster_ok = true;
+  // grid tail solver: unsplit copies of the hot stage templates
+  b->tmpl_ok = true;
   Plan* src[6] = {&b->pBJ1, &b->pBJ2, &b->pBJ3, &b->pS, &b->pF, &b->pB};
   for (int i = 0; i < 6; ++i) {
     if (i >= 4 && !b->spectral) break;
     if (!src[i]->v2) {
       if (i < 4) {
-        b->cluster_ok = false;
+        b->tmpl_ok = false;
         break;
       }
       continue;
@@ -716,7 +734,7 @@ void build_plans(smpm_batch* b) {
   }
   b->dws.alloc(static_cast<size_t>(std::max(1LL, wst)) * GEMM_BM * GEMM_BN);
   // grid tail solver: the unsplit templates of the four hot stages (pc)
-  b->grid_ok = b->cluster_ok;
+  b->grid_ok = b->tmpl_ok;
   b->dgbar.alloc(1);
 }
 
@@ -1012,7 +1030,6 @@ void finalize(smpm_batch* b) {
   CUDA_CHECK(cudaMemsetAsync(b->dcount.p, 0, sizeof(int) * (b->nsys + 1), st));
   b->dsel.alloc(static_cast<size_t>(b->nsys));
   b->dalist.alloc(2 * static_cast<size_t>(b->nsys) + 2);
-  b->dclq.alloc(1 + kMaxClusters);
   b->dcnt.alloc(4);
   CUDA_CHECK(cudaHostAlloc(&b->hcnt, 4 * sizeof(int), cudaHostAllocMapped));
   CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&b->hcnt_dev), b->hcnt, 0));
@@ -1033,23 +1050,26 @@ void need_final(smpm_batch* b) {
 struct Chunking {
   int chunk, nchunk;
 };
-Chunking chunking(const smpm_batch* b) {
+Chunking chunking(const smpm_batch* b, long long len = -1) {
+  if (len < 0) len = b->k;
   const long long target_ctas = 4LL * b->ctx->num_sms;
   long long per_sys = std::max(1LL, target_ctas / b->nsys);
-  long long chunk = (b->k + per_sys - 1) / per_sys;
+  long long chunk = (len + per_sys - 1) / per_sys;
   chunk = std::max(128LL, std::min(2048LL, (chunk + 31) / 32 * 32));
   Chunking c;
   c.chunk = static_cast<int>(chunk);
-  c.nchunk = static_cast<int>((b->k + chunk - 1) / chunk);
+  c.nchunk = static_cast<int>(std::max(1LL, (len + chunk - 1) / chunk));
   return c;
 }
 
 // out[s] = x_s . y_s  (device)
-void batched_dot(smpm_batch* b, const double* x, const double* y, double* out, const int* act, cudaStream_t st) {
-  const Chunking c = chunking(b);
+void batched_dot(smpm_batch* b, const double* x, const double* y, double* out, const int* act, cudaStream_t st,
+                 long long len = -1) {
+  if (len < 0) len = b->k;
+  const Chunking c = chunking(b, len);
   b->dpart.alloc(std::max<size_t>(b->dpart.n, static_cast<size_t>(b->nsys) * c.nchunk));
   dim3 grid(c.nchunk, b->nsys);
-  batched_dot_kernel<<<grid, VEC_THREADS, 0, st>>>(b->nsys, b->k, c.chunk, c.nchunk, act, x, y, b->dpart.p, b->dcount.p,
+  batched_dot_kernel<<<grid, VEC_THREADS, 0, st>>>(b->nsys, len, c.chunk, c.nchunk, act, x, y, b->dpart.p, b->dcount.p,
                                                    out);
   check_launch(b);
 }
@@ -1147,7 +1167,7 @@ SpecParams spec_params(const smpm_batch* b) {
   sp.cadd = nullptr;
   sp.nmc = (b->sp_nmode + SP_MODES - 1) / SP_MODES;
   sp.segb = SP_SEGB;
-  if (const char* e = std::getenv("SMPM_SEGB")) sp.segb = std::max(1, std::min(SP_SEGB, std::atoi(e)));
+  if (b->tune.segb > 0) sp.segb = std::max(1, std::min(SP_SEGB, b->tune.segb));
   sp.nseg = (b->nbf + (b->single ? 1 : 0) + sp.segb - 1) / sp.segb;
   return sp;
 }
@@ -1175,7 +1195,7 @@ bool xform_try(smpm_batch* b, int P) {
 
 void setup_xform(smpm_batch* b) {
   b->xf_P = 0;
-  if (b->w % 16 != 0 || std::getenv("SMPM_NO_XFORM")) return;
+  if (b->w % 16 != 0 || !b->tune.xform) return;
   for (int P = 1; P <= 4; ++P) {
     const int need = (b->w / 8 + P - 1) / P;
     if (need <= 4 ? xform_try<4>(b, P) : need <= 8 ? xform_try<8>(b, P) : need <= 11 ? xform_try<11>(b, P) : false)
@@ -1230,8 +1250,8 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
   P.alist = lv.alist;
   P.acount = lv.acount;
   const dim3 grid(sp.nmc * ((sp.nseg + SP_WARPS - 1) / SP_WARPS), lv.nslots);
-  // staged slot rows (SMPM_SP_NO_STAGE=1: direct loads)
-  sp.stage = sp.segb <= SP_SEGB && std::getenv("SMPM_SP_NO_STAGE") == nullptr ? 1 : 0;
+  // staged slot rows (tuning sp_stage = 0: direct loads)
+  sp.stage = sp.segb <= SP_SEGB && b->tune.sp_stage ? 1 : 0;
   const size_t shm = (cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0) +
                      (sp.stage ? sizeof(double) * SP_STAGE_DOUBLES : 0);
   if (sp.stage && !b->sp_smem_set) {
@@ -1254,7 +1274,7 @@ void spec_Minv(smpm_batch* b, const double* v, double* u, double* su, const Live
   run_xform(b, false, b->dvh2.p, u, lv, st, su ? b->dth.p : nullptr, su);
 }
 
-bool spec_on(const smpm_batch* b) { return b->spectral && std::getenv("SMPM_NO_SPECTRAL") == nullptr; }
+bool spec_on(const smpm_batch* b) { return b->spectral && b->tune.spectral; }
 
 bool spec_ok(const smpm_batch* b, const SolveCfg& c) {
   return spec_on(b) && (c.method == SMPM_SCHUR || c.method == SMPM_BJ || c.method == SMPM_DBJ);
@@ -1264,7 +1284,7 @@ bool spec_ok(const smpm_batch* b, const SolveCfg& c) {
 // add two grid barriers per step; measured: per-stage spectral 2LAS with one live
 // system is slower than the dense tail, 12.1 vs 10.2 ms on C3)
 bool spec_2las(const smpm_batch* b, const SolveCfg& c) {
-  return spec_on(b) && c.method == SMPM_2LAS && std::getenv("SMPM_NO_SPEC_2LAS") == nullptr;
+  return spec_on(b) && c.method == SMPM_2LAS && b->tune.spec_2las;
 }
 
 // S M^{-1} v (bj) or S v through the spectral form; out may be any buffer
@@ -1415,9 +1435,9 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
       const GmState_ G1 = chunked(b->cgs3_kres[0], g1), G2 = chunked(b->cgs3_kres[1], g2),
                      G3 = chunked(b->cgs3_kres[2], g3);
       launch_pdl(b, cgs3_dot_kernel, g1, dim3(V3_THREADS), 0, st, G1, V, wv, tdefl, P, cbuf);
-      // ncols <= 16: update and dots in one read of V (SMPM_NO_P2FUSE=1: two reads)
+      // ncols <= 16: update and dots in one read of V (tuning p2fuse = 0: two reads)
       launch_pdl(b, cgs3_pass2n_kernel, g2, dim3(V3_THREADS), 0, st, G2, static_cast<const double*>(V), wv,
-                 std::getenv("SMPM_NO_P2FUSE") ? 0 : 1);
+                 b->tune.p2fuse ? 1 : 0);
       launch_pdl(b, cgs3_pass3s_kernel, g3, dim3(V3_THREADS), 0, st, G3, V, wv, vin);
       return;
     }
@@ -1494,85 +1514,6 @@ __global__ void select_state_kernel(const int* state, int nsys, int want, int* s
   if (s < nsys) sel[s] = state[s] == want ? 1 : 0;
 }
 
-// Runs the live systems' Arnoldi steps until each stops, in one
-// cluster-persistent launch (cluster.cuh).
-void arnoldi_cluster(smpm_batch* b, const SolveCfg& c, const int* alist, const int* acount, int nlive,
-                     cudaStream_t st) {
-  ProfScope ps(b, 5, st);  // class 5: cluster-persistent Arnoldi
-  GmState_& G = b->G;
-  const size_t smem = G2_SMEM + sizeof(double) * (256 + 2 * static_cast<size_t>(b->d));
-  if (const char* e = std::getenv("SMPM_CLUSTER")) b->cl_size = std::max(1, std::min(16, std::atoi(e)));
-  const int csz = b->cl_size;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = csz;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cfg.blockDim = dim3(G2_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  if (b->cl_max == 0) {
-    CUDA_CHECK(cudaFuncSetAttribute(arnoldi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    if (csz > 8)
-      CUDA_CHECK(cudaFuncSetAttribute(arnoldi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cfg.gridDim = dim3(csz * 64);
-    int n = 0;
-    CUDA_CHECK(cudaOccupancyMaxActiveClusters(&n, arnoldi_cluster_kernel, &cfg));
-    b->cl_max = std::max(1, std::min(n, kMaxClusters));
-  }
-  const int ncl = std::max(1, std::min(nlive, b->cl_max));
-  const size_t stride = static_cast<size_t>(G.m + 2);
-  b->dclpart.alloc(std::max(b->dclpart.n, static_cast<size_t>(kMaxClusters) * csz * stride));
-  b->dclzsum.alloc(std::max(b->dclzsum.n, static_cast<size_t>(kMaxClusters) * b->d));
-  ClusterArgs A{};
-  for (int i = 0; i < 4; ++i) {
-    A.jobs[i] = b->pc[i].djobs.p;
-    A.tiles[i] = b->pc[i].dtiles2.p;
-    A.ntiles[i] = b->pc[i].ntiles;
-  }
-  A.a_stride = b->mstride;
-  A.vin = b->vbuf[2].p;
-  A.w = b->vbuf[3].p;
-  A.u = b->vbuf[4].p;
-  A.t = b->vbuf[5].p;
-  A.tmp = b->vbuf[9].p;
-  A.V = b->dV.p;
-  A.part = b->dclpart.p;
-  A.zsum = b->dclzsum.p;
-  A.queue = b->dclq.p;
-  A.publish = b->dclq.p + 1;
-  A.alist = alist;
-  A.acount = acount;
-  A.method = c.method;
-  A.G = G;
-  A.P = deflate_params(b, nullptr);
-  CUDA_CHECK(cudaMemsetAsync(b->dclq.p, 0, sizeof(int), st));
-  cfg.gridDim = dim3(csz * ncl);
-  // debug: SMPM_CL_TRACE=<path> dumps per-phase timestamps of every cluster's first 64 steps
-  const char* tpath = std::getenv("SMPM_CL_TRACE");
-  DevArray<unsigned long long> dtr;
-  if (tpath) {
-    dtr.alloc(static_cast<size_t>(ncl) * 64 * 12);
-    CUDA_CHECK(cudaMemsetAsync(dtr.p, 0, dtr.n * sizeof(unsigned long long), st));
-    A.trace = dtr.p;
-  }
-  CUDA_CHECK(cudaLaunchKernelEx(&cfg, arnoldi_cluster_kernel, A));
-  check_launch(b);
-  if (tpath) {
-    std::vector<unsigned long long> h(dtr.n);
-    CUDA_CHECK(cudaMemcpyAsync(h.data(), dtr.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    if (FILE* f = std::fopen(tpath, "ab")) {
-      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
-      std::fclose(f);
-    }
-  }
-}
-
 // Runs the remaining Arnoldi steps of the current cycle of the (few) live
 // systems in one cooperative, grid-persistent launch (grid.cuh).
 // grid of the tail solver: as many CTAs (multiple of the cluster size) as
@@ -1584,7 +1525,7 @@ int grid_blocks(smpm_batch* b) {
   const size_t rest = sizeof(double) * (3 * GT_MAXCOL + 2 * static_cast<size_t>(b->d));
   size_t region = GT_SMEM;
   int vmode = 2;  // 0: no V-row block, 1: within the ring region, 2: as large as 2 CTAs / SM allow (measured best)
-  if (const char* e = std::getenv("SMPM_GT_VBLOCK")) vmode = std::atoi(e);
+  vmode = b->tune.gt_vblock;
   if (vmode >= 2) {
     cudaFuncAttributes fa{};
     CUDA_CHECK(cudaFuncGetAttributes(&fa, arnoldi_grid_kernel));
@@ -1614,7 +1555,7 @@ int grid_blocks(smpm_batch* b) {
   int per = 0;
   CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, arnoldi_grid_kernel, G2_THREADS, smem));
   int cap = 2;
-  if (const char* e = std::getenv("SMPM_GRID_PER_SM")) cap = std::max(1, std::atoi(e));
+  cap = std::max(1, b->tune.grid_per_sm);
   const int want = b->ctx->num_sms * std::max(1, std::min(per, cap));
   // every CTA must be resident: bound by the cluster occupancy calculator
   cfg.gridDim = dim3(want / GT_CL * GT_CL);
@@ -1622,12 +1563,13 @@ int grid_blocks(smpm_batch* b) {
   CUDA_CHECK(cudaOccupancyMaxActiveClusters(&ncl, arnoldi_grid_kernel, &cfg));
   if (ncl < 1) fail(SMPM_ECUDA, "grid tail kernel cannot be resident");
   b->gt_blocks = std::min(want / GT_CL, ncl) * GT_CL;
-  if (const char* e = std::getenv("SMPM_GT_CTAS"))  // experiment: cap the tail grid (multiple of the cluster size)
-    b->gt_blocks = std::max(GT_CL, std::min(b->gt_blocks, std::atoi(e) / GT_CL * GT_CL));
+  if (b->tune.gt_ctas > 0)  // experiment: cap the tail grid (multiple of the cluster size)
+    b->gt_blocks = std::max(GT_CL, std::min(b->gt_blocks, b->tune.gt_ctas / GT_CL * GT_CL));
   return b->gt_blocks;
 }
 
-void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int* acount, cudaStream_t st) {
+// Returns false (nothing launched) when the cooperative launch is rejected.
+bool arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int* acount, cudaStream_t st) {
   ProfScope ps(b, 6, st);  // class 6: grid-persistent tail
   GmState_& G = b->G;
   grid_blocks(b);
@@ -1692,14 +1634,14 @@ void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
   A.vcap = b->gt_vcap;
   A.G = G;
   A.P = deflate_params(b, nullptr);
-  const char* tpath = std::getenv("SMPM_GT_TRACE");
+  const char* tpath = b->tune.gt_trace.empty() ? nullptr : b->tune.gt_trace.c_str();
   DevArray<unsigned long long> dtr;
   if (tpath) {
     dtr.alloc(64 * 16);
     CUDA_CHECK(cudaMemsetAsync(dtr.p, 0, dtr.n * sizeof(unsigned long long), st));
     A.trace = dtr.p;
   }
-  const char* t2path = std::getenv("SMPM_GT_TRACE2");
+  const char* t2path = b->tune.gt_trace2.empty() ? nullptr : b->tune.gt_trace2.c_str();
   DevArray<unsigned long long> dtr2;
   if (t2path) {
     dtr2.alloc(static_cast<size_t>(16) * nb * 8);
@@ -1708,16 +1650,15 @@ void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
   }
   CUDA_CHECK(cudaMemsetAsync(b->dgbar.p, 0, sizeof(unsigned), st));
   cfg.gridDim = dim3(nb);
-  if (std::getenv("SMPM_GRID_NOCOOP")) b->gt_nocoop = true;  // plain cluster launch (e.g. under a profiler)
-  cfg.numAttrs = b->gt_nocoop ? 1 : 2;
+  // opt-in plain cluster launch (profilers only: co-residency is then not guaranteed)
+  cfg.numAttrs = b->tune.grid_nocoop ? 1 : 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, arnoldi_grid_kernel, A);
-  if (e != cudaSuccess && !b->gt_nocoop) {
-    // cooperative cluster launch rejected: the grid is already bounded by
-    // the cluster occupancy of an otherwise idle stream, launch it plainly
+  if (e != cudaSuccess && !b->tune.grid_nocoop) {
+    // cooperative cluster launch rejected (e.g. MPS, or co-residency not
+    // guaranteed): the software grid barrier needs every CTA resident, so the
+    // caller runs the rest of the cycle with the per-step kernels instead
     (void)cudaGetLastError();
-    b->gt_nocoop = true;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, arnoldi_grid_kernel, A);
+    return false;
   }
   CUDA_CHECK(e);
   check_launch(b);
@@ -1741,6 +1682,7 @@ void arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
       std::fclose(f);
     }
   }
+  return true;
 }
 
 void stack_sum(smpm_batch* b, double* v, cudaStream_t st) {
@@ -1752,8 +1694,8 @@ void stack_sum(smpm_batch* b, double* v, cudaStream_t st) {
 void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_report* reps, double* history,
            cudaStream_t st, double* xS_host = nullptr) {
   need_final(b);
-  b->pdl = std::getenv("SMPM_NO_PDL") == nullptr;
-  b->pythag = std::getenv("SMPM_NO_PYTHAG") == nullptr;
+  b->pdl = b->tune.pdl != 0;
+  b->pythag = b->tune.pythag != 0;
   if (c.max_iter < 1) fail(SMPM_EINVAL, "max_iter must be >= 1");
   const int mtot = static_cast<int>(std::min<long long>(c.max_iter, b->k));
   int m = c.restart > 0 ? std::min(c.restart, mtot) : mtot;
@@ -1824,49 +1766,6 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   G.alist = alist;
   G.acount = acount;
 
-  const bool use_cluster = b->cluster_ok && !c.stacked && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= 128 &&
-                           (c.method != SMPM_DBJ || c.fused) && std::getenv("SMPM_CLUSTER") != nullptr;
-  if (use_cluster) {
-    // ---- cluster-persistent Arnoldi: one launch per GMRES cycle
-    int nlive = ns;
-    for (;;) {
-      arnoldi_cluster(b, c, alist, acount, nlive, st);
-      compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist2, acount2, b->dcnt.p);
-      check_launch(b);
-      CUDA_CHECK(cudaMemcpyAsync(hcnt, b->dcnt.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-      CUDA_CHECK(cudaStreamSynchronize(st));
-      const int ncyc = hcnt[1];
-      if (ncyc == 0) break;
-      // ---- restart (GMRES(m) extension): x += V y ; r = b - op(x) ; new cycle
-      select_state_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, GM_CYCLE, dsel);
-      check_launch(b);
-      compact_kernel<<<1, 1024, 0, st>>>(dsel, nullptr, ns, alist2, acount2, nullptr);
-      check_launch(b);
-      Live lr;
-      lr.alist = alist2;
-      lr.acount = acount2;
-      lr.nslots = ncyc;
-      lr.active = dsel;
-      gm_backsolve_kernel<<<ns, 32, 0, st>>>(G, dsel);
-      check_launch(b);
-      gm_combine_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, x, dsel, 1);
-      check_launch(b);
-      apply_op(b, c, x, r, lr, st);
-      ++op_applies;
-      axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, dsel, nullptr, 1.0, rhs, -1.0, r);
-      check_launch(b);
-      batched_dot(b, r, r, nr2, dsel, st);
-    if (c.stacked) stack_sum(b, nr2, st);
-      if (c.stacked) stack_sum(b, nr2, st);
-      gm_start_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G, nr2, nb2, c.tol, 0, G.state);
-      check_launch(b);
-      gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, r, vin);
-      check_launch(b);
-      compact_kernel<<<1, 1024, 0, st>>>(G.active, nullptr, ns, alist, acount, nullptr);
-      check_launch(b);
-      nlive = ncyc;
-    }
-  }
   int steps = 0;
   // ---- Arnoldi steps; device flags are polled one step behind the launches
   // (step i+1 is queued before the host waits on step i's counters). Grids
@@ -1888,12 +1787,14 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     CUDA_CHECK(cudaEventRecord(ev[slot], st));
   };
   // few live systems: the rest of the cycle runs grid-persistent (grid.cuh)
-  const bool use_grid = b->grid_ok && !c.stacked && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= GT_MAXCOL &&
-                        (c.method != SMPM_DBJ || c.fused) && std::getenv("SMPM_NO_GRID") == nullptr;
-  int grid_max = 8;  // measured on C4 with the PDL step chain: 8-10 live systems is the crossover
-  if (const char* e = std::getenv("SMPM_GRID_MAX")) grid_max = std::max(0, std::min(GT_MAXSYS, std::atoi(e)));
+  bool use_grid = b->grid_ok && !c.stacked && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= GT_MAXCOL &&
+                        (c.method != SMPM_DBJ || c.fused) && b->tune.grid;
+  // measured on C4 with the PDL step chain: 8-10 live systems is the crossover
+  int grid_max = std::max(0, std::min(GT_MAXSYS, b->tune.grid_max));
   if (use_grid) grid_max = std::min(grid_max, grid_blocks(b) / GT_CL);  // one cluster per live system at least
+  int cycles = 0;  // restarts issued: each cycle end may cost one speculative (empty) step
   auto restart = [&](int ncycv) {
+    ++cycles;
     // ---- restart (GMRES(m) extension): x += V y ; r = b - op(x) ; new cycle
     select_state_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, GM_CYCLE, dsel);
     check_launch(b);
@@ -1913,6 +1814,9 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, dsel, nullptr, 1.0, rhs, -1.0, r);
     check_launch(b);
     batched_dot(b, r, r, nr2, dsel, st);
+    // stacked: the new cycle starts from the norm of the stacked residual
+    // (proj/src/helmholtz.cpp:193-201), as the first cycle does
+    if (c.stacked) stack_sum(b, nr2, st);
     gm_start_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G, nr2, nb2, c.tol, 0, G.state);
     check_launch(b);
     gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, r, vin);
@@ -1928,7 +1832,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   double* u = b->vbuf[4].p;
   double* tq = b->vbuf[5].p;
   const bool fuse_post = spec_ok(b, c) && ((c.method == SMPM_DBJ && c.fused) || c.method == SMPM_BJ);
-  const bool post_one_pass = fuse_post && c.method == SMPM_DBJ && std::getenv("SMPM_NO_POST_FUSE") == nullptr;
+  const bool post_one_pass = fuse_post && c.method == SMPM_DBJ && b->tune.post_fuse;
   auto epilogue_dbj = [&](const Live& lv, const int* sel, cudaStream_t s2) {
     launch_pdl(b, gm_backsolve_kernel, dim3(ns), dim3(32), 0, s2, G, sel);
     launch_pdl(b, gm_combine_kernel, vg, dim3(256), 0, s2, G, static_cast<const double*>(b->dV.p), x, sel, 1);
@@ -1949,8 +1853,8 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   // finished before it (same total work), so that their rows of x_S can travel to
   // the host (solve_host) on a side stream while the tail runs. Running the epilogue
   // itself beside the tail was measured slower: its kernels compete with the
-  // latency-bound tail for the SMs. SMPM_NO_EARLY=1: off.
-  const bool early_ok = post_one_pass && xS_host && std::getenv("SMPM_NO_EARLY") == nullptr;
+  // latency-bound tail for the SMs. Tuning early = 0: off.
+  const bool early_ok = post_one_pass && xS_host && b->tune.early;
   bool early_done = false;
   int* eflag = b->dearly.p;
   int* elist = eflag + ns;
@@ -1984,17 +1888,22 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       CUDA_CHECK(cudaEventRecord(b->eev[2], b->st2));
       early_done = true;
     }
-    arnoldi_grid(b, c, alist, acount, st);
+    return arnoldi_grid(b, c, alist, acount, st);
   };
   int cur = 0;
-  if (!use_cluster) issue(cur);
-  for (; !use_cluster;) {
+  issue(cur);
+  for (;;) {
     // invariant here: exactly one step is in flight, in slot `cur`
     if (use_grid && bound <= grid_max) {
       CUDA_CHECK(cudaEventSynchronize(ev[cur]));
       int nrun = hcnt[2 * cur], ncyc = hcnt[2 * cur + 1];
       if (nrun > 0) {
-        launch_tail(nrun);
+        if (!launch_tail(nrun)) {
+          // no cooperative launch: the per-step kernels finish the solve
+          use_grid = false;
+          issue(cur);
+          continue;
+        }
         ++steps;
         compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->hcnt_dev + 2 * cur);
         check_launch(b);
@@ -2011,7 +1920,10 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       }
       break;
     }
-    const bool more = steps < mtot + 1;
+    // the device caps every system at max_iter (GM_MAXED); the host bound is a
+    // safety limit only: max_iter steps, one speculative step per cycle end
+    const int step_limit = mtot + cycles + 2;
+    const bool more = steps < step_limit;
     if (more) issue(cur ^ 1);
     CUDA_CHECK(cudaEventSynchronize(ev[cur]));
     const int nrun = hcnt[2 * cur], ncyc = hcnt[2 * cur + 1];
@@ -2021,7 +1933,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     if (more) CUDA_CHECK(cudaEventSynchronize(ev[cur]));  // drain the speculative step
     const int nrun2 = more ? hcnt[2 * cur] : nrun;
     const int ncyc2 = more ? hcnt[2 * cur + 1] : ncyc;
-    if (nrun2 > 0 && steps < mtot + 1) {
+    if (nrun2 > 0 && steps < step_limit) {
       bound = std::min(bound, nrun2);
       issue(cur);
       continue;
@@ -2329,6 +2241,8 @@ void need_strip(smpm_batch* b) {
 
 // ---- transverse Fourier transforms (fourier.cuh) ----------------------------
 // twiddle tables exp(sign 2 pi i k / m), k < m / 2, per (device, m, sign), kept for the process
+int g_fy_tile = 0;  // transverse FFT rows per CTA override (smpm_batch_set_tuning(NULL, "fy_tile", v))
+
 const double2* fy_twiddles(int m, int sign) {
   static std::vector<std::pair<long long, double*>> cache;
   static std::mutex mu;
@@ -2361,7 +2275,7 @@ void fourier_launch(long long r, int m_y, const double* in, double* out, int sig
   // nodes per CTA: 16 (128-byte coalesced runs per plane) while the padded complex
   // tile stays <= 66 KB (3 CTAs per SM), fewer for long transforms
   a.tile = std::max(1, std::min(16, 4224 / (m_y + 1)));
-  if (const char* e = std::getenv("SMPM_FY_TILE")) a.tile = std::max(1, std::min(64, std::atoi(e)));
+  if (g_fy_tile > 0) a.tile = std::max(1, std::min(64, g_fy_tile));
   a.tw = fy_twiddles(m_y, sign);
   const size_t smem = sizeof(double2) * static_cast<size_t>(a.tile) * (m_y + 1);
   const unsigned grid = static_cast<unsigned>((r + a.tile - 1) / a.tile);
@@ -2739,11 +2653,14 @@ int smpm_inverse_fourier_y(long long r, int m_y, const double* coeff, double* fi
 int smpm_project_out(smpm_batch* b, long long len, const double* v, const double* dir, double* out, void* stream) {
   return guard([&] {
     need_final(b);
-    if (len != b->k) fail(SMPM_EINVAL, "smpm_project_out: only interface-length vectors are supported");
+    // any per-system length: interface vectors (u_S on b_S, len = k) or node
+    // vectors (u_L on f, len = r; proj/src/solver.cpp:46, proj/src/helmholtz.cpp:159-160)
+    if (len < 1) fail(SMPM_EINVAL, "smpm_project_out: len must be >= 1");
+    if (!v || !dir || !out) fail(SMPM_EINVAL, "null vector");
     cudaStream_t st = b->st(stream);
     double* dots = b->dsmall.p;
-    batched_dot(b, dir, v, dots, nullptr, st);
-    project_kernel<<<grid_for(b->nsys * b->k), 256, 0, st>>>(b->nsys, b->k, dots, v, dir, out);
+    batched_dot(b, dir, v, dots, nullptr, st, len);
+    project_kernel<<<grid_for(b->nsys * len), 256, 0, st>>>(b->nsys, len, dots, v, dir, out);
     check_launch(b);
   });
 }
@@ -2800,6 +2717,53 @@ int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x
 }
 
 long long smpm_batch_launch_count(const smpm_batch* b) { return b ? b->launches : 0; }
+
+int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
+  return guard([&] {
+    if (!key) fail(SMPM_EINVAL, "null tuning key");
+    const std::string k(key);
+    if (!b) {
+      if (k == "fy_tile") {
+        g_fy_tile = static_cast<int>(value);
+        return;
+      }
+      fail(SMPM_EINVAL, "null batch");
+    }
+    Tuning& t = b->tune;
+    const int v = static_cast<int>(value);
+    struct Knob {
+      const char* name;
+      int* field;
+    };
+    const Knob knobs[] = {{"segb", &t.segb}, {"xform", &t.xform}, {"sp_stage", &t.sp_stage},
+                          {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse},
+                          {"gt_vblock", &t.gt_vblock}, {"grid_per_sm", &t.grid_per_sm}, {"gt_ctas", &t.gt_ctas},
+                          {"grid_nocoop", &t.grid_nocoop}, {"pdl", &t.pdl}, {"pythag", &t.pythag},
+                          {"grid", &t.grid}, {"grid_max", &t.grid_max}, {"post_fuse", &t.post_fuse},
+                          {"early", &t.early}};
+    for (const Knob& kb : knobs)
+      if (k == kb.name) {
+        *kb.field = v;
+        // grid geometry and transform plans depend on some knobs: recompute lazily
+        if (k == "gt_vblock" || k == "grid_per_sm" || k == "gt_ctas") b->gt_blocks = 0;
+        if (k == "xform" && b->finalized) setup_xform(b);
+        return;
+      }
+    fail(SMPM_EINVAL, "unknown tuning key '" + k + "'");
+  });
+}
+
+int smpm_batch_set_trace(smpm_batch* b, int which, const char* path) {
+  return guard([&] {
+    if (!b) fail(SMPM_EINVAL, "null batch");
+    if (which == 0)
+      b->tune.gt_trace = path ? path : "";
+    else if (which == 1)
+      b->tune.gt_trace2 = path ? path : "";
+    else
+      fail(SMPM_EINVAL, "trace: which must be 0 (per-step phases) or 1 (per-CTA)");
+  });
+}
 
 int smpm_batch_profile(smpm_batch* b, int enable, double* ms, long long* counts, int nclass) {
   return guard([&] {

@@ -157,7 +157,7 @@ class ProblemSet:
     u_L: np.ndarray | None
     b_S: np.ndarray  # (nsys, k); None until load_batch computes it on the device (device_rhs)
     fdm: StripFDM
-    f: object = None  # device_rhs: torch (nsys, r) forcing (mode 0 already projected with u_L)
+    f: object = None  # device_rhs: torch (nsys, r) forcing (mode 0 projected with u_L in load_batch)
 
 
 def build_problem(cfg: Config, modes=None, device=None, device_rhs=False) -> ProblemSet:
@@ -178,12 +178,8 @@ def build_problem(cfg: Config, modes=None, device=None, device_rhs=False) -> Pro
     if device_rhs:
         import torch
 
+        # the mode-0 u_L projection of f runs in load_batch (smpm_project_out)
         f = manufactured_batch(geo, cfg.kmax, cfg.decay, cfg.seed, modes, mus, device)
-        if u_L is not None:
-            uL = torch.tensor(u_L, device=device)
-            for i, mu in enumerate(mus):
-                if mu == 0.0:
-                    f[i] -= uL * torch.dot(uL, f[i])
         return ProblemSet(cfg, list(modes), mus, GW, GI, GE, u_S, u_L, None, F, f)
     bs = []
     for m, mu in zip(modes, mus):
@@ -219,7 +215,14 @@ def load_batch(ctx, ps: ProblemSet, spectral: bool = True):
         # (proj/src/helmholtz.cpp:159-176)
         import torch
 
-        bS = b.schur_rhs(ps.f)
+        f = ps.f
+        if ps.u_L is not None:
+            sing = torch.tensor([mu == 0.0 for mu in ps.mus], device=f.device)
+            uL = torch.tensor(ps.u_L, device=f.device)
+            dl = torch.where(sing[:, None], uL[None, :], torch.zeros_like(uL)[None, :]).contiguous()
+            f = b.project_out(f, dl)
+            ps.f = f
+        bS = b.schur_rhs(f)
         if ps.u_S is not None:
             sing = torch.tensor([mu == 0.0 for mu in ps.mus], device=bS.device)
             uS = torch.tensor(ps.u_S, device=bS.device)

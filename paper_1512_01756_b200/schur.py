@@ -79,6 +79,7 @@ class SchurBatch:
         check(lib().smpm_batch_dims(h, C.byref(k), C.byref(d), C.byref(w)))
         self.n, self.m_x, self.m_z, self.nsys = n, m_x, m_z, nsys
         self.k, self.d, self.w = k.value, d.value, w.value
+        self.spectral = False
         self._keep = []
 
     def close(self):
@@ -116,6 +117,7 @@ class SchurBatch:
             raise SmpmError(1, "gamma must be (nsys, 6, w - npairs)")
         gv = g.view(np.float64)
         check(lib().smpm_batch_set_spectral(self.h, int(npairs), _hptr(t), _hptr(ti), _hptr(gv)))
+        self.spectral = True
 
     def set_interface_blocks(self, sys: int, blocks):
         """blocks: list of (entries[rows x 2w], [(start, len), ...]) in the
@@ -233,11 +235,14 @@ class SchurBatch:
         return y
 
     def project_out(self, v, direction):  # proj/src/nullspace.cpp:92
+        """v - dir (dir . v) per system; any per-system length (k for u_S on b_S,
+        r for u_L on f).  A zero direction row leaves that system's row unchanged."""
         torch = _torch()
-        v = self._vec(v, self.k)
-        dr = self._vec(direction, self.k)
+        n = v.numel() // self.nsys if isinstance(v, torch.Tensor) else -1
+        v = self._vec(v, n)
+        dr = self._vec(direction, n)
         y = torch.empty_like(v)
-        check(lib().smpm_project_out(self.h, C.c_longlong(self.k), _dptr(v), _dptr(dr), _dptr(y), self._stream()))
+        check(lib().smpm_project_out(self.h, C.c_longlong(n), _dptr(v), _dptr(dr), _dptr(y), self._stream()))
         return y
 
     # ---- strip solves (SURVEY §8(f)-2) -------------------------------------
@@ -326,6 +331,32 @@ class SchurBatch:
         reps = (Report * self.nsys)()
         check(lib().smpm_solve_host(self.h, METHODS[method], _hptr(b), _hptr(x), C.byref(o), reps, None))
         return self._collect(x, reps, None, 0)
+
+    def tune(self, **knobs):
+        """Performance knobs (smpm_batch_set_tuning), e.g. tune(grid_max=4, pdl=0)."""
+        for k, v in knobs.items():
+            check(lib().smpm_batch_set_tuning(self.h, k.encode(), int(v)))
+        return self
+
+    def trace(self, which: int, path):
+        """Grid-tail phase trace into `path` (smpm_batch_set_trace); None: off."""
+        check(lib().smpm_batch_set_trace(self.h, int(which), path.encode() if path else None))
+
+    def tune_from_env(self):
+        """Tools only: SMPM_<KNOB>=<int> environment variables -> tune(); the
+        library itself reads no environment."""
+        import os
+
+        from ._lib import TUNING_KEYS
+
+        for k in TUNING_KEYS:
+            v = os.environ.get("SMPM_" + k.upper())
+            if v is not None:
+                self.tune(**{k: int(v)})
+        for which, name in ((0, "SMPM_GT_TRACE"), (1, "SMPM_GT_TRACE2")):
+            if os.environ.get(name):
+                self.trace(which, os.environ[name])
+        return self
 
     def profile(self, enable=None):
         """Per-kernel-class device time (ms) and launch counts accumulated since

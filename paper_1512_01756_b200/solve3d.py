@@ -88,7 +88,9 @@ class Fourier3D:
         uL = torch.tensor(self.u_L, device=fh.device)
         uS = torch.tensor(self.u_S, device=fh.device)
         # j = 0 consistency projections (proj/src/helmholtz.cpp:159-160, 168-169)
-        fh[0:2] -= (fh[0:2] @ uL)[:, None] * uL[None, :]
+        dl = torch.zeros_like(fh)
+        dl[0:2] = uL
+        fh = b.project_out(fh, dl)
         bS = b.schur_rhs(fh)
         dirs = torch.zeros_like(bS)
         dirs[0:2] = uS

@@ -113,3 +113,44 @@ def test_project_out(setup):
 
     for i in range(b.nsys):
         assert rel(y[i], O.project_out(v[i], d[i])) < 1e-14
+
+
+def test_project_out_node_length(setup):
+    """smpm_project_out at node length r (u_L on f, proj/src/solver.cpp:46), with a
+    zero direction row leaving that system unchanged."""
+    import torch
+
+    case, b = setup
+    r = b.r
+    v = _rand(b.nsys, r, 9)
+    d = _rand(b.nsys, r, 10)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    d[-1] = 0.0
+    y = b.project_out(torch.tensor(v, device="cuda"), torch.tensor(d, device="cuda")).cpu().numpy()
+    from oracle import oracle as O
+
+    for i in range(b.nsys):
+        assert rel(y[i], O.project_out(v[i], d[i])) < 1e-14
+    assert np.array_equal(y[-1], v[-1])
+
+
+def test_tuning_knobs(setup):
+    """smpm_batch_set_tuning: unknown keys are rejected; switching the grid tail or
+    the step-chain PDL off leaves the solve's iteration counts unchanged."""
+    import torch
+
+    from paper_1512_01756_b200 import SmpmError
+
+    case, b = setup
+    with pytest.raises(SmpmError):
+        b.tune(no_such_knob=1)
+    bS = torch.tensor(case.b_S, device="cuda")
+    base = b.solve(bS, "dbj", 1e-10, 100)
+    b.tune(grid=0, pdl=0)
+    try:
+        alt = b.solve(bS, "dbj", 1e-10, 100)
+    finally:
+        b.tune(grid=1, pdl=1)
+    for i in range(b.nsys):
+        assert abs(alt.iterations[i] - base.iterations[i]) <= 1
+        assert rel(alt.x_S[i].cpu().numpy(), base.x_S[i].cpu().numpy()) < 1e-9

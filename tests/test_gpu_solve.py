@@ -81,3 +81,20 @@ def test_long_cycle_batched_helmholtz(ctx):
     case = build_case(7, 6, 4, 6.0, 1.0, mus, kmax=4, decay=True)
     b = gpu_batch(ctx, case)
     check_solve(case, b, "dbj", max_iter=150, restart=0)
+
+
+@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
+@pytest.mark.parametrize("method", ["schur", "dbj"])
+def test_restart_not_converging_reaches_max_iter(ctx, orth, method):
+    """Restarted GMRES that cannot converge (tol below rounding) runs exactly
+    max_iter iterations over 10 cycles on the GPU as in the oracle: the host
+    step loop must not stop early at cycle ends (MGS never uses the grid tail)."""
+    import torch
+
+    case = build_case(6, 6, 4, 24.0, 4.0, (0.0,))
+    b = gpu_batch(ctx, case)
+    res = b.solve(torch.tensor(case.b_S, device="cuda"), method, 1e-17, 60, 6, orth, True)
+    ref = case.systems[0].solve(case.b_S[0], method, 1e-17, 60, 6)
+    assert ref.iterations == 60 and not ref.converged
+    assert res.iterations[0] == 60, res.iterations
+    assert not res.converged[0]

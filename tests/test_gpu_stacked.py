@@ -55,11 +55,29 @@ def test_stacked_modes_2las(ctx):
     check_stacked(case, b, "2las", max_iter=100)
 
 
-def test_stacked_restart(ctx):
+@pytest.mark.parametrize("restart", [2, 3])
+def test_stacked_restart(ctx, restart):
+    """GMRES(m) cycles of the stacked solve: each new cycle starts from the norm of
+    the stacked residual (the restart must sum the per-system norms, as the first
+    cycle does).  The oracle needs 5 iterations here, so m = 2 / 3 restarts 2-3 times."""
     mus = [0.0, (2 * np.pi / 3.0) ** 2]
     case = build_case(6, 5, 4, 7.5, 1.0, mus, kmax=3, decay=True)
     b = gpu_batch(ctx, case, spectral=True)
-    check_stacked(case, b, "dbj", max_iter=60, restart=6)
+    res, ref = check_stacked(case, b, "dbj", max_iter=60, restart=restart)
+    assert ref.iterations > restart, "the case must restart"
+
+
+def test_stacked_restart_not_converging(ctx):
+    """Unreachable tolerance: every cycle restarts until max_iter, on both sides."""
+    import torch
+
+    mus = [0.0, (2 * np.pi / 3.0) ** 2]
+    case = build_case(6, 5, 4, 7.5, 1.0, mus, kmax=3, decay=True)
+    b = gpu_batch(ctx, case, spectral=True)
+    res = b.solve_stacked(torch.tensor(case.b_S, device="cuda"), "dbj", 1e-17, 20, 3)
+    ref = O.solve_stacked(case.systems, case.b_S, "dbj", 1e-17, 20, 3)
+    assert ref.iterations == 20 and not ref.converged
+    assert res.iterations[0] == 20 and not res.converged[0]
 
 
 def test_stacked_single_system_equals_independent(ctx):

@@ -64,7 +64,7 @@ def run_c5(ctx, cfg, chunk):
         modes = list(range(c0, min(cfg.modes, c0 + chunk)))
         t0 = time.perf_counter()
         ps = build_problem(cfg, modes, device="cuda", device_rhs=True)
-        b = load_batch(ctx, ps)
+        b = load_batch(ctx, ps).tune_from_env()
         setup_s += time.perf_counter() - t0
         bS = torch.tensor(ps.b_S, device="cuda")
         for key, sp in regimes.items():
@@ -161,7 +161,7 @@ def main():
         sp = bench.solve_params(cfg)
         t0 = time.perf_counter()
         ps = build_problem(cfg, device="cuda")  # host FDM b_S, as bench.py
-        b = load_batch(ctx, ps)
+        b = load_batch(ctx, ps).tune_from_env()
         setup_s = time.perf_counter() - t0
         bS = torch.tensor(ps.b_S, device="cuda")
         for method in cfg.methods:

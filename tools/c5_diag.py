@@ -23,7 +23,7 @@ modes = [int(m) for m in a.modes.split(",")]
 t0 = time.time()
 ps = build_problem(cfg, modes, device="cuda", device_rhs=True)
 print(f"setup {time.time() - t0:.1f}s for {len(modes)} modes", flush=True)
-b = load_batch(Context(0), ps)
+b = load_batch(Context(0), ps).tune_from_env()
 bS = torch.tensor(ps.b_S, device="cuda")
 for restart in (cfg.max_iter, 0):
     t0 = time.time()

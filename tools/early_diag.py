@@ -20,11 +20,11 @@ bS = torch.tensor(ps.b_S, device="cuda")
 hb = torch.tensor(ps.b_S).pin_memory()
 hx = torch.empty_like(hb).pin_memory()
 out = {}
-for setting in ["", "SMPM_NO_EARLY=1"]:
-    os.environ.pop("SMPM_NO_EARLY", None)
+for setting in ["", "SMPM_EARLY=0"]:
+    os.environ.pop("SMPM_EARLY", None)
     if setting:
-        os.environ["SMPM_NO_EARLY"] = "1"
-    b = load_batch(ctx, ps)
+        os.environ["SMPM_EARLY"] = "0"
+    b = load_batch(ctx, ps).tune_from_env()
     args = ("dbj", 1e-10, 10 * cfg.max_iter, cfg.max_iter, "cgs2", True)
     for _ in range(3):
         r = b.solve(bS, *args, history=False)
@@ -47,5 +47,5 @@ for setting in ["", "SMPM_NO_EARLY=1"]:
     out[setting or "default"] = (xd, xh)
     print(f"{setting or 'default':20s} device {np.median(ts):.3f} ms  host e2e {np.median(th):.3f} ms  "
           f"host==device {np.array_equal(xd, xh)}", flush=True)
-a, c = out["default"], out["SMPM_NO_EARLY=1"]
+a, c = out["default"], out["SMPM_EARLY=0"]
 print("early vs no-early: device bit-equal", np.array_equal(a[0], c[0]), "max abs diff", float(np.abs(a[0] - c[0]).max()))

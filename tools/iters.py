@@ -16,7 +16,7 @@ ap.add_argument("--config", default="C4")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 ps = build_problem(cfg, device="cuda")
-b = load_batch(Context(0), ps)
+b = load_batch(Context(0), ps).tune_from_env()
 bS = torch.tensor(ps.b_S, device="cuda")
 for i in range(2):
     r = b.solve(bS, "dbj", 1e-10, 10 * cfg.max_iter, cfg.max_iter, "cgs2", True, history=False)

@@ -19,7 +19,7 @@ a = ap.parse_args()
 cfg = CONFIGS[a.config]
 ps = build_problem(cfg, device="cuda")
 ctx = Context(0)
-b = load_batch(ctx, ps)
+b = load_batch(ctx, ps).tune_from_env()
 bS = torch.tensor(ps.b_S, device="cuda")
 n0 = b.launch_count
 for i in range(a.solves):

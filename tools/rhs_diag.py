@@ -16,7 +16,7 @@ cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C4"]
 check = [int(m) for m in (sys.argv[2] if len(sys.argv) > 2 else "1,37,40,41,42,43,55,86,87,88").split(",")]
 host = build_problem(cfg, device="cuda")
 dev = build_problem(cfg, device="cuda", device_rhs=True)
-load_batch(Context(0), dev)
+load_batch(Context(0), dev).tune_from_env()
 rel = np.linalg.norm(dev.b_S - host.b_S, axis=1) / np.linalg.norm(host.b_S, axis=1)
 order = np.argsort(-rel)
 print("largest host/device b_S differences:", [(int(m), f"{rel[m]:.2e}") for m in order[:12]])

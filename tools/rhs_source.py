@@ -20,7 +20,7 @@ for sd in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "0,1,2").split
     cfg = dataclasses.replace(CONFIGS["C4"], seed=1234 + sd)
     host = build_problem(cfg, device="cuda")
     dev = build_problem(cfg, device="cuda", device_rhs=True)
-    b = load_batch(ctx, dev)
+    b = load_batch(ctx, dev).tune_from_env()
     srcs = {"host": host.b_S, "device": dev.b_S}
     if sd == 0:
         O.set_threads(16)

@@ -31,7 +31,7 @@ for sd in range(nseeds):
         for kv in filter(None, st.split(",")):
             k, v = kv.split("=")
             os.environ[k] = v
-        b = load_batch(ctx, ps)
+        b = load_batch(ctx, ps).tune_from_env()
         bS = torch.tensor(ps.b_S, device="cuda")
         for _ in range(2):
             r = b.solve(bS, "dbj", 1e-10, 10 * cfg.max_iter, cfg.max_iter, "cgs2", True, history=False)

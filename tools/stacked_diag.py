@@ -14,7 +14,7 @@ from paper_1512_01756_b200.problems import build_problem, load_batch  # noqa: E4
 cfg = CONFIGS["C4"]
 modes = [int(m) for m in (sys.argv[1] if len(sys.argv) > 1 else "0,1,2,5,37,127").split(",")]
 ps = build_problem(cfg, modes, device="cuda")
-b = load_batch(Context(0), ps)
+b = load_batch(Context(0), ps).tune_from_env()
 O.set_threads(8)
 prob = O.Problem(cfg.n, cfg.m_x, cfg.m_z, cfg.l_x, cfg.l_z, cfg.c_tau)
 systems = []

@@ -25,7 +25,7 @@ for setting in [""] + sys.argv[1:]:
     for kv in filter(None, setting.split(",")):
         k, v = kv.split("=")
         os.environ[k] = v
-    b = load_batch(ctx, ps)
+    b = load_batch(ctx, ps).tune_from_env()
     for _ in range(3):
         r = b.solve(bS, "dbj", 1e-10, 10 * cfg.max_iter, cfg.max_iter, "cgs2", True, history=False)
     torch.cuda.synchronize()

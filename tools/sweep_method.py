@@ -1,6 +1,6 @@
 """Median device time of warm solves of one config with a given method under SMPM_* settings.
 
-    SWEEP_CONFIG=C3 python tools/sweep_method.py 2las "" "SMPM_NO_GRID=1"
+    SWEEP_CONFIG=C3 python tools/sweep_method.py 2las "" "SMPM_GRID=0"
 """
 import os
 import sys
@@ -24,7 +24,7 @@ for setting in sys.argv[2:] or [""]:
     for kv in filter(None, setting.split(",")):
         k, v = kv.split("=")
         os.environ[k] = v
-    b = load_batch(ctx, ps)
+    b = load_batch(ctx, ps).tune_from_env()
     for _ in range(2):
         r = b.solve(bS, method, 1e-10, 10 * cfg.max_iter, cfg.max_iter, "cgs2", True, history=False)
     torch.cuda.synchronize()

@@ -20,7 +20,7 @@ a = ap.parse_args()
 cfg = CONFIGS[a.config]
 ps = build_problem(cfg, device="cuda")
 ctx = Context(0)
-b = load_batch(ctx, ps)
+b = load_batch(ctx, ps).tune_from_env()
 bS = torch.tensor(ps.b_S, device="cuda")
 for _ in range(2):
     b.solve(bS, "dbj", 1e-10, 10 * cfg.max_iter, cfg.max_iter, "cgs2", True, history=False)
