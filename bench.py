@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--orth", default="cgs2")
     p.add_argument("--cpu-sample", type=int, default=16, help="modes in the CPU-baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--tune", default="", help="performance knobs, e.g. grid_max=2,grid_nocoop=1 (smpm_batch_set_tuning)")
     return p.parse_args()
 
 
@@ -364,6 +365,8 @@ def run_ours(args, cfg):
     ps = build_problem(cfg, modes, device=f"cuda:{local}", device_rhs=device_rhs(cfg))
     ctx = Context(local)
     b = load_batch(ctx, ps)
+    if args.tune:
+        b.tune(**{kv.split("=")[0]: int(kv.split("=")[1]) for kv in args.tune.split(",")})
     bS = torch.tensor(ps.b_S, device=dev)
     setup_s = time.perf_counter() - t_setup
     # measured fp64 peaks of this device

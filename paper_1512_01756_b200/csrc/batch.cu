@@ -29,6 +29,7 @@
 #include "grid.cuh"
 #include "spectral.cuh"
 #include "xform.cuh"
+#include "xformk.cuh"
 #include "strip.cuh"
 #include "fourier.cuh"
 
@@ -297,6 +298,7 @@ struct smpm_batch {
   Plan pF, pB;
   DevArray<double> dTfrag, dTifrag;    // T, T^{-1} in the xform fragment order
   int xf_P = 0, xf_MB = 0;
+  bool xf_stream = false;  // K-streamed transform kernel (xformk.cuh) instead of the resident slice
   long long cgs3_res = 0;  // resident CTAs of the CGS2 pass kernels (device)
   long long cgs3_kres[3] = {0, 0, 0};  // per kernel: pass 1, pass 2', pass 3' (norm-from-h2 path)
   bool pythag = true;  // norm from the second CGS2 reduction (cgs3_pass2n / cgs3_pass3s); tuning pythag
@@ -1193,13 +1195,69 @@ bool xform_try(smpm_batch* b, int P) {
   return true;
 }
 
+// K-streamed kernel (xformk.cuh) for w whose resident slice does not fit
+template <int MB, int NS>
+bool xformk_try(smpm_batch* b, int P) {
+  const int w = b->w;
+  const size_t smem = xformk_smem<MB, NS>();
+  if (smem > 232448 || 8 * MB * P < w || P > b->ctx->num_sms) return false;
+  CUDA_CHECK(cudaFuncSetAttribute(xformk_kernel<MB, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  std::vector<double> f(static_cast<size_t>(P) * (w / 8) * MB * 64), fi(f.size());
+  xform_frag_order(b->hT.data(), w, P, MB, f.data());
+  xform_frag_order(b->hTi.data(), w, P, MB, fi.data());
+  b->dTfrag.upload(f, b->ctx->stream);
+  b->dTifrag.upload(fi, b->ctx->stream);
+  CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
+  b->xf_P = P;
+  b->xf_MB = MB;
+  b->xf_smem = smem;
+  b->xf_stream = true;
+  return true;
+}
+
 void setup_xform(smpm_batch* b) {
   b->xf_P = 0;
+  b->xf_stream = false;
   if (b->w % 16 != 0 || !b->tune.xform) return;
   for (int P = 1; P <= 4; ++P) {
     const int need = (b->w / 8 + P - 1) / P;
     if (need <= 4 ? xform_try<4>(b, P) : need <= 8 ? xform_try<8>(b, P) : need <= 11 ? xform_try<11>(b, P) : false)
       return;
+  }
+  // w > 176: A streams with the columns; P row slices of at most 34 m-blocks
+  const int K8 = b->w / 8;
+  const int P = (K8 + 33) / 34;
+  const int need = (K8 + P - 1) / P;
+  if (need <= 26) {
+    if (xformk_try<26, 5>(b, P)) return;
+  } else if (need <= 34) {
+    if (xformk_try<34, 4>(b, P)) return;
+  }
+}
+
+// one transform launch over the columns described by `a` (a.P set), groups column groups
+void launch_xform(smpm_batch* b, const XformArgs& a, int groups, cudaStream_t st, bool pdl) {
+  const dim3 grid(groups * a.P), blk(XF_THREADS);
+  auto go = [&](auto kern) {
+    if (pdl) {
+      launch_pdl(b, kern, grid, blk, b->xf_smem, st, a);
+    } else {
+      kern<<<grid, blk, b->xf_smem, st>>>(a);
+      check_launch(b);
+    }
+  };
+  if (b->xf_stream) {
+    if (b->xf_MB == 26)
+      go(xformk_kernel<26, 5>);
+    else
+      go(xformk_kernel<34, 4>);
+    return;
+  }
+  switch (b->xf_MB) {
+    case 4: go(xform_kernel<4>); break;
+    case 8: go(xform_kernel<8>); break;
+    default: go(xform_kernel<11>); break;
   }
 }
 
@@ -1230,12 +1288,7 @@ void run_xform(smpm_batch* b, bool inverse, const double* in, double* out, const
   // column groups: every SM busy unless a group's share would drop below 16 columns
   const long long nch = (static_cast<long long>(lv.nslots) * a.ncol_sys * a.nv + 15) / 16;
   const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / a.P, nch)));
-  const dim3 grid(groups * a.P);
-  switch (b->xf_MB) {
-    case 4: launch_pdl(b, xform_kernel<4>, grid, dim3(XF_THREADS), b->xf_smem, st, a); break;
-    case 8: launch_pdl(b, xform_kernel<8>, grid, dim3(XF_THREADS), b->xf_smem, st, a); break;
-    default: launch_pdl(b, xform_kernel<11>, grid, dim3(XF_THREADS), b->xf_smem, st, a); break;
-  }
+  launch_xform(b, a, groups, st, true);
 }
 
 // th = S^ M^^{-1} vh (bj) or S^ vh in T-coordinates; with cout, also
@@ -2187,12 +2240,7 @@ void xf_columns(smpm_batch* b, bool inverse, const double* in, double* out, int 
     a.P = b->xf_P;
     const long long nch = (static_cast<long long>(b->nsys) * ncol_sys + 15) / 16;
     const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / a.P, nch)));
-    switch (b->xf_MB) {
-      case 4: xform_kernel<4><<<groups * a.P, XF_THREADS, b->xf_smem, st>>>(a); break;
-      case 8: xform_kernel<8><<<groups * a.P, XF_THREADS, b->xf_smem, st>>>(a); break;
-      default: xform_kernel<11><<<groups * a.P, XF_THREADS, b->xf_smem, st>>>(a); break;
-    }
-    check_launch(b);
+    launch_xform(b, a, groups, st, false);
     return;
   }
   if (sys_stride != static_cast<long long>(ncol_sys) * b->w) fail(SMPM_EINVAL, "strip columns must be contiguous");
