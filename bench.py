@@ -273,63 +273,63 @@ def run_reference(args, cfg):
 # GPU arm
 # ---------------------------------------------------------------------------
 def algorithmic_counts(cfg, its, grid_max=8):
-    """Algorithmic FLOPs and HBM bytes of one batched solve,
-    from the per-system iteration counts `its` of that solve.
+    """Algorithmic work of one batched solve from the per-system iteration counts
+    `its`, per kernel class: [flops, bytes, bytes (implementation
+    minimum)].
 
     Per system and Arnoldi step j (ncols = j + 1 basis vectors), spectral dbj path:
-      transforms  T^{-1}, T : 2 GEMMs of 2 w^2 x 2d           -> 8 w^2 d flops, 4 k doubles moved
-      per-mode pass          : ~24 flops per (slot, mode)      -> 2 k doubles moved
-      CGS2 (+ fused P, norm) : 8 k ncols + 12 k flops          -> (4 ncols + 8) k doubles moved
-    A step runs in the grid-persistent tail when at most `grid_max` systems are
-    live at its start (the host switches on the live count), else in the
-    per-stage kernels.  Outside the loop: final residual + solution recovery
-    (~2 operator applications per system)."""
+      transforms T^{-1}, T : two GEMMs of the w x w matrix with 2d columns
+                             -> 8 w^2 d flops; 4 k doubles of vectors
+      per-mode pass         : ~24 flops per (slot, mode); 2 k doubles
+      orthogonalization     : §8(d) counts MGS, B = 8 k (j + 2) bytes, F = 4 (j + 1) k;
+                              the CGS2 passes as implemented read V three times and
+                              move 7 k doubles of vectors: 8 k (3 (j + 1) + 7) bytes,
+                              F = 8 (j + 1) k + 12 k
+    A step runs in the grid-persistent tail when at most `grid_max` systems are live
+    at its start, else in the per-stage kernels.  Outside the loop: final residual +
+    solution recovery (~1.5 transform pairs and one per-mode pass per system)."""
     w, d, k = cfg.w, cfg.m_x - 1, cfg.k
     its = np.asarray(its, dtype=np.int64)
-    tr_f, tr_b = 8.0 * w * w * d, 4.0 * k * 8    # T^{-1} and T: two shared-matrix GEMMs
-    sp_f, sp_b = 24.0 * k, 2.0 * k * 8          # per-mode pass
-    out = {"grid_tail": [0.0, 0.0], "transform": [0.0, 0.0], "spectral_op": [0.0, 0.0],
-           "orthogonalization": [0.0, 0.0]}
+    tr = (8.0 * w * w * d, 4.0 * k * 8, 4.0 * k * 8)
+    sp = (24.0 * k, 2.0 * k * 8, 2.0 * k * 8)
+    out = {c: [0.0, 0.0, 0.0] for c in ("grid_tail", "transform", "spectral_op", "orthogonalization")}
     for j in range(int(its.max()) if its.size else 0):
         live = int((its > j).sum())
-        cg_f = (8.0 * (j + 1) + 12.0) * k
-        cg_b = (4.0 * (j + 1) + 8.0) * k * 8
+        cg = ((8.0 * (j + 1) + 12.0) * k, 8.0 * k * (j + 2), 8.0 * k * (3 * (j + 1) + 7))
         if live <= grid_max:
-            out["grid_tail"][0] += live * (tr_f + sp_f + cg_f)
-            out["grid_tail"][1] += live * (tr_b + sp_b + cg_b)
+            for q in range(3):
+                out["grid_tail"][q] += live * (tr[q] + sp[q] + cg[q])
         else:
-            out["transform"][0] += live * tr_f
-            out["transform"][1] += live * tr_b
-            out["spectral_op"][0] += live * sp_f
-            out["spectral_op"][1] += live * sp_b
-            out["orthogonalization"][0] += live * cg_f
-            out["orthogonalization"][1] += live * cg_b
-    # after the loop: one T^{-1} and a two-input T (solution recovery + final residual)
-    out["transform"][0] += its.size * 1.5 * tr_f
-    out["transform"][1] += its.size * 1.5 * tr_b
-    out["spectral_op"][0] += its.size * sp_f
-    out["spectral_op"][1] += its.size * sp_b
+            for q in range(3):
+                out["transform"][q] += live * tr[q]
+                out["spectral_op"][q] += live * sp[q]
+                out["orthogonalization"][q] += live * cg[q]
+    for q in range(3):
+        out["transform"][q] += its.size * 1.5 * tr[q]
+        out["spectral_op"][q] += its.size * sp[q]
     return out
 
 
 def roofline_kernel_name(cls):
-    return {"grid_tail": "arnoldi_grid_kernel", "transform": "xform_kernel (T^-1 / T)",
+    return {"grid_tail": "arnoldi_grid_kernel", "transform": "xform_kernel / xformk_kernel (T^-1 / T)",
             "spectral_op": "spec_op_kernel (per-mode pass)",
-            "orthogonalization": "cgs3_dot_kernel + cgs3_pass2n_kernel + cgs3_pass3s_kernel (CGS2 passes)"}.get(cls, cls)
+            "orthogonalization": "cgs3_dot_kernel + cgs3_pass2n/2t_kernel + cgs3_pass3s_kernel (CGS2 passes)"}.get(cls, cls)
 
 
-def measured_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the newest committed ncu summary
-    (profiles/rNN/traffic.json), or None."""
+def measured_traffic(cls):
+    """ncu DRAM traffic of one launch group of kernel class `cls` at a stated
+    point (live systems, Arnoldi index j) next to the algorithmic bytes of the
+    SAME launch group, from the newest committed profiles/rNN/traffic.json:
+    traffic / impl_min_bytes is the wasted-traffic ratio.  None if absent."""
     import glob
 
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
         try:
-            v = json.load(open(path)).get(kernel)
+            v = json.load(open(path)).get("classes", {}).get(cls)
         except Exception:
             v = None
         if v is not None:
-            return {"bytes_per_launch": v, "source": os.path.relpath(path, ROOT)}
+            return {**v, "source": os.path.relpath(path, ROOT)}
     return None
 
 
@@ -464,7 +464,9 @@ def run_ours(args, cfg):
 
     # ---- roofline of the dominant kernel class (live CUDA-event timing)
     per_solve_its = its_tot / args.steps
-    work = algorithmic_counts(cfg, np.rint(per_solve_its))
+    # the tail's live-count threshold as the library applies it (tuning grid_max, tail_rows)
+    gm_eff = min(8, 200_000 // cfg.k)
+    work = algorithmic_counts(cfg, np.rint(per_solve_its), grid_max=gm_eff)
     classes = {}
     try:
         peak_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
@@ -476,32 +478,37 @@ def run_ours(args, cfg):
             continue
         c = {"ms": cms, "launches": n, "share": cms / ms_prof if ms_prof else None}
         if name in work and cms > 0:
-            fl, by = work[name][0] * args.steps, work[name][1] * args.steps
+            fl, by, bi = (q * args.steps for q in work[name])
             c["achieved_tflops"] = fl / (cms * 1e-3) / 1e12
-            c["achieved_gbs"] = by / (cms * 1e-3) / 1e9
+            c["achieved_gbs_s8d"] = by / (cms * 1e-3) / 1e9
+            c["achieved_gbs_impl_min"] = bi / (cms * 1e-3) / 1e9
         classes[name] = c
     dom = max((n for n in work if n in prof), key=lambda n: prof[n][0])
     dms, dn = prof[dom]
     nlaunch = max(dn, 1)
-    fl, by = work[dom][0] * args.steps, work[dom][1] * args.steps
+    fl, by, bi = (q * args.steps for q in work[dom])
     # the binding roof: whichever of fp64 MMA and HBM takes longer for this work
-    t_tensor, t_hbm = fl / (peak_fp64 * 1e12), by / (peak_hbm * 1e9)
+    t_tensor, t_hbm = fl / (peak_fp64 * 1e12), bi / (peak_hbm * 1e9)
+    tr = measured_traffic(dom)
     if t_tensor >= t_hbm:
         bound, achieved, peak, unit, per_launch = "tensor", fl / (dms * 1e-3) / 1e12, peak_fp64, "TFLOP/s", fl / nlaunch
+        extra = {}
     else:
         bound, achieved, peak, unit, per_launch = "hbm", by / (dms * 1e-3) / 1e9, peak_hbm, "GB/s", by / nlaunch
+        ach_impl = bi / (dms * 1e-3) / 1e9
+        extra = {"achieved_impl_min": ach_impl, "frac_impl_min": ach_impl / peak_hbm,
+                 "bytes_note": "achieved/frac use SURVEY §8(d) algorithmic bytes (MGS: 8k(j+2) per system-step); "
+                               "*_impl_min use the minimum the CGS2 passes as implemented must move "
+                               "(three reads of V plus 7k vector doubles: 8k(3(j+1)+7))"}
     roofline = {
         "kernel": roofline_kernel_name(dom),
         "class": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-        "frac": achieved / peak if peak else None,
+        "frac": achieved / peak if peak else None, **extra,
         "peak_source": (f"measured in-run fp64 microbenchmark (DFMA {dfma.value:.1f}, DMMA {dmma.value:.1f} TFLOP/s)"
                         if bound == "tensor" else hbm_src),
-        "traffic": (measured_traffic(roofline_kernel_name(dom)) or {}).get("bytes_per_launch"),
-        "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
-        "traffic_source": (measured_traffic(roofline_kernel_name(dom)) or {}).get("source"),
-        "traffic_note": "ncu DRAM bytes of one launch of the named kernel(s) on the first full-batch Arnoldi step "
-                        "(for the CGS2 class: the three passes of that step); algorithmic_per_launch is the class "
-                        "average per timed span (one span = one step's launches of the class)",
+        "traffic": tr.get("dram_bytes") if tr else None,
+        "traffic_unit": "bytes per launch group (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+        "traffic_point": tr,
         "algorithmic_per_launch": per_launch,
         "avg_launch_ms": dms / nlaunch,
         "fp64_peak_tflops": peak_fp64, "hbm_peak_gbs": peak_hbm,

@@ -239,7 +239,8 @@ int smpm_batch_profile(smpm_batch* b, int enable, double* ms, long long* counts,
  * measured-best settings). Keys: segb, xform, sp_stage, spectral, spec_2las,
  * p2fuse, gt_vblock, grid_per_sm, gt_ctas, grid_nocoop (profilers only: the
  * tail then launches without the co-residency guarantee of a cooperative
- * launch), pdl, pythag, grid, grid_max, post_fuse, early; with b = NULL:
+ * launch), pdl, pythag, grid, grid_max, tail_rows (the tail runs only while
+ * live systems x k <= tail_rows; default 200000), post_fuse, early; with b = NULL:
  * fy_tile (transverse FFT). SMPM_EINVAL for an unknown key. The library reads
  * no environment variables. */
 int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value);

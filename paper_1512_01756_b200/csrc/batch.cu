@@ -257,6 +257,7 @@ struct Tuning {
   int pythag = 1;        // norm from the second CGS2 reduction
   int grid = 1;          // grid-persistent tail
   int grid_max = 8;      // live systems at which the tail takes over
+  long long tail_rows = 200000;  // ... and at most this many live interface rows (0: no cap)
   int post_fuse = 1;     // one-pass dbj epilogue
   int early = 1;         // early epilogue + x_S copy during the tail (solve_host)
   std::string gt_trace, gt_trace2;  // phase-trace dump files of the grid tail
@@ -301,6 +302,9 @@ struct smpm_batch {
   bool xf_stream = false;  // K-streamed transform kernel (xformk.cuh) instead of the resident slice
   long long cgs3_res = 0;  // resident CTAs of the CGS2 pass kernels (device)
   long long cgs3_kres[3] = {0, 0, 0};  // per kernel: pass 1, pass 2', pass 3' (norm-from-h2 path)
+  long long p2t_res[V2_MAXCOL + 1] = {};  // resident CTAs of the tiled pass 2' per column capacity
+  bool p2t_attr = false;
+  int jhost = 0;  // Arnoldi index of the next step (all live systems of a cycle share it)
   bool pythag = true;  // norm from the second CGS2 reduction (cgs3_pass2n / cgs3_pass3s); tuning pythag
   bool pdl = true;  // programmatic dependent launch for the Arnoldi step chain (tuning pdl)
   size_t xf_smem = 0;
@@ -1488,10 +1492,32 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
       const GmState_ G1 = chunked(b->cgs3_kres[0], g1), G2 = chunked(b->cgs3_kres[1], g2),
                      G3 = chunked(b->cgs3_kres[2], g3);
       launch_pdl(b, cgs3_dot_kernel, g1, dim3(V3_THREADS), 0, st, G1, V, wv, tdefl, P, cbuf);
-      // ncols <= 16: update and dots in one read of V (tuning p2fuse = 0: two reads)
-      launch_pdl(b, cgs3_pass2n_kernel, g2, dim3(V3_THREADS), 0, st, G2, static_cast<const double*>(V), wv,
-                 b->tune.p2fuse ? 1 : 0);
+      const int ncols_h = b->jhost + 1;
+      if (b->tune.p2fuse && ncols_h > 2 * V3_GRP && ncols_h <= 8 * P2T_MAXC && ncols_h <= G.m + 1) {
+        // more than 16 columns: update and dots in one read of V through
+        // shared-memory row tiles (cgs3_pass2t_kernel)
+        const size_t smem = sizeof(double) * p2t_smem_doubles(ncols_h);
+        if (!b->p2t_attr) {
+          CUDA_CHECK(cudaFuncSetAttribute(cgs3_pass2t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(sizeof(double) * p2t_smem_doubles(8 * P2T_MAXC))));
+          b->p2t_attr = true;
+        }
+        if (b->p2t_res[ncols_h] == 0) {
+          int o = 0;
+          CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs3_pass2t_kernel, V3_THREADS, smem));
+          b->p2t_res[ncols_h] = std::max(1, o) * b->ctx->num_sms;
+        }
+        dim3 g2t;
+        const GmState_ G2t = chunked(b->p2t_res[ncols_h], g2t);
+        launch_pdl(b, cgs3_pass2t_kernel, g2t, dim3(V3_THREADS), smem, st, G2t, static_cast<const double*>(V), wv,
+                   ncols_h);
+      } else {
+        // ncols <= 16: update and dots in one read of V (tuning p2fuse = 0: two reads)
+        launch_pdl(b, cgs3_pass2n_kernel, g2, dim3(V3_THREADS), 0, st, G2, static_cast<const double*>(V), wv,
+                   b->tune.p2fuse ? 1 : 0);
+      }
       launch_pdl(b, cgs3_pass3s_kernel, g3, dim3(V3_THREADS), 0, st, G3, V, wv, vin);
+      ++b->jhost;
       return;
     }
     launch_pdl(b, cgs3_dot_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, tdefl, P, cbuf);
@@ -1504,6 +1530,7 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
   (void)hsm;
   dim3 sg(std::max(1, std::min(G.nchunk, 64)), lv.nslots);
   launch_pdl(b, gm_scale_kernel, sg, dim3(256), 0, st, G, V, wv, vin);
+  ++b->jhost;
 }
 
 // Compacted list of live systems (ascending index, so deterministic) from a
@@ -1818,6 +1845,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
              static_cast<const int*>(nullptr), ns, alist, acount, static_cast<int*>(nullptr));
   G.alist = alist;
   G.acount = acount;
+  b->jhost = 0;
 
   int steps = 0;
   // ---- Arnoldi steps; device flags are polled one step behind the launches
@@ -1842,12 +1870,18 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   // few live systems: the rest of the cycle runs grid-persistent (grid.cuh)
   bool use_grid = b->grid_ok && !c.stacked && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= GT_MAXCOL &&
                         (c.method != SMPM_DBJ || c.fused) && b->tune.grid;
-  // measured on C4 with the PDL step chain: 8-10 live systems is the crossover
+  // The tail pays off while a step is latency-bound: measured crossovers are
+  // 8-10 live systems on C4 (k = 22,176) and none on C5 (k = 277,440: the
+  // per-stage kernels are faster even for one live system), so the live-count
+  // threshold scales with the work per system: grid_max <= tail_rows / k.
   int grid_max = std::max(0, std::min(GT_MAXSYS, b->tune.grid_max));
+  if (b->tune.tail_rows > 0)
+    grid_max = static_cast<int>(std::min<long long>(grid_max, b->tune.tail_rows / std::max(1LL, b->k)));
   if (use_grid) grid_max = std::min(grid_max, grid_blocks(b) / GT_CL);  // one cluster per live system at least
   int cycles = 0;  // restarts issued: each cycle end may cost one speculative (empty) step
   auto restart = [&](int ncycv) {
     ++cycles;
+    b->jhost = 0;
     // ---- restart (GMRES(m) extension): x += V y ; r = b - op(x) ; new cycle
     select_state_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, GM_CYCLE, dsel);
     check_launch(b);
@@ -2783,6 +2817,10 @@ int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
       const char* name;
       int* field;
     };
+    if (k == "tail_rows") {
+      t.tail_rows = value;
+      return;
+    }
     const Knob knobs[] = {{"segb", &t.segb}, {"xform", &t.xform}, {"sp_stage", &t.sp_stage},
                           {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse},
                           {"gt_vblock", &t.gt_vblock}, {"grid_per_sm", &t.grid_per_sm}, {"gt_ctas", &t.gt_ctas},

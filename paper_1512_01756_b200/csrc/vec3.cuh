@@ -388,6 +388,159 @@ __global__ void __launch_bounds__(V3_THREADS, CGS3_MINB) cgs3_pass2n_kernel(GmSt
   givens_step(G, s, j, sqrt(fmax(nsq - hh, 0.0)));
 }
 
+// ---- pass 2' beyond 16 columns: one read of V through shared-memory row tiles ----
+// The CTA walks its rows in tiles of TR rows (double-buffered cp.async, 16-byte
+// copies: a tile is ncols contiguous column segments of TR doubles).  From the
+// staged tile it first forms w1 = w - V h1 for the tile's rows (thread t: row
+// t % 64 (+64, ...) over column quarter t / 64, quarters combined in fixed
+// order), then accumulates h2 += V^T w1 (warp q owns columns q, q + 8, ...,
+// lane l rows l, l + 32, ... of the tile).  Same reduction tree for every
+// launch and batch: deterministic.  Returns this thread's ||w1||^2 part.
+constexpr int P2T_MAXC = 16;  // columns per warp in the dots phase (ncols <= 8 * 16)
+__host__ __device__ __forceinline__ int p2t_rows(int ncols) { return ncols <= 32 ? 128 : ncols <= 64 ? 64 : 32; }
+__host__ __device__ __forceinline__ size_t p2t_smem_doubles(int cap) {
+  const int tr = p2t_rows(cap);
+  return 2 * static_cast<size_t>(tr) * cap + 2 * tr + 4 * tr + tr;
+}
+
+__device__ __forceinline__ double pass2_tiled(const double* __restrict__ Vs, long long k, int ncols,
+                                              const double* hs, double* ws, int r0, int r1, double* sm,
+                                              double (&acc)[P2T_MAXC]) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int TR = p2t_rows(ncols);
+  double* tile = sm;                                     // [2][ncols][TR]
+  double* wt = tile + 2 * static_cast<size_t>(TR) * ncols;  // [2][TR]
+  double* qp = wt + 2 * TR;                              // [4][TR]
+  double* nvs = qp + 4 * TR;                             // [TR]
+  const int ntile = (r1 - r0 + TR - 1) / TR;
+  const int pieces = TR / 2;  // 16-byte pieces per column segment
+  auto issue = [&](int it) {
+    const int a = r0 + it * TR;
+    double* tb = tile + static_cast<size_t>(it & 1) * TR * ncols;
+    for (int p = t; p < ncols * pieces; p += V3_THREADS) {
+      const int c = p / pieces, q = p - c * pieces;
+      const int r = a + 2 * q;
+      cp_async16(tb + c * TR + 2 * q, Vs + static_cast<long long>(c) * k + (r < r1 ? r : r0), r < r1);
+    }
+    for (int q = t; q < pieces; q += V3_THREADS) {
+      const int r = a + 2 * q;
+      cp_async16(wt + (it & 1) * TR + 2 * q, ws + (r < r1 ? r : r0), r < r1);
+    }
+  };
+  double sq = 0.0;
+  issue(0);
+  cp_async_commit();
+  const int quarter = t >> 6, qrow = t & 63;
+  const int qc = (ncols + 3) >> 2;  // columns per quarter (contiguous ranges)
+  const int c0q = quarter * qc, c1q = min(ncols, c0q + qc);
+  for (int it = 0; it < ntile; ++it) {
+    if (it + 1 < ntile) issue(it + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* tb = tile + static_cast<size_t>(it & 1) * TR * ncols;
+    const double* wb = wt + (it & 1) * TR;
+    // update partials: quarter sums of V[r][c] h[c], c ascending
+    for (int r = qrow; r < TR; r += 64) {
+      double a0 = 0.0, a1 = 0.0;
+      int c = c0q;
+      for (; c + 1 < c1q; c += 2) {
+        a0 = fma(tb[c * TR + r], hs[c], a0);
+        a1 = fma(tb[(c + 1) * TR + r], hs[c + 1], a1);
+      }
+      if (c < c1q) a0 = fma(tb[c * TR + r], hs[c], a0);
+      qp[quarter * TR + r] = a0 + a1;
+    }
+    __syncthreads();
+    const int a = r0 + it * TR;
+    for (int r = t; r < TR; r += V3_THREADS) {
+      const double nv = (a + r < r1) ? wb[r] - ((qp[r] + qp[TR + r]) + (qp[2 * TR + r] + qp[3 * TR + r])) : 0.0;
+      nvs[r] = nv;
+      if (a + r < r1) {
+        ws[a + r] = nv;
+        sq = fma(nv, nv, sq);
+      }
+    }
+    __syncthreads();
+    // reorthogonalisation dots from the same tile
+#pragma unroll
+    for (int i = 0; i < P2T_MAXC; ++i) {
+      const int c = warp + 8 * i;
+      if (c < ncols) {
+        const double* col = tb + c * TR;
+        for (int r = lane; r < TR; r += 32) acc[i] = fma(col[r], nvs[r], acc[i]);
+      }
+    }
+    __syncthreads();  // the tile buffer and nvs are refilled next
+  }
+  cp_async_wait<0>();
+  return sq;
+}
+
+// pass 2' for ncols > 16 (tiled single read); ncols > cap (not expected: the host
+// sizes cap from the step index) falls back to the two-read form
+__global__ void __launch_bounds__(V3_THREADS, 2) cgs3_pass2t_kernel(GmState_ G, const double* __restrict__ V, double* w,
+                                                                 int cap) {
+  pdl_wait();
+  pdl_launch();
+  extern __shared__ __align__(16) double p2t_sm[];
+  __shared__ double hs[V2_MAXCOL];
+  __shared__ double red[V3_THREADS / 32][V3_GRP];
+  int s;
+  if (!gm_slot(G, blockIdx.y, s)) return;
+  const int j = G.jcyc[s];
+  const int ncols = j + 1;
+  const int stride = G.m + 2;
+  const double* hin = G.h1 + static_cast<long long>(s) * stride;
+  for (int i = threadIdx.x; i < ncols; i += V3_THREADS) hs[i] = hin[i];
+  __syncthreads();
+  const int ch = blockIdx.x;
+  const int r0 = static_cast<int>(min(G.k, static_cast<long long>(ch) * G.chunk));
+  const int r1 = static_cast<int>(min(G.k, static_cast<long long>(r0) + G.chunk));
+  const double* Vs = V + s * G.vstride;
+  double* ws = w + s * G.k;
+  double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
+  double sq;
+  if (ncols <= cap && ncols <= 8 * P2T_MAXC) {
+    double acc[P2T_MAXC];
+#pragma unroll
+    for (int i = 0; i < P2T_MAXC; ++i) acc[i] = 0.0;
+    sq = pass2_tiled(Vs, G.k, ncols, hs, ws, r0, r1, p2t_sm, acc);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < P2T_MAXC; ++i) {
+      const int c = warp + 8 * i;
+      const double v = warp_sum(acc[i]);
+      if (lane == 0 && c < ncols) part[c] = v;
+    }
+  } else {
+    sq = rows_update_long(Vs, G.k, ncols, hs, ws, r0, r1);
+    __syncthreads();
+    cta_dots_long(Vs, G.k, ncols, ws, r0, r1, part, red);
+  }
+  sq = warp_sum(sq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][0] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tsum = 0.0;
+    for (int q = 0; q < V3_THREADS / 32; ++q) tsum += red[q][0];
+    part[ncols] = tsum;
+  }
+  if (!last_cta(G.counter + s, G.nchunk)) return;
+  double* h2 = G.h2 + static_cast<long long>(s) * stride;
+  reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols + 1, h2);
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  double hh = 0.0;
+  for (int i = threadIdx.x; i < ncols; i += 32) hh = fma(h2[i], h2[i], hh);
+  hh = warp_sum(hh);
+  const double nsq = h2[ncols];
+  __syncwarp();
+  if (threadIdx.x == 0) h2[ncols] = 0.0;
+  __syncwarp();
+  givens_step(G, s, j, sqrt(fmax(nsq - hh, 0.0)));
+}
+
 // pass 3': w -= V h2 and v_{j+1} = w / ||w|| into the basis and the operator input
 // (the scale kernel folded in; runs after the Givens step, so stopped systems skip it)
 __global__ void __launch_bounds__(V3_THREADS) cgs3_pass3s_kernel(GmState_ G, double* __restrict__ V, double* w,

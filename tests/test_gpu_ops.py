@@ -153,4 +153,7 @@ def test_tuning_knobs(setup):
         b.tune(grid=1, pdl=1)
     for i in range(b.nsys):
         assert abs(alt.iterations[i] - base.iterations[i]) <= 1
-        assert rel(alt.x_S[i].cpu().numpy(), base.x_S[i].cpu().numpy()) < 1e-9
+        xa, xb = alt.x_S[i].cpu().numpy(), base.x_S[i].cpu().numpy()
+        if case.mus[i] == 0.0:  # x_S is defined up to the constant null direction
+            xa, xb = xa - xa.mean(), xb - xb.mean()
+        assert rel(xa, xb) < 1e-9
