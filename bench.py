@@ -464,7 +464,6 @@ def run_ours(args, cfg):
 
     # ---- roofline of the dominant kernel class (live CUDA-event timing)
     per_solve_its = its_tot / args.steps
-    # the tail's live-count threshold as the library applies it (tuning grid_max, tail_rows)
     gm_eff = min(8, 200_000 // cfg.k)
     work = algorithmic_counts(cfg, np.rint(per_solve_its), grid_max=gm_eff)
     classes = {}
