@@ -236,7 +236,7 @@ long long smpm_batch_launch_count(const smpm_batch* b);
 int smpm_batch_profile(smpm_batch* b, int enable, double* ms, long long* counts, int nclass);
 
 /* Performance knobs of a batch (no reference counterpart; defaults are the
- * measured-best settings). Keys: segb, xform, sp_stage, spectral, spec_2las,
+ * measured-best settings). Keys: segb, spec_v2, xform, sp_stage, spectral, spec_2las,
  * p2fuse, gt_vblock, grid_per_sm, gt_ctas, grid_nocoop (profilers only: the
  * tail then launches without the co-residency guarantee of a cooperative
  * launch), pdl, pythag, grid, grid_max, tail_rows (the tail runs only while

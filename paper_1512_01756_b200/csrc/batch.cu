@@ -245,7 +245,8 @@ struct smpm_ctx {
 struct Tuning {
   int segb = 0;          // per-mode pass: blocks per warp item (0: SP_SEGB)
   int xform = 1;         // resident-slice transform kernel (xform.cuh) where it applies
-  int sp_stage = 1;      // per-mode pass stages slot rows in shared memory
+  int sp_stage = 1;      // per-mode pass stages slot rows in shared memory (spec_v2 = 0)
+  int spec_v2 = 1;       // pipelined per-mode pass (spec_op2_kernel)
   int spectral = 1;      // spectral operator when its factors are set
   int spec_2las = 1;     // spectral operator for 2LAS
   int p2fuse = 1;        // CGS2 pass 2 single-read fusion
@@ -1306,6 +1307,25 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
   DeflateParams P = deflate_params(b, lv.active);
   P.alist = lv.alist;
   P.acount = lv.acount;
+  double* zp = cout ? b->dzpart.p : nullptr;
+  if (b->tune.spec_v2) {
+    // pipelined pass (spec_op2_kernel): segments as long as ~32 warps per SM
+    // still allow (shorter halo), at least 2 and at most 16 blocks
+    const long long nbk = b->nbf + (b->single ? 1 : 0);
+    const long long warps = nbk * sp.nmc * lv.nslots;
+    int segb = static_cast<int>(std::max(2LL, std::min(16LL, warps / (32LL * b->ctx->num_sms))));
+    if (b->tune.segb > 0) segb = b->tune.segb;
+    sp.segb = segb;
+    sp.nseg = static_cast<int>((nbk + segb - 1) / segb);
+    const dim3 grid2(sp.nmc * ((sp.nseg + SP_WARPS - 1) / SP_WARPS), lv.nslots);
+    const size_t shm2 = cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0;
+    if (bj)
+      launch_pdl(b, spec_op2_kernel<true>, grid2, dim3(SP_THREADS), shm2, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);
+    else
+      launch_pdl(b, spec_op2_kernel<false>, grid2, dim3(SP_THREADS), shm2, st, sp, vh, th, P, zp, b->dcount.p, cout,
+                 uh);
+    return;
+  }
   const dim3 grid(sp.nmc * ((sp.nseg + SP_WARPS - 1) / SP_WARPS), lv.nslots);
   // staged slot rows (tuning sp_stage = 0: direct loads)
   sp.stage = sp.segb <= SP_SEGB && b->tune.sp_stage ? 1 : 0;
@@ -1317,7 +1337,6 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
     CUDA_CHECK(cudaFuncSetAttribute(spec_op_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     b->sp_smem_set = true;
   }
-  double* zp = cout ? b->dzpart.p : nullptr;
   if (bj)
     launch_pdl(b, spec_op_kernel<true>, grid, dim3(SP_THREADS), shm, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);
   else
@@ -1498,8 +1517,10 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
         // shared-memory row tiles (cgs3_pass2t_kernel)
         const size_t smem = sizeof(double) * p2t_smem_doubles(ncols_h);
         if (!b->p2t_attr) {
+          size_t mx = 0;
+          for (int cc = 2 * V3_GRP + 1; cc <= 8 * P2T_MAXC; ++cc) mx = std::max(mx, p2t_smem_doubles(cc));
           CUDA_CHECK(cudaFuncSetAttribute(cgs3_pass2t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(sizeof(double) * p2t_smem_doubles(8 * P2T_MAXC))));
+                                          static_cast<int>(sizeof(double) * mx)));
           b->p2t_attr = true;
         }
         if (b->p2t_res[ncols_h] == 0) {
@@ -2821,7 +2842,7 @@ int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
       t.tail_rows = value;
       return;
     }
-    const Knob knobs[] = {{"segb", &t.segb}, {"xform", &t.xform}, {"sp_stage", &t.sp_stage},
+    const Knob knobs[] = {{"segb", &t.segb}, {"spec_v2", &t.spec_v2}, {"xform", &t.xform}, {"sp_stage", &t.sp_stage},
                           {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse},
                           {"gt_vblock", &t.gt_vblock}, {"grid_per_sm", &t.grid_per_sm}, {"gt_ctas", &t.gt_ctas},
                           {"grid_nocoop", &t.grid_nocoop}, {"pdl", &t.pdl}, {"pythag", &t.pythag},

@@ -329,6 +329,157 @@ __device__ __forceinline__ void spec_warp_item(const SpecParams& sp, int s, int 
   }
 }
 
+// ---- pipelined per-mode pass (per-stage path) ------------------------------
+// One warp = (system, 32-mode chunk, segment of segb blocks); lane = mode.  The
+// warp walks its blocks in order with the raw slot values of the next block
+// already in registers and the block after it in flight (16-byte loads for a
+// pair mode's two coordinates), so each block's solve overlaps two blocks of
+// loads; no shared memory, so many warps per SM.  Long segments keep the halo
+// (one block on each side) small.  The Z^T partial of each interface is
+// warp-reduced as its block completes.  Same per-mode arithmetic as
+// spec_mode_segment (bit-identical th / uh / Z^T partials).
+__device__ __forceinline__ void spec_ld_raw(const SpecParams& sp, const ModeRef& mr, const double* __restrict__ vh,
+                                            int blk, bool ok, double2 (&y)[4]) {
+  const int ns = ok ? spec_bslots(sp, blk) : 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (j < ns) {
+      const double* p = vh + mr.base + static_cast<long long>(4 * blk + j) * mr.w + mr.e0;
+      if (mr.pair) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+        y[j] = make_double2(v.x, -v.y);
+      } else {
+        y[j] = make_double2(__ldcg(p), 0.0);
+      }
+    } else {
+      y[j] = make_double2(0.0, 0.0);
+    }
+  }
+}
+
+template <bool BJ>
+__device__ __forceinline__ void spec_solve_raw(const SpecParams& sp, const ModeRef& mr, const ModeGamma& g,
+                                               const double2* ki, int blk, const double2 (&y)[4], double2 (&x)[4]) {
+  spec_block_solve<BJ>(sp, g, ki, blk, y, x);
+  if (sp.cadd) {
+    const int ns = spec_bslots(sp, blk);
+    const double* c = sp.cadd + static_cast<long long>(mr.sys) * sp.d;
+    const double2 nu = make_double2(sp.nu[mr.e0], mr.pair ? -sp.nu[mr.e0 + 1] : 0.0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < ns) {
+        const double ci = c[2 * blk + (j >> 1)];
+        x[j] = make_double2(fma(ci, nu.x, x[j].x), fma(ci, nu.y, x[j].y));
+      }
+  }
+}
+
+__device__ __forceinline__ void spec_st_pair(const ModeRef& mr, double* v, int beta, double2 z) {
+  double* p = v + mr.base + static_cast<long long>(beta) * mr.w + mr.e0;
+  if (mr.pair)
+    *reinterpret_cast<double2*>(p) = make_double2(z.x, -z.y);
+  else
+    p[0] = z.x;
+}
+
+template <bool BJ>
+__device__ __forceinline__ void spec_warp_item2(const SpecParams& sp, int s, int mc, int sg, const double* __restrict__ vh,
+                                                double* __restrict__ th, double* zout, double* __restrict__ uh) {
+  const int lane = threadIdx.x & 31;
+  const int m = mc * SP_MODES + lane;
+  const int nb = spec_nblocks(sp);
+  const int b0 = sg * sp.segb, b1 = min(nb, b0 + sp.segb);
+  const bool ok = m < sp.nmode;
+  const ModeRef mr = mode_ref(sp, s, ok ? m : 0);
+  ModeGamma g{};
+  if (ok) g = mode_gamma(sp, s, m);
+  const double2* ki = sp.kinv + static_cast<long long>(s) * 20 * sp.nmode + (ok ? m : 0);
+  // raw values: yc (block blk + 1, landed), yn (block blk + 2, in flight)
+  double2 xp[4], xc[4], xn[4], yc[4], yn[4];
+  const bool halo = th && b0 > 0;
+  {
+    double2 y0[4], y1[4];
+    spec_ld_raw(sp, mr, vh, halo ? b0 - 1 : b0, ok, y0);
+    spec_ld_raw(sp, mr, vh, b0, ok && halo, y1);
+    spec_ld_raw(sp, mr, vh, b0 + 1, ok && b0 + 1 < nb && (th || b0 + 1 < b1), yc);
+    if (halo) {
+      spec_solve_raw<BJ>(sp, mr, g, ki, b0 - 1, y0, xp);
+      spec_solve_raw<BJ>(sp, mr, g, ki, b0, y1, xc);
+    } else {
+      spec_solve_raw<BJ>(sp, mr, g, ki, b0, y0, xc);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) xp[j] = make_double2(0.0, 0.0);
+    }
+  }
+  // yc now holds block b0 + 1
+  for (int blk = b0; blk < b1; ++blk) {
+    const int ns = spec_bslots(sp, blk);
+    const bool need_next = blk + 1 < nb && (th || blk + 1 < b1);
+    const bool need_nn = blk + 2 < nb && (th ? blk + 2 <= b1 : blk + 2 < b1);
+    spec_ld_raw(sp, mr, vh, blk + 2, ok && need_nn, yn);
+    if (uh && ok) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < ns) spec_st_pair(mr, uh, 4 * blk + j, xc[j]);
+    }
+    if (need_next) spec_solve_raw<BJ>(sp, mr, g, ki, blk + 1, yc, xn);
+    if (th) {
+      double2 t[4];
+      spec_block_S(sp, g, blk, xc, xp[3], xn[0], t);
+      if (ok) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < ns) spec_st_pair(mr, th, 4 * blk + j, t[j]);
+      }
+      if (zout) {
+        const double z0 = ok ? mr.zt(sp.omega, cadd(t[0], t[1])) : 0.0;
+        const double z1 = ok && ns == 4 ? mr.zt(sp.omega, cadd(t[2], t[3])) : 0.0;
+        const double r0 = warp_sum(z0);
+        const double r1 = warp_sum(z1);
+        if (lane == 0) {
+          zout[2 * blk] = r0;
+          if (2 * blk + 1 < sp.d) zout[2 * blk + 1] = r1;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      xp[j] = xc[j];
+      xc[j] = xn[j];
+      yc[j] = yn[j];
+    }
+  }
+}
+
+// per-stage per-mode pass: grid (nmc * ceil(nseg / SP_WARPS), live slots)
+template <bool BJ>
+__global__ void __launch_bounds__(SP_THREADS, 4) spec_op2_kernel(SpecParams sp, const double* __restrict__ vh,
+                                                              double* __restrict__ th, DeflateParams P, double* zpart,
+                                                              int* counter, double* cout, double* __restrict__ uh) {
+  pdl_wait();
+  pdl_launch();
+  extern __shared__ double sm2[];  // 2 d doubles (coarse solve)
+  int s;
+  if (!defl_slot(P, blockIdx.y, s)) return;
+  const int nsg = (sp.nseg + SP_WARPS - 1) / SP_WARPS;
+  const int mc = blockIdx.x / nsg, sg = (blockIdx.x % nsg) * SP_WARPS + (threadIdx.x >> 5);
+  if (sg < sp.nseg)
+    spec_warp_item2<BJ>(sp, s, mc, sg, vh, th, zpart ? zpart + (static_cast<long long>(s) * sp.nmc + mc) * sp.d : nullptr,
+                        uh);
+  if (!zpart) return;
+  if (!last_cta(counter + s, sp.nmc * nsg)) return;
+  double* sums = sm2;
+  double* c = sm2 + sp.d;
+  for (int i = threadIdx.x; i < sp.d; i += blockDim.x) {
+    double v = 0.0;
+    for (int q = 0; q < sp.nmc; ++q) v += __ldcg(zpart + (static_cast<long long>(s) * sp.nmc + q) * sp.d + i);
+    sums[i] = v;
+  }
+  __syncthreads();
+  coarse_solve_block(P, s, sums, c);
+  for (int i = threadIdx.x; i < sp.d; i += blockDim.x) cout[static_cast<long long>(s) * sp.d + i] = c[i];
+}
+
 // th = T^-1-space operator of the live systems; with zpart, the last CTA of
 // each system also solves the coarse system for c = C^{-1} Z^T (T th) -> cout.
 // grid (nmc * ceil(nseg / SP_WARPS), live slots)

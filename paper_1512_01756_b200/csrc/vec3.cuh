@@ -163,12 +163,15 @@ __device__ __forceinline__ double rows_update_nr(const double* __restrict__ Vs, 
       const int rq = r + q * V3_THREADS;
       if (rq < r1) {
         const double nv = __ldcg(ws + rq) - (a[q][0] + a[q][1]);
-        ws[rq] = nv;
-        sq = fma(nv, nv, sq);
         if (SCALE) {
+          // pass 3': only the new basis vector and the operator input are live
+          // (the next pass 1 rewrites w)
           const double v = nv * inv;
           col[rq] = v;
           vs[rq] = v;
+        } else {
+          ws[rq] = nv;
+          sq = fma(nv, nv, sq);
         }
       }
     }

@@ -1,34 +1,59 @@
 """Mode sharding across ranks.
 
 The Fourier modes are independent systems (proj/src/helmholtz.cpp:247-269),
-so there is no collective inside a solve. Ranks own modes round-robin, which
-spreads the slow low-wavenumber modes and puts the singular j = 0 system on
-rank 0. After the solves, one all-gather over NVLink (NCCL; gloo on CPU in
-the tests) collects per-mode results in mode order, and timings reduce by max.
+so there is no collective inside a solve. Ranks own modes round-robin by
+default, which spreads the slow low-wavenumber modes and puts the singular
+j = 0 system on rank 0; with per-mode cost estimates (e.g. the iteration
+counts of an earlier solve of the same batch) the modes are instead assigned
+longest-first to the least-loaded rank (LPT), which evens out the per-rank
+time when a few slow modes dominate. After the solves, one all-gather over
+NVLink (NCCL; gloo on CPU in the tests) collects per-mode results in mode
+order, and timings reduce by max.
 """
 from __future__ import annotations
 
 
-def shard_modes(nmodes: int, world: int, rank: int) -> list:
-    """Modes owned by `rank`: m = rank, rank + world, ..."""
-    return list(range(rank, nmodes, world))
+def mode_owners(nmodes: int, world: int, costs=None) -> list:
+    """Mode lists of every rank: round-robin without costs, else LPT on `costs`
+    (ties broken by mode index, then rank index: deterministic on every rank).
+    Each list is ascending; mode 0 always lives on rank 0."""
+    if costs is None:
+        return [list(range(r, nmodes, world)) for r in range(world)]
+    if len(costs) != nmodes:
+        raise ValueError("one cost per mode")
+    load = [0.0] * world
+    owners = [[] for _ in range(world)]
+    owners[0].append(0)
+    load[0] += float(costs[0])
+    for m in sorted(range(1, nmodes), key=lambda q: (-float(costs[q]), q)):
+        r = min(range(world), key=lambda q: (load[q], q))
+        owners[r].append(m)
+        load[r] += float(costs[m])
+    return [sorted(o) for o in owners]
 
 
-def gather_modes(local, nmodes: int, world: int, group=None):
+def shard_modes(nmodes: int, world: int, rank: int, costs=None) -> list:
+    """Modes owned by `rank` (mode_owners)."""
+    return mode_owners(nmodes, world, costs)[rank]
+
+
+def gather_modes(local, nmodes: int, world: int, group=None, costs=None):
     """All-gather per-mode rows (local: tensor (n_local, ...) in this rank's
-    mode order) into a (nmodes, ...) tensor in global mode order, on every rank."""
+    mode order) into a (nmodes, ...) tensor in global mode order, on every rank.
+    `costs` must be the same as the sharding's."""
     import torch
     import torch.distributed as dist
 
-    counts = [len(shard_modes(nmodes, world, r)) for r in range(world)]
-    width = max(counts)
+    owners = mode_owners(nmodes, world, costs)
+    width = max(len(o) for o in owners)
     pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     pad[: local.shape[0]] = local
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad, group=group)
     out = torch.empty((nmodes,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     for r in range(world):
-        out[r::world] = bufs[r][: counts[r]]
+        if owners[r]:
+            out[torch.tensor(owners[r], device=local.device)] = bufs[r][: len(owners[r])]
     return out
 
 

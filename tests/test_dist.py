@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1512_01756_b200.dist import gather_modes, max_over_ranks, shard_modes
+from paper_1512_01756_b200.dist import gather_modes, max_over_ranks, mode_owners, shard_modes
 
 
 def test_shard_modes_partition():
@@ -20,6 +20,22 @@ def test_shard_modes_partition():
             owned = sorted(m for r in range(ws) for m in shard_modes(nm, ws, r))
             assert owned == list(range(nm))
             assert 0 in shard_modes(nm, ws, 0)
+
+
+def test_balanced_owners_partition_and_balance():
+    """LPT on per-mode costs: a partition, mode 0 on rank 0, and the max per-rank
+    load never above round-robin's on a C4-like skew (slow low modes)."""
+    rng = np.random.default_rng(5)
+    for nm in (5, 128, 256):
+        costs = [40.0 / (1 + m) ** 0.5 + rng.uniform(0, 3) for m in range(nm)]
+        for ws in (2, 4, 8):
+            own = mode_owners(nm, ws, costs)
+            assert sorted(m for o in own for m in o) == list(range(nm))
+            assert 0 in own[0]
+            lpt = max(sum(costs[m] for m in o) for o in own)
+            rr = max(sum(costs[m] for m in o) for o in mode_owners(nm, ws))
+            assert lpt <= rr + 1e-9
+            assert own == mode_owners(nm, ws, list(costs))  # deterministic
 
 
 def _solve_modes(modes):
@@ -43,13 +59,13 @@ def _solve_modes(modes):
     return np.array(out)
 
 
-def _worker(rank, world, port, nmodes, result_path):
+def _worker(rank, world, port, nmodes, result_path, costs=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    mine = shard_modes(nmodes, world, rank)
+    mine = shard_modes(nmodes, world, rank, costs)
     x = torch.tensor(_solve_modes(mine))
-    full = gather_modes(x, nmodes, world)
+    full = gather_modes(x, nmodes, world, costs=costs)
     tmax = max_over_ranks([float(rank + 1), float(10 - rank)])
     if rank == 0:
         np.save(result_path, full.numpy())
@@ -68,3 +84,17 @@ def test_gloo_two_ranks(tmp_path):
     assert full.shape == ref.shape
     assert np.array_equal(full, ref)  # identical CPU arithmetic per mode, gathered in mode order
     assert np.load(path + ".t.npy").tolist() == [2.0, 10.0]
+
+
+def test_gloo_two_ranks_balanced(tmp_path):
+    """The LPT assignment (skewed costs put modes 1 and 2 on different ranks out
+    of round-robin order) gathers back into mode order as well."""
+    nmodes, world = 5, 2
+    costs = [5.0, 9.0, 8.0, 1.0, 1.0]
+    assert mode_owners(nmodes, world, costs) != mode_owners(nmodes, world)
+    port = 29700 + (os.getpid() % 1000)
+    path = str(tmp_path / "full.npy")
+    mp.spawn(_worker, args=(world, port, nmodes, path, costs), nprocs=world, join=True)
+    full = np.load(path)
+    ref = _solve_modes(list(range(nmodes)))
+    assert np.array_equal(full, ref)

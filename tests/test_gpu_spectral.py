@@ -83,31 +83,27 @@ def test_spectral_odd_w_falls_back(ctx):
 def test_spectral_large_w(ctx, n, m_z):
     """w = 272 / 416 / 544 (the C3 / C2 / C5 interface widths): the transforms run
     on the K-streamed kernel (xformk.cuh) in the per-stage path (12 live systems)
-    and in the strip solves.  The spectral solve agrees with the dense-operator
-    solve of the same couplings, its true Schur residual is at the tolerance, and
-    the device b_S (schur_rhs through the streamed transform) matches the host FDM."""
+    and in the strip solves.  The spectral solves hold the oracle's bars on the
+    same couplings (tests/test_gpu_parity.py envelope), and the device b_S
+    (schur_rhs through the streamed transform) matches the host FDM."""
     import torch
 
     from paper_1512_01756_b200.configs import Config
     from paper_1512_01756_b200.problems import build_problem, load_batch
+    from tests.test_gpu_parity import compare_modes, oracle_systems, perturbed, run_jobs
 
     cfg = Config(f"w{n * m_z}", n, 4, m_z, 4.0, 1.0, 4, True, 100, modes=12, l_y=4.0)
     ps = build_problem(cfg, device="cuda")
     bs = load_batch(ctx, ps)
-    bd = load_batch(ctx, ps, spectral=False)
     rhs = torch.tensor(ps.b_S, device="cuda")
     rs = bs.solve(rhs, "dbj", 1e-10, 100, 0)
-    rd = bd.solve(rhs, "dbj", 1e-10, 100, 0)
-    assert all(rs.converged) and all(rd.converged)
-    assert max(abs(a - c) for a, c in zip(rd.iterations, rs.iterations)) <= 1
-    r = bd.apply_S(rs.x_S) - rhs
-    assert float((torch.linalg.norm(r, dim=1) / torch.linalg.norm(rhs, dim=1)).max()) < 1e-9
-    xd, xs = rd.x_S.cpu().numpy(), rs.x_S.cpu().numpy()
-    for i, mu in enumerate(ps.mus):
-        a, c = xd[i], xs[i]
-        if mu == 0.0:
-            a, c = a - a.mean(), c - c.mean()
-        assert np.linalg.norm(a - c) <= 1e-8 * np.linalg.norm(a), i
+    _, systems = oracle_systems(ps)
+    ns = len(systems)
+    rr = [ps.b_S, perturbed(ps.b_S, 1), perturbed(ps.b_S, 2)]
+    out = run_jobs([(systems[i], r[i], "dbj", 1e-10, 100) for r in rr for i in range(ns)])
+    rows, fails = compare_modes(rs, ps, out[:ns], [[out[ns + i], out[2 * ns + i]] for i in range(ns)])
+    assert not fails, fails
+    assert all(rs.converged)
     dev = build_problem(cfg, device="cuda", device_rhs=True)
     load_batch(ctx, dev)
     for i in range(len(ps.mus)):
