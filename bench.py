@@ -90,6 +90,16 @@ def dedup_layout(cfg):
     return cfg.k > 100_000
 
 
+def bench_config(cfg, args, sp):
+    """The workload description both arms print (identical by construction)."""
+    return {"workload": cfg.name,
+            "grid": f"n={cfg.n} (p={cfg.n - 1}), {cfg.m_x}x{cfg.m_z} elements, [0,{cfg.l_x:g}]x[0,{cfg.l_z:g}]",
+            "systems": max(cfg.modes, 1), "k_per_system": cfg.k, "fourier_modes": cfg.modes, "l_y": cfg.l_y,
+            "method": args.method, **sp,
+            "rhs": "seeded cosine-mode manufactured forcing, seed 1234, stream per mode (SURVEY §8(d))",
+            "l2": "no flush: every step streams > 10 GB (C5; C4 0.4 GB) through the 126 MB L2"}
+
+
 def sample_modes(cfg, count):
     """A bounded, labelled CPU sample of the config's systems: `count` modes evenly
     spaced over the batch.  C5: spaced over modes 16..255 -- the low modes 1..12
@@ -256,8 +266,10 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "sample_modes": modes, "method": args.method, **sp},
+        "scaling": "strong" if cfg.modes else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": bench_config(cfg, args, sp),
+        "solver": {"orthogonalization": "Householder (reference)", "sample_modes": modes,
+                   "parallelism": f"{th} host threads, one system each"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": "port",
                          "sample": f"{len(modes)} of {max(cfg.modes, 1)} {cfg.name} systems (modes {modes}) per "
                                    f"step; oracle port of the reference ({layout}, Householder GMRES), one system "
@@ -517,11 +529,8 @@ def run_ours(args, cfg):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong" if cfg.modes else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "grid": f"n={cfg.n} (p={cfg.n - 1}), {cfg.m_x}x{cfg.m_z} elements, "
-                                               f"[0,{cfg.l_x:g}]x[0,{cfg.l_z:g}]",
-                   "systems": nm if cfg.modes else 1, "k_per_system": cfg.k, "method": args.method,
-                   "orth": args.orth, "parallelism": f"modes sharded round-robin over {ws} GPU(s)",
-                   "l2": "no flush: each step touches ~0.4 GB (Krylov basis + work vectors) > 126 MB L2", **sp,
+        "config": bench_config(cfg, args, sp),
+        "solver": {"orth": args.orth, "parallelism": f"modes sharded round-robin over {ws} GPU(s)",
                    "mean_iterations": float(np.mean(its_all)), "max_iterations": float(np.max(its_all)),
                    "converged_systems": conv_all, "b_S": "device strip solves (schur_rhs)" if device_rhs(cfg)
                    else "host FDM", "setup_s_untimed": round(setup_s, 2),

@@ -121,8 +121,11 @@ class Problem:
         self.tau, self.h_x, self.h_z, self.eta = list(dinfo)
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().orc_problem_free(C.c_void_p(self.h))
+        if getattr(self, "h", None) and _lib is not None and C is not None:  # not at interpreter exit
+            try:
+                lib().orc_problem_free(C.c_void_p(self.h))
+            except Exception:
+                pass
             self.h = None
 
     def coords(self):
@@ -214,8 +217,11 @@ class System:
         self.coarse = None
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().orc_system_free(C.c_void_p(self.h))
+        if getattr(self, "h", None) and _lib is not None and C is not None:  # not at interpreter exit
+            try:
+                lib().orc_system_free(C.c_void_p(self.h))
+            except Exception:
+                pass
             self.h = None
 
     @property
@@ -311,8 +317,11 @@ class Coarse:
         self.h, self.d = h, d
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().orc_coarse_free(C.c_void_p(self.h))
+        if getattr(self, "h", None) and _lib is not None and C is not None:  # not at interpreter exit
+            try:
+                lib().orc_coarse_free(C.c_void_p(self.h))
+            except Exception:
+                pass
             self.h = None
 
     def info(self):

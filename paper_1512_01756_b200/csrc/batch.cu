@@ -1310,10 +1310,10 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
   double* zp = cout ? b->dzpart.p : nullptr;
   if (b->tune.spec_v2) {
     // pipelined pass (spec_op2_kernel): segments as long as ~32 warps per SM
-    // still allow (shorter halo), at least 2 and at most 16 blocks
+    // still allow (shorter halo), at least 4 and at most 16 blocks
     const long long nbk = b->nbf + (b->single ? 1 : 0);
     const long long warps = nbk * sp.nmc * lv.nslots;
-    int segb = static_cast<int>(std::max(2LL, std::min(16LL, warps / (32LL * b->ctx->num_sms))));
+    int segb = static_cast<int>(std::max(4LL, std::min(16LL, warps / (32LL * b->ctx->num_sms))));
     if (b->tune.segb > 0) segb = b->tune.segb;
     sp.segb = segb;
     sp.nseg = static_cast<int>((nbk + segb - 1) / segb);

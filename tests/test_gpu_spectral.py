@@ -101,7 +101,8 @@ def test_spectral_large_w(ctx, n, m_z):
     ns = len(systems)
     rr = [ps.b_S, perturbed(ps.b_S, 1), perturbed(ps.b_S, 2)]
     out = run_jobs([(systems[i], r[i], "dbj", 1e-10, 100) for r in rr for i in range(ns)])
-    rows, fails = compare_modes(rs, ps, out[:ns], [[out[ns + i], out[2 * ns + i]] for i in range(ns)])
+    rows, fails = compare_modes(rs, ps, out[:ns], [[out[ns + i], out[2 * ns + i]] for i in range(ns)],
+                                systems=systems)
     assert not fails, fails
     assert all(rs.converged)
     dev = build_problem(cfg, device="cuda", device_rhs=True)
