@@ -221,3 +221,34 @@ def test_c4_full_batch_self_consistent(ctx):
     r = b.apply_S(res.x_S) - bS
     rel = (torch.linalg.norm(r, dim=1) / torch.linalg.norm(bS, dim=1)).cpu().numpy()
     assert rel.max() < 1e-9
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_null_vectors_at_scale(ctx, name):
+    """u_S / u_L of the singular j = 0 system at full size (SURVEY §8(f)-3,
+    proj/src/nullspace.cpp:21-90): the reference's inverse iteration is out of
+    reach at C5 (r = 2.4M nodes), so the product's null vectors are held to the
+    defining properties through the C ABI: u_S^T S = 0 (smpm_apply_St),
+    ||u_S|| = 1, and the mode-0 right-hand side built with them is compatible
+    (u_S . b_S = 0) with a converged solve whose true residual is at tol."""
+    import torch
+
+    cfg = configs.CONFIGS[name]
+    ps = build_problem(cfg, [0, 1], device="cuda", device_rhs=True)
+    b = load_batch(ctx, ps)
+    uS = torch.tensor(ps.u_S, device="cuda")
+    assert abs(float(torch.linalg.norm(uS)) - 1.0) < 1e-12
+    v = torch.stack([uS, uS])
+    StU = b.apply_St(v)[0]
+    # ||S^T u_S|| relative to ||S^T|| ~ ||S^T v|| of a random unit v
+    rv = torch.randn_like(v)
+    rv /= torch.linalg.norm(rv, dim=1, keepdim=True)
+    scale = float(torch.linalg.norm(b.apply_St(rv)[0]))
+    assert float(torch.linalg.norm(StU)) <= 1e-11 * scale
+    bS = torch.tensor(ps.b_S, device="cuda")
+    assert abs(float(torch.dot(uS, bS[0]))) <= 1e-12 * float(torch.linalg.norm(bS[0]))
+    res = b.solve(bS, "dbj", 1e-10, 300, 0, history=False)
+    assert all(res.converged)
+    r = b.apply_S(res.x_S) - bS
+    assert float((torch.linalg.norm(r, dim=1) / torch.linalg.norm(bS, dim=1)).max()) < 1e-9

@@ -5,7 +5,12 @@ import io
 import subprocess
 import sys
 
-raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if sys.argv[1].endswith((".csv", ".csv.gz")):  # raw page exported on the GPU box (ncu -i X --page raw --csv)
+    import gzip
+
+    raw = (gzip.open if sys.argv[1].endswith(".gz") else open)(sys.argv[1], "rt").read()
+else:
+    raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
 col = {h: i for i, h in enumerate(hdr)}
