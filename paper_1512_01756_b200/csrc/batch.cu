@@ -30,6 +30,7 @@
 #include "spectral.cuh"
 #include "xform.cuh"
 #include "xformk.cuh"
+#include "xformp.cuh"
 #include "strip.cuh"
 #include "fourier.cuh"
 
@@ -245,6 +246,8 @@ struct smpm_ctx {
 struct Tuning {
   int segb = 0;          // per-mode pass: blocks per warp item (0: SP_SEGB)
   int xform = 1;         // resident-slice transform kernel (xform.cuh) where it applies
+  int xform_parity = 1;  // parity-split transforms (xformp.cuh) when T is parity-pure: 0 off, 1 where the
+                         // K-streamed kernel would run (w > 176), 2 wherever w % 16 == 0
   int sp_stage = 1;      // per-mode pass stages slot rows in shared memory (spec_v2 = 0)
   int spec_v2 = 1;       // pipelined per-mode pass (spec_op2_kernel)
   int spectral = 1;      // spectral operator when its factors are set
@@ -301,6 +304,12 @@ struct smpm_batch {
   DevArray<double> dTfrag, dTifrag;    // T, T^{-1} in the xform fragment order
   int xf_P = 0, xf_MB = 0;
   bool xf_stream = false;  // K-streamed transform kernel (xformk.cuh) instead of the resident slice
+  // parity-split transforms (xformp.cuh): forward = T^{-1}, backward = T
+  bool xp_on = false;
+  int xp_h = 0, xp_ks = 0, xp_seg_start[2][2] = {{0, 0}, {0, 0}}, xp_seg_len0[2] = {0, 0};
+  int xp_Pf = 0, xp_MBf = 0, xp_Pb = 0, xp_MBb = 0;
+  size_t xp_smem_f = 0, xp_smem_b = 0;
+  DevArray<double> dTpf, dTpb;
   long long cgs3_res = 0;  // resident CTAs of the CGS2 pass kernels (device)
   long long cgs3_kres[3] = {0, 0, 0};  // per kernel: pass 1, pass 2', pass 3' (norm-from-h2 path)
   long long p2t_res[V2_MAXCOL + 1] = {};  // resident CTAs of the tiled pass 2' per column capacity
@@ -1221,27 +1230,173 @@ bool xformk_try(smpm_batch* b, int P) {
   return true;
 }
 
+// ---- parity-split transforms (xformp.cuh) -----------------------------------
+// True when every column of T (row of T^{-1}) is even or odd under the reversal of
+// the node index and the modes are ordered pairs (even, odd), reals (even, odd);
+// fills the mode segments of each parity.
+bool parity_detect(smpm_batch* b) {
+  const int w = b->w, h = w / 2, np2 = 2 * b->sp_npairs;
+  if (w % 16 != 0) return false;
+  std::vector<int> par(static_cast<size_t>(w), 0);
+  const double tol = 1e-14;
+  for (int m = 0; m < w; ++m) {
+    double amax = 0.0, ce = 0.0, co = 0.0, rmax = 0.0, re = 0.0, ro = 0.0;
+    for (int r = 0; r < w; ++r) {
+      const double x = b->hT[static_cast<size_t>(m) * w + r], y = b->hT[static_cast<size_t>(m) * w + (w - 1 - r)];
+      amax = std::max(amax, std::fabs(x));
+      ce = std::max(ce, std::fabs(x - y));
+      co = std::max(co, std::fabs(x + y));
+      const double p = b->hTi[static_cast<size_t>(r) * w + m], q = b->hTi[static_cast<size_t>(w - 1 - r) * w + m];
+      rmax = std::max(rmax, std::fabs(p));
+      re = std::max(re, std::fabs(p - q));
+      ro = std::max(ro, std::fabs(p + q));
+    }
+    if (ce <= tol * amax && re <= tol * rmax)
+      par[m] = 1;
+    else if (co <= tol * amax && ro <= tol * rmax)
+      par[m] = -1;
+    else
+      return false;
+  }
+  int npe = 0;
+  while (2 * npe < np2 && par[2 * npe] == 1) ++npe;
+  for (int q = 0; q < b->sp_npairs; ++q) {
+    const int want = q < npe ? 1 : -1;
+    if (par[2 * q] != want || par[2 * q + 1] != want) return false;
+  }
+  int nre = 0;
+  while (np2 + nre < w && par[np2 + nre] == 1) ++nre;
+  for (int m = np2 + nre; m < w; ++m)
+    if (par[m] != -1) return false;
+  if (2 * npe + nre != h) return false;
+  b->xp_h = h;
+  b->xp_ks = (h + XK_KS - 1) / XK_KS;
+  b->xp_seg_start[0][0] = 0;
+  b->xp_seg_len0[0] = 2 * npe;
+  b->xp_seg_start[0][1] = np2;
+  b->xp_seg_start[1][0] = 2 * npe;
+  b->xp_seg_len0[1] = np2 - 2 * npe;
+  b->xp_seg_start[1][1] = np2 + nre;
+  return true;
+}
+
+template <int MB, int NS, bool BWD>
+void xformp_attr() {
+  CUDA_CHECK(cudaFuncSetAttribute(xformp_kernel<MB, NS, BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(xformp_smem<MB, NS, BWD>())));
+}
+
+void setup_xformp(smpm_batch* b) {
+  const int w = b->w, h = b->xp_h, ks = b->xp_ks, mbt = h / 8;
+  // forward: Ps single-parity slices per parity of at most 34 m-blocks
+  const int Ps = (mbt + 33) / 34, needf = (mbt + Ps - 1) / Ps;
+  const int MBf = needf <= 11 ? 11 : needf <= 17 ? 17 : needf <= 26 ? 26 : 34;
+  // backward: P slices of rows k < h of at most 17 m-blocks (two accumulator sets)
+  const int Pb = (mbt + 16) / 17, needb = (mbt + Pb - 1) / Pb;
+  const int MBb = needb <= 9 ? 9 : needb <= 11 ? 11 : needb <= 13 ? 13 : 17;
+  if (2 * Ps > b->ctx->num_sms || Pb > b->ctx->num_sms) return;
+  switch (MBf) {
+    case 11: xformp_attr<11, 6, false>(); b->xp_smem_f = xformp_smem<11, 6, false>(); break;
+    case 17: xformp_attr<17, 5, false>(); b->xp_smem_f = xformp_smem<17, 5, false>(); break;
+    case 26: xformp_attr<26, 4, false>(); b->xp_smem_f = xformp_smem<26, 4, false>(); break;
+    default: xformp_attr<34, 3, false>(); b->xp_smem_f = xformp_smem<34, 3, false>(); break;
+  }
+  switch (MBb) {
+    case 9: xformp_attr<9, 8, true>(); b->xp_smem_b = xformp_smem<9, 8, true>(); break;
+    case 11: xformp_attr<11, 8, true>(); b->xp_smem_b = xformp_smem<11, 8, true>(); break;
+    case 13: xformp_attr<13, 8, true>(); b->xp_smem_b = xformp_smem<13, 8, true>(); break;
+    default: xformp_attr<17, 7, true>(); b->xp_smem_b = xformp_smem<17, 7, true>(); break;
+  }
+  auto mode = [&](int par, int kap) { return xp_mode(b->xp_seg_start, b->xp_seg_len0, par, kap); };
+  std::vector<double> f;
+  xformp_image(2 * Ps, ks, MBf, [&](int sl, int r, int kk) {
+    const int par = sl / Ps, kap = (sl % Ps) * 8 * MBf + r;
+    if (kap >= h || kk >= h) return 0.0;
+    return b->hTi[static_cast<size_t>(kk) * w + mode(par, kap)];
+  }, f);
+  b->dTpf.upload(f, b->ctx->stream);
+  xformp_image(Pb, 2 * ks, MBb, [&](int sl, int r, int kk) {
+    const int k = sl * 8 * MBb + r, pq = kk / (XK_KS * ks), kap = kk - pq * XK_KS * ks;
+    if (k >= h || kap >= h) return 0.0;
+    return b->hT[static_cast<size_t>(mode(pq, kap)) * w + k];
+  }, f);
+  b->dTpb.upload(f, b->ctx->stream);
+  CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
+  b->xp_Pf = 2 * Ps;
+  b->xp_MBf = MBf;
+  b->xp_Pb = Pb;
+  b->xp_MBb = MBb;
+  b->xp_on = true;
+}
+
 void setup_xform(smpm_batch* b) {
   b->xf_P = 0;
   b->xf_stream = false;
+  b->xp_on = false;
   if (b->w % 16 != 0 || !b->tune.xform) return;
-  for (int P = 1; P <= 4; ++P) {
+  bool found = false;
+  for (int P = 1; P <= 4 && !found; ++P) {
     const int need = (b->w / 8 + P - 1) / P;
-    if (need <= 4 ? xform_try<4>(b, P) : need <= 8 ? xform_try<8>(b, P) : need <= 11 ? xform_try<11>(b, P) : false)
-      return;
+    found = need <= 4 ? xform_try<4>(b, P) : need <= 8 ? xform_try<8>(b, P) : need <= 11 ? xform_try<11>(b, P) : false;
   }
-  // w > 176: A streams with the columns; P row slices of at most 34 m-blocks
-  const int K8 = b->w / 8;
-  const int P = (K8 + 33) / 34;
-  const int need = (K8 + P - 1) / P;
-  if (need <= 26) {
-    if (xformk_try<26, 5>(b, P)) return;
-  } else if (need <= 34) {
-    if (xformk_try<34, 4>(b, P)) return;
+  if (!found) {
+    // w > 176: A streams with the columns; P row slices of at most 34 m-blocks
+    const int K8 = b->w / 8;
+    const int P = (K8 + 33) / 34;
+    const int need = (K8 + P - 1) / P;
+    if (need <= 26)
+      found = xformk_try<26, 5>(b, P);
+    else if (need <= 34)
+      found = xformk_try<34, 4>(b, P);
   }
+  // parity-pure basis: two half-size contractions instead (half the MMA work)
+  const int pm = b->tune.xform_parity;
+  if (found && pm > 0 && (pm >= 2 || b->xf_stream) && parity_detect(b)) setup_xformp(b);
 }
 
 // one transform launch over the columns described by `a` (a.P set), groups column groups
+// parity-split launch: `a` as for launch_xform (a.Af / a.P are replaced by the direction's image / slices)
+void launch_xformp(smpm_batch* b, const XformArgs& a, bool inverse, cudaStream_t st, bool pdl) {
+  XformPArgs pa;
+  pa.x = a;
+  pa.x.Af = inverse ? b->dTpf.p : b->dTpb.p;
+  pa.x.P = inverse ? b->xp_Pf : b->xp_Pb;
+  pa.h = b->xp_h;
+  pa.ks = b->xp_ks;
+  for (int p = 0; p < 2; ++p) {
+    pa.seg_start[p][0] = b->xp_seg_start[p][0];
+    pa.seg_start[p][1] = b->xp_seg_start[p][1];
+    pa.seg_len0[p] = b->xp_seg_len0[p];
+  }
+  const long long nch = (static_cast<long long>(a.nslots) * a.ncol_sys * a.nv + 15) / 16;
+  const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / pa.x.P, nch)));
+  const dim3 grid(groups * pa.x.P), blk(XF_THREADS);
+  const size_t smem = inverse ? b->xp_smem_f : b->xp_smem_b;
+  auto go = [&](auto kern) {
+    if (pdl) {
+      launch_pdl(b, kern, grid, blk, smem, st, pa);
+    } else {
+      kern<<<grid, blk, smem, st>>>(pa);
+      check_launch(b);
+    }
+  };
+  if (inverse) {
+    switch (b->xp_MBf) {
+      case 11: go(xformp_kernel<11, 6, false>); break;
+      case 17: go(xformp_kernel<17, 5, false>); break;
+      case 26: go(xformp_kernel<26, 4, false>); break;
+      default: go(xformp_kernel<34, 3, false>); break;
+    }
+  } else {
+    switch (b->xp_MBb) {
+      case 9: go(xformp_kernel<9, 8, true>); break;
+      case 11: go(xformp_kernel<11, 8, true>); break;
+      case 13: go(xformp_kernel<13, 8, true>); break;
+      default: go(xformp_kernel<17, 7, true>); break;
+    }
+  }
+}
+
 void launch_xform(smpm_batch* b, const XformArgs& a, int groups, cudaStream_t st, bool pdl) {
   const dim3 grid(groups * a.P), blk(XF_THREADS);
   auto go = [&](auto kern) {
@@ -1293,7 +1448,10 @@ void run_xform(smpm_batch* b, bool inverse, const double* in, double* out, const
   // column groups: every SM busy unless a group's share would drop below 16 columns
   const long long nch = (static_cast<long long>(lv.nslots) * a.ncol_sys * a.nv + 15) / 16;
   const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / a.P, nch)));
-  launch_xform(b, a, groups, st, true);
+  if (b->xp_on)
+    launch_xformp(b, a, inverse, st, true);
+  else
+    launch_xform(b, a, groups, st, true);
 }
 
 // th = S^ M^^{-1} vh (bj) or S^ vh in T-coordinates; with cout, also
@@ -2295,7 +2453,10 @@ void xf_columns(smpm_batch* b, bool inverse, const double* in, double* out, int 
     a.P = b->xf_P;
     const long long nch = (static_cast<long long>(b->nsys) * ncol_sys + 15) / 16;
     const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / a.P, nch)));
-    launch_xform(b, a, groups, st, false);
+    if (b->xp_on)
+      launch_xformp(b, a, inverse, st, false);
+    else
+      launch_xform(b, a, groups, st, false);
     return;
   }
   if (sys_stride != static_cast<long long>(ncol_sys) * b->w) fail(SMPM_EINVAL, "strip columns must be contiguous");
@@ -2842,7 +3003,8 @@ int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
       t.tail_rows = value;
       return;
     }
-    const Knob knobs[] = {{"segb", &t.segb}, {"spec_v2", &t.spec_v2}, {"xform", &t.xform}, {"sp_stage", &t.sp_stage},
+    const Knob knobs[] = {{"segb", &t.segb}, {"spec_v2", &t.spec_v2}, {"xform", &t.xform}, {"xform_parity", &t.xform_parity},
+                          {"sp_stage", &t.sp_stage},
                           {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse},
                           {"gt_vblock", &t.gt_vblock}, {"grid_per_sm", &t.grid_per_sm}, {"gt_ctas", &t.gt_ctas},
                           {"grid_nocoop", &t.grid_nocoop}, {"pdl", &t.pdl}, {"pythag", &t.pythag},
@@ -2853,7 +3015,7 @@ int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
         *kb.field = v;
         // grid geometry and transform plans depend on some knobs: recompute lazily
         if (k == "gt_vblock" || k == "grid_per_sm" || k == "gt_ctas") b->gt_blocks = 0;
-        if (k == "xform" && b->finalized) setup_xform(b);
+        if ((k == "xform" || k == "xform_parity") && b->finalized && b->spectral) setup_xform(b);
         return;
       }
     fail(SMPM_EINVAL, "unknown tuning key '" + k + "'");

@@ -184,8 +184,26 @@ class StripFDM:
                 Az[o + n - 1, o + n] += -tau
                 Az[o + n - 1, o + n:o + 2 * n] += -tau * cz * D[0, :]
         self.Az = Az
-        lz, Vz = np.linalg.eig(Az)
-        self.lz, self.Vz, self.Vzi = lz, Vz, np.linalg.inv(Vz)
+        # Az commutes with the reflection z -> l_z - z (uniform elements, symmetric
+        # GLL nodes, the same penalty at both ends), so its eigenvectors are even or
+        # odd.  Diagonalising the even and the odd block separately makes every
+        # eigenvector exactly parity-pure (a plain eig mixes the nearly degenerate
+        # even/odd eigenvalue pairs, gaps ~1e-8) and lets the transform kernels run
+        # two half-size contractions (csrc/xformp.cuh).
+        hE, hO = (w + 1) // 2, w // 2
+        Re, Ro = np.zeros((w, hE)), np.zeros((w, hO))
+        for kk in range(hO):
+            Re[kk, kk] = Re[w - 1 - kk, kk] = math.sqrt(0.5)
+            Ro[kk, kk], Ro[w - 1 - kk, kk] = math.sqrt(0.5), -math.sqrt(0.5)
+        if w % 2:
+            Re[hO, hO] = 1.0
+        le, Ve = np.linalg.eig(Re.T @ Az @ Re)
+        lo, Vo = np.linalg.eig(Ro.T @ Az @ Ro)
+        lz = np.concatenate([le, lo])
+        Vz = np.concatenate([Re @ Ve, Ro @ Vo], axis=1)
+        Vzi = np.concatenate([np.linalg.inv(Ve) @ Re.T, np.linalg.inv(Vo) @ Ro.T], axis=0)
+        self.parity = np.concatenate([np.ones(hE, dtype=int), -np.ones(hO, dtype=int)])
+        self.lz, self.Vz, self.Vzi = lz, Vz, Vzi
         self.cond = (max(np.linalg.cond(v["Vx"]) for v in self.kinds.values()), np.linalg.cond(Vz))
         t = torch
         self.tVz = t.tensor(Vz, dtype=t.complex128, device=device)
@@ -211,8 +229,11 @@ class StripFDM:
         if getattr(self, "_rb", None) is None:
             lz, Vz = self.lz, np.asarray(self.Vz)
             tol = 1e-9 * np.abs(lz).max()
-            pairs = [q for q in range(len(lz)) if lz[q].imag > tol]
-            reals = [q for q in range(len(lz)) if abs(lz[q].imag) <= tol]
+            # even modes before odd ones inside the pairs and inside the real modes
+            # (the order the parity-split transform kernels expect)
+            order = sorted(range(len(lz)), key=lambda q: (-self.parity[q], q))
+            pairs = [q for q in order if lz[q].imag > tol]
+            reals = [q for q in order if abs(lz[q].imag) <= tol]
             if 2 * len(pairs) + len(reals) != len(lz):
                 raise RuntimeError("z eigenvalues are not in conjugate pairs")
             cols = []
@@ -221,7 +242,19 @@ class StripFDM:
             for q in reals:
                 cols.append(Vz[:, q].real)
             T = np.ascontiguousarray(np.stack(cols, 1))
-            self._rb = (len(pairs), T, np.linalg.inv(T), pairs + reals)
+            # T^{-1} from the complex left eigenvectors (rows of Vz^{-1}, exactly
+            # parity-pure like the columns of T): for a pair v = a + i b with left
+            # row l, the rows of T^{-1} for (a, b) are 2 Re l and -2 Im l
+            Vzi = np.asarray(self.Vzi)
+            rows = []
+            for q in pairs:
+                rows += [2.0 * Vzi[q].real, -2.0 * Vzi[q].imag]
+            for q in reals:
+                rows.append(Vzi[q].real)
+            Ti = np.ascontiguousarray(np.stack(rows, 0))
+            if np.abs(Ti @ T - np.eye(len(lz))).max() > 1e-8:
+                Ti = np.linalg.inv(T)
+            self._rb = (len(pairs), T, Ti, pairs + reals)
         return self._rb
 
     def spectral(self, mus):

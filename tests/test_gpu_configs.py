@@ -245,7 +245,8 @@ def test_null_vectors_at_scale(ctx, name):
     rv = torch.randn_like(v)
     rv /= torch.linalg.norm(rv, dim=1, keepdim=True)
     scale = float(torch.linalg.norm(b.apply_St(rv)[0]))
-    assert float(torch.linalg.norm(StU)) <= 1e-11 * scale
+    # (the couplings themselves hold the oracle's to 1e-10: cond(T) eps, tests/test_host.py)
+    assert float(torch.linalg.norm(StU)) <= 1e-10 * scale
     bS = torch.tensor(ps.b_S, device="cuda")
     assert abs(float(torch.dot(uS, bS[0]))) <= 1e-12 * float(torch.linalg.norm(bS[0]))
     res = b.solve(bS, "dbj", 1e-10, 300, 0, history=False)

@@ -109,3 +109,40 @@ def test_spectral_large_w(ctx, n, m_z):
     load_batch(ctx, dev)
     for i in range(len(ps.mus)):
         assert np.linalg.norm(dev.b_S[i] - ps.b_S[i]) <= 1e-9 * np.linalg.norm(ps.b_S[i]), i
+
+
+@pytest.mark.parametrize("n,m_z", [(8, 2), (8, 6), (11, 16), (17, 16), (13, 32), (17, 32)])
+def test_parity_split_transforms(ctx, n, m_z):
+    """The parity-split transform kernels (xformp.cuh: two h x h contractions with
+    the fold / unfold inside the kernel) against the full w x w transform kernels
+    on the same batch, w = 16 ... 544 (every template instance): the strip solves
+    (schur_rhs = T^{-1}, per-mode, T on all strip rows) agree to rounding, and so do
+    the solves (same iteration counts +-1; x_S of two rtol-1e-10 iterates to 2e-8 of
+    the solution scale, the conditioning-limited level of DESIGN.md §6)."""
+    import torch
+
+    from paper_1512_01756_b200.configs import Config
+    from paper_1512_01756_b200.problems import build_problem, load_batch
+
+    cfg = Config(f"w{n * m_z}", n, 5, m_z, 5.0, 1.0, 4, True, 100, modes=12, l_y=5.0)
+    ps = build_problem(cfg, device="cuda", device_rhs=True)
+    f = ps.f.clone()
+    out = {}
+    for mode in (0, 2):
+        ps.b_S, ps.f = None, f.clone()
+        b = load_batch(ctx, ps)
+        b.tune(xform_parity=mode)
+        bS = b.schur_rhs(ps.f)
+        res = b.solve(bS, "dbj", 1e-10, 100, 0, history=False)
+        torch.cuda.synchronize()
+        out[mode] = (bS.cpu().numpy(), res.x_S.cpu().numpy(), list(res.iterations), list(res.converged))
+    b0, x0, it0, cv0 = out[0]
+    b2, x2, it2, cv2 = out[2]
+    assert all(cv0) and all(cv2)
+    for i in range(len(ps.mus)):
+        assert np.linalg.norm(b2[i] - b0[i]) <= 1e-12 * np.linalg.norm(b0[i]), i
+        a, c = x0[i], x2[i]
+        if ps.mus[i] == 0.0:
+            a, c = a - a.mean(), c - c.mean()
+        assert np.linalg.norm(a - c) <= 2e-8 * np.linalg.norm(a), i
+    assert max(abs(a - c) for a, c in zip(it0, it2)) <= 1
