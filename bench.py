@@ -284,30 +284,35 @@ def run_reference(args, cfg):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-def algorithmic_counts(cfg, its, grid_max=8):
+def algorithmic_counts(cfg, its, grid_max=8, parity=False, defer=False):
     """Algorithmic work of one batched solve from the per-system iteration counts
     `its`, per kernel class: [flops, bytes, bytes (implementation
     minimum)].
 
     Per system and Arnoldi step j (ncols = j + 1 basis vectors), spectral dbj path:
       transforms T^{-1}, T : two GEMMs of the w x w matrix with 2d columns
-                             -> 8 w^2 d flops; 4 k doubles of vectors
+                             -> 8 w^2 d flops (4 w^2 d executed when the basis is
+                             parity-pure: two half-size contractions each, `parity`);
+                             4 k doubles of vectors
       per-mode pass         : ~24 flops per (slot, mode); 2 k doubles
       orthogonalization     : §8(d) counts MGS, B = 8 k (j + 2) bytes, F = 4 (j + 1) k;
                               the CGS2 passes as implemented read V three times and
                               move 7 k doubles of vectors: 8 k (3 (j + 1) + 7) bytes,
-                              F = 8 (j + 1) k + 12 k
+                              F = 8 (j + 1) k + 12 k; with the reorthogonalisation update
+                              deferred into the next pass 1 (`defer`, vec4.cuh) two reads
+                              of V and 5 k vector doubles: 8 k (2 (j + 1) + 5) bytes
     A step runs in the grid-persistent tail when at most `grid_max` systems are live
     at its start, else in the per-stage kernels.  Outside the loop: final residual +
     solution recovery (~1.5 transform pairs and one per-mode pass per system)."""
     w, d, k = cfg.w, cfg.m_x - 1, cfg.k
     its = np.asarray(its, dtype=np.int64)
-    tr = (8.0 * w * w * d, 4.0 * k * 8, 4.0 * k * 8)
+    tr = ((4.0 if parity else 8.0) * w * w * d, 4.0 * k * 8, 4.0 * k * 8)
     sp = (24.0 * k, 2.0 * k * 8, 2.0 * k * 8)
     out = {c: [0.0, 0.0, 0.0] for c in ("grid_tail", "transform", "spectral_op", "orthogonalization")}
     for j in range(int(its.max()) if its.size else 0):
         live = int((its > j).sum())
-        cg = ((8.0 * (j + 1) + 12.0) * k, 8.0 * k * (j + 2), 8.0 * k * (3 * (j + 1) + 7))
+        cg = ((8.0 * (j + 1) + 12.0) * k, 8.0 * k * (j + 2),
+              8.0 * k * ((2 * (j + 1) + 5) if defer and live > grid_max else (3 * (j + 1) + 7)))
         if live <= grid_max:
             for q in range(3):
                 out["grid_tail"][q] += live * (tr[q] + sp[q] + cg[q])
@@ -323,9 +328,11 @@ def algorithmic_counts(cfg, its, grid_max=8):
 
 
 def roofline_kernel_name(cls):
-    return {"grid_tail": "arnoldi_grid_kernel", "transform": "xform_kernel / xformk_kernel (T^-1 / T)",
-            "spectral_op": "spec_op_kernel (per-mode pass)",
-            "orthogonalization": "cgs3_dot_kernel + cgs3_pass2n/2t_kernel + cgs3_pass3s_kernel (CGS2 passes)"}.get(cls, cls)
+    return {"grid_tail": "arnoldi_grid_kernel",
+            "transform": "xformp_kernel (parity-split T^-1 / T) / xform_kernel / xformk_kernel",
+            "spectral_op": "spec_op2_kernel (per-mode pass)",
+            "orthogonalization": "cgs4_pass1b/1bt_kernel + cgs3_pass2n/2t_kernel (deferred CGS2 passes; "
+                                 "cgs3_dot / cgs3_pass3s without deferral)"}.get(cls, cls)
 
 
 def measured_traffic(cls):
@@ -477,7 +484,8 @@ def run_ours(args, cfg):
     # ---- roofline of the dominant kernel class (live CUDA-event timing)
     per_solve_its = its_tot / args.steps
     gm_eff = min(8, 200_000 // cfg.k)
-    work = algorithmic_counts(cfg, np.rint(per_solve_its), grid_max=gm_eff)
+    parity, defer = bool(b.query("xform_parity")), bool(b.query("cgs_defer")) and args.method == "dbj"
+    work = algorithmic_counts(cfg, np.rint(per_solve_its), grid_max=gm_eff, parity=parity, defer=defer)
     classes = {}
     try:
         peak_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
@@ -510,7 +518,8 @@ def run_ours(args, cfg):
         extra = {"achieved_impl_min": ach_impl, "frac_impl_min": ach_impl / peak_hbm,
                  "bytes_note": "achieved/frac use SURVEY §8(d) algorithmic bytes (MGS: 8k(j+2) per system-step); "
                                "*_impl_min use the minimum the CGS2 passes as implemented must move "
-                               "(three reads of V plus 7k vector doubles: 8k(3(j+1)+7))"}
+                               + ("(deferred CGS2: two reads of V plus 5k vector doubles: 8k(2(j+1)+5))" if defer else
+                                  "(three reads of V plus 7k vector doubles: 8k(3(j+1)+7))")}
     roofline = {
         "kernel": roofline_kernel_name(dom),
         "class": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
@@ -532,7 +541,7 @@ def run_ours(args, cfg):
         "config": bench_config(cfg, args, sp),
         "solver": {"orth": args.orth, "parallelism": f"modes sharded round-robin over {ws} GPU(s)",
                    "mean_iterations": float(np.mean(its_all)), "max_iterations": float(np.max(its_all)),
-                   "converged_systems": conv_all, "b_S": "device strip solves (schur_rhs)" if device_rhs(cfg)
+                   "converged_systems": conv_all, "transform_parity_split": parity, "cgs2_deferred_update": defer, "b_S": "device strip solves (schur_rhs)" if device_rhs(cfg)
                    else "host FDM", "setup_s_untimed": round(setup_s, 2),
                    "gathered_solution_bytes": gathered_bytes},
         "gpu_launches": int(launches),

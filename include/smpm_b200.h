@@ -217,6 +217,17 @@ int smpm_two_level_schwarz_solve(smpm_batch* b, const double* b_S, double* x_S, 
  * host, max_iter + 2 (nullable).  CGS2, fused deflation, restart <= 126. */
 int smpm_solve_stacked(smpm_batch* b, int method, const double* b_S, double* x_S, const smpm_solve_options* opt,
                        smpm_report* report, double* history, void* stream);
+/* Stacked solve across GPUs: the stack's systems (Fourier modes) are spread over
+ * ranks, each rank holding its own batch; every inner product of the stacked
+ * GMRES (proj/src/helmholtz.cpp:187-246: norms, the two CGS2 reductions, the
+ * Arnoldi norm) is summed over the local systems and then over the ranks by
+ * `fn(user, device_buf, count, stream)`: an in-place sum all-reduce of `count`
+ * doubles at `device_buf`, ordered on `stream` (ncclAllReduce(buf, buf, count,
+ * ncclDouble, ncclSum, comm, stream) in a C++ caller).  It
+ * must return 0 and leave bitwise-identical results on every rank (NCCL does),
+ * so all ranks take the same stopping decisions.  fn = NULL: single rank. */
+typedef int (*smpm_allreduce_fn)(void* user, double* device_buf, int count, void* stream);
+int smpm_batch_set_allreduce(smpm_batch* b, smpm_allreduce_fn fn, void* user);
 /* Same as smpm_solve with HOST b_S / x_S: the H2D and D2H copies are inside
  * the call (the reference-facing end-to-end path). */
 int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x_S_host,
@@ -237,13 +248,20 @@ int smpm_batch_profile(smpm_batch* b, int enable, double* ms, long long* counts,
 
 /* Performance knobs of a batch (no reference counterpart; defaults are the
  * measured-best settings). Keys: segb, spec_v2, xform, sp_stage, spectral, spec_2las,
- * p2fuse, gt_vblock, grid_per_sm, gt_ctas, grid_nocoop (profilers only: the
+ * p2fuse, cgs_defer, xform_parity, gt_vblock, grid_per_sm, gt_ctas, grid_nocoop (profilers only: the
  * tail then launches without the co-residency guarantee of a cooperative
  * launch), pdl, pythag, grid, grid_max, tail_rows (the tail runs only while
  * live systems x k <= tail_rows; default 200000), post_fuse, early; with b = NULL:
  * fy_tile (transverse FFT). SMPM_EINVAL for an unknown key. The library reads
  * no environment variables. */
 int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value);
+/* Which kernels a finalized batch runs (instrumentation for bench.py's work
+ * accounting). Keys: xform_kernel (0 tiled contraction plan, 1 resident-slice
+ * transform, 2 K-streamed transform, 3 parity-split transform), xform_parity
+ * (1 when T is parity-pure and the transforms run as two half-size
+ * contractions), cgs_defer (1 when the deferred CGS2 passes apply to fused dbj
+ * solves), spectral (1 when the spectral operator form is active). */
+int smpm_batch_query(const smpm_batch* b, const char* key, long long* value);
 /* Phase-trace dump of the grid-persistent tail into `path` (appended; NULL or
  * "" off): which = 0 per-step phase timestamps, 1 per-CTA timestamps. */
 int smpm_batch_set_trace(smpm_batch* b, int which, const char* path);

@@ -27,13 +27,17 @@ EXPORTS = [
     "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_batch_launch_count",
     "smpm_batch_profile", "smpm_fp64_peak", "smpm_batch_set_strip_factors", "smpm_schur_rhs",
     "smpm_recover_solution", "smpm_solve_stacked", "smpm_fourier_y", "smpm_inverse_fourier_y",
-    "smpm_batch_load_schur_blocks", "smpm_batch_set_tuning", "smpm_batch_set_trace",
+    "smpm_batch_load_schur_blocks", "smpm_batch_set_tuning", "smpm_batch_query", "smpm_batch_set_trace", "smpm_batch_set_allreduce",
 ]
 # smpm_batch_set_tuning keys (include/smpm_b200.h)
-TUNING_KEYS = ["segb", "spec_v2", "xform", "xform_parity", "sp_stage", "spectral", "spec_2las", "p2fuse", "gt_vblock", "grid_per_sm", "gt_ctas",
+TUNING_KEYS = ["segb", "spec_v2", "xform", "xform_parity", "sp_stage", "spectral", "spec_2las", "p2fuse", "cgs_defer", "gt_vblock", "grid_per_sm", "gt_ctas",
                "grid_nocoop", "pdl", "pythag", "grid", "grid_max", "tail_rows", "post_fuse", "early"]
 PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other", "reserved5", "grid_tail",
                    "spectral_op", "transform", "reserved"]
+
+
+# smpm_allreduce_fn: int fn(void* user, double* device_buf, int count, void* stream)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p)
 
 
 class SmpmError(RuntimeError):
@@ -130,6 +134,8 @@ def lib():
     L.smpm_inverse_fourier_y.argtypes = [llp, ip, dp, dp, vp]
     L.smpm_recover_solution.argtypes = [vp, dp, dp, dp, vp]
     L.smpm_batch_set_tuning.argtypes = [vp, C.c_char_p, llp]
+    L.smpm_batch_set_allreduce.argtypes = [vp, ALLREDUCE_FN, vp]
+    L.smpm_batch_query.argtypes = [vp, C.c_char_p, C.POINTER(C.c_longlong)]
     L.smpm_batch_set_trace.argtypes = [vp, ip, C.c_char_p]
     _lib = L
     return L

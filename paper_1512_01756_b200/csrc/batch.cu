@@ -26,6 +26,7 @@
 #include "vec.cuh"
 #include "vec2.cuh"
 #include "vec3.cuh"
+#include "vec4.cuh"
 #include "grid.cuh"
 #include "spectral.cuh"
 #include "xform.cuh"
@@ -253,6 +254,7 @@ struct Tuning {
   int spectral = 1;      // spectral operator when its factors are set
   int spec_2las = 1;     // spectral operator for 2LAS
   int p2fuse = 1;        // CGS2 pass 2 single-read fusion
+  int cgs_defer = 1;     // CGS2 reorthogonalisation update deferred into the next pass 1 (vec4.cuh): 2 reads of V
   int gt_vblock = 2;     // grid tail V-row block: 0 off, 1 ring size, 2 as large as 2 CTAs/SM allow
   int grid_per_sm = 2;   // grid tail CTAs per SM (cap)
   int gt_ctas = 0;       // grid tail CTA cap (0: none)
@@ -315,6 +317,13 @@ struct smpm_batch {
   long long p2t_res[V2_MAXCOL + 1] = {};  // resident CTAs of the tiled pass 2' per column capacity
   bool p2t_attr = false;
   int jhost = 0;  // Arnoldi index of the next step (all live systems of a cycle share it)
+  // stacked solve across ranks: the caller's all-reduce (NCCL over NVLink) and its buffer
+  smpm_allreduce_fn ar_fn = nullptr;
+  void* ar_user = nullptr;
+  DevArray<double> dstack;
+  bool pending = false;  // deferred CGS2: the newest basis vector is still the pending pair (w', h2) (vec4.cuh)
+  bool p1bt_attr = false;
+  long long p1b_res = 0, p1bt_res[V2_MAXCOL + 1] = {};  // resident CTAs of the pass 1B kernels
   bool pythag = true;  // norm from the second CGS2 reduction (cgs3_pass2n / cgs3_pass3s); tuning pythag
   bool pdl = true;  // programmatic dependent launch for the Arnoldi step chain (tuning pdl)
   size_t xf_smem = 0;
@@ -1575,6 +1584,77 @@ int apply_op(smpm_batch* b, const SolveCfg& c, const double* vin, double* wout, 
   fail(SMPM_EINVAL, "unknown method");
 }
 
+// ---- stacked solve: sums over all systems (vec.cuh); with an all-reduce hook
+// (smpm_batch_set_allreduce) the systems of the stack are spread over ranks and
+// every sum is all-reduced across them (one all-reduce per inner product,
+// proj/src/helmholtz.cpp:187-246 run across GPUs)
+void stack_allreduce(smpm_batch* b, int count, cudaStream_t st) {
+  const int rc = b->ar_fn(b->ar_user, b->dstack.p, count, st);
+  if (rc != 0) fail(SMPM_ERUNTIME, "all-reduce hook failed (" + std::to_string(rc) + ")");
+}
+void stack_sum(smpm_batch* b, double* v, cudaStream_t st) {
+  if (!b->ar_fn) {
+    launch_pdl(b, stack_sum_kernel, dim3(1), dim3(128), 0, st, b->nsys, v);
+    return;
+  }
+  stack_sum_local_kernel<<<1, 32, 0, st>>>(b->nsys, v, b->dstack.p);
+  check_launch(b);
+  stack_allreduce(b, 1, st);
+  stack_sum_bcast_kernel<<<1, 128, 0, st>>>(b->nsys, v, b->dstack.p);
+  check_launch(b);
+}
+void stack_h(smpm_batch* b, double* h, cudaStream_t st) {
+  if (!b->ar_fn) {
+    launch_pdl(b, stack_h_kernel, dim3(1), dim3(128), 0, st, b->G, h);
+    return;
+  }
+  stack_h_local_kernel<<<1, 128, 0, st>>>(b->G, h, b->dstack.p);
+  check_launch(b);
+  stack_allreduce(b, b->jhost + 1, st);
+  stack_h_bcast_kernel<<<1, 128, 0, st>>>(b->G, h, b->dstack.p);
+  check_launch(b);
+}
+void stack_givens(smpm_batch* b, cudaStream_t st) {
+  if (!b->ar_fn) {
+    launch_pdl(b, stack_givens_kernel, dim3(b->nsys), dim3(32), 0, st, b->G);
+    return;
+  }
+  stack_sum_local_kernel<<<1, 32, 0, st>>>(b->nsys, b->G.snsq, b->dstack.p);
+  check_launch(b);
+  stack_allreduce(b, 1, st);
+  stack_givens_global_kernel<<<b->nsys, 32, 0, st>>>(b->G, b->dstack.p);
+  check_launch(b);
+}
+
+// row chunking of a CGS2 pass kernel for `nslots` live systems: (live systems x chunks)
+// <= the kernel's resident CTA count `res` (one wave)
+GmState_ cgs3_chunked(smpm_batch* b, long long res, int nslots, dim3& g) {
+  GmState_ Gk = b->G;
+  const long long kc = std::max(1LL, res / std::max(1, nslots));
+  long long ck = (b->k + kc - 1) / kc;
+  ck = std::max(256LL, (ck + 255) / 256 * 256);
+  Gk.chunk = static_cast<int>(ck);
+  Gk.nchunk = static_cast<int>((b->k + ck - 1) / ck);
+  g = dim3(Gk.nchunk, nslots);
+  return Gk;
+}
+
+// deferred CGS2: materialise the pending basis vector (pass 3': v = (w' - V h2) / nrm
+// into the basis and the operator input) before a path that needs it
+void flush_pending(smpm_batch* b, int nslots, cudaStream_t st) {
+  if (!b->pending) return;
+  b->pending = false;
+  if (nslots <= 0) return;
+  if (b->cgs3_kres[2] == 0) {
+    int o = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs3_pass3s_kernel, V3_THREADS, 0));
+    b->cgs3_kres[2] = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
+  }
+  dim3 g3;
+  const GmState_ G3 = cgs3_chunked(b, b->cgs3_kres[2], nslots, g3);
+  launch_pdl(b, cgs3_pass3s_kernel, g3, dim3(V3_THREADS), 0, st, G3, b->dV.p, b->vbuf[3].p, b->vbuf[2].p);
+}
+
 void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t st) {
   GmState_& G = b->G;
   double* V = b->dV.p;
@@ -1585,15 +1665,20 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
   const bool fuse_into_cgs = c.method == SMPM_DBJ && c.fused && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= V2_MAXCOL;
   double* cbuf = b->dcoarse.p + static_cast<size_t>(b->nsys) * b->d;
   const double* tdefl = nullptr;
+  // deferred CGS2 (vec4.cuh): after a cycle's first step the newest basis vector stays
+  // pending as (w', h2); the operator runs on w' and pass 1B forms the vector
+  const bool defer = fuse_into_cgs && b->tune.cgs_defer && !G.stacked && b->pythag;
+  const bool pend = defer && b->pending;
+  const double* opin = pend ? wv : vin;
   if (fuse_into_cgs && spec_ok(b, c)) {
     // spectral: t = S M^{-1} v and c = C^{-1} Z^T t from the per-mode pass
     double* t = b->vbuf[5].p;
-    spec_SMinv(b, true, vin, t, cbuf, lv, st);
+    spec_SMinv(b, true, opin, t, cbuf, lv, st);
     tdefl = t;
   } else if (fuse_into_cgs) {
     double* u = b->vbuf[4].p;
     double* t = b->vbuf[5].p;
-    op_BJ(b, vin, u, lv, st);
+    op_BJ(b, opin, u, lv, st);
     op_S(b, u, t, lv, st);
     run_deflate(b, DEFL_COARSE, t, nullptr, nullptr, cbuf, lv, st);
     tdefl = t;
@@ -1655,21 +1740,46 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
         CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[2], cgs3_pass3s_kernel, V3_THREADS, 0));
         for (int i = 0; i < 3; ++i) b->cgs3_kres[i] = std::max(1, o[i]) * b->ctx->num_sms;
       }
-      auto chunked = [&](long long res, dim3& g) {
-        GmState_ Gk = G;
-        const long long kc = std::max(1LL, res / lv.nslots);
-        long long ck = (b->k + kc - 1) / kc;
-        ck = std::max(256LL, (ck + 255) / 256 * 256);
-        Gk.chunk = static_cast<int>(ck);
-        Gk.nchunk = static_cast<int>((b->k + ck - 1) / ck);
-        g = dim3(Gk.nchunk, lv.nslots);
-        return Gk;
-      };
+      auto chunked = [&](long long res, dim3& g) { return cgs3_chunked(b, res, lv.nslots, g); };
       dim3 g1, g2, g3;
       const GmState_ G1 = chunked(b->cgs3_kres[0], g1), G2 = chunked(b->cgs3_kres[1], g2),
                      G3 = chunked(b->cgs3_kres[2], g3);
-      launch_pdl(b, cgs3_dot_kernel, g1, dim3(V3_THREADS), 0, st, G1, V, wv, tdefl, P, cbuf);
       const int ncols_h = b->jhost + 1;
+      if (pend) {
+        // pass 1B: v_j = (w' - V h2) / nrm -> V[:, j], w = (P t) / nrm, h1 = [V, v_j]^T w
+        const int nold = b->jhost;
+        if (nold <= 2 * V3_GRP) {
+          if (b->p1b_res == 0) {
+            int o = 0;
+            CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs4_pass1b_kernel, V3_THREADS, 0));
+            b->p1b_res = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
+          }
+          dim3 gb;
+          const GmState_ Gb = chunked(b->p1b_res, gb);
+          launch_pdl(b, cgs4_pass1b_kernel, gb, dim3(V3_THREADS), 0, st, Gb, V, wv, tdefl, 1, P,
+                     static_cast<const double*>(cbuf));
+        } else {
+          const size_t smem = sizeof(double) * p1bt_smem_doubles(nold);
+          if (!b->p1bt_attr) {
+            size_t mx = 0;
+            for (int cc = 2 * V3_GRP + 1; cc <= 8 * P2T_MAXC; ++cc) mx = std::max(mx, p1bt_smem_doubles(cc));
+            CUDA_CHECK(cudaFuncSetAttribute(cgs4_pass1bt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(sizeof(double) * mx)));
+            b->p1bt_attr = true;
+          }
+          if (b->p1bt_res[nold] == 0) {
+            int o = 0;
+            CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs4_pass1bt_kernel, V3_THREADS, smem));
+            b->p1bt_res[nold] = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
+          }
+          dim3 gb;
+          const GmState_ Gb = chunked(b->p1bt_res[nold], gb);
+          launch_pdl(b, cgs4_pass1bt_kernel, gb, dim3(V3_THREADS), smem, st, Gb, V, wv, tdefl, 1, P,
+                     static_cast<const double*>(cbuf));
+        }
+      } else {
+        launch_pdl(b, cgs3_dot_kernel, g1, dim3(V3_THREADS), 0, st, G1, V, wv, tdefl, P, cbuf);
+      }
       if (b->tune.p2fuse && ncols_h > 2 * V3_GRP && ncols_h <= 8 * P2T_MAXC && ncols_h <= G.m + 1) {
         // more than 16 columns: update and dots in one read of V through
         // shared-memory row tiles (cgs3_pass2t_kernel)
@@ -1695,16 +1805,19 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
         launch_pdl(b, cgs3_pass2n_kernel, g2, dim3(V3_THREADS), 0, st, G2, static_cast<const double*>(V), wv,
                    b->tune.p2fuse ? 1 : 0);
       }
-      launch_pdl(b, cgs3_pass3s_kernel, g3, dim3(V3_THREADS), 0, st, G3, V, wv, vin);
+      if (defer)
+        b->pending = true;  // v_{j+1} is formed by the next step's pass 1B (or flush_pending)
+      else
+        launch_pdl(b, cgs3_pass3s_kernel, g3, dim3(V3_THREADS), 0, st, G3, V, wv, vin);
       ++b->jhost;
       return;
     }
     launch_pdl(b, cgs3_dot_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, tdefl, P, cbuf);
-    if (G.stacked) launch_pdl(b, stack_h_kernel, dim3(1), dim3(128), 0, st, G, G.h1);
+    if (G.stacked) stack_h(b, G.h1, st);
     launch_pdl(b, cgs3_update_kernel<false>, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv);
-    if (G.stacked) launch_pdl(b, stack_h_kernel, dim3(1), dim3(128), 0, st, G, G.h2);
+    if (G.stacked) stack_h(b, G.h2, st);
     launch_pdl(b, cgs3_update_kernel<true>, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv);
-    if (G.stacked) launch_pdl(b, stack_givens_kernel, dim3(b->nsys), dim3(32), 0, st, G);
+    if (G.stacked) stack_givens(b, st);
   }
   (void)hsm;
   dim3 sg(std::max(1, std::min(G.nchunk, 64)), lv.nslots);
@@ -1944,9 +2057,6 @@ bool arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
   return true;
 }
 
-void stack_sum(smpm_batch* b, double* v, cudaStream_t st) {
-  launch_pdl(b, stack_sum_kernel, dim3(1), dim3(128), 0, st, b->nsys, v);
-}
 
 // xS_host (optional, pinned): also deliver x_S to the host; with the early epilogue the
 // rows of the early systems are copied while the grid tail runs
@@ -2025,6 +2135,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   G.alist = alist;
   G.acount = acount;
   b->jhost = 0;
+  b->pending = false;
 
   int steps = 0;
   // ---- Arnoldi steps; device flags are polled one step behind the launches
@@ -2061,6 +2172,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   auto restart = [&](int ncycv) {
     ++cycles;
     b->jhost = 0;
+    b->pending = false;  // the cycle's last vector is never needed
     // ---- restart (GMRES(m) extension): x += V y ; r = b - op(x) ; new cycle
     select_state_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, GM_CYCLE, dsel);
     check_launch(b);
@@ -2154,6 +2266,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       CUDA_CHECK(cudaEventRecord(b->eev[2], b->st2));
       early_done = true;
     }
+    flush_pending(b, nrun, st);  // the tail starts from a materialised v_j
     return arnoldi_grid(b, c, alist, acount, st);
   };
   int cur = 0;
@@ -2311,6 +2424,8 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       CUDA_CHECK(cudaMemcpyAsync(xS_host, xS, sizeof(double) * nk, cudaMemcpyDeviceToHost, st));
     }
   }
+  // stacked across ranks: the true residual of the whole stack (every entry becomes the global sum)
+  if (c.stacked && b->ar_fn && c.final_check) stack_sum(b, nrf, st);
   // report data: queued on the stream into pinned staging (one host wait)
   const size_t rep_ints = static_cast<size_t>(ns) * 8, rep_dbl = static_cast<size_t>(ns) * (8 + (m + 1) + 3);
   const size_t rep_hist = history ? static_cast<size_t>(ns) * G.histcap : 0;
@@ -2358,7 +2473,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       if (c.final_check && bn > 0) {
         // stacked: the true residual of the stacked vector (proj/src/gmres.cpp:129-136)
         double r2 = hsm[static_cast<size_t>(2 * ns) + s];
-        if (c.stacked) {
+        if (c.stacked && !b->ar_fn) {
           r2 = 0.0;
           for (int t = 0; t < ns; ++t) r2 += hsm[static_cast<size_t>(2 * ns) + t];
         }
@@ -3005,7 +3120,7 @@ int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
     }
     const Knob knobs[] = {{"segb", &t.segb}, {"spec_v2", &t.spec_v2}, {"xform", &t.xform}, {"xform_parity", &t.xform_parity},
                           {"sp_stage", &t.sp_stage},
-                          {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse},
+                          {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse}, {"cgs_defer", &t.cgs_defer},
                           {"gt_vblock", &t.gt_vblock}, {"grid_per_sm", &t.grid_per_sm}, {"gt_ctas", &t.gt_ctas},
                           {"grid_nocoop", &t.grid_nocoop}, {"pdl", &t.pdl}, {"pythag", &t.pythag},
                           {"grid", &t.grid}, {"grid_max", &t.grid_max}, {"post_fuse", &t.post_fuse},
@@ -3019,6 +3134,32 @@ int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
         return;
       }
     fail(SMPM_EINVAL, "unknown tuning key '" + k + "'");
+  });
+}
+
+int smpm_batch_set_allreduce(smpm_batch* b, smpm_allreduce_fn fn, void* user) {
+  return guard([&] {
+    if (!b) fail(SMPM_EINVAL, "null batch");
+    b->ar_fn = fn;
+    b->ar_user = user;
+    if (fn) b->dstack.alloc(static_cast<size_t>(V2_MAXCOL + 2));
+  });
+}
+
+int smpm_batch_query(const smpm_batch* b, const char* key, long long* value) {
+  return guard([&] {
+    if (!b || !key || !value) fail(SMPM_EINVAL, "null argument");
+    const std::string k(key);
+    if (k == "xform_kernel")
+      *value = !b->spectral || b->xf_P == 0 ? 0 : b->xp_on ? 3 : b->xf_stream ? 2 : 1;
+    else if (k == "xform_parity")
+      *value = b->spectral && b->xp_on ? 1 : 0;
+    else if (k == "cgs_defer")
+      *value = b->tune.cgs_defer && b->tune.pythag ? 1 : 0;
+    else if (k == "spectral")
+      *value = b->spectral && b->tune.spectral ? 1 : 0;
+    else
+      fail(SMPM_EINVAL, "unknown query key '" + k + "'");
   });
 }
 

@@ -752,6 +752,44 @@ __global__ void stack_h_kernel(GmState_ G, double* __restrict__ h) {
   }
 }
 
+// ---- stacked solve across ranks (one all-reduce per inner product): the local sums
+// go to a small buffer, the caller's all-reduce hook sums it over the ranks, and the
+// result is broadcast to every local system.  Same local summation order as the
+// single-rank kernels above.
+__global__ void stack_sum_local_kernel(int nsys, const double* __restrict__ v, double* __restrict__ buf) {
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int t = 0; t < nsys; ++t) a += v[t];
+    buf[0] = a;
+  }
+}
+__global__ void stack_sum_bcast_kernel(int nsys, double* __restrict__ v, const double* __restrict__ buf) {
+  for (int s = threadIdx.x; s < nsys; s += blockDim.x) v[s] = buf[0];
+}
+__global__ void stack_h_local_kernel(GmState_ G, const double* __restrict__ h, double* __restrict__ buf) {
+  const int stride = G.m + 2;
+  const int ncols = G.jcyc[0] + 1;
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+    double a = 0.0;
+    for (int t = 0; t < G.nsys; ++t) a += h[static_cast<long long>(t) * stride + c];
+    buf[c] = a;
+  }
+}
+__global__ void stack_h_bcast_kernel(GmState_ G, double* __restrict__ h, const double* __restrict__ buf) {
+  const int stride = G.m + 2;
+  const int ncols = G.jcyc[0] + 1;
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+    const double a = buf[c];
+    for (int t = 0; t < G.nsys; ++t) h[static_cast<long long>(t) * stride + c] = a;
+  }
+}
+// Givens step of every system from the all-reduced ||w||^2 in buf[0]
+__global__ void stack_givens_global_kernel(GmState_ G, const double* __restrict__ buf) {
+  const int s = blockIdx.x;
+  if (!G.active[s]) return;
+  givens_step(G, s, G.jcyc[s], sqrt(buf[0]));
+}
+
 // global ||w|| from the per-system squares, then the Givens step of every system (warp each)
 __global__ void stack_givens_kernel(GmState_ G) {
   pdl_wait();

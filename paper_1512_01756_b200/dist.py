@@ -65,3 +65,44 @@ def max_over_ranks(values, device=None, group=None):
     t = torch.tensor(values, dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return t.tolist()
+
+
+class _DevPtr:
+    """A device buffer of `count` doubles as a zero-copy torch view (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def allreduce_hook(group=None):
+    """All-reduce hook for SchurBatch.set_allreduce: the stacked solve's inner
+    products summed over the ranks of `group` (NCCL over NVLink on GPUs), one
+    all-reduce per inner product (proj/src/helmholtz.cpp:187-246 across GPUs).
+
+    The library passes its own device buffer and the stream its kernels run on;
+    torch's NCCL all_reduce orders itself after the current stream's work and
+    makes the current stream wait for the result, so the hook runs it under
+    that stream.  NCCL leaves bitwise-identical sums on every rank, which the
+    stacked solve relies on (all ranks take the same stopping decisions)."""
+    import torch
+    import torch.distributed as dist
+
+    def hook(ptr: int, count: int, stream: int):
+        buf = torch.as_tensor(_DevPtr(ptr, count), device="cuda")
+        ext = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        with torch.cuda.stream(ext):
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+
+    return hook
+
+
+def stacked_norm(local_sq, group=None):
+    """sqrt of the sum over ranks of a rank's partial squared norms (host helper
+    for callers assembling the stacked right-hand-side norm themselves)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.as_tensor(local_sq, dtype=torch.float64).sum().reshape(1).clone()
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return float(t.sqrt())

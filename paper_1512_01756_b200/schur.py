@@ -338,6 +338,38 @@ class SchurBatch:
             check(lib().smpm_batch_set_tuning(self.h, k.encode(), int(v)))
         return self
 
+    def set_allreduce(self, fn):
+        """Stacked solve across ranks (smpm_batch_set_allreduce): fn(ptr, count,
+        stream) sums `count` doubles at device pointer `ptr` in place over the
+        ranks, ordered on CUDA stream `stream`; None: single rank.  See
+        dist.nccl_allreduce_hook."""
+        from ._lib import ALLREDUCE_FN
+
+        if fn is None:
+            self._ar = None
+            check(lib().smpm_batch_set_allreduce(self.h, C.cast(None, ALLREDUCE_FN), None))
+            return self
+
+        def thunk(_user, ptr, count, stream):
+            try:
+                fn(int(ptr), int(count), int(stream or 0))
+                return 0
+            except Exception:  # the C side turns a non-zero return into SMPM_ERUNTIME
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        self._ar = ALLREDUCE_FN(thunk)  # keep the callback alive
+        check(lib().smpm_batch_set_allreduce(self.h, self._ar, None))
+        return self
+
+    def query(self, key: str) -> int:
+        """Which kernels this batch runs (smpm_batch_query), e.g. query("xform_parity")."""
+        v = C.c_longlong()
+        check(lib().smpm_batch_query(self.h, key.encode(), C.byref(v)))
+        return int(v.value)
+
     def trace(self, which: int, path):
         """Grid-tail phase trace into `path` (smpm_batch_set_trace); None: off."""
         check(lib().smpm_batch_set_trace(self.h, int(which), path.encode() if path else None))

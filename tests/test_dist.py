@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1512_01756_b200.dist import gather_modes, max_over_ranks, mode_owners, shard_modes
+from paper_1512_01756_b200.dist import gather_modes, max_over_ranks, mode_owners, shard_modes, stacked_norm
 
 
 def test_shard_modes_partition():
@@ -98,3 +98,28 @@ def test_gloo_two_ranks_balanced(tmp_path):
     full = np.load(path)
     ref = _solve_modes(list(range(nmodes)))
     assert np.array_equal(full, ref)
+
+
+def _norm_worker(rank, world, port, path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(11)
+    v = rng.standard_normal((5, 40))
+    mine = shard_modes(5, world, rank)
+    n = stacked_norm([float(v[m] @ v[m]) for m in mine])
+    np.save(f"{path}.{rank}.npy", np.array([n, float(np.sqrt((v * v).sum()))]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_stacked_norm(tmp_path):
+    """The stacked right-hand-side norm over mode-sharded ranks (the reduction the
+    stacked solve's all-reduce hook performs per inner product): identical on
+    both ranks and equal to the single-process norm."""
+    port = 29900 + (os.getpid() % 1000)
+    path = str(tmp_path / "n")
+    mp.spawn(_norm_worker, args=(2, port, path), nprocs=2, join=True)
+    a, b = np.load(path + ".0.npy"), np.load(path + ".1.npy")
+    assert a[0] == b[0]
+    assert abs(a[0] - a[1]) <= 1e-14 * a[1]

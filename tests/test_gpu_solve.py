@@ -98,3 +98,43 @@ def test_restart_not_converging_reaches_max_iter(ctx, orth, method):
     assert ref.iterations == 60 and not ref.converged
     assert res.iterations[0] == 60, res.iterations
     assert not res.converged[0]
+
+
+@pytest.mark.parametrize("spectral", [False, True])
+@pytest.mark.parametrize("grid", [0, 1])
+def test_cgs_defer_modes(ctx, spectral, grid):
+    """Deferred CGS2 (vec4.cuh: the reorthogonalisation update formed inside the
+    next step's first pass, two reads of V per step) against the oracle, in the
+    per-stage kernels all the way (grid = 0: register pass 1B up to 16 columns,
+    tiled beyond) and with the hand-over to the grid tail (grid = 1: the pending
+    vector is materialised first), restarted and not; and against the three-pass
+    form (cgs_defer = 0) of the same batch: same iteration counts +-1."""
+    import torch
+
+    mus = [(2 * np.pi * j / 6.0) ** 2 for j in range(14)]
+    case = build_case(8, 6, 4, 6.0, 1.0, mus, kmax=4, decay=True)
+    b = gpu_batch(ctx, case, spectral=spectral)
+    b.tune(grid=grid, cgs_defer=1)
+    r1 = check_solve(case, b, "dbj", max_iter=100)
+    check_solve(case, b, "dbj", max_iter=120, restart=7)
+    b.tune(cgs_defer=0)
+    r0 = b.solve(torch.tensor(case.b_S, device="cuda"), "dbj", 1e-10, 100, 0)
+    assert max(abs(a - c) for a, c in zip(r0.iterations, r1.iterations)) <= 1
+    x0, x1 = r0.x_S.cpu().numpy(), r1.x_S.cpu().numpy()
+    for i in range(len(mus)):
+        a, c = x0[i], x1[i]
+        if mus[i] == 0.0:
+            a, c = a - a.mean(), c - c.mean()
+        assert np.linalg.norm(a - c) <= 2e-8 * np.linalg.norm(a), i
+
+
+def test_cgs_defer_long_basis(ctx):
+    """Solves that need 20 - 50 basis vectors in the per-stage kernels (short, tall
+    elements: the block-Jacobi preconditioner is weak): the tiled pass 1B (more
+    than 16 old columns) against the oracle."""
+    mus = [0.0] + [(2 * np.pi * j / 4.0) ** 2 for j in range(1, 10)]
+    case = build_case(6, 16, 8, 4.0, 1.0, mus, kmax=4, decay=True)
+    b = gpu_batch(ctx, case, spectral=True)
+    b.tune(grid=0)
+    res = check_solve(case, b, "dbj", max_iter=120)
+    assert max(res.iterations) > 40, res.iterations
