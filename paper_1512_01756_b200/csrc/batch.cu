@@ -254,6 +254,8 @@ struct Tuning {
   int spectral = 1;      // spectral operator when its factors are set
   int spec_2las = 1;     // spectral operator for 2LAS
   int p2fuse = 1;        // CGS2 pass 2 single-read fusion
+  int cgs_lanes = 1;     // CGS2 passes beyond 16 columns: eight lanes per row in registers (vec4.cuh) instead of
+                         // shared-memory row tiles
   int cgs_defer = 1;     // CGS2 reorthogonalisation update deferred into the next pass 1 (vec4.cuh): 2 reads of V
   int gt_vblock = 2;     // grid tail V-row block: 0 off, 1 ring size, 2 as large as 2 CTAs/SM allow
   int grid_per_sm = 2;   // grid tail CTAs per SM (cap)
@@ -324,6 +326,7 @@ struct smpm_batch {
   bool pending = false;  // deferred CGS2: the newest basis vector is still the pending pair (w', h2) (vec4.cuh)
   bool p1bt_attr = false;
   long long p1b_res = 0, p1bt_res[V2_MAXCOL + 1] = {};  // resident CTAs of the pass 1B kernels
+  long long p2l_res = 0, p1bl_res = 0;                  // ... of the lane-shared-row kernels
   bool pythag = true;  // norm from the second CGS2 reduction (cgs3_pass2n / cgs3_pass3s); tuning pythag
   bool pdl = true;  // programmatic dependent launch for the Arnoldi step chain (tuning pdl)
   size_t xf_smem = 0;
@@ -1758,6 +1761,16 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
           const GmState_ Gb = chunked(b->p1b_res, gb);
           launch_pdl(b, cgs4_pass1b_kernel, gb, dim3(V3_THREADS), 0, st, Gb, V, wv, tdefl, 1, P,
                      static_cast<const double*>(cbuf));
+        } else if (b->tune.cgs_lanes) {
+          if (b->p1bl_res == 0) {
+            int o = 0;
+            CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs5_pass1bl_kernel, V3_THREADS, 0));
+            b->p1bl_res = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
+          }
+          dim3 gb;
+          const GmState_ Gb = chunked(b->p1bl_res, gb);
+          launch_pdl(b, cgs5_pass1bl_kernel, gb, dim3(V3_THREADS), 0, st, Gb, V, wv, tdefl, 1, P,
+                     static_cast<const double*>(cbuf));
         } else {
           const size_t smem = sizeof(double) * p1bt_smem_doubles(nold);
           if (!b->p1bt_attr) {
@@ -1780,7 +1793,18 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
       } else {
         launch_pdl(b, cgs3_dot_kernel, g1, dim3(V3_THREADS), 0, st, G1, V, wv, tdefl, P, cbuf);
       }
-      if (b->tune.p2fuse && ncols_h > 2 * V3_GRP && ncols_h <= 8 * P2T_MAXC && ncols_h <= G.m + 1) {
+      if (b->tune.p2fuse && b->tune.cgs_lanes && ncols_h > 2 * V3_GRP && ncols_h <= LN_MAXCOL &&
+          ncols_h <= G.m + 1) {
+        // more than 16 columns: update and dots in one read of V, eight lanes per row (cgs5_pass2l_kernel)
+        if (b->p2l_res == 0) {
+          int o = 0;
+          CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs5_pass2l_kernel, V3_THREADS, 0));
+          b->p2l_res = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
+        }
+        dim3 g2l;
+        const GmState_ G2l = chunked(b->p2l_res, g2l);
+        launch_pdl(b, cgs5_pass2l_kernel, g2l, dim3(V3_THREADS), 0, st, G2l, static_cast<const double*>(V), wv);
+      } else if (b->tune.p2fuse && ncols_h > 2 * V3_GRP && ncols_h <= 8 * P2T_MAXC && ncols_h <= G.m + 1) {
         // more than 16 columns: update and dots in one read of V through
         // shared-memory row tiles (cgs3_pass2t_kernel)
         const size_t smem = sizeof(double) * p2t_smem_doubles(ncols_h);
@@ -3120,7 +3144,7 @@ int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
     }
     const Knob knobs[] = {{"segb", &t.segb}, {"spec_v2", &t.spec_v2}, {"xform", &t.xform}, {"xform_parity", &t.xform_parity},
                           {"sp_stage", &t.sp_stage},
-                          {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse}, {"cgs_defer", &t.cgs_defer},
+                          {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse}, {"cgs_defer", &t.cgs_defer}, {"cgs_lanes", &t.cgs_lanes},
                           {"gt_vblock", &t.gt_vblock}, {"grid_per_sm", &t.grid_per_sm}, {"gt_ctas", &t.gt_ctas},
                           {"grid_nocoop", &t.grid_nocoop}, {"pdl", &t.pdl}, {"pythag", &t.pythag},
                           {"grid", &t.grid}, {"grid_max", &t.grid_max}, {"post_fuse", &t.post_fuse},

@@ -400,26 +400,33 @@ __global__ void __launch_bounds__(V3_THREADS, CGS3_MINB) cgs3_pass2n_kernel(GmSt
 // lane l rows l, l + 32, ... of the tile).  Same reduction tree for every
 // launch and batch: deterministic.  Returns this thread's ||w1||^2 part.
 constexpr int P2T_MAXC = 16;  // columns per warp in the dots phase (ncols <= 8 * 16)
-__host__ __device__ __forceinline__ int p2t_rows(int ncols) { return ncols <= 32 ? 128 : ncols <= 64 ? 64 : 32; }
+// Tile rows and ring depth: a tile is ~25 KB, and NS - 1 tiles per CTA are in
+// flight while one is consumed (2 CTAs/SM: ~150 KB in flight per SM; the measured
+// loaded HBM latency of ~2 us needs ~100 KB per SM for full bandwidth — the
+// two-deep ring of round 1 had 40 KB in flight and ran at 0.45 of HBM).
+// (ring <= ~100 KB so that two CTAs fit an SM)
+__host__ __device__ __forceinline__ int p2t_rows(int ncols) { return ncols <= 23 ? 128 : ncols <= 46 ? 64 : 32; }
+__host__ __device__ __forceinline__ int p2t_stages(int ncols) { return ncols <= 93 ? 4 : 3; }
 __host__ __device__ __forceinline__ size_t p2t_smem_doubles(int cap) {
-  const int tr = p2t_rows(cap);
-  return 2 * static_cast<size_t>(tr) * cap + 2 * tr + 4 * tr + tr;
+  const int tr = p2t_rows(cap), ns = p2t_stages(cap);
+  return static_cast<size_t>(ns) * tr * cap + static_cast<size_t>(ns) * tr + 4 * tr + tr;
 }
 
+template <int NS>
 __device__ __forceinline__ double pass2_tiled(const double* __restrict__ Vs, long long k, int ncols,
                                               const double* hs, double* ws, int r0, int r1, double* sm,
                                               double (&acc)[P2T_MAXC]) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int TR = p2t_rows(ncols);
-  double* tile = sm;                                     // [2][ncols][TR]
-  double* wt = tile + 2 * static_cast<size_t>(TR) * ncols;  // [2][TR]
-  double* qp = wt + 2 * TR;                              // [4][TR]
-  double* nvs = qp + 4 * TR;                             // [TR]
+  double* tile = sm;                                               // [NS][ncols][TR]
+  double* wt = tile + static_cast<size_t>(NS) * TR * ncols;        // [NS][TR]
+  double* qp = wt + NS * TR;                                       // [4][TR]
+  double* nvs = qp + 4 * TR;                                       // [TR]
   const int ntile = (r1 - r0 + TR - 1) / TR;
   const int pieces = TR / 2;  // 16-byte pieces per column segment
   auto issue = [&](int it) {
     const int a = r0 + it * TR;
-    double* tb = tile + static_cast<size_t>(it & 1) * TR * ncols;
+    double* tb = tile + static_cast<size_t>(it % NS) * TR * ncols;
     for (int p = t; p < ncols * pieces; p += V3_THREADS) {
       const int c = p / pieces, q = p - c * pieces;
       const int r = a + 2 * q;
@@ -427,22 +434,25 @@ __device__ __forceinline__ double pass2_tiled(const double* __restrict__ Vs, lon
     }
     for (int q = t; q < pieces; q += V3_THREADS) {
       const int r = a + 2 * q;
-      cp_async16(wt + (it & 1) * TR + 2 * q, ws + (r < r1 ? r : r0), r < r1);
+      cp_async16(wt + (it % NS) * TR + 2 * q, ws + (r < r1 ? r : r0), r < r1);
     }
   };
   double sq = 0.0;
-  issue(0);
-  cp_async_commit();
+#pragma unroll
+  for (int s0 = 0; s0 < NS - 1; ++s0) {
+    if (s0 < ntile) issue(s0);
+    cp_async_commit();
+  }
   const int quarter = t >> 6, qrow = t & 63;
   const int qc = (ncols + 3) >> 2;  // columns per quarter (contiguous ranges)
   const int c0q = quarter * qc, c1q = min(ncols, c0q + qc);
   for (int it = 0; it < ntile; ++it) {
-    if (it + 1 < ntile) issue(it + 1);
+    if (it + NS - 1 < ntile) issue(it + NS - 1);  // into the slot consumed in iteration it - 1
     cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<NS - 1>();
     __syncthreads();
-    const double* tb = tile + static_cast<size_t>(it & 1) * TR * ncols;
-    const double* wb = wt + (it & 1) * TR;
+    const double* tb = tile + static_cast<size_t>(it % NS) * TR * ncols;
+    const double* wb = wt + (it % NS) * TR;
     // update partials: quarter sums of V[r][c] h[c], c ascending
     for (int r = qrow; r < TR; r += 64) {
       double a0 = 0.0, a1 = 0.0;
@@ -474,7 +484,7 @@ __device__ __forceinline__ double pass2_tiled(const double* __restrict__ Vs, lon
         for (int r = lane; r < TR; r += 32) acc[i] = fma(col[r], nvs[r], acc[i]);
       }
     }
-    __syncthreads();  // the tile buffer and nvs are refilled next
+    __syncthreads();  // the tile slot, qp and nvs are reused next
   }
   cp_async_wait<0>();
   return sq;
@@ -508,7 +518,8 @@ __global__ void __launch_bounds__(V3_THREADS, 2) cgs3_pass2t_kernel(GmState_ G, 
     double acc[P2T_MAXC];
 #pragma unroll
     for (int i = 0; i < P2T_MAXC; ++i) acc[i] = 0.0;
-    sq = pass2_tiled(Vs, G.k, ncols, hs, ws, r0, r1, p2t_sm, acc);
+    sq = p2t_stages(ncols) == 4 ? pass2_tiled<4>(Vs, G.k, ncols, hs, ws, r0, r1, p2t_sm, acc)
+                                : pass2_tiled<3>(Vs, G.k, ncols, hs, ws, r0, r1, p2t_sm, acc);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int i = 0; i < P2T_MAXC; ++i) {
