@@ -261,7 +261,7 @@ struct Tuning {
   int grid_per_sm = 2;   // grid tail CTAs per SM (cap)
   int gt_ctas = 0;       // grid tail CTA cap (0: none)
   int grid_nocoop = 0;   // opt-in: plain (non-cooperative) cluster launch of the tail, for profilers only
-  int pdl = 1;           // programmatic dependent launch of the step chain
+  int pdl = -1;          // programmatic dependent launch of the step chain: 1 on, 0 off, -1 auto (on for k <= 100,000)
   int pythag = 1;        // norm from the second CGS2 reduction
   int grid = 1;          // grid-persistent tail
   int grid_max = 8;      // live systems at which the tail takes over
@@ -2087,7 +2087,11 @@ bool arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
 void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_report* reps, double* history,
            cudaStream_t st, double* xS_host = nullptr) {
   need_final(b);
-  b->pdl = b->tune.pdl != 0;
+  // programmatic dependent launch hides launch latency when the step's kernels are short
+  // (C4: +4 %); at C5 sizes (k = 277,440, ms-scale kernels) dependents that become resident
+  // early only take SM resources from the running kernel (measured -5 %): auto = off above
+  // 100,000 unknowns per system
+  b->pdl = b->tune.pdl < 0 ? b->k <= 100000 : b->tune.pdl != 0;
   b->pythag = b->tune.pythag != 0;
   if (c.max_iter < 1) fail(SMPM_EINVAL, "max_iter must be >= 1");
   const int mtot = static_cast<int>(std::min<long long>(c.max_iter, b->k));

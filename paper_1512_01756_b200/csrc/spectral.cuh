@@ -457,7 +457,6 @@ __global__ void __launch_bounds__(SP_THREADS, 4) spec_op2_kernel(SpecParams sp, 
                                                               double* __restrict__ th, DeflateParams P, double* zpart,
                                                               int* counter, double* cout, double* __restrict__ uh) {
   pdl_wait();
-  pdl_launch();
   extern __shared__ double sm2[];  // 2 d doubles (coarse solve)
   int s;
   if (!defl_slot(P, blockIdx.y, s)) return;
@@ -466,6 +465,7 @@ __global__ void __launch_bounds__(SP_THREADS, 4) spec_op2_kernel(SpecParams sp, 
   if (sg < sp.nseg)
     spec_warp_item2<BJ>(sp, s, mc, sg, vh, th, zpart ? zpart + (static_cast<long long>(s) * sp.nmc + mc) * sp.d : nullptr,
                         uh);
+  pdl_launch();  // dependents may start launching: this CTA's main work is done
   if (!zpart) return;
   if (!last_cta(counter + s, sp.nmc * nsg)) return;
   double* sums = sm2;

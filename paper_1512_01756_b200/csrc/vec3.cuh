@@ -233,7 +233,6 @@ __global__ void __launch_bounds__(V3_THREADS, 3) cgs3_dot_kernel(GmState_ G, con
                                                               const double* __restrict__ tdefl, DeflateParams P,
                                                               const double* __restrict__ cbuf) {
   pdl_wait();
-  pdl_launch();
   __shared__ double red[V3_THREADS / 32][V3_GRP];
   int s;
   if (!gm_slot(G, blockIdx.y, s)) return;
@@ -255,6 +254,7 @@ __global__ void __launch_bounds__(V3_THREADS, 3) cgs3_dot_kernel(GmState_ G, con
   } else {
     cta_dots_long(V + s * G.vstride, G.k, ncols, ws, r0, r1, part, red);
   }
+  pdl_launch();  // the row work is done: dependents may start launching
   if (last_cta(G.counter + s, G.nchunk))
     reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols,
                  G.h1 + static_cast<long long>(s) * stride);
@@ -264,7 +264,6 @@ __global__ void __launch_bounds__(V3_THREADS, 3) cgs3_dot_kernel(GmState_ G, con
 template <bool NORM>
 __global__ void __launch_bounds__(V3_THREADS) cgs3_update_kernel(GmState_ G, const double* __restrict__ V, double* w) {
   pdl_wait();
-  pdl_launch();
   __shared__ double hs[V2_MAXCOL];
   __shared__ double red[V3_THREADS / 32][V3_GRP];
   int s;
@@ -285,6 +284,7 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_update_kernel(GmState_ G, con
   if (!NORM) {
     __syncthreads();
     cta_dots_long(Vs, G.k, ncols, ws, r0, r1, part, red);
+    pdl_launch();  // the row work is done: dependents may start launching
     if (last_cta(G.counter + s, G.nchunk))
       reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols,
                    G.h2 + static_cast<long long>(s) * stride);
@@ -315,7 +315,6 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_update_kernel(GmState_ G, con
 __global__ void __launch_bounds__(V3_THREADS, CGS3_MINB) cgs3_pass2n_kernel(GmState_ G, const double* __restrict__ V, double* w,
                                                                  int fuse) {
   pdl_wait();
-  pdl_launch();
   __shared__ double hs[V2_MAXCOL];
   __shared__ double red[V3_THREADS / 32][V3_GRP];
   int s;
@@ -376,6 +375,7 @@ __global__ void __launch_bounds__(V3_THREADS, CGS3_MINB) cgs3_pass2n_kernel(GmSt
     for (int q = 0; q < V3_THREADS / 32; ++q) tsum += red[q][0];
     part[ncols] = tsum;
   }
+  pdl_launch();  // the row work is done: dependents may start launching
   if (!last_cta(G.counter + s, G.nchunk)) return;
   double* h2 = G.h2 + static_cast<long long>(s) * stride;
   reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols + 1, h2);
@@ -495,7 +495,6 @@ __device__ __forceinline__ double pass2_tiled(const double* __restrict__ Vs, lon
 __global__ void __launch_bounds__(V3_THREADS, 2) cgs3_pass2t_kernel(GmState_ G, const double* __restrict__ V, double* w,
                                                                  int cap) {
   pdl_wait();
-  pdl_launch();
   extern __shared__ __align__(16) double p2t_sm[];
   __shared__ double hs[V2_MAXCOL];
   __shared__ double red[V3_THREADS / 32][V3_GRP];
@@ -540,6 +539,7 @@ __global__ void __launch_bounds__(V3_THREADS, 2) cgs3_pass2t_kernel(GmState_ G, 
     for (int q = 0; q < V3_THREADS / 32; ++q) tsum += red[q][0];
     part[ncols] = tsum;
   }
+  pdl_launch();  // the row work is done: dependents may start launching
   if (!last_cta(G.counter + s, G.nchunk)) return;
   double* h2 = G.h2 + static_cast<long long>(s) * stride;
   reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols + 1, h2);
@@ -560,7 +560,6 @@ __global__ void __launch_bounds__(V3_THREADS, 2) cgs3_pass2t_kernel(GmState_ G, 
 __global__ void __launch_bounds__(V3_THREADS) cgs3_pass3s_kernel(GmState_ G, double* __restrict__ V, double* w,
                                                                  double* __restrict__ vin) {
   pdl_wait();
-  pdl_launch();
   __shared__ double hs[V2_MAXCOL];
   int s;
   if (!gm_slot(G, blockIdx.y, s)) return;
@@ -584,6 +583,7 @@ __global__ void __launch_bounds__(V3_THREADS) cgs3_pass3s_kernel(GmState_ G, dou
     rows_update_nr<4, 4, true>(Vs, G.k, ncols, hs, ws, r0, r1, inv, col, vs);
   else
     rows_update_nr<2, V3_GRP, true>(Vs, G.k, ncols, hs, ws, r0, r1, inv, col, vs);
+  pdl_launch();
 }
 
 }  // namespace smpm

@@ -159,7 +159,6 @@ __global__ void __launch_bounds__(V3_THREADS, CGS3_MINB) cgs4_pass1b_kernel(GmSt
                                                                             DeflateParams P,
                                                                             const double* __restrict__ cbuf) {
   pdl_wait();
-  pdl_launch();
   __shared__ double hs[2 * V3_GRP];
   __shared__ double red[V3_THREADS / 32][V3_GRP];
   int s;
@@ -172,6 +171,7 @@ __global__ void __launch_bounds__(V3_THREADS, CGS3_MINB) cgs4_pass1b_kernel(GmSt
   } else {
     pass1b_body(G, V, w, t, XVal{}, s, hs, red);
   }
+  pdl_launch();
 }
 
 // ---- pass 1B beyond 16 old columns: shared-memory row tiles (as pass2_tiled) ----
@@ -310,7 +310,6 @@ __global__ void __launch_bounds__(V3_THREADS, 2) cgs4_pass1bt_kernel(GmState_ G,
                                                                      const double* __restrict__ t, int defl,
                                                                      DeflateParams P, const double* __restrict__ cbuf) {
   pdl_wait();
-  pdl_launch();
   extern __shared__ __align__(16) double p1bt_sm[];
   __shared__ double hs[V2_MAXCOL];
   __shared__ double red[V3_THREADS / 32];
@@ -324,6 +323,7 @@ __global__ void __launch_bounds__(V3_THREADS, 2) cgs4_pass1bt_kernel(GmState_ G,
   } else {
     pass1bt_body(G, V, w, t, XVal{}, s, hs, red, p1bt_sm);
   }
+  pdl_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -476,7 +476,6 @@ __device__ __forceinline__ void lanes_dispatch(const double* __restrict__ Vs, lo
 // pass 2' for 16 < ncols <= 128 (w -= V h1; h2 = V^T w; ||w||^2; Givens in the last CTA)
 __global__ void __launch_bounds__(V3_THREADS, 2) cgs5_pass2l_kernel(GmState_ G, const double* __restrict__ V, double* w) {
   pdl_wait();
-  pdl_launch();
   __shared__ double hs[V2_MAXCOL];
   __shared__ double red[(V3_THREADS / 32) * LN_RED];
   int s;
@@ -494,6 +493,7 @@ __global__ void __launch_bounds__(V3_THREADS, 2) cgs5_pass2l_kernel(GmState_ G, 
   double* ws = w + s * G.k;
   double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
   lanes_dispatch<false>(Vs, G.k, ncols, hs, ws, nullptr, XVal{}, 1.0, nullptr, r0, r1, part, red);
+  pdl_launch();  // the row work is done: dependents may start launching
   if (!last_cta(G.counter + s, G.nchunk)) return;
   double* h2 = G.h2 + static_cast<long long>(s) * stride;
   reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, ncols + 1, h2);
@@ -514,7 +514,6 @@ __global__ void __launch_bounds__(V3_THREADS, 2) cgs5_pass1bl_kernel(GmState_ G,
                                                                      const double* __restrict__ t, int defl,
                                                                      DeflateParams P, const double* __restrict__ cbuf) {
   pdl_wait();
-  pdl_launch();
   __shared__ double hs[V2_MAXCOL];
   __shared__ double red[(V3_THREADS / 32) * LN_RED];
   int s;
@@ -541,6 +540,7 @@ __global__ void __launch_bounds__(V3_THREADS, 2) cgs5_pass1bl_kernel(GmState_ G,
   } else {
     lanes_dispatch<true>(Vs, G.k, nold, hs, ws, ts, XVal{}, inv, col, r0, r1, part, red);
   }
+  pdl_launch();  // the row work is done: dependents may start launching
   if (last_cta(G.counter + s, G.nchunk))
     reduce_parts(G.part + static_cast<long long>(s) * G.nchunk * stride, G.nchunk, stride, nold + 1,
                  G.h1 + static_cast<long long>(s) * stride);

@@ -204,7 +204,6 @@ __device__ __forceinline__ void xf_warp(const XformArgs& a, const double* Af, do
 template <int MB>
 __global__ void __launch_bounds__(XF_THREADS, 1) xform_kernel(XformArgs a) {
   pdl_wait();
-  pdl_launch();
   extern __shared__ __align__(16) double xf_smem[];
   const int t = threadIdx.x, warp = t >> 5;
   const int K8 = a.w >> 3;
@@ -230,6 +229,7 @@ __global__ void __launch_bounds__(XF_THREADS, 1) xform_kernel(XformArgs a) {
     xf_warp<MB, MB0>(a, Af, ring, c0, c1, row0, 0, cps);
   else
     xf_warp<MB, MB - MB0>(a, Af, ring, c0, c1, row0, MB0, cps);
+  pdl_launch();  // dependents may start launching: this CTA's main work is done
 }
 
 }  // namespace smpm

@@ -142,7 +142,6 @@ __device__ __forceinline__ void xk_warp(const XformArgs& a, double* ring, unsign
 template <int MB, int NS>
 __global__ void __launch_bounds__(XF_THREADS, 1) xformk_kernel(XformArgs a) {
   pdl_wait();
-  pdl_launch();
   extern __shared__ __align__(128) double xk_smem[];
   constexpr int STAGE = xk_astage(MB) + XK_BSTAGE;
   double* ring = xk_smem;
@@ -168,6 +167,7 @@ __global__ void __launch_bounds__(XF_THREADS, 1) xformk_kernel(XformArgs a) {
     xk_warp<MB, MB0, NS>(a, ring, full, c0, c1, row0, 0, cps, Aslice);
   else
     xk_warp<MB, MB - MB0, NS>(a, ring, full, c0, c1, row0, MB0, cps, Aslice);
+  pdl_launch();  // dependents may start launching: this CTA's main work is done
 }
 
 template <int MB, int NS>

@@ -233,7 +233,6 @@ __device__ __forceinline__ void xp_warp(const XformPArgs& pa, double* ring, unsi
 template <int MB, int NS, bool BWD>
 __global__ void __launch_bounds__(XF_THREADS, 1) xformp_kernel(XformPArgs pa) {
   pdl_wait();
-  pdl_launch();
   extern __shared__ __align__(128) double xp_smem[];
   const XformArgs& a = pa.x;
   constexpr int STAGE = xk_astage(MB) + (BWD ? XK_BSTAGE : 2 * XK_BSTAGE);
@@ -259,6 +258,7 @@ __global__ void __launch_bounds__(XF_THREADS, 1) xformp_kernel(XformPArgs pa) {
     xp_warp<MB, MB0, NS, BWD>(pa, ring, full, c0, c1, slice, 0, cps, Aslice);
   else
     xp_warp<MB, MB - MB0, NS, BWD>(pa, ring, full, c0, c1, slice, MB0, cps, Aslice);
+  pdl_launch();  // dependents may start launching: this CTA's main work is done
 }
 
 template <int MB, int NS, bool BWD>
