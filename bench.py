@@ -187,7 +187,7 @@ def oracle_systems_from(ps, idx, threads):
     systems = []
     for i in idx:
         ref_layout = not dedup_layout(cfg)
-        s = O.System(prob, ps.mus[i], ref_layout, kinds=(ps.GW[i], ps.GI[i], ps.GE[i]))
+        s = O.System(prob, ps.mus[i], ref_layout, kinds=ps.kinds(i))
         s.build_bj(2 if ref_layout else 1)
         s.build_coarse(ps.u_S if ps.mus[i] == 0.0 else None)
         systems.append(s)
@@ -381,7 +381,7 @@ def run_ours(args, cfg):
     # but plateau modes' iteration counts move with O(1e-13) changes of b_S
     # (DESIGN.md §6), so each workload keeps one fixed b_S
     t_setup = time.perf_counter()
-    ps = build_problem(cfg, modes, device=f"cuda:{local}", device_rhs=device_rhs(cfg))
+    ps = build_problem(cfg, modes, device=f"cuda:{local}", device_rhs=device_rhs(cfg), device_setup=device_rhs(cfg))
     ctx = Context(local)
     b = load_batch(ctx, ps)
     if args.tune:
@@ -541,7 +541,9 @@ def run_ours(args, cfg):
         "config": bench_config(cfg, args, sp),
         "solver": {"orth": args.orth, "parallelism": f"modes sharded round-robin over {ws} GPU(s)",
                    "mean_iterations": float(np.mean(its_all)), "max_iterations": float(np.max(its_all)),
-                   "converged_systems": conv_all, "transform_parity_split": parity, "cgs2_deferred_update": defer, "b_S": "device strip solves (schur_rhs)" if device_rhs(cfg)
+                   "converged_systems": conv_all,
+                   "setup": "device (smpm_batch_set_fdm: couplings, block inverses, coarse data by the library's own "
+                            "kernels)" if ps.GW is None else "host/torch FDM couplings (smpm_batch_set_couplings)", "transform_parity_split": parity, "cgs2_deferred_update": defer, "b_S": "device strip solves (schur_rhs)" if device_rhs(cfg)
                    else "host FDM", "setup_s_untimed": round(setup_s, 2),
                    "gathered_solution_bytes": gathered_bytes},
         "gpu_launches": int(launches),

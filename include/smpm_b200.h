@@ -184,6 +184,21 @@ typedef struct {
   const double* mu;        /* nsys Helmholtz shifts k_j^2 (0: Poisson) */
 } smpm_strip_factors;
 int smpm_batch_set_strip_factors(smpm_batch* b, const smpm_strip_factors* f);
+/* Device-side per-mode setup: INSTEAD of per-system couplings
+ * (smpm_batch_set_couplings) and spectral diagonals (smpm_batch_set_spectral) the
+ * caller hands over the geometry-level fast-diagonalisation factors once — the
+ * shared z eigenbasis T, T^{-1} (w x w, column-major, npairs complex pairs first)
+ * and the strip factors with the per-system shifts mu — and smpm_batch_finalize
+ * builds, with this library's own kernels, for every system: the spectral
+ * diagonals gamma(mu), the dense couplings G_kind = T diag(gamma) T^{-1}
+ * (replacing build_kind_coupling's LU per kind, proj/src/schur.cpp:19-69, and the
+ * per-shift real-Schur solves, proj/src/helmholtz.cpp:58-143), the block-Jacobi
+ * inverses K^{-1} = T diag(kinv) T^{-1} (replacing the LU of build_block_jacobi,
+ * proj/src/schur.cpp:188-216), the strip row sums and the coarse matrix
+ * (proj/src/deflation.cpp:24-69).  Also stores the strip factors (as
+ * smpm_batch_set_strip_factors).  Needs w % 16 == 0.  The singular system's left
+ * null vector still comes through smpm_batch_set_nullspace. */
+int smpm_batch_set_fdm(smpm_batch* b, int npairs, const double* T, const double* T_inv, const smpm_strip_factors* f);
 /* b_S = B (A - mu)^{-1} f per system; f: device, nsys x r (r = m_x m_z n^2, reference node order
  * ((ex m_z + ez) n + ix) n + iz, proj/src/mesh.cpp:27-40); b_S: device nsys x k */
 int smpm_schur_rhs(smpm_batch* b, const double* f, double* b_S, void* stream);             /* proj/src/schur.cpp:182-186 */

@@ -25,7 +25,7 @@ EXPORTS = [
     "smpm_batch_coarse_info", "smpm_apply_S", "smpm_apply_St", "smpm_apply_block_jacobi_inv", "smpm_apply_Z",
     "smpm_apply_Zt", "smpm_coarse_solve", "smpm_apply_P", "smpm_apply_Q", "smpm_project_out", "smpm_solve",
     "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_batch_launch_count",
-    "smpm_batch_profile", "smpm_fp64_peak", "smpm_batch_set_strip_factors", "smpm_schur_rhs",
+    "smpm_batch_profile", "smpm_fp64_peak", "smpm_batch_set_strip_factors", "smpm_batch_set_fdm", "smpm_schur_rhs",
     "smpm_recover_solution", "smpm_solve_stacked", "smpm_fourier_y", "smpm_inverse_fourier_y",
     "smpm_batch_load_schur_blocks", "smpm_batch_set_tuning", "smpm_batch_query", "smpm_batch_set_trace", "smpm_batch_set_allreduce",
 ]
@@ -129,6 +129,7 @@ def lib():
     L.smpm_batch_profile.argtypes = [vp, ip, C.POINTER(C.c_double), C.POINTER(C.c_longlong), ip]
     L.smpm_fp64_peak.argtypes = [ip, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.smpm_batch_set_strip_factors.argtypes = [vp, C.POINTER(StripFactors)]
+    L.smpm_batch_set_fdm.argtypes = [vp, ip, dp, dp, C.POINTER(StripFactors)]
     L.smpm_schur_rhs.argtypes = [vp, dp, dp, vp]
     L.smpm_fourier_y.argtypes = [llp, ip, dp, dp, vp]
     L.smpm_inverse_fourier_y.argtypes = [llp, ip, dp, dp, vp]

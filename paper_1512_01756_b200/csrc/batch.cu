@@ -319,6 +319,11 @@ struct smpm_batch {
   long long p2t_res[V2_MAXCOL + 1] = {};  // resident CTAs of the tiled pass 2' per column capacity
   bool p2t_attr = false;
   int jhost = 0;  // Arnoldi index of the next step (all live systems of a cycle share it)
+  // device-side fast-diagonalisation setup (smpm_batch_set_fdm): couplings, block inverses
+  // and row sums are built on the device from the spectral data at finalize
+  bool from_fdm = false;
+  std::vector<double> fdm_a, fdm_lx, fdm_lz, fdm_mu;  // 6 x n, 6 x n, nmode (complex), nsys
+  double fdm_tau = 0.0;
   // stacked solve across ranks: the caller's all-reduce (NCCL over NVLink) and its buffer
   smpm_allreduce_fn ar_fn = nullptr;
   void* ar_user = nullptr;
@@ -407,6 +412,10 @@ struct smpm_batch {
   double* Kinv(int s, int v) const { return dmat.p + s * mstride + oK[v]; }
   double* Ksingle(int s) const { return dmat.p + s * mstride + oKs; }
 };
+
+// out = A in for every w-long column of nsys x ncol_sys columns (defined with the strip solver below)
+void xf_columns(smpm_batch* b, bool inverse, const double* in, double* out, int ncol_sys, long long sys_stride,
+                cudaStream_t st, int nsys_ = -1);
 
 namespace {
 
@@ -893,25 +902,33 @@ void build_coarse(smpm_batch* b) {
   b->hC.assign(static_cast<size_t>(nsys) * d * d, 0.0);
   b->htri.assign(static_cast<size_t>(nsys), 1);
   b->hsing.assign(static_cast<size_t>(nsys), 0);
+  if (b->from_fdm) {
+    // the couplings live on the device only: row sums by fdm_rowsum_kernel (fdm_device_setup)
+    CUDA_CHECK(cudaMemcpyAsync(rows.data(), b->drowsum.p, sizeof(double) * rows.size(), cudaMemcpyDeviceToHost,
+                               b->ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
+  }
   for (int s = 0; s < nsys; ++s) {
-    const double* GW = b->hG.data() + s * gsz;
-    const double* GI = GW + static_cast<long long>(w) * w;
-    const double* GE = GI + 4LL * w * w;
     double* rs = rows.data() + static_cast<size_t>(s) * 6 * w;
     double* rWI = rs;
     double* rEI = rs + 2 * w;
     double* rEW = rs + 4 * w;
     double* rWE = rs + 5 * w;
-    for (int c = 0; c < w; ++c)
-      for (int r = 0; r < 2 * w; ++r) {
-        rWI[r] += GI[static_cast<long long>(c) * 2 * w + r];
-        rEI[r] += GI[static_cast<long long>(c + w) * 2 * w + r];
-      }
-    for (int c = 0; c < w; ++c)
-      for (int r = 0; r < w; ++r) {
-        rEW[r] += GW[static_cast<long long>(c) * w + r];
-        rWE[r] += GE[static_cast<long long>(c) * w + r];
-      }
+    if (!b->from_fdm) {
+      const double* GW = b->hG.data() + s * gsz;
+      const double* GI = GW + static_cast<long long>(w) * w;
+      const double* GE = GI + 4LL * w * w;
+      for (int c = 0; c < w; ++c)
+        for (int r = 0; r < 2 * w; ++r) {
+          rWI[r] += GI[static_cast<long long>(c) * 2 * w + r];
+          rEI[r] += GI[static_cast<long long>(c + w) * 2 * w + r];
+        }
+      for (int c = 0; c < w; ++c)
+        for (int r = 0; r < w; ++r) {
+          rEW[r] += GW[static_cast<long long>(c) * w + r];
+          rWE[r] += GE[static_cast<long long>(c) * w + r];
+        }
+    }
     auto sum = [](const double* p, int n) {
       double a = 0.0;
       for (int i = 0; i < n; ++i) a += p[i];
@@ -978,7 +995,7 @@ void build_coarse(smpm_batch* b) {
     }
   }
   cudaStream_t st = b->ctx->stream;
-  b->drowsum.upload(rows, st);
+  if (!b->from_fdm) b->drowsum.upload(rows, st);
   b->dcinv.upload(cinv, st);
   b->duc.upload(uc, st);
   b->dthomas.upload(th, st);
@@ -987,6 +1004,174 @@ void build_coarse(smpm_batch* b) {
 }
 
 SpecParams spec_params(const smpm_batch* b);
+
+// --------------------------------------------------------------------------
+// Device-side fast-diagonalisation setup (smpm_batch_set_fdm).
+// Replaces, per system (Fourier mode), the reference's build_kind_coupling
+// (proj/src/schur.cpp:19-69: one dense LU of a q x q strip block per kind, and
+// per Helmholtz shift the real-Schur solves of proj/src/helmholtz.cpp:58-143)
+// and the LU of every block-Jacobi block (proj/src/schur.cpp:188-216):
+//   gamma_kind(mu)[q] = -tau sum_p a_kind[p] / (lx_kind[p] + lz[q] - mu)
+//   G_kind[X,Y](mu)   = T diag(gamma_kind,XY) T^{-1}
+//   K_v^{-1}[X,Y]     = T diag(kinv_v,XY) T^{-1}    (the reduced block inverses:
+//                       K = I - G' D is diagonalised by T as well: no LU)
+// Every dense block of a system's pool is T times a diagonally (pairs: 2 x 2)
+// scaled T^{-1}: one scaling kernel and ONE launch of the shared-matrix
+// transform kernel over all the pool's w-blocks.
+// --------------------------------------------------------------------------
+__global__ void fdm_gamma_kernel(int nsys, int nmode, int n, const double2* __restrict__ a,
+                                 const double2* __restrict__ lx, const double2* __restrict__ lz,
+                                 const double* __restrict__ mu, double tau, double2* __restrict__ gam) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long long>(nsys) * SK_NUM * nmode) return;
+  const int m = static_cast<int>(idx % nmode);
+  const int kd = static_cast<int>((idx / nmode) % SK_NUM);
+  const int s = static_cast<int>(idx / (static_cast<long long>(nmode) * SK_NUM));
+  const double2 z = lz[m];
+  double sr = 0.0, si = 0.0;
+  for (int p = 0; p < n; ++p) {
+    const double2 l = lx[kd * n + p], ap = a[kd * n + p];
+    const double dr = l.x + z.x - mu[s], di = l.y + z.y;
+    const double den = fma(dr, dr, di * di);
+    sr += fma(ap.x, dr, ap.y * di) / den;
+    si += fma(ap.y, dr, -ap.x * di) / den;
+  }
+  gam[idx] = make_double2(-tau * sr, -tau * si);
+}
+
+struct FdmRegion {
+  int start, count;  // w-blocks [start, start + count) of a system's pool
+  int type;          // 0: w x w block of gamma kind `idx`; 1: 2w x 2w interior coupling; 2: 2w x 2w K variant `idx`;
+  int idx;           // 3: w x w single-interface inverse
+};
+struct FdmRegions {
+  FdmRegion r[8];
+  int n;
+};
+
+// M[s][cc][:] = Diag(cc) T^{-1}[:, c(cc)] for every w-block cc of the pools of systems [s0, s0 + ns)
+__global__ void fdm_scale_kernel(FdmRegions R, int w, int npairs, int nmode, long long mstride, int s0,
+                                 const double* __restrict__ Ti, const double2* __restrict__ gam,
+                                 const double2* __restrict__ kinv, double* __restrict__ M) {
+  const int cc = blockIdx.x, sl = blockIdx.y, s = s0 + sl;
+  const double2* diag = nullptr;
+  int c = 0;
+  for (int q = 0; q < R.n; ++q) {
+    const FdmRegion g = R.r[q];
+    if (cc < g.start || cc >= g.start + g.count) continue;
+    const int o = cc - g.start;
+    if (g.type == 0) {
+      diag = gam + (static_cast<long long>(s) * SK_NUM + g.idx) * nmode;
+      c = o;
+    } else if (g.type == 3) {
+      diag = kinv + (static_cast<long long>(s) * 20 + 16) * nmode;
+      c = o;
+    } else {
+      const int col = o >> 1, X = o & 1, Y = col >= w ? 1 : 0;
+      c = col - Y * w;
+      if (g.type == 1)
+        diag = gam + (static_cast<long long>(s) * SK_NUM + (X == 0 ? (Y ? SK_I_WE : SK_I_WW) : (Y ? SK_I_EE : SK_I_EW))) * nmode;
+      else
+        diag = kinv + (static_cast<long long>(s) * 20 + g.idx * 4 + 2 * X + Y) * nmode;
+    }
+  }
+  double* out = M + static_cast<long long>(sl) * mstride + static_cast<long long>(cc) * w;
+  if (!diag) {  // padding past the last region
+    for (int r = threadIdx.x; r < w; r += blockDim.x) out[r] = 0.0;
+    return;
+  }
+  const double* tc = Ti + static_cast<long long>(c) * w;
+  for (int m = threadIdx.x; m < nmode; m += blockDim.x) {
+    const double2 g = diag[m];
+    if (m < npairs) {
+      // coordinates (a, b) <-> z = a - i b; z' = g z: a' = gr a + gi b, b' = gr b - gi a
+      const double a = tc[2 * m], bb = tc[2 * m + 1];
+      out[2 * m] = fma(g.x, a, g.y * bb);
+      out[2 * m + 1] = fma(g.x, bb, -g.y * a);
+    } else {
+      out[npairs + m] = g.x * tc[npairs + m];
+    }
+  }
+}
+
+// strip row sums of the couplings (the fused deflation's S Z c): rW_I(2w) rE_I(2w) rE_W(w) rW_E(w)
+__global__ void fdm_rowsum_kernel(int w, long long mstride, long long oGW, long long oGI, long long oGE,
+                                  const double* __restrict__ pool, double* __restrict__ rows) {
+  const int s = blockIdx.y;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= 2 * w) return;
+  const double* base = pool + static_cast<long long>(s) * mstride;
+  double* rs = rows + static_cast<long long>(s) * 6 * w;
+  double a = 0.0, e = 0.0;
+  for (int c = 0; c < w; ++c) {
+    a += base[oGI + static_cast<long long>(c) * 2 * w + r];
+    e += base[oGI + static_cast<long long>(c + w) * 2 * w + r];
+  }
+  rs[r] = a;
+  rs[2 * w + r] = e;
+  if (r < w) {
+    double gw = 0.0, ge = 0.0;
+    for (int c = 0; c < w; ++c) {
+      gw += base[oGW + static_cast<long long>(c) * w + r];
+      ge += base[oGE + static_cast<long long>(c) * w + r];
+    }
+    rs[4 * w + r] = gw;
+    rs[5 * w + r] = ge;
+  }
+}
+
+void fdm_gamma(smpm_batch* b, cudaStream_t st) {
+  const int n = b->n, nm = b->sp_nmode;
+  DevArray<double> da, dlx, dlz, dmu;
+  da.upload(b->fdm_a, st);
+  dlx.upload(b->fdm_lx, st);
+  dlz.upload(b->fdm_lz, st);
+  dmu.upload(b->fdm_mu, st);
+  b->dgam.alloc(static_cast<size_t>(b->nsys) * SK_NUM * nm * 2);
+  const long long tot = static_cast<long long>(b->nsys) * SK_NUM * nm;
+  fdm_gamma_kernel<<<static_cast<int>((tot + 127) / 128), 128, 0, st>>>(
+      b->nsys, nm, n, reinterpret_cast<const double2*>(da.p), reinterpret_cast<const double2*>(dlx.p),
+      reinterpret_cast<const double2*>(dlz.p), dmu.p, b->fdm_tau, reinterpret_cast<double2*>(b->dgam.p));
+  check_launch(b);
+  CUDA_CHECK(cudaStreamSynchronize(st));  // the staging arrays go out of scope
+}
+
+// dense couplings, block-Jacobi inverses and row sums of every system, on the device
+void fdm_device_setup(smpm_batch* b, cudaStream_t st) {
+  const int w = b->w;
+  const long long ww = 1LL * w * w;
+  if (b->xf_P == 0) fail(SMPM_EINVAL, "smpm_batch_set_fdm needs w % 16 == 0 (the shared-matrix transform kernels)");
+  if (b->mstride % w != 0) fail(SMPM_ERUNTIME, "pool stride is not a whole number of w-blocks");
+  FdmRegions R{};
+  auto add = [&](long long off, long long count, int type, int idx) {
+    R.r[R.n++] = FdmRegion{static_cast<int>(off / w), static_cast<int>(count), type, idx};
+  };
+  add(b->oGW, w, 0, SK_W_EE);
+  add(b->oGI, 4LL * w, 1, 0);
+  add(b->oGE, w, 0, SK_E_WW);
+  for (int v = 0; v < 4; ++v)
+    if (b->kneeded[v]) add(b->oK[v], 4LL * w, 2, v);
+  if (b->single) add(b->oKs, w, 3, 0);
+  const int nblk = static_cast<int>(b->mstride / w);
+  // systems per pass: scaled T^{-1} copies of at most ~1.5 GB
+  const int chunk = static_cast<int>(std::max<long long>(1, std::min<long long>(b->nsys, (3LL << 27) / b->mstride)));
+  DevArray<double> M;
+  M.alloc(static_cast<size_t>(chunk) * b->mstride);
+  for (int s0 = 0; s0 < b->nsys; s0 += chunk) {
+    const int ns = std::min(chunk, b->nsys - s0);
+    fdm_scale_kernel<<<dim3(nblk, ns), 128, 0, st>>>(R, w, b->sp_npairs, b->sp_nmode, b->mstride, s0, b->dTi.p,
+                                                       reinterpret_cast<const double2*>(b->dgam.p),
+                                                       reinterpret_cast<const double2*>(b->dkinv.p), M.p);
+    check_launch(b);
+    xf_columns(b, false, M.p, b->dmat.p + static_cast<long long>(s0) * b->mstride, nblk, b->mstride, st, ns);
+  }
+  b->drowsum.alloc(static_cast<size_t>(b->nsys) * 6 * w);
+  fdm_rowsum_kernel<<<dim3((2 * w + 127) / 128, b->nsys), 128, 0, st>>>(w, b->mstride, b->oGW, b->oGI, b->oGE, b->dmat.p,
+                                                                       b->drowsum.p);
+  check_launch(b);
+  CUDA_CHECK(cudaStreamSynchronize(st));
+  (void)ww;
+}
 
 void finalize(smpm_batch* b) {
   if (b->finalized) return;
@@ -1014,13 +1199,17 @@ void finalize(smpm_batch* b) {
   }
   b->mstride = (off + 31) / 32 * 32;
   b->dmat.alloc(static_cast<size_t>(b->mstride) * b->nsys);
-  for (int s = 0; s < b->nsys; ++s)
-    CUDA_CHECK(cudaMemcpyAsync(b->GW(s), b->hG.data() + s * 6LL * w * w, sizeof(double) * 6LL * w * w,
-                               cudaMemcpyHostToDevice, st));
+  if (!b->from_fdm)
+    for (int s = 0; s < b->nsys; ++s)
+      CUDA_CHECK(cudaMemcpyAsync(b->GW(s), b->hG.data() + s * 6LL * w * w, sizeof(double) * 6LL * w * w,
+                                 cudaMemcpyHostToDevice, st));
   if (b->spectral) {
     b->dT.upload(b->hT, st);
     b->dTi.upload(b->hTi, st);
-    b->dgam.upload(b->hgam, st);
+    if (b->from_fdm)
+      fdm_gamma(b, st);
+    else
+      b->dgam.upload(b->hgam, st);
     std::vector<double> om(static_cast<size_t>(w), 0.0);  // omega = T^T 1
     for (int e = 0; e < w; ++e)
       for (int r = 0; r < w; ++r) om[e] += b->hT[static_cast<size_t>(e) * w + r];
@@ -1045,8 +1234,14 @@ void finalize(smpm_batch* b) {
     spec_setup_kernel<<<static_cast<int>((n + 127) / 128), 128, 0, st>>>(sp, reinterpret_cast<double2*>(b->dkinv.p), b->nsys);
     check_launch(b);
   }
-  build_bj_inverses(b);
+  if (b->from_fdm) {
+    if (!b->spectral) fail(SMPM_EINVAL, "smpm_batch_set_fdm needs an even interface width w");
+    fdm_device_setup(b, st);
+  } else {
+    build_bj_inverses(b);
+  }
   build_coarse(b);
+  std::vector<double>().swap(b->hG);  // the host staging copy is not needed any more
   for (auto& v : b->vbuf) v.alloc(static_cast<size_t>(b->nsys) * b->k);
   b->dsmall.alloc(static_cast<size_t>(b->nsys) * (d + 8));
   b->dcoarse.alloc(static_cast<size_t>(b->nsys) * 2 * d);
@@ -2578,7 +2773,8 @@ StripParams strip_params(const smpm_batch* b) {
 // out = A in for every w-long column of nsys x ncol_sys columns (system stride
 // sys_stride): the resident-slice transform kernel, or a plain cuBLAS GEMM
 void xf_columns(smpm_batch* b, bool inverse, const double* in, double* out, int ncol_sys, long long sys_stride,
-                cudaStream_t st) {
+                cudaStream_t st, int nsys_) {
+  const int nsys = nsys_ < 0 ? b->nsys : nsys_;
   if (b->xf_P > 0) {
     XformArgs a;
     a.Af = inverse ? b->dTifrag.p : b->dTfrag.p;
@@ -2587,14 +2783,14 @@ void xf_columns(smpm_batch* b, bool inverse, const double* in, double* out, int 
     a.k = sys_stride;
     a.alist = nullptr;
     a.acount = nullptr;
-    a.nslots = b->nsys;
+    a.nslots = nsys;
     a.nv = 1;
     a.in[0] = in;
     a.out[0] = out;
     a.in[1] = nullptr;
     a.out[1] = nullptr;
     a.P = b->xf_P;
-    const long long nch = (static_cast<long long>(b->nsys) * ncol_sys + 15) / 16;
+    const long long nch = (static_cast<long long>(nsys) * ncol_sys + 15) / 16;
     const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / a.P, nch)));
     if (b->xp_on)
       launch_xformp(b, a, inverse, st, false);
@@ -2608,7 +2804,7 @@ void xf_columns(smpm_batch* b, bool inverse, const double* in, double* out, int 
   if (cublasSetStream(ctx->blas, st) != CUBLAS_STATUS_SUCCESS) fail(SMPM_ECUDA, "cublasSetStream failed");
   const double one = 1.0, zero = 0.0;
   const int w = b->w;
-  const long long ncols = static_cast<long long>(b->nsys) * ncol_sys;
+  const long long ncols = static_cast<long long>(nsys) * ncol_sys;
   if (ncols > INT_MAX) fail(SMPM_EINVAL, "too many strip columns");
   if (cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, w, static_cast<int>(ncols), w, &one,
                   inverse ? b->dTi.p : b->dT.p, w, in, w, &zero, out, w) != CUBLAS_STATUS_SUCCESS)
@@ -2758,7 +2954,6 @@ int smpm_batch_create(smpm_ctx* ctx, int n, int m_x, int m_z, int nsys, smpm_bat
     b->k = 2LL * b->w * b->d;
     b->nbf = b->d / 2;
     b->single = (b->d % 2) == 1;
-    b->hG.assign(static_cast<size_t>(nsys) * 6 * b->w * b->w, 0.0);
     b->have.assign(static_cast<size_t>(nsys), 0);
     b->huS.assign(static_cast<size_t>(nsys), {});
     *out = b.release();
@@ -2784,6 +2979,7 @@ int smpm_batch_set_couplings(smpm_batch* b, int sys, const double* G_W, const do
     if (b->finalized) fail(SMPM_EINVAL, "batch already finalized");
     if (!G_W || !G_E || (b->mx >= 3 && !G_I)) fail(SMPM_EINVAL, "null coupling matrix");
     const long long ww = 1LL * b->w * b->w;
+    if (b->hG.empty()) b->hG.assign(static_cast<size_t>(b->nsys) * 6 * ww, 0.0);  // host staging, on first use
     double* dst = b->hG.data() + sys * 6 * ww;
     std::memcpy(dst, G_W, sizeof(double) * ww);
     if (G_I) std::memcpy(dst + ww, G_I, sizeof(double) * 4 * ww);
@@ -2913,6 +3109,7 @@ int smpm_batch_set_interface_blocks(smpm_batch* b, int sys, const double* const*
       (void)seg_len;
     }
     const long long ww2 = ww;
+    if (b->hG.empty()) b->hG.assign(static_cast<size_t>(b->nsys) * 6 * ww, 0.0);
     double* dst = b->hG.data() + sys * 6 * ww2;
     std::memcpy(dst, GW.data(), sizeof(double) * ww);
     std::memcpy(dst + ww, GI.data(), sizeof(double) * 4 * ww);
@@ -2975,10 +3172,67 @@ int smpm_apply_P(smpm_batch* b, const double* v, double* y, int fused, void* str
   });
 }
 
+void store_strip_factors(smpm_batch* b, const smpm_strip_factors* f);
+
 int smpm_batch_set_strip_factors(smpm_batch* b, const smpm_strip_factors* f) {
   return guard([&] {
     if (!b || !f) fail(SMPM_EINVAL, "null argument");
     if (!b->spectral || b->hT.empty()) fail(SMPM_EINVAL, "strip factors need the spectral basis (smpm_batch_set_spectral)");
+    store_strip_factors(b, f);
+  });
+}
+
+int smpm_batch_set_fdm(smpm_batch* b, int npairs, const double* T, const double* T_inv, const smpm_strip_factors* f) {
+  return guard([&] {
+    if (!b || !f) fail(SMPM_EINVAL, "null argument");
+    if (b->finalized) fail(SMPM_EINVAL, "batch already finalized");
+    if (!T || !T_inv) fail(SMPM_EINVAL, "null spectral basis");
+    if (npairs < 0 || 2 * npairs > b->w) fail(SMPM_EINVAL, "bad number of complex pairs");
+    if (b->w % 16 != 0) fail(SMPM_EINVAL, "smpm_batch_set_fdm needs w % 16 == 0 (use smpm_batch_set_couplings)");
+    const int n = b->n, w = b->w;
+    const size_t ww = static_cast<size_t>(w) * w;
+    b->sp_npairs = npairs;
+    b->sp_nmode = w - npairs;
+    b->hT.assign(T, T + ww);
+    b->hTi.assign(T_inv, T_inv + ww);
+    b->spectral = true;
+    if (b->mx >= 3) store_strip_factors(b, f);
+    for (int kd = 0; kd < 3; ++kd)
+      if (!f->Vx[kd] || !f->Vx_inv[kd] || !f->lx[kd]) fail(SMPM_EINVAL, "null x factor");
+    if (!f->lz || !f->tW || !f->tE || !f->mu) fail(SMPM_EINVAL, "null strip factor");
+    // a_kind[p] = (t_X . Vx[:, p]) Vx^{-1}[p, y_Y] for the six couplings (readers X, owner Y):
+    // W_EE (west-boundary strip), I_WW, I_WE, I_EW, I_EE (interior strip), E_WW (east-boundary strip)
+    const int strip_of[SK_NUM] = {0, 1, 1, 1, 1, 2};
+    const int X_of[SK_NUM] = {1, 0, 0, 1, 1, 0}, Y_of[SK_NUM] = {1, 0, 1, 0, 1, 0};  // 0 = W, 1 = E
+    b->fdm_a.assign(static_cast<size_t>(SK_NUM) * n * 2, 0.0);
+    b->fdm_lx.assign(static_cast<size_t>(SK_NUM) * n * 2, 0.0);
+    for (int kd = 0; kd < SK_NUM; ++kd) {
+      const int sk = strip_of[kd];
+      const double* tX = X_of[kd] ? f->tE : f->tW;
+      const int y = Y_of[kd] ? n - 1 : 0;
+      for (int p = 0; p < n; ++p) {
+        double tr = 0.0, ti = 0.0;
+        for (int ix = 0; ix < n; ++ix) {
+          tr += tX[ix] * f->Vx[sk][2 * (ix + p * n)];
+          ti += tX[ix] * f->Vx[sk][2 * (ix + p * n) + 1];
+        }
+        const double yr = f->Vx_inv[sk][2 * (p + y * n)], yi = f->Vx_inv[sk][2 * (p + y * n) + 1];
+        b->fdm_a[2 * (kd * n + p)] = tr * yr - ti * yi;
+        b->fdm_a[2 * (kd * n + p) + 1] = tr * yi + ti * yr;
+        b->fdm_lx[2 * (kd * n + p)] = f->lx[sk][2 * p];
+        b->fdm_lx[2 * (kd * n + p) + 1] = f->lx[sk][2 * p + 1];
+      }
+    }
+    b->fdm_lz.assign(f->lz, f->lz + 2 * static_cast<size_t>(b->sp_nmode));
+    b->fdm_mu.assign(f->mu, f->mu + b->nsys);
+    b->fdm_tau = f->tau;
+    b->from_fdm = true;
+    std::fill(b->have.begin(), b->have.end(), 1);
+  });
+}
+
+void store_strip_factors(smpm_batch* b, const smpm_strip_factors* f) {
+  {
     if (b->mx < 3) fail(SMPM_EINVAL, "strip solver needs m_x >= 3");
     const int n = b->n;
     for (int kd = 0; kd < 3; ++kd)
@@ -3014,7 +3268,7 @@ int smpm_batch_set_strip_factors(smpm_batch* b, const smpm_strip_factors* f) {
     b->strip_tau = f->tau;
     CUDA_CHECK(cudaStreamSynchronize(st));
     b->strip_ok = true;
-  });
+  }
 }
 
 int smpm_schur_rhs(smpm_batch* b, const double* f, double* b_S, void* stream) {

@@ -159,19 +159,33 @@ class ProblemSet:
     fdm: StripFDM
     f: object = None  # device_rhs: torch (nsys, r) forcing (mode 0 projected with u_L in load_batch)
 
+    def kinds(self, i):
+        """(G_W, G_I, G_E) of system i: the stored dense couplings, or (device_setup
+        problems, which never build them) the host/torch FDM product for that system."""
+        if self.GW is not None:
+            return self.GW[i], self.GI[i], self.GE[i]
+        gw, gi, ge = self.fdm.couplings([self.mus[i]])
+        return gw[0], gi[0], ge[0]
 
-def build_problem(cfg: Config, modes=None, device=None, device_rhs=False) -> ProblemSet:
+
+def build_problem(cfg: Config, modes=None, device=None, device_rhs=False, device_setup=False) -> ProblemSet:
     """Product setup for `modes` of a 3D config (all modes by default) or the
     single system of a 2D config.  device_rhs: the seeded forcings are built on
     the device and b_S = B (A - mu)^{-1} f is left to load_batch, which runs it
-    through the C ABI's schur_rhs (strip.cuh) instead of the host FDM."""
+    through the C ABI's schur_rhs (strip.cuh) instead of the host FDM.
+    device_setup: no dense couplings are built here; load_batch hands the
+    geometry-level factors to smpm_batch_set_fdm and the library builds every
+    system's couplings, block inverses and coarse data with its own kernels."""
     geo = Geometry(cfg.n, cfg.m_x, cfg.m_z, cfg.l_x, cfg.l_z, cfg.c_tau)
     F = StripFDM(geo, device)
     mus_all = cfg.mus()
     if modes is None:
         modes = list(range(len(mus_all)))
     mus = [mus_all[m] for m in modes]
-    GW, GI, GE = F.couplings(mus)
+    if device_setup and geo.w % 16 == 0:
+        GW = GI = GE = None
+    else:
+        GW, GI, GE = F.couplings(mus)
     u_S = u_L = None
     if any(mu == 0.0 for mu in mus):
         u_S, u_L = F.nullspace()
@@ -200,16 +214,25 @@ def load_batch(ctx, ps: ProblemSet, spectral: bool = True):
 
     cfg = ps.cfg
     b = SchurBatch(ctx, cfg.n, cfg.m_x, cfg.m_z, len(ps.modes))
-    for i in range(len(ps.modes)):
-        b.set_couplings(i, ps.GW[i], ps.GI[i] if cfg.m_x > 2 else None, ps.GE[i])
-        if ps.mus[i] == 0.0:
-            b.set_nullspace(i, ps.u_S)
-    if spectral:
-        npairs, T, Ti, gam = ps.fdm.spectral(ps.mus)
-        b.set_spectral(npairs, T, Ti, gam)
-    b.finalize()
-    if spectral and b.m_x >= 3 and 4 <= b.n <= 17:
-        b.set_strip_factors(ps.fdm.strip_factors(ps.mus))
+    if ps.GW is None:
+        # device-side setup: geometry-level factors only (smpm_batch_set_fdm)
+        npairs, T, Ti, _ = ps.fdm.real_basis()
+        b.set_fdm(npairs, T, Ti, ps.fdm.strip_factors(ps.mus))
+        for i in range(len(ps.modes)):
+            if ps.mus[i] == 0.0:
+                b.set_nullspace(i, ps.u_S)
+        b.finalize()
+    else:
+        for i in range(len(ps.modes)):
+            b.set_couplings(i, ps.GW[i], ps.GI[i] if cfg.m_x > 2 else None, ps.GE[i])
+            if ps.mus[i] == 0.0:
+                b.set_nullspace(i, ps.u_S)
+        if spectral:
+            npairs, T, Ti, gam = ps.fdm.spectral(ps.mus)
+            b.set_spectral(npairs, T, Ti, gam)
+        b.finalize()
+        if spectral and b.m_x >= 3 and 4 <= b.n <= 17:
+            b.set_strip_factors(ps.fdm.strip_factors(ps.mus))
     if ps.b_S is None:
         # device b_S = B (A - mu)^{-1} f, then the mode-0 projection with u_S
         # (proj/src/helmholtz.cpp:159-176)

@@ -143,10 +143,31 @@ class SchurBatch:
             raise SmpmError(1, "u_S must have length k")
         check(lib().smpm_batch_set_nullspace(self.h, sys, _hptr(u)))
 
+    def set_fdm(self, npairs: int, T, T_inv, fac: dict):
+        """Device-side setup (smpm_batch_set_fdm): the shared z eigenbasis and the
+        strip factors (StripFDM.strip_factors(mus)); finalize() then builds every
+        system's spectral diagonals, dense couplings, block-Jacobi inverses, row
+        sums and coarse matrix on the device.  Replaces set_couplings +
+        set_spectral (+ set_strip_factors)."""
+        w = self.w
+        t = np.asfortranarray(T, dtype=np.float64)
+        ti = np.asfortranarray(T_inv, dtype=np.float64)
+        if t.shape != (w, w) or ti.shape != (w, w):
+            raise SmpmError(1, "T/T_inv must be w x w")
+        sf, keep = self._strip_struct(fac)
+        check(lib().smpm_batch_set_fdm(self.h, int(npairs), _hptr(t), _hptr(ti), C.byref(sf)))
+        self.spectral = True
+        del keep
+
     def set_strip_factors(self, fac: dict):
         """Fast-diagonalisation factors of the strip operator (smpm_batch_set_strip_factors):
         fac from StripFDM.strip_factors(mus) — Vx, Vx_inv, lx (3 kinds each, complex),
         lz (nmode complex), tW, tE (n), tau, mu (nsys)."""
+        sf, keep = self._strip_struct(fac)
+        check(lib().smpm_batch_set_strip_factors(self.h, C.byref(sf)))
+        del keep
+
+    def _strip_struct(self, fac: dict):
         keep = []
 
         def cplx(a):
@@ -172,7 +193,7 @@ class SchurBatch:
         if mu.size != self.nsys:
             raise SmpmError(1, "mu must have one shift per system")
         sf.mu = real(mu)
-        check(lib().smpm_batch_set_strip_factors(self.h, C.byref(sf)))
+        return sf, keep
 
     def finalize(self):
         check(lib().smpm_batch_finalize(self.h))

@@ -139,3 +139,40 @@ def test_oracle_golden_regression():
     out = O.solve_poisson(setup, f, "dbj", 1e-10, 50, 50)
     assert out["res"].iterations == int(g["iterations"])
     assert np.linalg.norm(out["res"].x_S - g["x_S"]) <= 1e-12 * np.linalg.norm(g["x_S"])
+
+
+def test_parity_pure_spectral_basis():
+    """The z factor commutes with the reflection of the node index, and the
+    product's spectral basis is built parity-pure from its even / odd blocks
+    (fdm.StripFDM): every column of T (row of T^{-1}) is exactly even or odd,
+    the modes are ordered pairs (even, odd) then reals (even, odd) — the
+    structure the parity-split transform kernels detect (xformp.cuh) — and
+    T diag T^{-1} still reproduces the operator."""
+    from paper_1512_01756_b200.fdm import Geometry, StripFDM
+
+    for n, m_z in ((6, 4), (9, 4), (11, 16)):
+        geo = Geometry(n, 4, m_z, 4.0, 1.0)
+        F = StripFDM(geo, device="cpu")
+        w = geo.w
+        J = np.eye(w)[::-1]
+        assert np.abs(J @ F.Az @ J - F.Az).max() <= 1e-14 * np.abs(F.Az).max()
+        npairs, T, Ti, rep = F.real_basis()
+        assert np.abs(Ti @ T - np.eye(w)).max() < 1e-11
+        par = []
+        for m in range(w):
+            even = np.array_equal(T[:, m], T[::-1, m]) and np.array_equal(Ti[m], Ti[m, ::-1])
+            odd = np.array_equal(T[:, m], -T[::-1, m]) and np.array_equal(Ti[m], -Ti[m, ::-1])
+            assert even != odd, m  # exactly one, bit for bit
+            par.append(1 if even else -1)
+        pp, pr = par[: 2 * npairs], par[2 * npairs:]
+        assert pp == sorted(pp, reverse=True) and pr == sorted(pr, reverse=True)
+        assert all(pp[2 * q] == pp[2 * q + 1] for q in range(npairs))
+        assert par.count(1) == par.count(-1) == w // 2
+        # the eigen-relation in the real basis: Az T = T B with B block diagonal (2x2 per pair)
+        B = Ti @ F.Az @ T
+        mask = np.zeros((w, w), dtype=bool)
+        for q in range(npairs):
+            mask[2 * q:2 * q + 2, 2 * q:2 * q + 2] = True
+        for m in range(2 * npairs, w):
+            mask[m, m] = True
+        assert np.abs(B[~mask]).max() <= 1e-9 * np.abs(B).max()

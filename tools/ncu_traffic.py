@@ -39,7 +39,7 @@ def launches(path):
             return float(v) * SCALE.get(units[col[name]], 1.0)
 
         dur = float(r[col["gpu__time_duration.sum"]].replace(",", ""))
-        dscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(units[col["gpu__time_duration.sum"]], 1e-9)
+        dscale = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1.0, "s": 1.0}.get(units[col["gpu__time_duration.sum"]], 1e-9)
         out.append({"kernel": r[col["Kernel Name"]].split("(")[0].replace("smpm::", ""), "grid": r[col["Grid Size"]],
                     "dram_bytes": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
                     "duration_s": dur * dscale})

@@ -24,7 +24,7 @@ if a.modes:
     lo, _, hi = a.modes.partition("-")
     modes = list(range(int(lo), int(hi or lo) + 1))
 drhs = cfg.k > 100_000 if a.device_rhs < 0 else bool(a.device_rhs)
-ps = build_problem(cfg, modes, device="cuda", device_rhs=drhs)
+ps = build_problem(cfg, modes, device="cuda", device_rhs=drhs, device_setup=drhs)
 ctx = Context(0)
 b = load_batch(ctx, ps).tune_from_env()
 bS = torch.tensor(ps.b_S, device="cuda")
