@@ -30,7 +30,8 @@ def stale() -> bool:
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    deps = [os.path.join(CSRC, f) for f in SOURCES] + glob.glob(os.path.join(CSRC, "*.cuh"))
+    deps = [os.path.join(CSRC, f) for f in SOURCES] + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        glob.glob(os.path.join(CSRC, "*.inl"))
     deps.append(os.path.join(HERE, "..", "include", "smpm_b200.h"))
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 

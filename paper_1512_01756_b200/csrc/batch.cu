@@ -592,2888 +592,12 @@ int grid_for(long long elems) {
   return static_cast<int>(std::min<long long>((elems + 255) / 256, 148LL * 8));
 }
 
-// --------------------------------------------------------------------------
-// Operators (device vectors nsys x k)
-// --------------------------------------------------------------------------
-void op_S(smpm_batch* b, const double* v, double* y, const Live& lv, cudaStream_t st) {
-  ProfScope ps(b, PC_SCHUR, st);
-  run_plan(b, b->pS, v, y, nullptr, lv, st);
-}
-void op_St(smpm_batch* b, const double* v, double* y, const Live& lv, cudaStream_t st) {
-  run_plan(b, b->pSt, v, y, nullptr, lv, st);
-}
-// structured block-Jacobi: three dependent GEMM stages
-void op_BJ(smpm_batch* b, const double* v, double* y, const Live& lv, cudaStream_t st) {
-  ProfScope ps(b, PC_BJ, st);
-  double* tmp = b->vbuf[9].p;
-  run_plan(b, b->pBJ1, v, y, tmp, lv, st);
-  run_plan(b, b->pBJ2, v, y, tmp, lv, st);
-  run_plan(b, b->pBJ3, v, y, tmp, lv, st);
-}
-// P v = v - S Z c(Z^T v)
-void op_P(smpm_batch* b, const double* v, double* y, bool fused, const Live& lv, cudaStream_t st) {
-  if (fused) {
-    run_deflate(b, DEFL_P_FUSED, v, v, y, nullptr, lv, st);
-    return;
-  }
-  double* c = b->dsmall.p;
-  double* z = b->vbuf[7].p;
-  double* sz = b->vbuf[8].p;
-  run_deflate(b, DEFL_COARSE, v, nullptr, nullptr, c, lv, st);
-  zbroadcast_kernel<<<grid_for(b->nsys * b->k), 256, 0, st>>>(b->nsys, b->d, 2 * b->w, b->k, lv.active, c, z);
-  check_launch(b);
-  op_S(b, z, sz, lv, st);
-  run_deflate(b, DEFL_SUB_T, sz, v, y, nullptr, lv, st);
-}
-// Q v = v - Z c(Z^T S v)
-void op_Q(smpm_batch* b, const double* v, double* y, const Live& lv, cudaStream_t st) {
-  double* t = b->vbuf[8].p;
-  op_S(b, v, t, lv, st);
-  run_deflate(b, DEFL_Q_TAIL, t, v, y, nullptr, lv, st);
-}
-
-// --------------------------------------------------------------------------
-// Setup: plans, structured block-Jacobi inverses, coarse spaces
-// --------------------------------------------------------------------------
-void build_plans(smpm_batch* b) {
-  const int w = b->w, d = b->d, mx = b->mx;
-  const long long k = b->k;
-  const long long w2 = 2LL * w;
-  cudaStream_t st = b->ctx->stream;
-  b->pS.jobs.clear();
-  b->pSt.jobs.clear();
-  b->pBJ1.jobs.clear();
-  b->pBJ2.jobs.clear();
-  b->pBJ3.jobs.clear();
-  b->pF.jobs.clear();
-  b->pB.jobs.clear();
-  b->pF.shared_a = b->pB.shared_a = true;
-  for (int s = 0; s < b->nsys; ++s) {
-    const long long o = s * k;
-    if (b->spectral) {
-      // every w-block through T^{-1} (forward) / T (back): w x 2d per system
-      b->pF.add(b->dTi.p, w, false, w, 2 * d, w, s, view(BUF_IN, o, w), view(BUF_OUT, o, w), kNoView, 1.0, 0.0);
-      b->pB.add(b->dT.p, w, false, w, 2 * d, w, s, view(BUF_IN, o, w), view(BUF_OUT, o, w), kNoView, 1.0, 0.0);
-    }
-    // ---- S v = v + sum_s G_s [v_{2s-1}; v_{2s}] -> [y_{2s-2}; y_{2s+1}]
-    if (mx >= 3)
-      b->pS.add(b->GI(s), w2, false, 2 * w, mx - 2, 2 * w, s, view(BUF_IN, o + w, w2),
-                view(BUF_OUT, o, w2, w, 2LL * w), view(BUF_IN, o, w2, w, 2LL * w), 1.0, 1.0);
-    b->pS.add(b->GW(s), w, false, w, 1, w, s, view(BUF_IN, o), view(BUF_OUT, o + w), view(BUF_IN, o + w), 1.0, 1.0);
-    b->pS.add(b->GE(s), w, false, w, 1, w, s, view(BUF_IN, o + (2LL * d - 1) * w), view(BUF_OUT, o + (2LL * d - 2) * w),
-              view(BUF_IN, o + (2LL * d - 2) * w), 1.0, 1.0);
-    // ---- S^T: own blocks += G^T reader blocks
-    if (mx >= 3)
-      b->pSt.add(b->GI(s), w2, true, 2 * w, mx - 2, 2 * w, s, view(BUF_IN, o, w2, w, 2LL * w),
-                 view(BUF_OUT, o + w, w2), view(BUF_IN, o + w, w2), 1.0, 1.0);
-    b->pSt.add(b->GW(s), w, true, w, 1, w, s, view(BUF_IN, o + w), view(BUF_OUT, o), view(BUF_IN, o), 1.0, 1.0);
-    b->pSt.add(b->GE(s), w, true, w, 1, w, s, view(BUF_IN, o + (2LL * d - 2) * w), view(BUF_OUT, o + (2LL * d - 1) * w),
-               view(BUF_IN, o + (2LL * d - 1) * w), 1.0, 1.0);
-
-    // ---- block-Jacobi, blocks of two interfaces b = 0..nbf-1 (w-blocks 4b..4b+3):
-    //   r = [v0; v3] - G'[v1; v2] ; [x0; x3] = K_b^{-1} r ; x1 = v1 - Gee x0 ; x2 = v2 - Gww x3
-    const int nbf = b->nbf;
-    const long long w4 = 4LL * w;
-    if (nbf > 0)
-      b->pBJ1.add(b->GI(s), w2, false, 2 * w, nbf, 2 * w, s, view(BUF_IN, o + w, w4), view(BUF_TMP, o, w4),
-                  view(BUF_IN, o, w4, w, 2LL * w), -1.0, 1.0);
-    for (int bb = 0; bb < nbf;) {
-      const bool first = bb == 0;
-      const bool last = 2 * bb + 2 == mx - 1;
-      int e = bb + 1;
-      while (e < nbf && (e == 0) == first && (2 * e + 2 == mx - 1) == last) ++e;
-      const int var = (first ? 1 : 0) | (last ? 2 : 0);
-      b->pBJ2.add(b->Kinv(s, var), w2, false, 2 * w, e - bb, 2 * w, s, view(BUF_TMP, o + bb * w4, w4),
-                  view(BUF_OUT, o + bb * w4, w4, w, 2LL * w), kNoView, 1.0, 0.0);
-      bb = e;
-    }
-    if (nbf > 0) {
-      // x1 = v1 - Gee0 x0 : strip 2b is the west-boundary strip for b = 0
-      b->pBJ3.add(b->GW(s), w, false, w, 1, w, s, view(BUF_OUT, o), view(BUF_OUT, o + w), view(BUF_IN, o + w), -1.0, 1.0);
-      if (nbf > 1)
-        b->pBJ3.add(b->GI(s) + w2 * w + w, w2, false, w, nbf - 1, w, s, view(BUF_OUT, o + w4, w4),
-                    view(BUF_OUT, o + w4 + w, w4), view(BUF_IN, o + w4 + w, w4), -1.0, 1.0);
-      // x2 = v2 - Gww2 x3 : strip 2b+2 is the east-boundary strip when 2b+2 == mx-1
-      const bool last_east = 2 * (nbf - 1) + 2 == mx - 1;
-      const int ninner = last_east ? nbf - 1 : nbf;
-      if (ninner > 0)
-        b->pBJ3.add(b->GI(s), w2, false, w, ninner, w, s, view(BUF_OUT, o + 3LL * w, w4), view(BUF_OUT, o + 2LL * w, w4),
-                    view(BUF_IN, o + 2LL * w, w4), -1.0, 1.0);
-      if (last_east) {
-        const long long ob = o + (nbf - 1) * w4;
-        b->pBJ3.add(b->GE(s), w, false, w, 1, w, s, view(BUF_OUT, ob + 3LL * w), view(BUF_OUT, ob + 2LL * w),
-                    view(BUF_IN, ob + 2LL * w), -1.0, 1.0);
-      }
-    }
-    if (b->single) {
-      // trailing interface d-1 (w-blocks 2d-2, 2d-1): r = v0 - G_E v1 ; x0 = K_s^{-1} r ; x1 = v1 - Gee x0
-      const long long o0 = o + (2LL * d - 2) * w, o1 = o0 + w;
-      b->pBJ1.add(b->GE(s), w, false, w, 1, w, s, view(BUF_IN, o1), view(BUF_TMP, o0), view(BUF_IN, o0), -1.0, 1.0);
-      b->pBJ2.add(b->Ksingle(s), w, false, w, 1, w, s, view(BUF_TMP, o0), view(BUF_OUT, o0), kNoView, 1.0, 0.0);
-      const double* gee = d >= 2 ? b->GI(s) + w2 * w + w : b->GW(s);
-      const long long ldee = d >= 2 ? w2 : w;
-      b->pBJ3.add(gee, ldee, false, w, 1, w, s, view(BUF_OUT, o0), view(BUF_OUT, o1), view(BUF_IN, o1), -1.0, 1.0);
-    }
-  }
-  const int sms = b->ctx->num_sms;
-  for (Plan* p : {&b->pS, &b->pBJ1, &b->pBJ2, &b->pBJ3, &b->pF, &b->pB}) {
-    if (p->jobs.empty()) continue;
-    if (!p->v2_ok()) {
-      // odd w (16-byte alignment impossible): per-system jobs on the v1 kernel
-      p->build(sms, st);
-      continue;
-    }
-    // every system's jobs are system 0's shifted by s*mstride (matrices) and
-    // s*k (vectors): keep system 0's as the per-system template
-    std::vector<GemmJob> tmpl;
-    for (const auto& j : p->jobs)
-      if (j.sys == 0) tmpl.push_back(j);
-    p->jobs.swap(tmpl);
-    // tail variant: K split 4 ways so a handful of live systems still
-    // spreads over many SMs (used when <= kTailSystems systems are live)
-    p->tail = std::make_unique<Plan>();
-    p->tail->jobs = p->jobs;
-    p->tail->shared_a = p->shared_a;
-    p->tail->build2(std::max(1, sms / b->nsys), st, 4);
-    // split-K only when even the whole batch cannot fill the GPU
-    p->build2(std::max(1, sms / b->nsys), st);
-  }
-  b->pSt.build(sms, st);
-  // grid tail solver: unsplit copies of the hot stage templates
-  b->tmpl_ok = true;
-  Plan* src[6] = {&b->pBJ1, &b->pBJ2, &b->pBJ3, &b->pS, &b->pF, &b->pB};
-  for (int i = 0; i < 6; ++i) {
-    if (i >= 4 && !b->spectral) break;
-    if (!src[i]->v2) {
-      if (i < 4) {
-        b->tmpl_ok = false;
-        break;
-      }
-      continue;
-    }
-    b->pc[i].shared_a = src[i]->shared_a;
-    b->pc[i].jobs = src[i]->jobs;
-    for (auto& j : b->pc[i].jobs) j.splitk = 1;
-    b->pc[i].build2(0, st);
-    std::vector<Tile2> gv;
-    for (size_t ji = 0; ji < b->pc[i].jobs.size(); ++ji)
-      if (b->pc[i].jobs[ji].N == 1)
-        for (int m0 = 0; m0 < b->pc[i].jobs[ji].M; m0 += GT_GVR) gv.push_back(Tile2{static_cast<int>(ji), m0, 0, -1});
-    b->pc[i].dgv.upload(gv, st);
-    b->pc[i].ngv = static_cast<int>(gv.size());
-  }
-  // v2 templates hold per-system workspace counts; v1 plans hold totals
-  const long long ns = b->nsys;
-  long long wst = b->pSt.ws_tiles;
-  for (Plan* p : {&b->pS, &b->pBJ1, &b->pBJ2, &b->pBJ3, &b->pF, &b->pB}) {
-    wst = std::max(wst, p->ws_tiles * (p->v2 ? ns : 1));
-    if (p->tail) wst = std::max(wst, p->tail->ws_tiles * ns);
-  }
-  b->dws.alloc(static_cast<size_t>(std::max(1LL, wst)) * GEMM_BM * GEMM_BN);
-  // grid tail solver: the unsplit templates of the four hot stages (pc)
-  b->grid_ok = b->tmpl_ok;
-  b->dgbar.alloc(1);
-}
-
-__global__ void add_identity_kernel(double* A, long long lda, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) A[i * lda + i] += 1.0;
-}
-__global__ void set_identity_kernel(double* A, long long lda, int n) {
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(n) * n;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long c = e / n, r = e % n;
-    A[c * lda + r] = (r == c) ? 1.0 : 0.0;
-  }
-}
-
-// K = I - G' diag(Gee0, Gww2) (2w x 2w) or K_single = I - G_E Gee (w x w),
-// formed with the GEMM kernel, inverted with cuSOLVER getrf/getrs.
-void build_bj_inverses(smpm_batch* b) {
-  const int w = b->w, mx = b->mx, d = b->d;
-  const long long w2 = 2LL * w;
-  cudaStream_t st = b->ctx->stream;
-  DevArray<double> Kt;
-  Kt.alloc(static_cast<size_t>(4LL * w * w));
-  DevArray<int> ipiv, info;
-  ipiv.alloc(static_cast<size_t>(2 * w));
-  info.alloc(1);
-  int lwork = 0;
-  CUSOLVER_CHECK(cusolverDnDgetrf_bufferSize(b->ctx->solver, 2 * w, 2 * w, Kt.p, 2 * w, &lwork));
-  DevArray<double> work;
-  work.alloc(static_cast<size_t>(std::max(lwork, 1)));
-  auto invert = [&](double* K, int nn, double* out) {
-    CUSOLVER_CHECK(cusolverDnDgetrf(b->ctx->solver, nn, nn, K, nn, work.p, ipiv.p, info.p));
-    set_identity_kernel<<<64, 256, 0, st>>>(out, nn, nn);
-    check_launch(b);
-    CUSOLVER_CHECK(cusolverDnDgetrs(b->ctx->solver, CUBLAS_OP_N, nn, nn, K, nn, ipiv.p, out, nn, info.p));
-    int hinfo = 0;
-    CUDA_CHECK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    if (hinfo != 0) fail(SMPM_ESINGULAR, "block-Jacobi: singular preconditioner block");
-  };
-  for (int s = 0; s < b->nsys; ++s) {
-    for (int var = 0; var < 4; ++var) {
-      if (!b->kneeded[var]) continue;
-      const bool first = var & 1, last = var & 2;
-      const double* gee = first ? b->GW(s) : b->GI(s) + w2 * w + w;
-      const long long ldee = first ? w : w2;
-      const double* gww = last ? b->GE(s) : b->GI(s);
-      const long long ldww = last ? w : w2;
-      Plan p;
-      // K[:, 0:w] = -G'[:, 0:w] Gee ; K[:, w:2w] = -G'[:, w:2w] Gww ; then + I
-      BufTable t;
-      t.p[BUF_IN] = const_cast<double*>(gee);
-      t.p[BUF_OUT] = Kt.p;
-      t.p[BUF_TMP] = const_cast<double*>(gww);
-      t.p[BUF_TMP2] = nullptr;
-      p.add(b->GI(s), w2, false, 2 * w, w, w, 0, view(BUF_IN, 0, ldee), view(BUF_OUT, 0, w2), kNoView, -1.0, 0.0);
-      p.add(b->GI(s) + w2 * w, w2, false, 2 * w, w, w, 0, view(BUF_TMP, 0, ldww), view(BUF_OUT, w2 * w, w2), kNoView,
-            -1.0, 0.0);
-      p.build(0, st);  // no split-K for setup products
-      gemm_jobs_kernel<<<p.ntiles, 128, 0, st>>>(p.djobs.p, p.dtiles.p, t, nullptr, nullptr);
-      check_launch(b);
-      add_identity_kernel<<<8, 256, 0, st>>>(Kt.p, w2, 2 * w);
-      check_launch(b);
-      invert(Kt.p, 2 * w, b->Kinv(s, var));
-    }
-    if (b->single) {
-      const double* gee = d >= 2 ? b->GI(s) + w2 * w + w : b->GW(s);
-      const long long ldee = d >= 2 ? w2 : w;
-      Plan p;
-      BufTable t;
-      t.p[BUF_IN] = const_cast<double*>(gee);
-      t.p[BUF_OUT] = Kt.p;
-      t.p[BUF_TMP] = nullptr;
-      t.p[BUF_TMP2] = nullptr;
-      p.add(b->GE(s), w, false, w, w, w, 0, view(BUF_IN, 0, ldee), view(BUF_OUT, 0, w), kNoView, -1.0, 0.0);
-      p.build(0, st);
-      gemm_jobs_kernel<<<p.ntiles, 128, 0, st>>>(p.djobs.p, p.dtiles.p, t, nullptr, nullptr);
-      check_launch(b);
-      add_identity_kernel<<<8, 256, 0, st>>>(Kt.p, w, w);
-      check_launch(b);
-      invert(Kt.p, w, b->Ksingle(s));
-    }
-  }
-  (void)mx;
-}
-
-// dense inverse with partial pivoting (host, d <= a few hundred)
-std::vector<double> host_inverse(std::vector<double> A, int n) {
-  std::vector<double> inv(static_cast<size_t>(n) * n, 0.0);
-  for (int i = 0; i < n; ++i) inv[static_cast<size_t>(i) * n + i] = 1.0;
-  auto at = [n](std::vector<double>& M, int r, int c) -> double& { return M[static_cast<size_t>(c) * n + r]; };
-  for (int c = 0; c < n; ++c) {
-    int p = c;
-    for (int r = c + 1; r < n; ++r)
-      if (std::fabs(at(A, r, c)) > std::fabs(at(A, p, c))) p = r;
-    if (at(A, p, c) == 0.0) fail(SMPM_ESINGULAR, "coarse matrix is singular");
-    if (p != c)
-      for (int j = 0; j < n; ++j) {
-        std::swap(at(A, p, j), at(A, c, j));
-        std::swap(at(inv, p, j), at(inv, c, j));
-      }
-    const double piv = at(A, c, c);
-    for (int r = 0; r < n; ++r) {
-      if (r == c) continue;
-      const double f = at(A, r, c) / piv;
-      if (f == 0.0) continue;
-      for (int j = 0; j < n; ++j) {
-        at(A, r, j) -= f * at(A, c, j);
-        at(inv, r, j) -= f * at(inv, c, j);
-      }
-    }
-  }
-  for (int r = 0; r < n; ++r) {
-    const double piv = at(A, r, r);
-    for (int j = 0; j < n; ++j) at(inv, r, j) /= piv;
-  }
-  return inv;
-}
-
-// C = Z^T S Z from the couplings' row sums (S Z 1_j only touches interfaces
-// j-1, j, j+1; proj/src/deflation.cpp:24-42), rank-one shift or Thomas data.
-void build_coarse(smpm_batch* b) {
-  const int w = b->w, d = b->d, mx = b->mx, nsys = b->nsys;
-  const long long gsz = 6LL * w * w;
-  std::vector<double> rows(static_cast<size_t>(nsys) * 6 * w, 0.0);
-  std::vector<double> cinv(static_cast<size_t>(nsys) * d * d, 0.0), uc(static_cast<size_t>(nsys) * d, 0.0),
-      th(static_cast<size_t>(nsys) * 3 * d, 0.0);
-  std::vector<int> cmode(static_cast<size_t>(nsys), 0);
-  b->hC.assign(static_cast<size_t>(nsys) * d * d, 0.0);
-  b->htri.assign(static_cast<size_t>(nsys), 1);
-  b->hsing.assign(static_cast<size_t>(nsys), 0);
-  if (b->from_fdm) {
-    // the couplings live on the device only: row sums by fdm_rowsum_kernel (fdm_device_setup)
-    CUDA_CHECK(cudaMemcpyAsync(rows.data(), b->drowsum.p, sizeof(double) * rows.size(), cudaMemcpyDeviceToHost,
-                               b->ctx->stream));
-    CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
-  }
-  for (int s = 0; s < nsys; ++s) {
-    double* rs = rows.data() + static_cast<size_t>(s) * 6 * w;
-    double* rWI = rs;
-    double* rEI = rs + 2 * w;
-    double* rEW = rs + 4 * w;
-    double* rWE = rs + 5 * w;
-    if (!b->from_fdm) {
-      const double* GW = b->hG.data() + s * gsz;
-      const double* GI = GW + static_cast<long long>(w) * w;
-      const double* GE = GI + 4LL * w * w;
-      for (int c = 0; c < w; ++c)
-        for (int r = 0; r < 2 * w; ++r) {
-          rWI[r] += GI[static_cast<long long>(c) * 2 * w + r];
-          rEI[r] += GI[static_cast<long long>(c + w) * 2 * w + r];
-        }
-      for (int c = 0; c < w; ++c)
-        for (int r = 0; r < w; ++r) {
-          rEW[r] += GW[static_cast<long long>(c) * w + r];
-          rWE[r] += GE[static_cast<long long>(c) * w + r];
-        }
-    }
-    auto sum = [](const double* p, int n) {
-      double a = 0.0;
-      for (int i = 0; i < n; ++i) a += p[i];
-      return a;
-    };
-    double* C = b->hC.data() + static_cast<size_t>(s) * d * d;
-    auto Cat = [&](int i, int j) -> double& { return C[static_cast<size_t>(j) * d + i]; };
-    for (int j = 0; j < d; ++j) {
-      Cat(j, j) += 2.0 * w;
-      if (j == 0) {
-        Cat(0, 0) += sum(rEW, w);
-      } else {
-        Cat(j - 1, j) += sum(rEI, w);
-        Cat(j, j) += sum(rEI + w, w);
-      }
-      if (j + 1 == mx - 1) {
-        Cat(j, j) += sum(rWE, w);
-      } else {
-        Cat(j, j) += sum(rWI, w);
-        Cat(j + 1, j) += sum(rWI + w, w);
-      }
-    }
-    if (!b->huS[s].empty()) {
-      b->hsing[s] = 1;
-      const std::vector<double>& us = b->huS[s];
-      double* u = uc.data() + static_cast<size_t>(s) * d;
-      double nn = 0.0;
-      for (int i = 0; i < d; ++i) {
-        double a = 0.0;
-        for (int e = 0; e < 2 * w; ++e) a += us[static_cast<size_t>(i) * 2 * w + e];
-        u[i] = a;
-        nn += a * a;
-      }
-      nn = std::sqrt(nn);
-      int imax = 0;
-      for (int i = 0; i < d; ++i) {
-        u[i] /= nn;
-        if (std::fabs(u[i]) > std::fabs(u[imax])) imax = i;
-      }
-      if (u[imax] < 0.0)
-        for (int i = 0; i < d; ++i) u[i] = -u[i];
-      std::vector<double> Cs(C, C + static_cast<size_t>(d) * d);
-      for (int j = 0; j < d; ++j)
-        for (int i = 0; i < d; ++i) Cs[static_cast<size_t>(j) * d + i] += u[i] * u[j];
-      const std::vector<double> inv = host_inverse(Cs, d);
-      std::copy(inv.begin(), inv.end(), cinv.begin() + static_cast<long long>(s) * d * d);
-      cmode[s] = 0;
-    } else {
-      // Thomas pivots (proj/src/deflation.cpp:77-90)
-      double* sub = th.data() + static_cast<size_t>(s) * 3 * d;
-      double* cp = sub + d;
-      double* piv = cp + d;
-      for (int i = 0; i + 1 < d; ++i) sub[i] = Cat(i + 1, i);
-      piv[0] = Cat(0, 0);
-      for (int i = 1; i < d; ++i) {
-        cp[i - 1] = Cat(i - 1, i) / piv[i - 1];
-        piv[i] = Cat(i, i) - sub[i - 1] * cp[i - 1];
-      }
-      for (int i = 0; i < d; ++i) {
-        if (piv[i] == 0.0) fail(SMPM_ESINGULAR, "coarse matrix is singular");
-        piv[i] = 1.0 / piv[i];  // the device multiplies by reciprocal pivots
-      }
-      cmode[s] = 1;
-    }
-  }
-  cudaStream_t st = b->ctx->stream;
-  if (!b->from_fdm) b->drowsum.upload(rows, st);
-  b->dcinv.upload(cinv, st);
-  b->duc.upload(uc, st);
-  b->dthomas.upload(th, st);
-  b->dcmode.upload(cmode, st);
-  b->dsingular.upload(b->hsing, st);
-}
-
-SpecParams spec_params(const smpm_batch* b);
-
-// --------------------------------------------------------------------------
-// Device-side fast-diagonalisation setup (smpm_batch_set_fdm).
-// Replaces, per system (Fourier mode), the reference's build_kind_coupling
-// (proj/src/schur.cpp:19-69: one dense LU of a q x q strip block per kind, and
-// per Helmholtz shift the real-Schur solves of proj/src/helmholtz.cpp:58-143)
-// and the LU of every block-Jacobi block (proj/src/schur.cpp:188-216):
-//   gamma_kind(mu)[q] = -tau sum_p a_kind[p] / (lx_kind[p] + lz[q] - mu)
-//   G_kind[X,Y](mu)   = T diag(gamma_kind,XY) T^{-1}
-//   K_v^{-1}[X,Y]     = T diag(kinv_v,XY) T^{-1}    (the reduced block inverses:
-//                       K = I - G' D is diagonalised by T as well: no LU)
-// Every dense block of a system's pool is T times a diagonally (pairs: 2 x 2)
-// scaled T^{-1}: one scaling kernel and ONE launch of the shared-matrix
-// transform kernel over all the pool's w-blocks.
-// --------------------------------------------------------------------------
-__global__ void fdm_gamma_kernel(int nsys, int nmode, int n, const double2* __restrict__ a,
-                                 const double2* __restrict__ lx, const double2* __restrict__ lz,
-                                 const double* __restrict__ mu, double tau, double2* __restrict__ gam) {
-  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= static_cast<long long>(nsys) * SK_NUM * nmode) return;
-  const int m = static_cast<int>(idx % nmode);
-  const int kd = static_cast<int>((idx / nmode) % SK_NUM);
-  const int s = static_cast<int>(idx / (static_cast<long long>(nmode) * SK_NUM));
-  const double2 z = lz[m];
-  double sr = 0.0, si = 0.0;
-  for (int p = 0; p < n; ++p) {
-    const double2 l = lx[kd * n + p], ap = a[kd * n + p];
-    const double dr = l.x + z.x - mu[s], di = l.y + z.y;
-    const double den = fma(dr, dr, di * di);
-    sr += fma(ap.x, dr, ap.y * di) / den;
-    si += fma(ap.y, dr, -ap.x * di) / den;
-  }
-  gam[idx] = make_double2(-tau * sr, -tau * si);
-}
-
-struct FdmRegion {
-  int start, count;  // w-blocks [start, start + count) of a system's pool
-  int type;          // 0: w x w block of gamma kind `idx`; 1: 2w x 2w interior coupling; 2: 2w x 2w K variant `idx`;
-  int idx;           // 3: w x w single-interface inverse
-};
-struct FdmRegions {
-  FdmRegion r[8];
-  int n;
-};
-
-// M[s][cc][:] = Diag(cc) T^{-1}[:, c(cc)] for every w-block cc of the pools of systems [s0, s0 + ns)
-__global__ void fdm_scale_kernel(FdmRegions R, int w, int npairs, int nmode, long long mstride, int s0,
-                                 const double* __restrict__ Ti, const double2* __restrict__ gam,
-                                 const double2* __restrict__ kinv, double* __restrict__ M) {
-  const int cc = blockIdx.x, sl = blockIdx.y, s = s0 + sl;
-  const double2* diag = nullptr;
-  int c = 0;
-  for (int q = 0; q < R.n; ++q) {
-    const FdmRegion g = R.r[q];
-    if (cc < g.start || cc >= g.start + g.count) continue;
-    const int o = cc - g.start;
-    if (g.type == 0) {
-      diag = gam + (static_cast<long long>(s) * SK_NUM + g.idx) * nmode;
-      c = o;
-    } else if (g.type == 3) {
-      diag = kinv + (static_cast<long long>(s) * 20 + 16) * nmode;
-      c = o;
-    } else {
-      const int col = o >> 1, X = o & 1, Y = col >= w ? 1 : 0;
-      c = col - Y * w;
-      if (g.type == 1)
-        diag = gam + (static_cast<long long>(s) * SK_NUM + (X == 0 ? (Y ? SK_I_WE : SK_I_WW) : (Y ? SK_I_EE : SK_I_EW))) * nmode;
-      else
-        diag = kinv + (static_cast<long long>(s) * 20 + g.idx * 4 + 2 * X + Y) * nmode;
-    }
-  }
-  double* out = M + static_cast<long long>(sl) * mstride + static_cast<long long>(cc) * w;
-  if (!diag) {  // padding past the last region
-    for (int r = threadIdx.x; r < w; r += blockDim.x) out[r] = 0.0;
-    return;
-  }
-  const double* tc = Ti + static_cast<long long>(c) * w;
-  for (int m = threadIdx.x; m < nmode; m += blockDim.x) {
-    const double2 g = diag[m];
-    if (m < npairs) {
-      // coordinates (a, b) <-> z = a - i b; z' = g z: a' = gr a + gi b, b' = gr b - gi a
-      const double a = tc[2 * m], bb = tc[2 * m + 1];
-      out[2 * m] = fma(g.x, a, g.y * bb);
-      out[2 * m + 1] = fma(g.x, bb, -g.y * a);
-    } else {
-      out[npairs + m] = g.x * tc[npairs + m];
-    }
-  }
-}
-
-// strip row sums of the couplings (the fused deflation's S Z c): rW_I(2w) rE_I(2w) rE_W(w) rW_E(w)
-__global__ void fdm_rowsum_kernel(int w, long long mstride, long long oGW, long long oGI, long long oGE,
-                                  const double* __restrict__ pool, double* __restrict__ rows) {
-  const int s = blockIdx.y;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= 2 * w) return;
-  const double* base = pool + static_cast<long long>(s) * mstride;
-  double* rs = rows + static_cast<long long>(s) * 6 * w;
-  double a = 0.0, e = 0.0;
-  for (int c = 0; c < w; ++c) {
-    a += base[oGI + static_cast<long long>(c) * 2 * w + r];
-    e += base[oGI + static_cast<long long>(c + w) * 2 * w + r];
-  }
-  rs[r] = a;
-  rs[2 * w + r] = e;
-  if (r < w) {
-    double gw = 0.0, ge = 0.0;
-    for (int c = 0; c < w; ++c) {
-      gw += base[oGW + static_cast<long long>(c) * w + r];
-      ge += base[oGE + static_cast<long long>(c) * w + r];
-    }
-    rs[4 * w + r] = gw;
-    rs[5 * w + r] = ge;
-  }
-}
-
-void fdm_gamma(smpm_batch* b, cudaStream_t st) {
-  const int n = b->n, nm = b->sp_nmode;
-  DevArray<double> da, dlx, dlz, dmu;
-  da.upload(b->fdm_a, st);
-  dlx.upload(b->fdm_lx, st);
-  dlz.upload(b->fdm_lz, st);
-  dmu.upload(b->fdm_mu, st);
-  b->dgam.alloc(static_cast<size_t>(b->nsys) * SK_NUM * nm * 2);
-  const long long tot = static_cast<long long>(b->nsys) * SK_NUM * nm;
-  fdm_gamma_kernel<<<static_cast<int>((tot + 127) / 128), 128, 0, st>>>(
-      b->nsys, nm, n, reinterpret_cast<const double2*>(da.p), reinterpret_cast<const double2*>(dlx.p),
-      reinterpret_cast<const double2*>(dlz.p), dmu.p, b->fdm_tau, reinterpret_cast<double2*>(b->dgam.p));
-  check_launch(b);
-  CUDA_CHECK(cudaStreamSynchronize(st));  // the staging arrays go out of scope
-}
-
-// dense couplings, block-Jacobi inverses and row sums of every system, on the device
-void fdm_device_setup(smpm_batch* b, cudaStream_t st) {
-  const int w = b->w;
-  const long long ww = 1LL * w * w;
-  if (b->xf_P == 0) fail(SMPM_EINVAL, "smpm_batch_set_fdm needs w % 16 == 0 (the shared-matrix transform kernels)");
-  if (b->mstride % w != 0) fail(SMPM_ERUNTIME, "pool stride is not a whole number of w-blocks");
-  FdmRegions R{};
-  auto add = [&](long long off, long long count, int type, int idx) {
-    R.r[R.n++] = FdmRegion{static_cast<int>(off / w), static_cast<int>(count), type, idx};
-  };
-  add(b->oGW, w, 0, SK_W_EE);
-  add(b->oGI, 4LL * w, 1, 0);
-  add(b->oGE, w, 0, SK_E_WW);
-  for (int v = 0; v < 4; ++v)
-    if (b->kneeded[v]) add(b->oK[v], 4LL * w, 2, v);
-  if (b->single) add(b->oKs, w, 3, 0);
-  const int nblk = static_cast<int>(b->mstride / w);
-  // systems per pass: scaled T^{-1} copies of at most ~1.5 GB
-  const int chunk = static_cast<int>(std::max<long long>(1, std::min<long long>(b->nsys, (3LL << 27) / b->mstride)));
-  DevArray<double> M;
-  M.alloc(static_cast<size_t>(chunk) * b->mstride);
-  for (int s0 = 0; s0 < b->nsys; s0 += chunk) {
-    const int ns = std::min(chunk, b->nsys - s0);
-    fdm_scale_kernel<<<dim3(nblk, ns), 128, 0, st>>>(R, w, b->sp_npairs, b->sp_nmode, b->mstride, s0, b->dTi.p,
-                                                       reinterpret_cast<const double2*>(b->dgam.p),
-                                                       reinterpret_cast<const double2*>(b->dkinv.p), M.p);
-    check_launch(b);
-    xf_columns(b, false, M.p, b->dmat.p + static_cast<long long>(s0) * b->mstride, nblk, b->mstride, st, ns);
-  }
-  b->drowsum.alloc(static_cast<size_t>(b->nsys) * 6 * w);
-  fdm_rowsum_kernel<<<dim3((2 * w + 127) / 128, b->nsys), 128, 0, st>>>(w, b->mstride, b->oGW, b->oGI, b->oGE, b->dmat.p,
-                                                                       b->drowsum.p);
-  check_launch(b);
-  CUDA_CHECK(cudaStreamSynchronize(st));
-  (void)ww;
-}
-
-void finalize(smpm_batch* b) {
-  if (b->finalized) return;
-  for (int s = 0; s < b->nsys; ++s)
-    if (!b->have[s]) fail(SMPM_EINVAL, "smpm_batch_finalize: couplings of system " + std::to_string(s) + " not set");
-  const int w = b->w, mx = b->mx, d = b->d;
-  cudaStream_t st = b->ctx->stream;
-  // which K variants occur ([first][last] over the two-interface blocks)
-  for (int bb = 0; bb < b->nbf; ++bb) b->kneeded[(bb == 0 ? 1 : 0) | (2 * bb + 2 == mx - 1 ? 2 : 0)] = true;
-  long long off = 0;
-  b->oGW = off;
-  off += 1LL * w * w;
-  b->oGI = off;
-  off += 4LL * w * w;
-  b->oGE = off;
-  off += 1LL * w * w;
-  for (int v = 0; v < 4; ++v)
-    if (b->kneeded[v]) {
-      b->oK[v] = off;
-      off += 4LL * w * w;
-    }
-  if (b->single) {
-    b->oKs = off;
-    off += 1LL * w * w;
-  }
-  b->mstride = (off + 31) / 32 * 32;
-  b->dmat.alloc(static_cast<size_t>(b->mstride) * b->nsys);
-  if (!b->from_fdm)
-    for (int s = 0; s < b->nsys; ++s)
-      CUDA_CHECK(cudaMemcpyAsync(b->GW(s), b->hG.data() + s * 6LL * w * w, sizeof(double) * 6LL * w * w,
-                                 cudaMemcpyHostToDevice, st));
-  if (b->spectral) {
-    b->dT.upload(b->hT, st);
-    b->dTi.upload(b->hTi, st);
-    if (b->from_fdm)
-      fdm_gamma(b, st);
-    else
-      b->dgam.upload(b->hgam, st);
-    std::vector<double> om(static_cast<size_t>(w), 0.0);  // omega = T^T 1
-    for (int e = 0; e < w; ++e)
-      for (int r = 0; r < w; ++r) om[e] += b->hT[static_cast<size_t>(e) * w + r];
-    b->domega.upload(om, st);
-    std::vector<double> nu(static_cast<size_t>(w), 0.0);  // nu = T^{-1} 1
-    for (int c2 = 0; c2 < w; ++c2)
-      for (int r = 0; r < w; ++r) nu[r] += b->hTi[static_cast<size_t>(c2) * w + r];
-    b->dnu.upload(nu, st);
-    const int nmc = (b->sp_nmode + SP_MODES - 1) / SP_MODES;
-    b->dzpart.alloc(static_cast<size_t>(b->nsys) * nmc * d);
-    b->dkinv.alloc(static_cast<size_t>(b->nsys) * 20 * b->sp_nmode * 2);
-    b->dvh.alloc(static_cast<size_t>(b->nsys) * b->k);
-    b->dth.alloc(static_cast<size_t>(b->nsys) * b->k);
-    b->dvh2.alloc(static_cast<size_t>(b->nsys) * b->k);
-  }
-  build_plans(b);
-  if (b->spectral && !(b->pF.v2 && b->pB.v2)) b->spectral = false;  // odd w: dense operator path
-  if (b->spectral) setup_xform(b);
-  if (b->spectral) {
-    const SpecParams sp = spec_params(b);
-    const long long n = 1LL * b->nsys * b->sp_nmode;
-    spec_setup_kernel<<<static_cast<int>((n + 127) / 128), 128, 0, st>>>(sp, reinterpret_cast<double2*>(b->dkinv.p), b->nsys);
-    check_launch(b);
-  }
-  if (b->from_fdm) {
-    if (!b->spectral) fail(SMPM_EINVAL, "smpm_batch_set_fdm needs an even interface width w");
-    fdm_device_setup(b, st);
-  } else {
-    build_bj_inverses(b);
-  }
-  build_coarse(b);
-  std::vector<double>().swap(b->hG);  // the host staging copy is not needed any more
-  for (auto& v : b->vbuf) v.alloc(static_cast<size_t>(b->nsys) * b->k);
-  b->dsmall.alloc(static_cast<size_t>(b->nsys) * (d + 8));
-  b->dcoarse.alloc(static_cast<size_t>(b->nsys) * 2 * d);
-  b->dczb.alloc(static_cast<size_t>(b->nsys) * d);
-  b->dpost.alloc(static_cast<size_t>(b->nsys) * 64);
-  std::vector<int> ones(static_cast<size_t>(b->nsys), 1);
-  b->dones.upload(ones, st);
-  b->dcount.alloc(static_cast<size_t>(b->nsys) + 1);
-  CUDA_CHECK(cudaMemsetAsync(b->dcount.p, 0, sizeof(int) * (b->nsys + 1), st));
-  b->dsel.alloc(static_cast<size_t>(b->nsys));
-  b->dalist.alloc(2 * static_cast<size_t>(b->nsys) + 2);
-  b->dcnt.alloc(4);
-  CUDA_CHECK(cudaHostAlloc(&b->hcnt, 4 * sizeof(int), cudaHostAllocMapped));
-  CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&b->hcnt_dev), b->hcnt, 0));
-  b->dearly.alloc(4 * static_cast<size_t>(b->nsys) + 2);
-  CUDA_CHECK(cudaHostAlloc(&b->hearly, sizeof(int) * b->nsys, cudaHostAllocMapped));
-  CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&b->hearly_dev), b->hearly, 0));
-  CUDA_CHECK(cudaStreamSynchronize(st));
-  b->finalized = true;
-}
-
-void need_final(smpm_batch* b) {
-  if (!b || !b->finalized) fail(SMPM_EINVAL, "batch not finalized");
-}
-
-// --------------------------------------------------------------------------
-// Batched reductions
-// --------------------------------------------------------------------------
-struct Chunking {
-  int chunk, nchunk;
-};
-Chunking chunking(const smpm_batch* b, long long len = -1) {
-  if (len < 0) len = b->k;
-  const long long target_ctas = 4LL * b->ctx->num_sms;
-  long long per_sys = std::max(1LL, target_ctas / b->nsys);
-  long long chunk = (len + per_sys - 1) / per_sys;
-  chunk = std::max(128LL, std::min(2048LL, (chunk + 31) / 32 * 32));
-  Chunking c;
-  c.chunk = static_cast<int>(chunk);
-  c.nchunk = static_cast<int>(std::max(1LL, (len + chunk - 1) / chunk));
-  return c;
-}
-
-// out[s] = x_s . y_s  (device)
-void batched_dot(smpm_batch* b, const double* x, const double* y, double* out, const int* act, cudaStream_t st,
-                 long long len = -1) {
-  if (len < 0) len = b->k;
-  const Chunking c = chunking(b, len);
-  b->dpart.alloc(std::max<size_t>(b->dpart.n, static_cast<size_t>(b->nsys) * c.nchunk));
-  dim3 grid(c.nchunk, b->nsys);
-  batched_dot_kernel<<<grid, VEC_THREADS, 0, st>>>(b->nsys, len, c.chunk, c.nchunk, act, x, y, b->dpart.p, b->dcount.p,
-                                                   out);
-  check_launch(b);
-}
-
-// --------------------------------------------------------------------------
-// GMRES driver
-// --------------------------------------------------------------------------
-void ensure_gmres(smpm_batch* b, int m, int mtot) {
-  const int histcap = mtot + 2;
-  Chunking c;
-  c.chunk = V2_CHUNK;
-  c.nchunk = static_cast<int>((b->k + V2_CHUNK - 1) / V2_CHUNK);
-  if (b->gm_m != m || b->gm_hist != histcap || b->G.nchunk != c.nchunk) {
-    const size_t ns = static_cast<size_t>(b->nsys);
-    b->dV.alloc(ns * (m + 1) * b->k);
-    b->dR.alloc(ns * (m + 1) * m);
-    b->dcs.alloc(ns * m);
-    b->dsn.alloc(ns * m);
-    b->dg.alloc(ns * (m + 1));
-    b->dh1.alloc(ns * (m + 2));
-    b->dh2.alloc(ns * (m + 2));
-    b->dy.alloc(ns * m);
-    b->dhist.alloc(ns * histcap);
-    b->dgpart.alloc(ns * ((b->k + 127) / 128) * (m + 2));  // adaptive chunks down to 128 rows
-    b->dscal.alloc(ns * 8);
-    b->dgint.alloc(ns * 8);
-    b->gm_m = m;
-    b->gm_hist = histcap;
-  }
-  GmState_& G = b->G;
-  int* ip = b->dgint.p;
-  const int ns = b->nsys;
-  G.jcyc = ip;
-  G.iters = ip + ns;
-  G.state = ip + 2 * ns;
-  G.active = ip + 3 * ns;
-  G.counter = ip + 4 * ns;
-  G.hist_len = ip + 5 * ns;
-  double* dp = b->dscal.p;
-  G.bnorm = dp;
-  G.target = dp + ns;
-  G.hmax = dp + 2 * ns;
-  G.nrm = dp + 3 * ns;
-  G.R = b->dR.p;
-  G.cs = b->dcs.p;
-  G.sn = b->dsn.p;
-  G.g = b->dg.p;
-  G.h1 = b->dh1.p;
-  G.h2 = b->dh2.p;
-  G.y = b->dy.p;
-  G.hist = b->dhist.p;
-  G.part = b->dgpart.p;
-  G.m = m;
-  G.m_total = mtot;
-  G.histcap = histcap;
-  G.k = b->k;
-  G.vstride = static_cast<long long>(m + 1) * b->k;
-  // Arnoldi passes: fixed 512-row chunks (thread-per-row kernels, vec2.cuh)
-  G.chunk = V2_CHUNK;
-  G.nchunk = static_cast<int>((b->k + V2_CHUNK - 1) / V2_CHUNK);
-  G.nsys = ns;
-  b->dsnsq.alloc(static_cast<size_t>(ns));
-  G.snsq = b->dsnsq.p;
-  G.stacked = 0;
-  (void)c;
-  b->gm_mtot = mtot;
-  CUDA_CHECK(cudaMemsetAsync(b->dgint.p, 0, sizeof(int) * ns * 8, b->ctx->stream));
-}
-
-struct SolveCfg {
-  int method;
-  double tol;
-  int max_iter, restart, orth;
-  bool fused, final_check;
-  bool stacked = false;  // one GMRES over all systems (proj/src/helmholtz.cpp:187-246)
-};
-
-// --------------------------------------------------------------------------
-// Spectral operator (spectral.cuh): T^{-1} GEMM, per-mode S^ M^^{-1}, T GEMM
-// --------------------------------------------------------------------------
-SpecParams spec_params(const smpm_batch* b) {
-  SpecParams sp{};
-  sp.w = b->w;
-  sp.d = b->d;
-  sp.mx = b->mx;
-  sp.nbf = b->nbf;
-  sp.single = b->single ? 1 : 0;
-  sp.npairs = b->sp_npairs;
-  sp.nmode = b->sp_nmode;
-  sp.k = b->k;
-  sp.gam = reinterpret_cast<const double2*>(b->dgam.p);
-  sp.kinv = reinterpret_cast<const double2*>(b->dkinv.p);
-  sp.omega = b->domega.p;
-  sp.nu = b->dnu.p;
-  sp.cadd = nullptr;
-  sp.nmc = (b->sp_nmode + SP_MODES - 1) / SP_MODES;
-  sp.segb = SP_SEGB;
-  if (b->tune.segb > 0) sp.segb = std::max(1, std::min(SP_SEGB, b->tune.segb));
-  sp.nseg = (b->nbf + (b->single ? 1 : 0) + sp.segb - 1) / sp.segb;
-  return sp;
-}
-
-// ---- shared-matrix transforms (xform.cuh): the largest row slice of T / T^{-1}
-// that fits in shared memory next to a two-deep column ring, P slices per column group
-template <int MB>
-bool xform_try(smpm_batch* b, int P) {
-  const int w = b->w;
-  const size_t smem =
-      sizeof(double) * (static_cast<size_t>(w / 8) * MB * 64 + static_cast<size_t>(XF_NS) * XF_NT * xf_bstr(w / 2));
-  if (smem > 232448 || 8 * MB * P < w || P > b->ctx->num_sms) return false;
-  CUDA_CHECK(cudaFuncSetAttribute(xform_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  std::vector<double> f(static_cast<size_t>(P) * (w / 8) * MB * 64), fi(f.size());
-  xform_frag_order(b->hT.data(), w, P, MB, f.data());
-  xform_frag_order(b->hTi.data(), w, P, MB, fi.data());
-  b->dTfrag.upload(f, b->ctx->stream);
-  b->dTifrag.upload(fi, b->ctx->stream);
-  CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
-  b->xf_P = P;
-  b->xf_MB = MB;
-  b->xf_smem = smem;
-  return true;
-}
-
-// K-streamed kernel (xformk.cuh) for w whose resident slice does not fit
-template <int MB, int NS>
-bool xformk_try(smpm_batch* b, int P) {
-  const int w = b->w;
-  const size_t smem = xformk_smem<MB, NS>();
-  if (smem > 232448 || 8 * MB * P < w || P > b->ctx->num_sms) return false;
-  CUDA_CHECK(cudaFuncSetAttribute(xformk_kernel<MB, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-  std::vector<double> f(static_cast<size_t>(P) * (w / 8) * MB * 64), fi(f.size());
-  xform_frag_order(b->hT.data(), w, P, MB, f.data());
-  xform_frag_order(b->hTi.data(), w, P, MB, fi.data());
-  b->dTfrag.upload(f, b->ctx->stream);
-  b->dTifrag.upload(fi, b->ctx->stream);
-  CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
-  b->xf_P = P;
-  b->xf_MB = MB;
-  b->xf_smem = smem;
-  b->xf_stream = true;
-  return true;
-}
-
-// ---- parity-split transforms (xformp.cuh) -----------------------------------
-// True when every column of T (row of T^{-1}) is even or odd under the reversal of
-// the node index and the modes are ordered pairs (even, odd), reals (even, odd);
-// fills the mode segments of each parity.
-bool parity_detect(smpm_batch* b) {
-  const int w = b->w, h = w / 2, np2 = 2 * b->sp_npairs;
-  if (w % 16 != 0) return false;
-  std::vector<int> par(static_cast<size_t>(w), 0);
-  const double tol = 1e-14;
-  for (int m = 0; m < w; ++m) {
-    double amax = 0.0, ce = 0.0, co = 0.0, rmax = 0.0, re = 0.0, ro = 0.0;
-    for (int r = 0; r < w; ++r) {
-      const double x = b->hT[static_cast<size_t>(m) * w + r], y = b->hT[static_cast<size_t>(m) * w + (w - 1 - r)];
-      amax = std::max(amax, std::fabs(x));
-      ce = std::max(ce, std::fabs(x - y));
-      co = std::max(co, std::fabs(x + y));
-      const double p = b->hTi[static_cast<size_t>(r) * w + m], q = b->hTi[static_cast<size_t>(w - 1 - r) * w + m];
-      rmax = std::max(rmax, std::fabs(p));
-      re = std::max(re, std::fabs(p - q));
-      ro = std::max(ro, std::fabs(p + q));
-    }
-    if (ce <= tol * amax && re <= tol * rmax)
-      par[m] = 1;
-    else if (co <= tol * amax && ro <= tol * rmax)
-      par[m] = -1;
-    else
-      return false;
-  }
-  int npe = 0;
-  while (2 * npe < np2 && par[2 * npe] == 1) ++npe;
-  for (int q = 0; q < b->sp_npairs; ++q) {
-    const int want = q < npe ? 1 : -1;
-    if (par[2 * q] != want || par[2 * q + 1] != want) return false;
-  }
-  int nre = 0;
-  while (np2 + nre < w && par[np2 + nre] == 1) ++nre;
-  for (int m = np2 + nre; m < w; ++m)
-    if (par[m] != -1) return false;
-  if (2 * npe + nre != h) return false;
-  b->xp_h = h;
-  b->xp_ks = (h + XK_KS - 1) / XK_KS;
-  b->xp_seg_start[0][0] = 0;
-  b->xp_seg_len0[0] = 2 * npe;
-  b->xp_seg_start[0][1] = np2;
-  b->xp_seg_start[1][0] = 2 * npe;
-  b->xp_seg_len0[1] = np2 - 2 * npe;
-  b->xp_seg_start[1][1] = np2 + nre;
-  return true;
-}
-
-template <int MB, int NS, bool BWD>
-void xformp_attr() {
-  CUDA_CHECK(cudaFuncSetAttribute(xformp_kernel<MB, NS, BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(xformp_smem<MB, NS, BWD>())));
-}
-
-void setup_xformp(smpm_batch* b) {
-  const int w = b->w, h = b->xp_h, ks = b->xp_ks, mbt = h / 8;
-  // forward: Ps single-parity slices per parity of at most 34 m-blocks
-  const int Ps = (mbt + 33) / 34, needf = (mbt + Ps - 1) / Ps;
-  const int MBf = needf <= 11 ? 11 : needf <= 17 ? 17 : needf <= 26 ? 26 : 34;
-  // backward: P slices of rows k < h of at most 17 m-blocks (two accumulator sets)
-  const int Pb = (mbt + 16) / 17, needb = (mbt + Pb - 1) / Pb;
-  const int MBb = needb <= 9 ? 9 : needb <= 11 ? 11 : needb <= 13 ? 13 : 17;
-  if (2 * Ps > b->ctx->num_sms || Pb > b->ctx->num_sms) return;
-  switch (MBf) {
-    case 11: xformp_attr<11, 6, false>(); b->xp_smem_f = xformp_smem<11, 6, false>(); break;
-    case 17: xformp_attr<17, 5, false>(); b->xp_smem_f = xformp_smem<17, 5, false>(); break;
-    case 26: xformp_attr<26, 4, false>(); b->xp_smem_f = xformp_smem<26, 4, false>(); break;
-    default: xformp_attr<34, 3, false>(); b->xp_smem_f = xformp_smem<34, 3, false>(); break;
-  }
-  switch (MBb) {
-    case 9: xformp_attr<9, 8, true>(); b->xp_smem_b = xformp_smem<9, 8, true>(); break;
-    case 11: xformp_attr<11, 8, true>(); b->xp_smem_b = xformp_smem<11, 8, true>(); break;
-    case 13: xformp_attr<13, 8, true>(); b->xp_smem_b = xformp_smem<13, 8, true>(); break;
-    default: xformp_attr<17, 7, true>(); b->xp_smem_b = xformp_smem<17, 7, true>(); break;
-  }
-  auto mode = [&](int par, int kap) { return xp_mode(b->xp_seg_start, b->xp_seg_len0, par, kap); };
-  std::vector<double> f;
-  xformp_image(2 * Ps, ks, MBf, [&](int sl, int r, int kk) {
-    const int par = sl / Ps, kap = (sl % Ps) * 8 * MBf + r;
-    if (kap >= h || kk >= h) return 0.0;
-    return b->hTi[static_cast<size_t>(kk) * w + mode(par, kap)];
-  }, f);
-  b->dTpf.upload(f, b->ctx->stream);
-  xformp_image(Pb, 2 * ks, MBb, [&](int sl, int r, int kk) {
-    const int k = sl * 8 * MBb + r, pq = kk / (XK_KS * ks), kap = kk - pq * XK_KS * ks;
-    if (k >= h || kap >= h) return 0.0;
-    return b->hT[static_cast<size_t>(mode(pq, kap)) * w + k];
-  }, f);
-  b->dTpb.upload(f, b->ctx->stream);
-  CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
-  b->xp_Pf = 2 * Ps;
-  b->xp_MBf = MBf;
-  b->xp_Pb = Pb;
-  b->xp_MBb = MBb;
-  b->xp_on = true;
-}
-
-void setup_xform(smpm_batch* b) {
-  b->xf_P = 0;
-  b->xf_stream = false;
-  b->xp_on = false;
-  if (b->w % 16 != 0 || !b->tune.xform) return;
-  bool found = false;
-  for (int P = 1; P <= 4 && !found; ++P) {
-    const int need = (b->w / 8 + P - 1) / P;
-    found = need <= 4 ? xform_try<4>(b, P) : need <= 8 ? xform_try<8>(b, P) : need <= 11 ? xform_try<11>(b, P) : false;
-  }
-  if (!found) {
-    // w > 176: A streams with the columns; P row slices of at most 34 m-blocks
-    const int K8 = b->w / 8;
-    const int P = (K8 + 33) / 34;
-    const int need = (K8 + P - 1) / P;
-    if (need <= 26)
-      found = xformk_try<26, 5>(b, P);
-    else if (need <= 34)
-      found = xformk_try<34, 4>(b, P);
-  }
-  // parity-pure basis: two half-size contractions instead (half the MMA work)
-  const int pm = b->tune.xform_parity;
-  if (found && pm > 0 && (pm >= 2 || b->xf_stream) && parity_detect(b)) setup_xformp(b);
-}
-
-// one transform launch over the columns described by `a` (a.P set), groups column groups
-// parity-split launch: `a` as for launch_xform (a.Af / a.P are replaced by the direction's image / slices)
-void launch_xformp(smpm_batch* b, const XformArgs& a, bool inverse, cudaStream_t st, bool pdl) {
-  XformPArgs pa;
-  pa.x = a;
-  pa.x.Af = inverse ? b->dTpf.p : b->dTpb.p;
-  pa.x.P = inverse ? b->xp_Pf : b->xp_Pb;
-  pa.h = b->xp_h;
-  pa.ks = b->xp_ks;
-  for (int p = 0; p < 2; ++p) {
-    pa.seg_start[p][0] = b->xp_seg_start[p][0];
-    pa.seg_start[p][1] = b->xp_seg_start[p][1];
-    pa.seg_len0[p] = b->xp_seg_len0[p];
-  }
-  const long long nch = (static_cast<long long>(a.nslots) * a.ncol_sys * a.nv + 15) / 16;
-  const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / pa.x.P, nch)));
-  const dim3 grid(groups * pa.x.P), blk(XF_THREADS);
-  const size_t smem = inverse ? b->xp_smem_f : b->xp_smem_b;
-  auto go = [&](auto kern) {
-    if (pdl) {
-      launch_pdl(b, kern, grid, blk, smem, st, pa);
-    } else {
-      kern<<<grid, blk, smem, st>>>(pa);
-      check_launch(b);
-    }
-  };
-  if (inverse) {
-    switch (b->xp_MBf) {
-      case 11: go(xformp_kernel<11, 6, false>); break;
-      case 17: go(xformp_kernel<17, 5, false>); break;
-      case 26: go(xformp_kernel<26, 4, false>); break;
-      default: go(xformp_kernel<34, 3, false>); break;
-    }
-  } else {
-    switch (b->xp_MBb) {
-      case 9: go(xformp_kernel<9, 8, true>); break;
-      case 11: go(xformp_kernel<11, 8, true>); break;
-      case 13: go(xformp_kernel<13, 8, true>); break;
-      default: go(xformp_kernel<17, 7, true>); break;
-    }
-  }
-}
-
-void launch_xform(smpm_batch* b, const XformArgs& a, int groups, cudaStream_t st, bool pdl) {
-  const dim3 grid(groups * a.P), blk(XF_THREADS);
-  auto go = [&](auto kern) {
-    if (pdl) {
-      launch_pdl(b, kern, grid, blk, b->xf_smem, st, a);
-    } else {
-      kern<<<grid, blk, b->xf_smem, st>>>(a);
-      check_launch(b);
-    }
-  };
-  if (b->xf_stream) {
-    if (b->xf_MB == 26)
-      go(xformk_kernel<26, 5>);
-    else
-      go(xformk_kernel<34, 4>);
-    return;
-  }
-  switch (b->xf_MB) {
-    case 4: go(xform_kernel<4>); break;
-    case 8: go(xform_kernel<8>); break;
-    default: go(xform_kernel<11>); break;
-  }
-}
-
-// out = A in (and out2 = A in2) for every w-block of the live systems, A = T^{-1} (inverse) or T
-void run_xform(smpm_batch* b, bool inverse, const double* in, double* out, const Live& lv, cudaStream_t st,
-               const double* in2 = nullptr, double* out2 = nullptr) {
-  if (lv.nslots == 0) return;
-  ProfScope psx(b, 8, st);  // class 8: shared-matrix transforms
-  if (b->xf_P == 0) {
-    run_plan(b, inverse ? b->pF : b->pB, in, out, nullptr, lv, st);
-    if (in2) run_plan(b, inverse ? b->pF : b->pB, in2, out2, nullptr, lv, st);
-    return;
-  }
-  XformArgs a;
-  a.Af = inverse ? b->dTifrag.p : b->dTfrag.p;
-  a.w = b->w;
-  a.ncol_sys = 2 * b->d;
-  a.k = b->k;
-  a.alist = lv.alist;
-  a.acount = lv.acount;
-  a.nslots = lv.nslots;
-  a.nv = in2 ? 2 : 1;
-  a.in[0] = in;
-  a.out[0] = out;
-  a.in[1] = in2;
-  a.out[1] = out2;
-  a.P = b->xf_P;
-  // column groups: every SM busy unless a group's share would drop below 16 columns
-  const long long nch = (static_cast<long long>(lv.nslots) * a.ncol_sys * a.nv + 15) / 16;
-  const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / a.P, nch)));
-  if (b->xp_on)
-    launch_xformp(b, a, inverse, st, true);
-  else
-    launch_xform(b, a, groups, st, true);
-}
-
-// th = S^ M^^{-1} vh (bj) or S^ vh in T-coordinates; with cout, also
-// c = C^{-1} Z^T (T th) per system (deflation coarse solve)
-void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* cout, const Live& lv, cudaStream_t st,
-                double* uh = nullptr, const double* cadd = nullptr) {
-  if (lv.nslots == 0) return;
-  ProfScope ps(b, 7, st);  // class 7: per-mode pass
-  SpecParams sp = spec_params(b);
-  sp.cadd = cadd;
-  DeflateParams P = deflate_params(b, lv.active);
-  P.alist = lv.alist;
-  P.acount = lv.acount;
-  double* zp = cout ? b->dzpart.p : nullptr;
-  if (b->tune.spec_v2) {
-    // pipelined pass (spec_op2_kernel): segments as long as ~32 warps per SM
-    // still allow (shorter halo), at least 4 and at most 16 blocks
-    const long long nbk = b->nbf + (b->single ? 1 : 0);
-    const long long warps = nbk * sp.nmc * lv.nslots;
-    int segb = static_cast<int>(std::max(4LL, std::min(16LL, warps / (32LL * b->ctx->num_sms))));
-    if (b->tune.segb > 0) segb = b->tune.segb;
-    sp.segb = segb;
-    sp.nseg = static_cast<int>((nbk + segb - 1) / segb);
-    const dim3 grid2(sp.nmc * ((sp.nseg + SP_WARPS - 1) / SP_WARPS), lv.nslots);
-    const size_t shm2 = cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0;
-    if (bj)
-      launch_pdl(b, spec_op2_kernel<true>, grid2, dim3(SP_THREADS), shm2, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);
-    else
-      launch_pdl(b, spec_op2_kernel<false>, grid2, dim3(SP_THREADS), shm2, st, sp, vh, th, P, zp, b->dcount.p, cout,
-                 uh);
-    return;
-  }
-  const dim3 grid(sp.nmc * ((sp.nseg + SP_WARPS - 1) / SP_WARPS), lv.nslots);
-  // staged slot rows (tuning sp_stage = 0: direct loads)
-  sp.stage = sp.segb <= SP_SEGB && b->tune.sp_stage ? 1 : 0;
-  const size_t shm = (cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0) +
-                     (sp.stage ? sizeof(double) * SP_STAGE_DOUBLES : 0);
-  if (sp.stage && !b->sp_smem_set) {
-    const int mx = static_cast<int>(sizeof(double) * (SP_STAGE_DOUBLES + 2 * 256));
-    CUDA_CHECK(cudaFuncSetAttribute(spec_op_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    CUDA_CHECK(cudaFuncSetAttribute(spec_op_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    b->sp_smem_set = true;
-  }
-  if (bj)
-    launch_pdl(b, spec_op_kernel<true>, grid, dim3(SP_THREADS), shm, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);
-  else
-    launch_pdl(b, spec_op_kernel<false>, grid, dim3(SP_THREADS), shm, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);
-}
-
-// u = M^{-1} v through the spectral form, and (su != nullptr) S u as well
-void spec_Minv(smpm_batch* b, const double* v, double* u, double* su, const Live& lv, cudaStream_t st) {
-  run_xform(b, true, v, b->dvh.p, lv, st);
-  spec_apply(b, true, b->dvh.p, su ? b->dth.p : nullptr, nullptr, lv, st, b->dvh2.p);
-  run_xform(b, false, b->dvh2.p, u, lv, st, su ? b->dth.p : nullptr, su);
-}
-
-bool spec_on(const smpm_batch* b) { return b->spectral && b->tune.spectral; }
-
-bool spec_ok(const smpm_batch* b, const SolveCfg& c) {
-  return spec_on(b) && (c.method == SMPM_SCHUR || c.method == SMPM_BJ || c.method == SMPM_DBJ);
-}
-// 2LAS through the spectral form in the per-stage steps (many live systems); the grid
-// tail keeps its dense stages for 2LAS (a coarse solve before the per-mode pass would
-// add two grid barriers per step; measured: per-stage spectral 2LAS with one live
-// system is slower than the dense tail, 12.1 vs 10.2 ms on C3)
-bool spec_2las(const smpm_batch* b, const SolveCfg& c) {
-  return spec_on(b) && c.method == SMPM_2LAS && b->tune.spec_2las;
-}
-
-// S M^{-1} v (bj) or S v through the spectral form; out may be any buffer
-void spec_SMinv(smpm_batch* b, bool bj, const double* v, double* out, double* cout, const Live& lv, cudaStream_t st) {
-  run_xform(b, true, v, b->dvh.p, lv, st);
-  spec_apply(b, bj, b->dvh.p, b->dth.p, cout, lv, st);
-  run_xform(b, false, b->dth.p, out, lv, st);
-}
-
-// the preconditioned operator GMRES iterates on (proj/src/deflation.cpp:105-107,131; proj/src/gmres.cpp:144-150)
-// returns the number of S applications it made per system
-int apply_op(smpm_batch* b, const SolveCfg& c, const double* vin, double* wout, const Live& act, cudaStream_t st) {
-  double* u = b->vbuf[4].p;
-  double* t = b->vbuf[5].p;
-  if (spec_ok(b, c)) {
-    if (c.method == SMPM_DBJ) {
-      spec_SMinv(b, true, vin, t, nullptr, act, st);
-      op_P(b, t, wout, c.fused, act, st);
-      return c.fused ? 1 : 2;
-    }
-    spec_SMinv(b, c.method == SMPM_BJ, vin, wout, nullptr, act, st);
-    return 1;
-  }
-  if (spec_2las(b, c)) {
-    // S (M^{-1} + Z C^{-1} Z^T) v: c = C^{-1} Z^T v, then one per-mode pass of
-    // T^{-1} v that adds Z c before S^ (proj/src/deflation.cpp:127-131)
-    double* cb = b->dcoarse.p + static_cast<size_t>(b->nsys) * b->d;
-    run_deflate(b, DEFL_COARSE, vin, nullptr, nullptr, cb, act, st);
-    run_xform(b, true, vin, b->dvh.p, act, st);
-    spec_apply(b, true, b->dvh.p, b->dth.p, nullptr, act, st, nullptr, cb);
-    run_xform(b, false, b->dth.p, wout, act, st);
-    return 1;
-  }
-  switch (c.method) {
-    case SMPM_SCHUR:
-      op_S(b, vin, wout, act, st);
-      return 1;
-    case SMPM_BJ:
-      op_BJ(b, vin, u, act, st);
-      op_S(b, u, wout, act, st);
-      return 1;
-    case SMPM_DBJ:
-      op_BJ(b, vin, u, act, st);
-      op_S(b, u, t, act, st);
-      op_P(b, t, wout, c.fused, act, st);
-      return c.fused ? 1 : 2;
-    case SMPM_2LAS: {
-      op_BJ(b, vin, u, act, st);
-      run_deflate(b, DEFL_ADD_ZC, vin, u, t, nullptr, act, st);  // minv = M^{-1} + Z C^{-1} Z^T
-      op_S(b, t, wout, act, st);
-      return 1;
-    }
-  }
-  fail(SMPM_EINVAL, "unknown method");
-}
-
-// ---- stacked solve: sums over all systems (vec.cuh); with an all-reduce hook
-// (smpm_batch_set_allreduce) the systems of the stack are spread over ranks and
-// every sum is all-reduced across them (one all-reduce per inner product,
-// proj/src/helmholtz.cpp:187-246 run across GPUs)
-void stack_allreduce(smpm_batch* b, int count, cudaStream_t st) {
-  const int rc = b->ar_fn(b->ar_user, b->dstack.p, count, st);
-  if (rc != 0) fail(SMPM_ERUNTIME, "all-reduce hook failed (" + std::to_string(rc) + ")");
-}
-void stack_sum(smpm_batch* b, double* v, cudaStream_t st) {
-  if (!b->ar_fn) {
-    launch_pdl(b, stack_sum_kernel, dim3(1), dim3(128), 0, st, b->nsys, v);
-    return;
-  }
-  stack_sum_local_kernel<<<1, 32, 0, st>>>(b->nsys, v, b->dstack.p);
-  check_launch(b);
-  stack_allreduce(b, 1, st);
-  stack_sum_bcast_kernel<<<1, 128, 0, st>>>(b->nsys, v, b->dstack.p);
-  check_launch(b);
-}
-void stack_h(smpm_batch* b, double* h, cudaStream_t st) {
-  if (!b->ar_fn) {
-    launch_pdl(b, stack_h_kernel, dim3(1), dim3(128), 0, st, b->G, h);
-    return;
-  }
-  stack_h_local_kernel<<<1, 128, 0, st>>>(b->G, h, b->dstack.p);
-  check_launch(b);
-  stack_allreduce(b, b->jhost + 1, st);
-  stack_h_bcast_kernel<<<1, 128, 0, st>>>(b->G, h, b->dstack.p);
-  check_launch(b);
-}
-void stack_givens(smpm_batch* b, cudaStream_t st) {
-  if (!b->ar_fn) {
-    launch_pdl(b, stack_givens_kernel, dim3(b->nsys), dim3(32), 0, st, b->G);
-    return;
-  }
-  stack_sum_local_kernel<<<1, 32, 0, st>>>(b->nsys, b->G.snsq, b->dstack.p);
-  check_launch(b);
-  stack_allreduce(b, 1, st);
-  stack_givens_global_kernel<<<b->nsys, 32, 0, st>>>(b->G, b->dstack.p);
-  check_launch(b);
-}
-
-// row chunking of a CGS2 pass kernel for `nslots` live systems: (live systems x chunks)
-// <= the kernel's resident CTA count `res` (one wave)
-GmState_ cgs3_chunked(smpm_batch* b, long long res, int nslots, dim3& g) {
-  GmState_ Gk = b->G;
-  const long long kc = std::max(1LL, res / std::max(1, nslots));
-  long long ck = (b->k + kc - 1) / kc;
-  ck = std::max(256LL, (ck + 255) / 256 * 256);
-  Gk.chunk = static_cast<int>(ck);
-  Gk.nchunk = static_cast<int>((b->k + ck - 1) / ck);
-  g = dim3(Gk.nchunk, nslots);
-  return Gk;
-}
-
-// deferred CGS2: materialise the pending basis vector (pass 3': v = (w' - V h2) / nrm
-// into the basis and the operator input) before a path that needs it
-void flush_pending(smpm_batch* b, int nslots, cudaStream_t st) {
-  if (!b->pending) return;
-  b->pending = false;
-  if (nslots <= 0) return;
-  if (b->cgs3_kres[2] == 0) {
-    int o = 0;
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs3_pass3s_kernel, V3_THREADS, 0));
-    b->cgs3_kres[2] = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
-  }
-  dim3 g3;
-  const GmState_ G3 = cgs3_chunked(b, b->cgs3_kres[2], nslots, g3);
-  launch_pdl(b, cgs3_pass3s_kernel, g3, dim3(V3_THREADS), 0, st, G3, b->dV.p, b->vbuf[3].p, b->vbuf[2].p);
-}
-
-void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t st) {
-  GmState_& G = b->G;
-  double* V = b->dV.p;
-  double* vin = b->vbuf[2].p;
-  double* wv = b->vbuf[3].p;
-  // dbj with fused P on the CGS2 path: the deflation update is applied inside
-  // the first Gram-Schmidt pass (only Z^T + the coarse solve run here)
-  const bool fuse_into_cgs = c.method == SMPM_DBJ && c.fused && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= V2_MAXCOL;
-  double* cbuf = b->dcoarse.p + static_cast<size_t>(b->nsys) * b->d;
-  const double* tdefl = nullptr;
-  // deferred CGS2 (vec4.cuh): after a cycle's first step the newest basis vector stays
-  // pending as (w', h2); the operator runs on w' and pass 1B forms the vector
-  const bool defer = fuse_into_cgs && b->tune.cgs_defer && !G.stacked && b->pythag;
-  const bool pend = defer && b->pending;
-  const double* opin = pend ? wv : vin;
-  if (fuse_into_cgs && spec_ok(b, c)) {
-    // spectral: t = S M^{-1} v and c = C^{-1} Z^T t from the per-mode pass
-    double* t = b->vbuf[5].p;
-    spec_SMinv(b, true, opin, t, cbuf, lv, st);
-    tdefl = t;
-  } else if (fuse_into_cgs) {
-    double* u = b->vbuf[4].p;
-    double* t = b->vbuf[5].p;
-    op_BJ(b, opin, u, lv, st);
-    op_S(b, u, t, lv, st);
-    run_deflate(b, DEFL_COARSE, t, nullptr, nullptr, cbuf, lv, st);
-    tdefl = t;
-  } else {
-    apply_op(b, c, vin, wv, lv, st);
-  }
-  ProfScope ps(b, PC_ORTH, st);
-  dim3 grid(G.nchunk, b->nsys);      // system-indexed kernels (MGS, long cycles)
-  dim3 sgrid(G.nchunk, lv.nslots);   // live-slot kernels
-  const size_t hsm = sizeof(double) * static_cast<size_t>(G.m + 2);
-  if (c.orth == SMPM_ORTH_MGS) {
-    for (int i = 0; i <= std::min(G.m, G.m_total); ++i) {
-      mgs_step_kernel<<<grid, VEC_THREADS, 0, st>>>(G, V, wv, i);
-      check_launch(b);
-    }
-    gm_zero_h2_kernel<<<b->nsys, 128, 0, st>>>(G);
-    check_launch(b);
-    cgs2_update_kernel<true><<<grid, V2_THREADS, 0, st>>>(G, V, wv, 0);  // norm + Givens only
-    check_launch(b);
-  } else if (G.m + 2 > V2_MAXCOL) {
-    // long cycles: column-count-agnostic kernels (dynamic shared memory)
-    cgs_dot_kernel<<<grid, VEC_THREADS, 0, st>>>(G, V, wv);
-    check_launch(b);
-    cgs_update_kernel<false><<<grid, VEC_THREADS, hsm, st>>>(G, V, wv, 1);
-    check_launch(b);
-    cgs_update_kernel<true><<<grid, VEC_THREADS, hsm, st>>>(G, V, wv, 1);
-    check_launch(b);
-  } else {
-    // long row chunks: (live systems x chunks) <= the resident CTA count of the
-    // passes, so a batch of live systems is one wave (a 5 % second wave would
-    // double the pass) and per-system partial sums stay few
-    GmState_ Gl = G;
-    if (b->cgs3_res == 0) {
-      int o1 = 0, o2 = 0, o3 = 0;
-      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, cgs3_dot_kernel, V3_THREADS, 0));
-      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, cgs3_update_kernel<false>, V3_THREADS, 0));
-      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, cgs3_update_kernel<true>, V3_THREADS, 0));
-      b->cgs3_res = std::max(1, std::min(o1, std::min(o2, o3))) * b->ctx->num_sms;
-    }
-    const long long target = b->cgs3_res;
-    const long long cps = std::max(1LL, target / lv.nslots);
-    long long chunk = (b->k + cps - 1) / cps;
-    chunk = std::max(256LL, (chunk + 255) / 256 * 256);
-    Gl.chunk = static_cast<int>(chunk);
-    Gl.nchunk = static_cast<int>((b->k + chunk - 1) / chunk);
-    dim3 cgrid(Gl.nchunk, lv.nslots);
-    DeflateParams P = deflate_params(b, nullptr);
-    if (!G.stacked && b->pythag) {
-      // ||w|| from the second reduction (||w1||^2 - ||h2||^2), the scale folded into pass 3:
-      // one reduction and one kernel less per step; iteration counts measured unchanged
-      // on 9 right-hand sides (tools/seed_sweep.py).
-      // Each pass gets its own row chunking sized to ITS resident CTA count (the
-      // passes differ in registers: one wave each; partials and counters are per
-      // kernel, the work vector is exchanged only between kernels)
-      if (b->cgs3_kres[0] == 0) {
-        int o[3] = {0, 0, 0};
-        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[0], cgs3_dot_kernel, V3_THREADS, 0));
-        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[1], cgs3_pass2n_kernel, V3_THREADS, 0));
-        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[2], cgs3_pass3s_kernel, V3_THREADS, 0));
-        for (int i = 0; i < 3; ++i) b->cgs3_kres[i] = std::max(1, o[i]) * b->ctx->num_sms;
-      }
-      auto chunked = [&](long long res, dim3& g) { return cgs3_chunked(b, res, lv.nslots, g); };
-      dim3 g1, g2, g3;
-      const GmState_ G1 = chunked(b->cgs3_kres[0], g1), G2 = chunked(b->cgs3_kres[1], g2),
-                     G3 = chunked(b->cgs3_kres[2], g3);
-      const int ncols_h = b->jhost + 1;
-      if (pend) {
-        // pass 1B: v_j = (w' - V h2) / nrm -> V[:, j], w = (P t) / nrm, h1 = [V, v_j]^T w
-        const int nold = b->jhost;
-        if (nold <= 2 * V3_GRP) {
-          if (b->p1b_res == 0) {
-            int o = 0;
-            CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs4_pass1b_kernel, V3_THREADS, 0));
-            b->p1b_res = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
-          }
-          dim3 gb;
-          const GmState_ Gb = chunked(b->p1b_res, gb);
-          launch_pdl(b, cgs4_pass1b_kernel, gb, dim3(V3_THREADS), 0, st, Gb, V, wv, tdefl, 1, P,
-                     static_cast<const double*>(cbuf));
-        } else if (b->tune.cgs_lanes) {
-          if (b->p1bl_res == 0) {
-            int o = 0;
-            CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs5_pass1bl_kernel, V3_THREADS, 0));
-            b->p1bl_res = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
-          }
-          dim3 gb;
-          const GmState_ Gb = chunked(b->p1bl_res, gb);
-          launch_pdl(b, cgs5_pass1bl_kernel, gb, dim3(V3_THREADS), 0, st, Gb, V, wv, tdefl, 1, P,
-                     static_cast<const double*>(cbuf));
-        } else {
-          const size_t smem = sizeof(double) * p1bt_smem_doubles(nold);
-          if (!b->p1bt_attr) {
-            size_t mx = 0;
-            for (int cc = 2 * V3_GRP + 1; cc <= 8 * P2T_MAXC; ++cc) mx = std::max(mx, p1bt_smem_doubles(cc));
-            CUDA_CHECK(cudaFuncSetAttribute(cgs4_pass1bt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(sizeof(double) * mx)));
-            b->p1bt_attr = true;
-          }
-          if (b->p1bt_res[nold] == 0) {
-            int o = 0;
-            CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs4_pass1bt_kernel, V3_THREADS, smem));
-            b->p1bt_res[nold] = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
-          }
-          dim3 gb;
-          const GmState_ Gb = chunked(b->p1bt_res[nold], gb);
-          launch_pdl(b, cgs4_pass1bt_kernel, gb, dim3(V3_THREADS), smem, st, Gb, V, wv, tdefl, 1, P,
-                     static_cast<const double*>(cbuf));
-        }
-      } else {
-        launch_pdl(b, cgs3_dot_kernel, g1, dim3(V3_THREADS), 0, st, G1, V, wv, tdefl, P, cbuf);
-      }
-      if (b->tune.p2fuse && b->tune.cgs_lanes && ncols_h > 2 * V3_GRP && ncols_h <= LN_MAXCOL &&
-          ncols_h <= G.m + 1) {
-        // more than 16 columns: update and dots in one read of V, eight lanes per row (cgs5_pass2l_kernel)
-        if (b->p2l_res == 0) {
-          int o = 0;
-          CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs5_pass2l_kernel, V3_THREADS, 0));
-          b->p2l_res = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
-        }
-        dim3 g2l;
-        const GmState_ G2l = chunked(b->p2l_res, g2l);
-        launch_pdl(b, cgs5_pass2l_kernel, g2l, dim3(V3_THREADS), 0, st, G2l, static_cast<const double*>(V), wv);
-      } else if (b->tune.p2fuse && ncols_h > 2 * V3_GRP && ncols_h <= 8 * P2T_MAXC && ncols_h <= G.m + 1) {
-        // more than 16 columns: update and dots in one read of V through
-        // shared-memory row tiles (cgs3_pass2t_kernel)
-        const size_t smem = sizeof(double) * p2t_smem_doubles(ncols_h);
-        if (!b->p2t_attr) {
-          size_t mx = 0;
-          for (int cc = 2 * V3_GRP + 1; cc <= 8 * P2T_MAXC; ++cc) mx = std::max(mx, p2t_smem_doubles(cc));
-          CUDA_CHECK(cudaFuncSetAttribute(cgs3_pass2t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(sizeof(double) * mx)));
-          b->p2t_attr = true;
-        }
-        if (b->p2t_res[ncols_h] == 0) {
-          int o = 0;
-          CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs3_pass2t_kernel, V3_THREADS, smem));
-          b->p2t_res[ncols_h] = std::max(1, o) * b->ctx->num_sms;
-        }
-        dim3 g2t;
-        const GmState_ G2t = chunked(b->p2t_res[ncols_h], g2t);
-        launch_pdl(b, cgs3_pass2t_kernel, g2t, dim3(V3_THREADS), smem, st, G2t, static_cast<const double*>(V), wv,
-                   ncols_h);
-      } else {
-        // ncols <= 16: update and dots in one read of V (tuning p2fuse = 0: two reads)
-        launch_pdl(b, cgs3_pass2n_kernel, g2, dim3(V3_THREADS), 0, st, G2, static_cast<const double*>(V), wv,
-                   b->tune.p2fuse ? 1 : 0);
-      }
-      if (defer)
-        b->pending = true;  // v_{j+1} is formed by the next step's pass 1B (or flush_pending)
-      else
-        launch_pdl(b, cgs3_pass3s_kernel, g3, dim3(V3_THREADS), 0, st, G3, V, wv, vin);
-      ++b->jhost;
-      return;
-    }
-    launch_pdl(b, cgs3_dot_kernel, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv, tdefl, P, cbuf);
-    if (G.stacked) stack_h(b, G.h1, st);
-    launch_pdl(b, cgs3_update_kernel<false>, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv);
-    if (G.stacked) stack_h(b, G.h2, st);
-    launch_pdl(b, cgs3_update_kernel<true>, cgrid, dim3(V3_THREADS), 0, st, Gl, V, wv);
-    if (G.stacked) stack_givens(b, st);
-  }
-  (void)hsm;
-  dim3 sg(std::max(1, std::min(G.nchunk, 64)), lv.nslots);
-  launch_pdl(b, gm_scale_kernel, sg, dim3(256), 0, st, G, V, wv, vin);
-  ++b->jhost;
-}
-
-// Compacted list of live systems (ascending index, so deterministic) from a
-// flag array, plus RUN / CYCLE state counts for the host; single CTA.
-__global__ void __launch_bounds__(1024) compact_kernel(const int* flags, const int* state, int nsys, int* alist,
-                                                       int* acount, int* counts) {
-  pdl_wait();
-  pdl_launch();
-  __shared__ int wsum[32];
-  __shared__ int base, run, cyc;
-  if (threadIdx.x == 0) {
-    base = 0;
-    run = 0;
-    cyc = 0;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int s0 = 0; s0 < nsys; s0 += blockDim.x) {
-    const int s = s0 + threadIdx.x;
-    const int f = (s < nsys && flags[s]) ? 1 : 0;
-    if (s < nsys && state) {
-      if (state[s] == GM_RUN) atomicAdd(&run, 1);
-      if (state[s] == GM_CYCLE) atomicAdd(&cyc, 1);
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) wsum[warp] = __popc(bal);
-    __syncthreads();
-    int off = base;
-    for (int q = 0; q < warp; ++q) off += wsum[q];
-    if (f) alist[off + __popc(bal & ((1u << lane) - 1u))] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int q = 0; q < nw; ++q) t += wsum[q];
-      base += t;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    *acount = base;
-    if (counts) {
-      counts[0] = run;
-      counts[1] = cyc;
-    }
-  }
-}
-
-// early / late split of the epilogue: systems in a final state (converged, breakdown,
-// iteration cap) when the grid tail starts, and the rest
-__global__ void early_select_kernel(const int* state, int nsys, int* early, int* late, int* hearly) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nsys) return;
-  const int f = (state[s] != GM_RUN && state[s] != GM_CYCLE) ? 1 : 0;
-  early[s] = f;
-  late[s] = 1 - f;
-  hearly[s] = f;
-}
-
-__global__ void select_state_kernel(const int* state, int nsys, int want, int* sel) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < nsys) sel[s] = state[s] == want ? 1 : 0;
-}
-
-// Runs the remaining Arnoldi steps of the current cycle of the (few) live
-// systems in one cooperative, grid-persistent launch (grid.cuh).
-// grid of the tail solver: as many CTAs (multiple of the cluster size) as
-// can be co-resident, up to SMPM_GRID_PER_SM (default 2) per SM
-int grid_blocks(smpm_batch* b) {
-  if (b->gt_blocks) return b->gt_blocks;
-  // the tile-ring region doubles as the per-step V-row block of the CGS2 passes
-  // (SMPM_GT_VBLOCK: 0 off, 1 ring size, 2 as large as two CTAs per SM allow)
-  const size_t rest = sizeof(double) * (3 * GT_MAXCOL + 2 * static_cast<size_t>(b->d));
-  size_t region = GT_SMEM;
-  int vmode = 2;  // 0: no V-row block, 1: within the ring region, 2: as large as 2 CTAs / SM allow (measured best)
-  vmode = b->tune.gt_vblock;
-  if (vmode >= 2) {
-    cudaFuncAttributes fa{};
-    CUDA_CHECK(cudaFuncGetAttributes(&fa, arnoldi_grid_kernel));
-    int dev = 0, per_sm = 0, resv = 0;
-    CUDA_CHECK(cudaGetDevice(&dev));
-    CUDA_CHECK(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-    CUDA_CHECK(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev));
-    const long long avail = static_cast<long long>(per_sm) / 2 - resv - static_cast<long long>(fa.sharedSizeBytes) -
-                            static_cast<long long>(rest);
-    region = std::max<size_t>(GT_SMEM, static_cast<size_t>(std::max(0LL, avail)) / 1024 * 1024);
-  }
-  b->gt_vcap = vmode > 0 ? static_cast<int>(region / sizeof(double)) : 0;
-  b->gt_smem = region + rest;
-  const size_t smem = b->gt_smem;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = GT_CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cfg.blockDim = dim3(G2_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  CUDA_CHECK(cudaFuncSetAttribute(arnoldi_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-  int per = 0;
-  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, arnoldi_grid_kernel, G2_THREADS, smem));
-  int cap = 2;
-  cap = std::max(1, b->tune.grid_per_sm);
-  const int want = b->ctx->num_sms * std::max(1, std::min(per, cap));
-  // every CTA must be resident: bound by the cluster occupancy calculator
-  cfg.gridDim = dim3(want / GT_CL * GT_CL);
-  int ncl = 0;
-  CUDA_CHECK(cudaOccupancyMaxActiveClusters(&ncl, arnoldi_grid_kernel, &cfg));
-  if (ncl < 1) fail(SMPM_ECUDA, "grid tail kernel cannot be resident");
-  b->gt_blocks = std::min(want / GT_CL, ncl) * GT_CL;
-  if (b->tune.gt_ctas > 0)  // experiment: cap the tail grid (multiple of the cluster size)
-    b->gt_blocks = std::max(GT_CL, std::min(b->gt_blocks, b->tune.gt_ctas / GT_CL * GT_CL));
-  return b->gt_blocks;
-}
-
-// Returns false (nothing launched) when the cooperative launch is rejected.
-bool arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int* acount, cudaStream_t st) {
-  ProfScope ps(b, 6, st);  // class 6: grid-persistent tail
-  GmState_& G = b->G;
-  grid_blocks(b);
-  const size_t smem = b->gt_smem;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = GT_CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeCooperative;
-  attr[1].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  cfg.blockDim = dim3(G2_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  grid_blocks(b);
-  const int nb = b->gt_blocks;
-  const size_t stride = static_cast<size_t>(G.m + 2);
-  b->dgtpart.alloc(std::max(b->dgtpart.n, 3 * static_cast<size_t>(nb / GT_CL) * stride));
-  b->dgtzsum.alloc(std::max(b->dgtzsum.n, static_cast<size_t>(GT_MAXSYS) * b->d));
-  GridArgs A{};
-  const bool spec = spec_ok(b, c) && b->pc[4].v2 && b->pc[5].v2;
-  for (int i = 0; i < (spec ? 6 : 4); ++i) {
-    const Plan& p = b->pc[i];
-    A.a_stride[i] = p.shared_a ? 0 : b->mstride;
-    A.jobs[i] = p.djobs.p;
-    A.tiles[i] = p.dtiles2.p;
-    A.ntiles[i] = p.ntiles;
-    A.ngemm[i] = p.ngemm;
-    A.gv[i] = p.dgv.p;
-    A.ngv[i] = p.ngv;
-    A.njobs[i] = static_cast<int>(p.jobs.size());
-  }
-  A.vin = b->vbuf[2].p;
-  A.w = b->vbuf[3].p;
-  A.u = b->vbuf[4].p;
-  A.t = b->vbuf[5].p;
-  A.tmp = b->vbuf[9].p;
-  A.V = b->dV.p;
-  A.part = b->dgtpart.p;
-  if (spec) {
-    A.spectral = 1;
-    A.sp = spec_params(b);
-    // latency-bound tail: one block per warp item (more warps, halo recomputed)
-    A.sp.segb = 1;
-    A.sp.nseg = b->nbf + (b->single ? 1 : 0);
-    A.vh = b->dvh.p;
-    A.th = b->dth.p;
-    b->dgtzp.alloc(std::max(b->dgtzp.n, static_cast<size_t>(GT_MAXSYS) * A.sp.nmc * b->d));
-    A.zp = b->dgtzp.p;
-    b->dgtcg.alloc(std::max(b->dgtcg.n, static_cast<size_t>(GT_MAXSYS) * b->d));
-    A.cg = b->dgtcg.p;
-  }
-  A.zsum = b->dgtzsum.p;
-  A.bar = b->dgbar.p;
-  A.alist = alist;
-  A.acount = acount;
-  A.method = c.method;
-  A.pythag = b->pythag ? 1 : 0;
-  A.vcap = b->gt_vcap;
-  A.G = G;
-  A.P = deflate_params(b, nullptr);
-  const char* tpath = b->tune.gt_trace.empty() ? nullptr : b->tune.gt_trace.c_str();
-  DevArray<unsigned long long> dtr;
-  if (tpath) {
-    dtr.alloc(64 * 16);
-    CUDA_CHECK(cudaMemsetAsync(dtr.p, 0, dtr.n * sizeof(unsigned long long), st));
-    A.trace = dtr.p;
-  }
-  const char* t2path = b->tune.gt_trace2.empty() ? nullptr : b->tune.gt_trace2.c_str();
-  DevArray<unsigned long long> dtr2;
-  if (t2path) {
-    dtr2.alloc(static_cast<size_t>(16) * nb * 8);
-    CUDA_CHECK(cudaMemsetAsync(dtr2.p, 0, dtr2.n * sizeof(unsigned long long), st));
-    A.trace2 = dtr2.p;
-  }
-  CUDA_CHECK(cudaMemsetAsync(b->dgbar.p, 0, sizeof(unsigned), st));
-  cfg.gridDim = dim3(nb);
-  // opt-in plain cluster launch (profilers only: co-residency is then not guaranteed)
-  cfg.numAttrs = b->tune.grid_nocoop ? 1 : 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, arnoldi_grid_kernel, A);
-  if (e != cudaSuccess && !b->tune.grid_nocoop) {
-    // cooperative cluster launch rejected (e.g. MPS, or co-residency not
-    // guaranteed): the software grid barrier needs every CTA resident, so the
-    // caller runs the rest of the cycle with the per-step kernels instead
-    (void)cudaGetLastError();
-    return false;
-  }
-  CUDA_CHECK(e);
-  check_launch(b);
-  if (tpath) {
-    std::vector<unsigned long long> h(dtr.n);
-    CUDA_CHECK(cudaMemcpyAsync(h.data(), dtr.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    if (FILE* f = std::fopen(tpath, "ab")) {
-      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
-      std::fclose(f);
-    }
-  }
-  if (t2path) {
-    std::vector<unsigned long long> h(dtr2.n);
-    CUDA_CHECK(cudaMemcpyAsync(h.data(), dtr2.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    if (FILE* f = std::fopen(t2path, "ab")) {
-      const unsigned long long hdr = static_cast<unsigned long long>(nb);
-      std::fwrite(&hdr, sizeof(hdr), 1, f);
-      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
-      std::fclose(f);
-    }
-  }
-  return true;
-}
-
-
-// xS_host (optional, pinned): also deliver x_S to the host; with the early epilogue the
-// rows of the early systems are copied while the grid tail runs
-void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_report* reps, double* history,
-           cudaStream_t st, double* xS_host = nullptr) {
-  need_final(b);
-  // programmatic dependent launch hides launch latency when the step's kernels are short
-  // (C4: +4 %); at C5 sizes (k = 277,440, ms-scale kernels) dependents that become resident
-  // early only take SM resources from the running kernel (measured -5 %): auto = off above
-  // 100,000 unknowns per system
-  b->pdl = b->tune.pdl < 0 ? b->k <= 100000 : b->tune.pdl != 0;
-  b->pythag = b->tune.pythag != 0;
-  if (c.max_iter < 1) fail(SMPM_EINVAL, "max_iter must be >= 1");
-  const int mtot = static_cast<int>(std::min<long long>(c.max_iter, b->k));
-  int m = c.restart > 0 ? std::min(c.restart, mtot) : mtot;
-  if (m > 4000) fail(SMPM_EINVAL, "Krylov cycle length above 4000 is not supported (use restart)");
-  ensure_gmres(b, m, mtot);
-  GmState_& G = b->G;
-  G.stacked = c.stacked ? 1 : 0;
-  if (c.stacked) {
-    if (c.orth != SMPM_ORTH_CGS2) fail(SMPM_EINVAL, "stacked solve: CGS2 orthogonalization only");
-    if (m + 2 > V2_MAXCOL) fail(SMPM_EINVAL, "stacked solve: cycle length above 126 (use restart)");
-    if (c.method == SMPM_DBJ && !c.fused) fail(SMPM_EINVAL, "stacked solve: fused deflation only");
-  }
-  const int ns = b->nsys;
-  const long long nk = static_cast<long long>(ns) * b->k;
-  double* rhs = b->vbuf[0].p;  // GMRES right-hand side (P b_S for dbj)
-  double* x = b->vbuf[1].p;    // Krylov iterate
-  double* vin = b->vbuf[2].p;
-  double* r = b->vbuf[6].p;
-  double* sc = b->dsmall.p + static_cast<size_t>(ns) * b->d;  // scratch scalars
-  double* nb2 = sc;        // ||b_S||^2
-  double* nr2 = sc + ns;   // ||rhs||^2 / ||r||^2
-  cudaEvent_t e0, e1, ev[2];
-  if (!b->sev[0]) {
-    CUDA_CHECK(cudaEventCreate(&b->sev[0]));
-    CUDA_CHECK(cudaEventCreate(&b->sev[1]));
-    CUDA_CHECK(cudaEventCreateWithFlags(&b->sev[2], cudaEventDisableTiming));
-    CUDA_CHECK(cudaEventCreateWithFlags(&b->sev[3], cudaEventDisableTiming));
-  }
-  e0 = b->sev[0];
-  e1 = b->sev[1];
-  ev[0] = b->sev[2];
-  ev[1] = b->sev[3];
-  int* dsel = b->dsel.p;
-  int* hcnt = b->hcnt;
-  CUDA_CHECK(cudaEventRecord(e0, st));
-  const long long launches0 = b->launches;
-  long long s_applies = 0, op_applies = 0;
-
-  const Live all = all_systems(b);
-  int* alist = b->dalist.p;
-  int* acount = b->dalist.p + ns;
-  int* alist2 = b->dalist.p + ns + 1;
-  int* acount2 = alist2 + ns;
-
-  // ---- right-hand side
-  if (c.method == SMPM_DBJ) {
-    op_P(b, bS, rhs, c.fused, all, st);  // pb = P b_S (proj/src/deflation.cpp:110)
-    // keep c_b = C^{-1} Z^T b_S for the solution (proj/src/deflation.cpp:118-120)
-    if (c.fused)
-      CUDA_CHECK(cudaMemcpyAsync(b->dczb.p, b->dcoarse.p + static_cast<size_t>(ns) * b->d,
-                                 sizeof(double) * ns * b->d, cudaMemcpyDeviceToDevice, st));
-  } else {
-    CUDA_CHECK(cudaMemcpyAsync(rhs, bS, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
-  }
-  batched_dot(b, bS, bS, nb2, nullptr, st);
-  batched_dot(b, rhs, rhs, nr2, nullptr, st);
-  if (c.stacked) {  // ||b|| and ||rhs|| of the stacked vector (proj/src/helmholtz.cpp:193-201)
-    stack_sum(b, nb2, st);
-    stack_sum(b, nr2, st);
-  }
-  CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double) * nk, st));
-  launch_pdl(b, gm_start_kernel, dim3((ns + 127) / 128), dim3(128), 0, st, G, static_cast<const double*>(nr2),
-             static_cast<const double*>(nb2), c.tol, 1, static_cast<const int*>(nullptr));
-  dim3 vg(std::max(1, std::min(G.nchunk, 64)), ns);
-  launch_pdl(b, gm_v0_kernel, vg, dim3(256), 0, st, G, b->dV.p, static_cast<const double*>(rhs), vin);
-  launch_pdl(b, compact_kernel, dim3(1), dim3(1024), 0, st, static_cast<const int*>(G.active),
-             static_cast<const int*>(nullptr), ns, alist, acount, static_cast<int*>(nullptr));
-  G.alist = alist;
-  G.acount = acount;
-  b->jhost = 0;
-  b->pending = false;
-
-  int steps = 0;
-  // ---- Arnoldi steps; device flags are polled one step behind the launches
-  // (step i+1 is queued before the host waits on step i's counters). Grids
-  // are sized by `bound`, the live count the host last read: systems only
-  // stop inside a cycle, so it bounds the device-compacted live list.
-  int bound = ns;
-  const int per_sys_applies = c.method == SMPM_DBJ && !c.fused ? 2 : 1;
-  auto issue = [&](int slot) {
-    Live lv;
-    lv.alist = alist;
-    lv.acount = acount;
-    lv.nslots = bound;
-    lv.active = G.active;
-    arnoldi_step(b, c, lv, st);
-    ++steps;
-    // live / cycle-end counts go straight into mapped host memory (no copy in the stream)
-    launch_pdl(b, compact_kernel, dim3(1), dim3(1024), 0, st, static_cast<const int*>(G.active),
-               static_cast<const int*>(G.state), ns, alist, acount, b->hcnt_dev + 2 * slot);
-    CUDA_CHECK(cudaEventRecord(ev[slot], st));
-  };
-  // few live systems: the rest of the cycle runs grid-persistent (grid.cuh)
-  bool use_grid = b->grid_ok && !c.stacked && c.orth == SMPM_ORTH_CGS2 && G.m + 2 <= GT_MAXCOL &&
-                        (c.method != SMPM_DBJ || c.fused) && b->tune.grid;
-  // The tail pays off while a step is latency-bound: measured crossovers are
-  // 8-10 live systems on C4 (k = 22,176) and none on C5 (k = 277,440: the
-  // per-stage kernels are faster even for one live system), so the live-count
-  // threshold scales with the work per system: grid_max <= tail_rows / k.
-  int grid_max = std::max(0, std::min(GT_MAXSYS, b->tune.grid_max));
-  if (b->tune.tail_rows > 0)
-    grid_max = static_cast<int>(std::min<long long>(grid_max, b->tune.tail_rows / std::max(1LL, b->k)));
-  if (use_grid) grid_max = std::min(grid_max, grid_blocks(b) / GT_CL);  // one cluster per live system at least
-  int cycles = 0;  // restarts issued: each cycle end may cost one speculative (empty) step
-  auto restart = [&](int ncycv) {
-    ++cycles;
-    b->jhost = 0;
-    b->pending = false;  // the cycle's last vector is never needed
-    // ---- restart (GMRES(m) extension): x += V y ; r = b - op(x) ; new cycle
-    select_state_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, GM_CYCLE, dsel);
-    check_launch(b);
-    compact_kernel<<<1, 1024, 0, st>>>(dsel, nullptr, ns, alist2, acount2, nullptr);
-    check_launch(b);
-    Live lr;
-    lr.alist = alist2;
-    lr.acount = acount2;
-    lr.nslots = ncycv;
-    lr.active = dsel;
-    gm_backsolve_kernel<<<ns, 32, 0, st>>>(G, dsel);
-    check_launch(b);
-    gm_combine_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, x, dsel, 1);
-    check_launch(b);
-    apply_op(b, c, x, r, lr, st);
-    ++op_applies;
-    axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, dsel, nullptr, 1.0, rhs, -1.0, r);
-    check_launch(b);
-    batched_dot(b, r, r, nr2, dsel, st);
-    // stacked: the new cycle starts from the norm of the stacked residual
-    // (proj/src/helmholtz.cpp:193-201), as the first cycle does
-    if (c.stacked) stack_sum(b, nr2, st);
-    gm_start_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G, nr2, nb2, c.tol, 0, G.state);
-    check_launch(b);
-    gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, r, vin);
-    check_launch(b);
-    compact_kernel<<<1, 1024, 0, st>>>(G.active, nullptr, ns, alist, acount, nullptr);
-    check_launch(b);
-  };
-  // ---- epilogue (spectral dbj): x' = V y, then one per-mode pass of x' gives both
-  // u = M^{-1} x' (the solution) and t = S M^{-1} x' (the final residual, proj/src/gmres.cpp:129-136),
-  // sharing T^{-1} x'; post_dbj_kernel forms x_S = Q u + Z c_b and ||r||^2
-  // (proj/src/deflation.cpp:118-120) in one pass
-  double* nrf = sc + 2 * ns;
-  double* u = b->vbuf[4].p;
-  double* tq = b->vbuf[5].p;
-  const bool fuse_post = spec_ok(b, c) && ((c.method == SMPM_DBJ && c.fused) || c.method == SMPM_BJ);
-  const bool post_one_pass = fuse_post && c.method == SMPM_DBJ && b->tune.post_fuse;
-  auto epilogue_dbj = [&](const Live& lv, const int* sel, cudaStream_t s2) {
-    launch_pdl(b, gm_backsolve_kernel, dim3(ns), dim3(32), 0, s2, G, sel);
-    launch_pdl(b, gm_combine_kernel, vg, dim3(256), 0, s2, G, static_cast<const double*>(b->dV.p), x, sel, 1);
-    run_xform(b, true, x, b->dvh.p, lv, s2);
-    spec_apply(b, true, b->dvh.p, b->dth.p, b->dcoarse.p + static_cast<size_t>(ns) * b->d, lv, s2, b->dvh2.p);
-    run_xform(b, false, b->dvh2.p, u, lv, s2, b->dth.p, tq);
-    ProfScope psd(b, PC_DEFL, s2);
-    DeflateParams P = deflate_params(b, sel);
-    P.alist = lv.alist;
-    P.acount = lv.acount;
-    const int gx = static_cast<int>(std::min<long long>((b->k + V2_THREADS * 4 - 1) / (V2_THREADS * 4), 64));
-    launch_pdl(b, post_dbj_kernel, dim3(gx, lv.nslots), dim3(V2_THREADS), 0, s2, P, static_cast<const double*>(tq),
-               static_cast<const double*>(u), static_cast<const double*>(rhs),
-               static_cast<const double*>(b->dcoarse.p + static_cast<size_t>(ns) * b->d),
-               static_cast<const double*>(b->dczb.p), xS, b->dpost.p, b->dcount.p, nrf, c.final_check ? 1 : 0);
-  };
-  // early epilogue: the systems that have stopped when the grid tail starts are
-  // finished before it (same total work), so that their rows of x_S can travel to
-  // the host (solve_host) on a side stream while the tail runs. Running the epilogue
-  // itself beside the tail was measured slower: its kernels compete with the
-  // latency-bound tail for the SMs. Tuning early = 0: off.
-  const bool early_ok = post_one_pass && xS_host && b->tune.early;
-  bool early_done = false;
-  int* eflag = b->dearly.p;
-  int* elist = eflag + ns;
-  int* ecount = elist + ns;
-  int* lflag = ecount + 1;
-  int* llist = lflag + ns;
-  int* lcount = llist + ns;
-  auto launch_tail = [&](int nrun) {
-    const bool early = early_ok && !early_done && nrun < ns;
-    if (early) {
-      if (!b->st2) {
-        int lo = 0, hi = 0;
-        CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        CUDA_CHECK(cudaStreamCreateWithPriority(&b->st2, cudaStreamNonBlocking, lo));
-        for (auto& e : b->eev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      }
-      early_select_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G.state, ns, eflag, lflag, b->hearly_dev);
-      check_launch(b);
-      compact_kernel<<<1, 1024, 0, st>>>(eflag, nullptr, ns, elist, ecount, nullptr);
-      check_launch(b);
-      Live le;
-      le.alist = elist;
-      le.acount = ecount;
-      le.nslots = ns - nrun;
-      le.active = eflag;
-      epilogue_dbj(le, eflag, st);
-      CUDA_CHECK(cudaEventRecord(b->eev[1], st));
-      // every row (the late systems' rows are copied again at the end)
-      CUDA_CHECK(cudaStreamWaitEvent(b->st2, b->eev[1], 0));
-      CUDA_CHECK(cudaMemcpyAsync(xS_host, xS, sizeof(double) * nk, cudaMemcpyDeviceToHost, b->st2));
-      CUDA_CHECK(cudaEventRecord(b->eev[2], b->st2));
-      early_done = true;
-    }
-    flush_pending(b, nrun, st);  // the tail starts from a materialised v_j
-    return arnoldi_grid(b, c, alist, acount, st);
-  };
-  int cur = 0;
-  issue(cur);
-  for (;;) {
-    // invariant here: exactly one step is in flight, in slot `cur`
-    if (use_grid && bound <= grid_max) {
-      CUDA_CHECK(cudaEventSynchronize(ev[cur]));
-      int nrun = hcnt[2 * cur], ncyc = hcnt[2 * cur + 1];
-      if (nrun > 0) {
-        if (!launch_tail(nrun)) {
-          // no cooperative launch: the per-step kernels finish the solve
-          use_grid = false;
-          issue(cur);
-          continue;
-        }
-        ++steps;
-        compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->hcnt_dev + 2 * cur);
-        check_launch(b);
-        CUDA_CHECK(cudaStreamSynchronize(st));
-        nrun = hcnt[2 * cur];
-        ncyc = hcnt[2 * cur + 1];
-        if (nrun > 0) fail(SMPM_ERUNTIME, "grid tail launch returned with running systems");
-      }
-      if (ncyc > 0) {
-        restart(ncyc);
-        bound = ncyc;
-        issue(cur);
-        continue;
-      }
-      break;
-    }
-    // the device caps every system at max_iter (GM_MAXED); the host bound is a
-    // safety limit only: max_iter steps, one speculative step per cycle end
-    const int step_limit = mtot + cycles + 2;
-    const bool more = steps < step_limit;
-    if (more) issue(cur ^ 1);
-    CUDA_CHECK(cudaEventSynchronize(ev[cur]));
-    const int nrun = hcnt[2 * cur], ncyc = hcnt[2 * cur + 1];
-    bound = std::min(bound, nrun);
-    cur ^= 1;
-    if (nrun > 0 && more) continue;
-    if (more) CUDA_CHECK(cudaEventSynchronize(ev[cur]));  // drain the speculative step
-    const int nrun2 = more ? hcnt[2 * cur] : nrun;
-    const int ncyc2 = more ? hcnt[2 * cur + 1] : ncyc;
-    if (nrun2 > 0 && steps < step_limit) {
-      bound = std::min(bound, nrun2);
-      issue(cur);
-      continue;
-    }
-    if (ncyc2 > 0) {
-      restart(ncyc2);
-      bound = ncyc2;
-      issue(cur);
-      continue;
-    }
-    break;
-  }
-  if (post_one_pass) {
-    if (early_done) {
-      // the systems not finished by the early epilogue
-      compact_kernel<<<1, 1024, 0, st>>>(lflag, nullptr, ns, llist, lcount, nullptr);
-      check_launch(b);
-      Live ll;
-      ll.alist = llist;
-      ll.acount = lcount;
-      ll.nslots = ns;
-      ll.active = lflag;
-      epilogue_dbj(ll, lflag, st);
-    } else {
-      epilogue_dbj(all, nullptr, st);
-    }
-  } else {
-    // ---- assemble x' = V y for the last cycle of every system
-    launch_pdl(b, gm_backsolve_kernel, dim3(ns), dim3(32), 0, st, G, static_cast<const int*>(nullptr));
-    launch_pdl(b, gm_combine_kernel, vg, dim3(256), 0, st, G, static_cast<const double*>(b->dV.p), x,
-               static_cast<const int*>(nullptr), 1);
-    // ---- final residual check (proj/src/gmres.cpp:129-136): r = rhs - op(x')
-    // Spectral dbj/bj: one per-mode pass of x' gives both u = M^{-1} x' (the
-    // solution) and t = S M^{-1} x' (the residual operator), sharing T^{-1} x'.
-    if (fuse_post) {
-      run_xform(b, true, x, b->dvh.p, all, st);
-      // dbj: the per-mode pass also yields c = C^{-1} Z^T (S u) for the residual and Q
-      spec_apply(b, true, b->dvh.p, b->dth.p, c.method == SMPM_DBJ ? b->dcoarse.p + static_cast<size_t>(ns) * b->d : nullptr,
-                 all, st, b->dvh2.p);
-      run_xform(b, false, b->dvh2.p, u, all, st, b->dth.p, tq);
-    }
-  }
-  if (c.final_check && !post_one_pass) {
-    if (fuse_post && c.method == SMPM_DBJ) {
-      run_deflate(b, DEFL_P_FUSED, tq, tq, r, nullptr, all, st);
-    } else if (fuse_post) {
-      CUDA_CHECK(cudaMemcpyAsync(r, tq, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
-    } else {
-      apply_op(b, c, x, r, all, st);
-    }
-    axpby_kernel<<<grid_for(nk), 256, 0, st>>>(ns, b->k, nullptr, nullptr, 1.0, rhs, -1.0, r);
-    check_launch(b);
-    batched_dot(b, r, r, nrf, nullptr, st);
-  }
-  // ---- solution (proj/src/deflation.cpp:118-120, :141; proj/src/gmres.cpp:148)
-  switch (c.method) {
-    case SMPM_SCHUR:
-      CUDA_CHECK(cudaMemcpyAsync(xS, x, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
-      break;
-    case SMPM_BJ:
-      if (fuse_post)
-        CUDA_CHECK(cudaMemcpyAsync(xS, u, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
-      else if (spec_on(b))
-        spec_Minv(b, x, xS, nullptr, all, st);
-      else
-        op_BJ(b, x, xS, all, st);
-      break;
-    case SMPM_DBJ: {
-      double* q = b->vbuf[6].p;
-      if (post_one_pass) break;
-      if (fuse_post) {
-        run_deflate(b, DEFL_Q_TAIL, tq, u, q, nullptr, all, st);  // Q u = u - Z c(Z^T S u)
-      } else if (spec_on(b)) {
-        // u = M^{-1} x and S u from one per-mode pass, then Q u = u - Z c(Z^T S u)
-        double* su = b->vbuf[8].p;
-        spec_Minv(b, x, u, su, all, st);
-        run_deflate(b, DEFL_Q_TAIL, su, u, q, nullptr, all, st);
-      } else {
-        op_BJ(b, x, u, all, st);
-        op_Q(b, u, q, all, st);
-      }
-      run_deflate(b, DEFL_ADD_ZC, bS, q, xS, nullptr, all, st);
-      break;
-    }
-    case SMPM_2LAS:
-      if (spec_on(b))
-        spec_Minv(b, x, u, nullptr, all, st);
-      else
-        op_BJ(b, x, u, all, st);
-      run_deflate(b, DEFL_ADD_ZC, x, u, xS, nullptr, all, st);
-      break;
-  }
-  if (xS_host) {
-    if (early_done) {
-      // the full copy of the early epilogue first, then the late systems' rows
-      CUDA_CHECK(cudaStreamWaitEvent(st, b->eev[2], 0));
-      for (int q = 0; q < ns;) {
-        if (b->hearly[q]) {
-          ++q;
-          continue;
-        }
-        int q1 = q + 1;
-        while (q1 < ns && !b->hearly[q1]) ++q1;  // one copy per run of late rows
-        CUDA_CHECK(cudaMemcpyAsync(xS_host + static_cast<size_t>(q) * b->k, xS + static_cast<size_t>(q) * b->k,
-                                   sizeof(double) * b->k * (q1 - q), cudaMemcpyDeviceToHost, st));
-        q = q1;
-      }
-    } else {
-      CUDA_CHECK(cudaMemcpyAsync(xS_host, xS, sizeof(double) * nk, cudaMemcpyDeviceToHost, st));
-    }
-  }
-  // stacked across ranks: the true residual of the whole stack (every entry becomes the global sum)
-  if (c.stacked && b->ar_fn && c.final_check) stack_sum(b, nrf, st);
-  // report data: queued on the stream into pinned staging (one host wait)
-  const size_t rep_ints = static_cast<size_t>(ns) * 8, rep_dbl = static_cast<size_t>(ns) * (8 + (m + 1) + 3);
-  const size_t rep_hist = history ? static_cast<size_t>(ns) * G.histcap : 0;
-  const size_t rep_bytes = rep_ints * sizeof(int) + (rep_dbl + rep_hist) * sizeof(double);
-  if (b->hrep_bytes < rep_bytes) {
-    if (b->hrep) cudaFreeHost(b->hrep);
-    b->hrep = nullptr;
-    CUDA_CHECK(cudaMallocHost(&b->hrep, rep_bytes));
-    b->hrep_bytes = rep_bytes;
-  }
-  double* hsc_p = reinterpret_cast<double*>(b->hrep);
-  double* hg_p = hsc_p + static_cast<size_t>(ns) * 8;
-  double* hsm_p = hg_p + static_cast<size_t>(ns) * (m + 1);
-  double* hh_p = hsm_p + static_cast<size_t>(ns) * 3;
-  int* hint_p = reinterpret_cast<int*>(hh_p + rep_hist);
-  if (reps || history) {
-    CUDA_CHECK(cudaMemcpyAsync(hint_p, b->dgint.p, sizeof(int) * ns * 8, cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaMemcpyAsync(hsc_p, b->dscal.p, sizeof(double) * ns * 8, cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaMemcpyAsync(hg_p, b->dg.p, sizeof(double) * ns * (m + 1), cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaMemcpyAsync(hsm_p, sc, sizeof(double) * ns * 3, cudaMemcpyDeviceToHost, st));
-    if (history)
-      CUDA_CHECK(cudaMemcpyAsync(hh_p, b->dhist.p, sizeof(double) * rep_hist, cudaMemcpyDeviceToHost, st));
-  }
-  CUDA_CHECK(cudaEventRecord(e1, st));
-  CUDA_CHECK(cudaEventSynchronize(e1));
-  prof_collect(b);
-  float ms = 0.f;
-  CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
-  G.alist = nullptr;
-  G.acount = nullptr;
-  (void)launches0;
-
-  // ---- reports
-  if (reps || history) {
-    const int* hint = hint_p;
-    const double *hsc = hsc_p, *hg = hg_p, *hsm = hsm_p, *hh = hh_p;
-    for (int s = 0; s < ns; ++s) {
-      const int iters = hint[static_cast<size_t>(ns) + s];
-      const int jc = hint[static_cast<size_t>(s)];
-      const int hl = hint[static_cast<size_t>(5 * ns) + s];
-      const double bn = hsc[static_cast<size_t>(s)];
-      const double tgt = hsc[static_cast<size_t>(ns) + s];
-      double frel = bn > 0 ? std::fabs(hg[static_cast<size_t>(s) * (m + 1) + jc]) / bn : 0.0;
-      bool mismatch = false;
-      if (c.final_check && bn > 0) {
-        // stacked: the true residual of the stacked vector (proj/src/gmres.cpp:129-136)
-        double r2 = hsm[static_cast<size_t>(2 * ns) + s];
-        if (c.stacked && !b->ar_fn) {
-          r2 = 0.0;
-          for (int t = 0; t < ns; ++t) r2 += hsm[static_cast<size_t>(2 * ns) + t];
-        }
-        const double true_rel = std::sqrt(r2) / bn;
-        if (true_rel * bn > 10.0 * std::max(tgt, frel * bn)) mismatch = true;
-        frel = true_rel;
-      }
-      const long long apps = iters + (c.final_check ? 1 : 0) + op_applies;
-      if (reps) {
-        smpm_report& R = reps[s];
-        R.iterations = iters;
-        R.history_len = hl;
-        R.final_rel_residual = frel;
-        R.converged = bn > 0 ? (frel * bn <= tgt * (1.0 + 1e-12)) : 1;
-        R.mismatch_warning = mismatch ? 1 : 0;
-        R.operator_applies = apps;
-        R.krylov_s_applies = apps * per_sys_applies;
-        R.wall_time_s = ms * 1e-3;
-      }
-      if (history)
-        for (int i = 0; i < G.histcap; ++i)
-          history[static_cast<size_t>(s) * G.histcap + i] = i < hl ? hh[static_cast<size_t>(s) * G.histcap + i] : 0.0;
-    }
-  }
-  (void)s_applies;
-}
-
-void launch_zt(smpm_batch* b, const double* v, double* y, cudaStream_t st) {
-  zt_kernel<<<(b->nsys * b->d * 32 + 255) / 256, 256, 0, st>>>(b->nsys, b->d, 2 * b->w, b->k, v, y);
-  check_launch(b);
-}
-void launch_z(smpm_batch* b, const double* c, double* y, cudaStream_t st) {
-  zbroadcast_kernel<<<grid_for(b->nsys * b->k), 256, 0, st>>>(b->nsys, b->d, 2 * b->w, b->k, nullptr, c, y);
-  check_launch(b);
-}
-
-SolveCfg cfg_from(int method, const smpm_solve_options* o) {
-  SolveCfg c;
-  c.method = method;
-  c.tol = o ? o->tol : 1e-10;
-  c.max_iter = o ? o->max_iter : 100;
-  c.restart = o ? o->restart : 0;
-  c.orth = o ? o->orth : SMPM_ORTH_CGS2;
-  c.fused = o ? o->fuse_deflation != 0 : true;
-  c.final_check = o ? o->final_residual_check != 0 : true;
-  if (c.method < 0 || c.method > 3) fail(SMPM_EINVAL, "unknown method");
-  return c;
-}
+#include "batch_ops.inl"
+#include "batch_setup.inl"
+#include "batch_gmres.inl"
+#include "batch_spectral.inl"
+#include "batch_solve.inl"
 
 }  // namespace
 
-// ============================================================================
-// C ABI
-// ============================================================================
-// ---- strip solver ------------------------------------------
-StripParams strip_params(const smpm_batch* b) {
-  StripParams P;
-  P.n = b->n;
-  P.mx = b->mx;
-  P.mz = b->mz;
-  P.w = b->w;
-  P.nmode = b->sp_nmode;
-  P.npairs = b->sp_npairs;
-  P.nsys = b->nsys;
-  P.r = static_cast<long long>(b->mx) * b->mz * b->n * b->n;
-  P.k = b->k;
-  P.fac = reinterpret_cast<const double2*>(b->dsfac.p);
-  P.lz = reinterpret_cast<const double2*>(b->dslz.p);
-  P.mu = b->dsmu.p;
-  P.tau = b->strip_tau;
-  return P;
-}
-
-// out = A in for every w-long column of nsys x ncol_sys columns (system stride
-// sys_stride): the resident-slice transform kernel, or a plain cuBLAS GEMM
-void xf_columns(smpm_batch* b, bool inverse, const double* in, double* out, int ncol_sys, long long sys_stride,
-                cudaStream_t st, int nsys_) {
-  const int nsys = nsys_ < 0 ? b->nsys : nsys_;
-  if (b->xf_P > 0) {
-    XformArgs a;
-    a.Af = inverse ? b->dTifrag.p : b->dTfrag.p;
-    a.w = b->w;
-    a.ncol_sys = ncol_sys;
-    a.k = sys_stride;
-    a.alist = nullptr;
-    a.acount = nullptr;
-    a.nslots = nsys;
-    a.nv = 1;
-    a.in[0] = in;
-    a.out[0] = out;
-    a.in[1] = nullptr;
-    a.out[1] = nullptr;
-    a.P = b->xf_P;
-    const long long nch = (static_cast<long long>(nsys) * ncol_sys + 15) / 16;
-    const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / a.P, nch)));
-    if (b->xp_on)
-      launch_xformp(b, a, inverse, st, false);
-    else
-      launch_xform(b, a, groups, st, false);
-    return;
-  }
-  if (sys_stride != static_cast<long long>(ncol_sys) * b->w) fail(SMPM_EINVAL, "strip columns must be contiguous");
-  smpm_ctx* ctx = b->ctx;
-  if (!ctx->blas && cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS) fail(SMPM_ECUDA, "cublasCreate failed");
-  if (cublasSetStream(ctx->blas, st) != CUBLAS_STATUS_SUCCESS) fail(SMPM_ECUDA, "cublasSetStream failed");
-  const double one = 1.0, zero = 0.0;
-  const int w = b->w;
-  const long long ncols = static_cast<long long>(nsys) * ncol_sys;
-  if (ncols > INT_MAX) fail(SMPM_EINVAL, "too many strip columns");
-  if (cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, w, static_cast<int>(ncols), w, &one,
-                  inverse ? b->dTi.p : b->dT.p, w, in, w, &zero, out, w) != CUBLAS_STATUS_SUCCESS)
-    fail(SMPM_ECUDA, "cublasDgemm failed");
-}
-
-template <bool TRACES>
-void strip_modes(smpm_batch* b, const double* Xh, double* out, cudaStream_t st) {
-  const StripParams P = strip_params(b);
-  const dim3 grid((P.nmode + 127) / 128, P.mx, P.nsys);
-  switch (P.n) {
-#define SMPM_STRIP_CASE(N) \
-  case N: strip_modes_kernel<N, TRACES><<<grid, 128, 0, st>>>(P, Xh, out); break;
-    SMPM_STRIP_CASE(4) SMPM_STRIP_CASE(5) SMPM_STRIP_CASE(6) SMPM_STRIP_CASE(7) SMPM_STRIP_CASE(8)
-    SMPM_STRIP_CASE(9) SMPM_STRIP_CASE(10) SMPM_STRIP_CASE(11) SMPM_STRIP_CASE(12) SMPM_STRIP_CASE(13)
-    SMPM_STRIP_CASE(14) SMPM_STRIP_CASE(15) SMPM_STRIP_CASE(16) SMPM_STRIP_CASE(17)
-#undef SMPM_STRIP_CASE
-    default: fail(SMPM_EINVAL, "strip solver: n must be in [4, 17]");
-  }
-  check_launch(b);
-}
-
-void strip_scratch(smpm_batch* b) {
-  const size_t r = static_cast<size_t>(b->mx) * b->mz * b->n * b->n;
-  if (b->dsx1.n < b->nsys * r) {
-    b->dsx1.alloc(b->nsys * r);
-    b->dsx2.alloc(b->nsys * r);
-  }
-  if (b->dsbh.n < static_cast<size_t>(b->nsys) * b->k) b->dsbh.alloc(static_cast<size_t>(b->nsys) * b->k);
-}
-
-void need_strip(smpm_batch* b) {
-  need_final(b);
-  if (!b->strip_ok) fail(SMPM_EINVAL, "strip factors not set (smpm_batch_set_strip_factors)");
-  strip_scratch(b);
-}
-
-// ---- transverse Fourier transforms (fourier.cuh) ----------------------------
-// twiddle tables exp(sign 2 pi i k / m), k < m / 2, per (device, m, sign), kept for the process
-int g_fy_tile = 0;  // transverse FFT rows per CTA override (smpm_batch_set_tuning(NULL, "fy_tile", v))
-
-const double2* fy_twiddles(int m, int sign) {
-  static std::vector<std::pair<long long, double*>> cache;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  int dev = 0;
-  CUDA_CHECK(cudaGetDevice(&dev));
-  const long long key = (static_cast<long long>(dev) << 32) | (static_cast<long long>(m) << 1) | (sign > 0 ? 1 : 0);
-  for (auto& e : cache)
-    if (e.first == key) return reinterpret_cast<const double2*>(e.second);
-  std::vector<double> h(static_cast<size_t>(m));
-  for (int k = 0; k < m / 2; ++k) {
-    const double ang = sign * 2.0 * M_PI * k / m;
-    h[2 * k] = std::cos(ang);
-    h[2 * k + 1] = std::sin(ang);
-  }
-  double* d = nullptr;
-  CUDA_CHECK(cudaMalloc(&d, sizeof(double) * h.size()));
-  CUDA_CHECK(cudaMemcpy(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
-  cache.emplace_back(key, d);
-  return reinterpret_cast<const double2*>(d);
-}
-
-void fourier_launch(long long r, int m_y, const double* in, double* out, int sign, cudaStream_t st) {
-  if (r < 1 || m_y < 2 || m_y > 4096 || (m_y & (m_y - 1)) != 0)
-    fail(SMPM_EINVAL, "fourier_y: m_y must be a power of two in [2, 4096] and r >= 1");
-  if (!in || !out) fail(SMPM_EINVAL, "null vector");
-  FourierArgs a;
-  a.r = r;
-  a.m_y = m_y;
-  // nodes per CTA: 16 (128-byte coalesced runs per plane) while the padded complex
-  // tile stays <= 66 KB (3 CTAs per SM), fewer for long transforms
-  a.tile = std::max(1, std::min(16, 4224 / (m_y + 1)));
-  if (g_fy_tile > 0) a.tile = std::max(1, std::min(64, g_fy_tile));
-  a.tw = fy_twiddles(m_y, sign);
-  const size_t smem = sizeof(double2) * static_cast<size_t>(a.tile) * (m_y + 1);
-  const unsigned grid = static_cast<unsigned>((r + a.tile - 1) / a.tile);
-  auto go = [&](auto kfwd, auto kinv) {
-    auto k = sign < 0 ? kfwd : kinv;
-    CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    k<<<grid, FY_THREADS, smem, st>>>(a, in, out);
-  };
-  switch (m_y) {  // register FFT for 64 <= m_y <= 512 (R = m_y / 32 per lane)
-    case 64: go(fourier_y_kernel<2>, inverse_fourier_y_kernel<2>); break;
-    case 128: go(fourier_y_kernel<4>, inverse_fourier_y_kernel<4>); break;
-    case 256: go(fourier_y_kernel<8>, inverse_fourier_y_kernel<8>); break;
-    case 512: go(fourier_y_kernel<16>, inverse_fourier_y_kernel<16>); break;
-    default: go(fourier_y_kernel<0>, inverse_fourier_y_kernel<0>); break;
-  }
-  CUDA_CHECK(cudaGetLastError());
-}
-
-extern "C" {
-
-const char* smpm_last_error(void) { return g_last_error.c_str(); }
-
-const char* smpm_version(void) { return "smpm_b200 0.1 (sm_100a, fp64)"; }
-
-int smpm_ctx_create(int device, smpm_ctx** out) {
-  return guard([&] {
-    if (!out) fail(SMPM_EINVAL, "null out");
-    int ndev = 0;
-    CUDA_CHECK(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) fail(SMPM_ECUDA, "no such CUDA device");
-    CUDA_CHECK(cudaSetDevice(device));
-    cudaDeviceProp prop;
-    CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
-    if (prop.major < 10) fail(SMPM_ECUDA, "smpm_b200 kernels are built for sm_100a; device is sm_" +
-                                              std::to_string(prop.major) + std::to_string(prop.minor));
-    auto ctx = std::make_unique<smpm_ctx>();
-    ctx->device = device;
-    ctx->num_sms = prop.multiProcessorCount;
-    // blocking stream: orders with the legacy default stream torch uses for handle 0
-    CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault));
-    CUSOLVER_CHECK(cusolverDnCreate(&ctx->solver));
-    CUSOLVER_CHECK(cusolverDnSetStream(ctx->solver, ctx->stream));
-    CUDA_CHECK(cudaFuncSetAttribute(gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM));
-    *out = ctx.release();
-  });
-}
-
-int smpm_ctx_destroy(smpm_ctx* ctx) {
-  return guard([&] {
-    if (!ctx) return;
-    if (ctx->solver) cusolverDnDestroy(ctx->solver);
-    if (ctx->blas) cublasDestroy(ctx->blas);
-    if (ctx->stream) cudaStreamDestroy(ctx->stream);
-    delete ctx;
-  });
-}
-
-void* smpm_ctx_stream(smpm_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
-
-int smpm_batch_create(smpm_ctx* ctx, int n, int m_x, int m_z, int nsys, smpm_batch** out) {
-  return guard([&] {
-    if (!ctx || !out) fail(SMPM_EINVAL, "null argument");
-    if (n < 2 || m_x < 2 || m_z < 1 || nsys < 1) fail(SMPM_EINVAL, "smpm_batch_create: need n>=2, m_x>=2, m_z>=1, nsys>=1");
-    CUDA_CHECK(cudaSetDevice(ctx->device));
-    auto b = std::make_unique<smpm_batch>();
-    b->ctx = ctx;
-    b->n = n;
-    b->mx = m_x;
-    b->mz = m_z;
-    b->nsys = nsys;
-    b->w = n * m_z;
-    b->d = m_x - 1;
-    b->k = 2LL * b->w * b->d;
-    b->nbf = b->d / 2;
-    b->single = (b->d % 2) == 1;
-    b->have.assign(static_cast<size_t>(nsys), 0);
-    b->huS.assign(static_cast<size_t>(nsys), {});
-    *out = b.release();
-  });
-}
-
-int smpm_batch_destroy(smpm_batch* b) {
-  return guard([&] { delete b; });
-}
-
-int smpm_batch_dims(const smpm_batch* b, long long* k, int* d, int* w) {
-  return guard([&] {
-    if (!b) fail(SMPM_EINVAL, "null batch");
-    if (k) *k = b->k;
-    if (d) *d = b->d;
-    if (w) *w = b->w;
-  });
-}
-
-int smpm_batch_set_couplings(smpm_batch* b, int sys, const double* G_W, const double* G_I, const double* G_E) {
-  return guard([&] {
-    if (!b || sys < 0 || sys >= b->nsys) fail(SMPM_EINVAL, "bad system index");
-    if (b->finalized) fail(SMPM_EINVAL, "batch already finalized");
-    if (!G_W || !G_E || (b->mx >= 3 && !G_I)) fail(SMPM_EINVAL, "null coupling matrix");
-    const long long ww = 1LL * b->w * b->w;
-    if (b->hG.empty()) b->hG.assign(static_cast<size_t>(b->nsys) * 6 * ww, 0.0);  // host staging, on first use
-    double* dst = b->hG.data() + sys * 6 * ww;
-    std::memcpy(dst, G_W, sizeof(double) * ww);
-    if (G_I) std::memcpy(dst + ww, G_I, sizeof(double) * 4 * ww);
-    std::memcpy(dst + 5 * ww, G_E, sizeof(double) * ww);
-    b->have[sys] = 1;
-  });
-}
-
-int smpm_batch_set_spectral(smpm_batch* b, int npairs, const double* T, const double* T_inv, const double* gamma) {
-  return guard([&] {
-    if (!b) fail(SMPM_EINVAL, "null batch");
-    if (b->finalized) fail(SMPM_EINVAL, "batch already finalized");
-    if (!T || !T_inv || !gamma) fail(SMPM_EINVAL, "null spectral factor");
-    if (npairs < 0 || 2 * npairs > b->w) fail(SMPM_EINVAL, "bad number of complex pairs");
-    const size_t ww = static_cast<size_t>(b->w) * b->w;
-    b->sp_npairs = npairs;
-    b->sp_nmode = b->w - npairs;
-    b->hT.assign(T, T + ww);
-    b->hTi.assign(T_inv, T_inv + ww);
-    const size_t ng = static_cast<size_t>(b->nsys) * SK_NUM * b->sp_nmode * 2;
-    b->hgam.assign(gamma, gamma + ng);
-    b->spectral = true;
-  });
-}
-
-int smpm_batch_load_schur_blocks(smpm_batch* b, int sys, const char* path) {
-  return guard([&] {
-    if (!b || !path) fail(SMPM_EINVAL, "null argument");
-    std::FILE* fp = std::fopen(path, "rb");
-    if (!fp) fail(SMPM_EINVAL, std::string("load_schur_blocks: cannot open ") + path);
-    std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard_fp(fp, std::fclose);
-    auto get = [&]() {
-      std::int64_t v = 0;
-      if (std::fread(&v, sizeof v, 1, fp) != 1) fail(SMPM_EINVAL, "load_schur_blocks: truncated file");
-      return static_cast<long long>(v);
-    };
-    const long long n = get(), mx = get(), mz = get(), k = get();
-    if (n != b->n || mx != b->mx || mz != b->mz || k != b->k)
-      fail(SMPM_EINVAL, "load_schur_blocks: file geometry differs from the batch");
-    const int d = b->d;
-    std::vector<std::vector<double>> ent(d);
-    std::vector<std::vector<long long>> st(d), ln(d);
-    std::vector<long long> rows(d);
-    std::vector<int> nseg(d);
-    for (int i = 0; i < d; ++i) {
-      rows[i] = get();
-      const long long cols = get(), ns = get();
-      if (cols != 2LL * b->w || rows[i] <= 0 || rows[i] > 4LL * b->w || ns < 1 || ns > 4)
-        fail(SMPM_EINVAL, "load_schur_blocks: unexpected block shape");
-      nseg[i] = static_cast<int>(ns);
-      for (long long q = 0; q < ns; ++q) {
-        st[i].push_back(get());
-        ln[i].push_back(get());
-      }
-      ent[i].resize(static_cast<size_t>(rows[i] * cols));
-      if (std::fread(ent[i].data(), sizeof(double), ent[i].size(), fp) != ent[i].size())
-        fail(SMPM_EINVAL, "load_schur_blocks: truncated file");
-    }
-    std::vector<const double*> ep(d);
-    std::vector<const long long*> sp(d), lp(d);
-    for (int i = 0; i < d; ++i) {
-      ep[i] = ent[i].data();
-      sp[i] = st[i].data();
-      lp[i] = ln[i].data();
-    }
-    const int rc = smpm_batch_set_interface_blocks(b, sys, ep.data(), rows.data(), sp.data(), lp.data(), nseg.data());
-    if (rc != SMPM_OK) fail(rc, smpm_last_error());
-  });
-}
-
-int smpm_batch_set_interface_blocks(smpm_batch* b, int sys, const double* const* entries, const long long* rows,
-                                    const long long* const* seg_start, const long long* const* seg_len,
-                                    const int* nseg) {
-  return guard([&] {
-    if (!b || sys < 0 || sys >= b->nsys) fail(SMPM_EINVAL, "bad system index");
-    const int w = b->w, d = b->d;
-    const long long w2 = 2LL * w, ww = 1LL * w * w;
-    std::vector<double> GW(ww), GI(4 * ww, 0.0), GE(ww);
-    std::vector<char> seenI(4, 0);
-    // copy-and-verify helper: dst (ld) <- entries rows [r0,r0+w) x cols [c0,c0+w)
-    auto take = [&](const double* e, long long nrows, long long r0, long long c0, double* dst, long long ld,
-                    bool verify) {
-      for (long long c = 0; c < w; ++c)
-        for (long long r = 0; r < w; ++r) {
-          const double v = e[(c0 + c) * nrows + r0 + r];
-          double& t = dst[c * ld + r];
-          if (verify && t != v) fail(SMPM_EINVAL, "interface blocks are not copies of strip-kind couplings");
-          t = v;
-        }
-    };
-    for (int i = 0; i < d; ++i) {
-      const bool has_a = i >= 1, has_d = i <= d - 2;
-      const int want = 2 + (has_a ? 1 : 0) + (has_d ? 1 : 0);
-      if (nseg[i] != want || rows[i] != static_cast<long long>(want) * w)
-        fail(SMPM_EINVAL, "interface block " + std::to_string(i) + " has an unexpected segment layout");
-      long long off = 0;
-      const double* e = entries[i];
-      const long long nr = rows[i];
-      int q = 0;
-      if (has_a) {  // rows: W-readers of strip i, cols: E-own of strip i (interior)
-        if (seg_start[i][q] != (i - 1) * w2) fail(SMPM_EINVAL, "segment start mismatch");
-        take(e, nr, off, 0, GI.data() + w * w2, w2, seenI[1]);
-        seenI[1] = 1;
-        off += w;
-        ++q;
-      }
-      // seg b: W-readers of strip i+1 x W-own of strip i+1 (cols w..2w)
-      if (i + 1 == d) {
-        take(e, nr, off, w, GE.data(), w, false);
-      } else {
-        take(e, nr, off, w, GI.data(), w2, seenI[0]);
-        seenI[0] = 1;
-      }
-      off += w;
-      // seg c: E-readers of strip i x E-own of strip i (cols 0..w)
-      if (i == 0) {
-        take(e, nr, off, 0, GW.data(), w, false);
-      } else {
-        take(e, nr, off, 0, GI.data() + w * w2 + w, w2, seenI[3]);
-        seenI[3] = 1;
-      }
-      off += w;
-      if (has_d) {  // E-readers of strip i+1 x W-own of strip i+1
-        take(e, nr, off, w, GI.data() + w, w2, seenI[2]);
-        seenI[2] = 1;
-      }
-      (void)seg_len;
-    }
-    const long long ww2 = ww;
-    if (b->hG.empty()) b->hG.assign(static_cast<size_t>(b->nsys) * 6 * ww, 0.0);
-    double* dst = b->hG.data() + sys * 6 * ww2;
-    std::memcpy(dst, GW.data(), sizeof(double) * ww);
-    std::memcpy(dst + ww, GI.data(), sizeof(double) * 4 * ww);
-    std::memcpy(dst + 5 * ww, GE.data(), sizeof(double) * ww);
-    b->have[sys] = 1;
-  });
-}
-
-int smpm_batch_set_nullspace(smpm_batch* b, int sys, const double* u_S) {
-  return guard([&] {
-    if (!b || sys < 0 || sys >= b->nsys) fail(SMPM_EINVAL, "bad system index");
-    if (b->finalized) fail(SMPM_EINVAL, "batch already finalized");
-    if (!u_S) {
-      b->huS[sys].clear();
-      return;
-    }
-    b->huS[sys].assign(u_S, u_S + b->k);
-  });
-}
-
-int smpm_batch_finalize(smpm_batch* b) {
-  return guard([&] {
-    if (!b) fail(SMPM_EINVAL, "null batch");
-    CUDA_CHECK(cudaSetDevice(b->ctx->device));
-    finalize(b);
-  });
-}
-
-int smpm_batch_coarse_info(smpm_batch* b, double* C, int* tridiagonal, int* singular) {
-  return guard([&] {
-    need_final(b);
-    if (C) std::copy(b->hC.begin(), b->hC.end(), C);
-    if (tridiagonal) std::copy(b->htri.begin(), b->htri.end(), tridiagonal);
-    if (singular) std::copy(b->hsing.begin(), b->hsing.end(), singular);
-  });
-}
-
-#define OP_ENTRY(name, body)                                                         \
-  int name(smpm_batch* b, const double* v, double* y, void* stream) {                \
-    return guard([&] {                                                               \
-      need_final(b);                                                                 \
-      if (!v || !y) fail(SMPM_EINVAL, "null vector");                                \
-      cudaStream_t st = b->st(stream);                                               \
-      body;                                                                          \
-    });                                                                              \
-  }
-OP_ENTRY(smpm_apply_S, op_S(b, v, y, all_systems(b), st))
-OP_ENTRY(smpm_apply_St, op_St(b, v, y, all_systems(b), st))
-OP_ENTRY(smpm_apply_block_jacobi_inv, op_BJ(b, v, y, all_systems(b), st))
-OP_ENTRY(smpm_apply_Q, op_Q(b, v, y, all_systems(b), st))
-OP_ENTRY(smpm_apply_Zt, launch_zt(b, v, y, st))
-OP_ENTRY(smpm_apply_Z, launch_z(b, v, y, st))
-OP_ENTRY(smpm_coarse_solve, run_deflate(b, DEFL_COARSE_DIRECT, v, nullptr, nullptr, y, all_systems(b), st))
-#undef OP_ENTRY
-
-int smpm_apply_P(smpm_batch* b, const double* v, double* y, int fused, void* stream) {
-  return guard([&] {
-    need_final(b);
-    op_P(b, v, y, fused != 0, all_systems(b), b->st(stream));
-  });
-}
-
-void store_strip_factors(smpm_batch* b, const smpm_strip_factors* f);
-
-int smpm_batch_set_strip_factors(smpm_batch* b, const smpm_strip_factors* f) {
-  return guard([&] {
-    if (!b || !f) fail(SMPM_EINVAL, "null argument");
-    if (!b->spectral || b->hT.empty()) fail(SMPM_EINVAL, "strip factors need the spectral basis (smpm_batch_set_spectral)");
-    store_strip_factors(b, f);
-  });
-}
-
-int smpm_batch_set_fdm(smpm_batch* b, int npairs, const double* T, const double* T_inv, const smpm_strip_factors* f) {
-  return guard([&] {
-    if (!b || !f) fail(SMPM_EINVAL, "null argument");
-    if (b->finalized) fail(SMPM_EINVAL, "batch already finalized");
-    if (!T || !T_inv) fail(SMPM_EINVAL, "null spectral basis");
-    if (npairs < 0 || 2 * npairs > b->w) fail(SMPM_EINVAL, "bad number of complex pairs");
-    if (b->w % 16 != 0) fail(SMPM_EINVAL, "smpm_batch_set_fdm needs w % 16 == 0 (use smpm_batch_set_couplings)");
-    const int n = b->n, w = b->w;
-    const size_t ww = static_cast<size_t>(w) * w;
-    b->sp_npairs = npairs;
-    b->sp_nmode = w - npairs;
-    b->hT.assign(T, T + ww);
-    b->hTi.assign(T_inv, T_inv + ww);
-    b->spectral = true;
-    if (b->mx >= 3) store_strip_factors(b, f);
-    for (int kd = 0; kd < 3; ++kd)
-      if (!f->Vx[kd] || !f->Vx_inv[kd] || !f->lx[kd]) fail(SMPM_EINVAL, "null x factor");
-    if (!f->lz || !f->tW || !f->tE || !f->mu) fail(SMPM_EINVAL, "null strip factor");
-    // a_kind[p] = (t_X . Vx[:, p]) Vx^{-1}[p, y_Y] for the six couplings (readers X, owner Y):
-    // W_EE (west-boundary strip), I_WW, I_WE, I_EW, I_EE (interior strip), E_WW (east-boundary strip)
-    const int strip_of[SK_NUM] = {0, 1, 1, 1, 1, 2};
-    const int X_of[SK_NUM] = {1, 0, 0, 1, 1, 0}, Y_of[SK_NUM] = {1, 0, 1, 0, 1, 0};  // 0 = W, 1 = E
-    b->fdm_a.assign(static_cast<size_t>(SK_NUM) * n * 2, 0.0);
-    b->fdm_lx.assign(static_cast<size_t>(SK_NUM) * n * 2, 0.0);
-    for (int kd = 0; kd < SK_NUM; ++kd) {
-      const int sk = strip_of[kd];
-      const double* tX = X_of[kd] ? f->tE : f->tW;
-      const int y = Y_of[kd] ? n - 1 : 0;
-      for (int p = 0; p < n; ++p) {
-        double tr = 0.0, ti = 0.0;
-        for (int ix = 0; ix < n; ++ix) {
-          tr += tX[ix] * f->Vx[sk][2 * (ix + p * n)];
-          ti += tX[ix] * f->Vx[sk][2 * (ix + p * n) + 1];
-        }
-        const double yr = f->Vx_inv[sk][2 * (p + y * n)], yi = f->Vx_inv[sk][2 * (p + y * n) + 1];
-        b->fdm_a[2 * (kd * n + p)] = tr * yr - ti * yi;
-        b->fdm_a[2 * (kd * n + p) + 1] = tr * yi + ti * yr;
-        b->fdm_lx[2 * (kd * n + p)] = f->lx[sk][2 * p];
-        b->fdm_lx[2 * (kd * n + p) + 1] = f->lx[sk][2 * p + 1];
-      }
-    }
-    b->fdm_lz.assign(f->lz, f->lz + 2 * static_cast<size_t>(b->sp_nmode));
-    b->fdm_mu.assign(f->mu, f->mu + b->nsys);
-    b->fdm_tau = f->tau;
-    b->from_fdm = true;
-    std::fill(b->have.begin(), b->have.end(), 1);
-  });
-}
-
-void store_strip_factors(smpm_batch* b, const smpm_strip_factors* f) {
-  {
-    if (b->mx < 3) fail(SMPM_EINVAL, "strip solver needs m_x >= 3");
-    const int n = b->n;
-    for (int kd = 0; kd < 3; ++kd)
-      if (!f->Vx[kd] || !f->Vx_inv[kd] || !f->lx[kd]) fail(SMPM_EINVAL, "null x factor");
-    if (!f->lz || !f->tW || !f->tE || !f->mu) fail(SMPM_EINVAL, "null strip factor");
-    const int L = strip_fac_len(n);
-    std::vector<double> fac(static_cast<size_t>(3) * L * 2);
-    for (int kd = 0; kd < 3; ++kd) {
-      double* o = fac.data() + static_cast<size_t>(kd) * L * 2;
-      std::copy(f->Vx[kd], f->Vx[kd] + 2 * n * n, o);
-      std::copy(f->Vx_inv[kd], f->Vx_inv[kd] + 2 * n * n, o + 2 * n * n);
-      std::copy(f->lx[kd], f->lx[kd] + 2 * n, o + 4 * n * n);
-      // tW Vx, tE Vx (row vector times the complex eigenvector matrix)
-      for (int p = 0; p < n; ++p) {
-        double wr = 0, wi = 0, er = 0, ei = 0;
-        for (int ix = 0; ix < n; ++ix) {
-          const double vr = f->Vx[kd][2 * (ix + p * n)], vi = f->Vx[kd][2 * (ix + p * n) + 1];
-          wr += f->tW[ix] * vr;
-          wi += f->tW[ix] * vi;
-          er += f->tE[ix] * vr;
-          ei += f->tE[ix] * vi;
-        }
-        o[4 * n * n + 2 * n + 2 * p] = wr;
-        o[4 * n * n + 2 * n + 2 * p + 1] = wi;
-        o[4 * n * n + 4 * n + 2 * p] = er;
-        o[4 * n * n + 4 * n + 2 * p + 1] = ei;
-      }
-    }
-    cudaStream_t st = b->ctx->stream;
-    b->dsfac.upload(fac, st);
-    b->dslz.upload(std::vector<double>(f->lz, f->lz + 2 * static_cast<size_t>(b->sp_nmode)), st);
-    b->dsmu.upload(std::vector<double>(f->mu, f->mu + b->nsys), st);
-    b->strip_tau = f->tau;
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    b->strip_ok = true;
-  }
-}
-
-int smpm_schur_rhs(smpm_batch* b, const double* f, double* b_S, void* stream) {
-  return guard([&] {
-    need_strip(b);
-    if (!f || !b_S) fail(SMPM_EINVAL, "null vector");
-    cudaStream_t st = b->st(stream);
-    const StripParams P = strip_params(b);
-    const long long tot = static_cast<long long>(b->nsys) * P.r;
-    strip_gather_kernel<<<grid_for(tot), 256, 0, st>>>(P, f, nullptr, b->dsx1.p);
-    check_launch(b);
-    xf_columns(b, true, b->dsx1.p, b->dsx2.p, b->mx * b->n, P.r, st);
-    strip_modes<true>(b, b->dsx2.p, b->dsbh.p, st);
-    xf_columns(b, false, b->dsbh.p, b_S, 2 * b->d, b->k, st);
-  });
-}
-
-int smpm_recover_solution(smpm_batch* b, const double* f, const double* x_S, double* u, void* stream) {
-  return guard([&] {
-    need_strip(b);
-    if (!f || !x_S || !u) fail(SMPM_EINVAL, "null vector");
-    cudaStream_t st = b->st(stream);
-    const StripParams P = strip_params(b);
-    const long long tot = static_cast<long long>(b->nsys) * P.r;
-    strip_gather_kernel<<<grid_for(tot), 256, 0, st>>>(P, f, x_S, b->dsx1.p);
-    check_launch(b);
-    xf_columns(b, true, b->dsx1.p, b->dsx2.p, b->mx * b->n, P.r, st);
-    strip_modes<false>(b, b->dsx2.p, b->dsx1.p, st);
-    xf_columns(b, false, b->dsx1.p, b->dsx2.p, b->mx * b->n, P.r, st);
-    strip_scatter_kernel<<<grid_for(tot), 256, 0, st>>>(P, b->dsx2.p, u);
-    check_launch(b);
-  });
-}
-
-int smpm_fourier_y(long long r, int m_y, const double* field, double* coeff, void* stream) {
-  return guard([&] { fourier_launch(r, m_y, field, coeff, -1, static_cast<cudaStream_t>(stream)); });
-}
-
-int smpm_inverse_fourier_y(long long r, int m_y, const double* coeff, double* field, void* stream) {
-  return guard([&] { fourier_launch(r, m_y, coeff, field, +1, static_cast<cudaStream_t>(stream)); });
-}
-
-int smpm_project_out(smpm_batch* b, long long len, const double* v, const double* dir, double* out, void* stream) {
-  return guard([&] {
-    need_final(b);
-    // any per-system length: interface vectors (u_S on b_S, len = k) or node
-    // vectors (u_L on f, len = r; proj/src/solver.cpp:46, proj/src/helmholtz.cpp:159-160)
-    if (len < 1) fail(SMPM_EINVAL, "smpm_project_out: len must be >= 1");
-    if (!v || !dir || !out) fail(SMPM_EINVAL, "null vector");
-    cudaStream_t st = b->st(stream);
-    double* dots = b->dsmall.p;
-    batched_dot(b, dir, v, dots, nullptr, st, len);
-    project_kernel<<<grid_for(b->nsys * len), 256, 0, st>>>(b->nsys, len, dots, v, dir, out);
-    check_launch(b);
-  });
-}
-
-int smpm_solve(smpm_batch* b, int method, const double* b_S, double* x_S, const smpm_solve_options* opt,
-               smpm_report* reports, double* history, void* stream) {
-  return guard([&] {
-    need_final(b);
-    if (!b_S || !x_S) fail(SMPM_EINVAL, "null vector");
-    solve(b, cfg_from(method, opt), b_S, x_S, reports, history, b->st(stream));
-  });
-}
-
-int smpm_deflated_solve(smpm_batch* b, const double* b_S, double* x_S, const smpm_solve_options* opt,
-                        smpm_report* reports, double* history, void* stream) {
-  return smpm_solve(b, SMPM_DBJ, b_S, x_S, opt, reports, history, stream);
-}
-
-int smpm_two_level_schwarz_solve(smpm_batch* b, const double* b_S, double* x_S, const smpm_solve_options* opt,
-                                 smpm_report* reports, double* history, void* stream) {
-  return smpm_solve(b, SMPM_2LAS, b_S, x_S, opt, reports, history, stream);
-}
-
-int smpm_solve_stacked(smpm_batch* b, int method, const double* b_S, double* x_S, const smpm_solve_options* opt,
-                       smpm_report* report, double* history, void* stream) {
-  return guard([&] {
-    need_final(b);
-    if (!b_S || !x_S) fail(SMPM_EINVAL, "null vector");
-    if (method != SMPM_DBJ && method != SMPM_2LAS) fail(SMPM_EINVAL, "stacked solve: dbj or 2las");
-    SolveCfg c = cfg_from(method, opt);
-    c.stacked = true;
-    // every system carries the same (global) report and history: keep one
-    std::vector<smpm_report> reps(static_cast<size_t>(b->nsys));
-    const int cap = static_cast<int>(std::min<long long>(c.max_iter, b->k)) + 2;  // solve's history stride
-    std::vector<double> hist(history ? static_cast<size_t>(b->nsys) * cap : 0);
-    solve(b, c, b_S, x_S, reps.data(), history ? hist.data() : nullptr, b->st(stream));
-    if (report) *report = reps[0];
-    if (history) std::copy(hist.begin(), hist.begin() + cap, history);
-  });
-}
-
-int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x_S_host,
-                    const smpm_solve_options* opt, smpm_report* reports, double* history) {
-  return guard([&] {
-    need_final(b);
-    cudaStream_t st = b->ctx->stream;
-    const size_t bytes = sizeof(double) * b->nsys * static_cast<size_t>(b->k);
-    double* din = b->vbuf[10].p;
-    double* dout = b->vbuf[11].p;
-    CUDA_CHECK(cudaMemcpyAsync(din, b_S_host, bytes, cudaMemcpyHostToDevice, st));
-    solve(b, cfg_from(method, opt), din, dout, reports, history, st, x_S_host);
-    CUDA_CHECK(cudaStreamSynchronize(st));
-  });
-}
-
-long long smpm_batch_launch_count(const smpm_batch* b) { return b ? b->launches : 0; }
-
-int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
-  return guard([&] {
-    if (!key) fail(SMPM_EINVAL, "null tuning key");
-    const std::string k(key);
-    if (!b) {
-      if (k == "fy_tile") {
-        g_fy_tile = static_cast<int>(value);
-        return;
-      }
-      fail(SMPM_EINVAL, "null batch");
-    }
-    Tuning& t = b->tune;
-    const int v = static_cast<int>(value);
-    struct Knob {
-      const char* name;
-      int* field;
-    };
-    if (k == "tail_rows") {
-      t.tail_rows = value;
-      return;
-    }
-    const Knob knobs[] = {{"segb", &t.segb}, {"spec_v2", &t.spec_v2}, {"xform", &t.xform}, {"xform_parity", &t.xform_parity},
-                          {"sp_stage", &t.sp_stage},
-                          {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse}, {"cgs_defer", &t.cgs_defer}, {"cgs_lanes", &t.cgs_lanes},
-                          {"gt_vblock", &t.gt_vblock}, {"grid_per_sm", &t.grid_per_sm}, {"gt_ctas", &t.gt_ctas},
-                          {"grid_nocoop", &t.grid_nocoop}, {"pdl", &t.pdl}, {"pythag", &t.pythag},
-                          {"grid", &t.grid}, {"grid_max", &t.grid_max}, {"post_fuse", &t.post_fuse},
-                          {"early", &t.early}};
-    for (const Knob& kb : knobs)
-      if (k == kb.name) {
-        *kb.field = v;
-        // grid geometry and transform plans depend on some knobs: recompute lazily
-        if (k == "gt_vblock" || k == "grid_per_sm" || k == "gt_ctas") b->gt_blocks = 0;
-        if ((k == "xform" || k == "xform_parity") && b->finalized && b->spectral) setup_xform(b);
-        return;
-      }
-    fail(SMPM_EINVAL, "unknown tuning key '" + k + "'");
-  });
-}
-
-int smpm_batch_set_allreduce(smpm_batch* b, smpm_allreduce_fn fn, void* user) {
-  return guard([&] {
-    if (!b) fail(SMPM_EINVAL, "null batch");
-    b->ar_fn = fn;
-    b->ar_user = user;
-    if (fn) b->dstack.alloc(static_cast<size_t>(V2_MAXCOL + 2));
-  });
-}
-
-int smpm_batch_query(const smpm_batch* b, const char* key, long long* value) {
-  return guard([&] {
-    if (!b || !key || !value) fail(SMPM_EINVAL, "null argument");
-    const std::string k(key);
-    if (k == "xform_kernel")
-      *value = !b->spectral || b->xf_P == 0 ? 0 : b->xp_on ? 3 : b->xf_stream ? 2 : 1;
-    else if (k == "xform_parity")
-      *value = b->spectral && b->xp_on ? 1 : 0;
-    else if (k == "cgs_defer")
-      *value = b->tune.cgs_defer && b->tune.pythag ? 1 : 0;
-    else if (k == "spectral")
-      *value = b->spectral && b->tune.spectral ? 1 : 0;
-    else
-      fail(SMPM_EINVAL, "unknown query key '" + k + "'");
-  });
-}
-
-int smpm_batch_set_trace(smpm_batch* b, int which, const char* path) {
-  return guard([&] {
-    if (!b) fail(SMPM_EINVAL, "null batch");
-    if (which == 0)
-      b->tune.gt_trace = path ? path : "";
-    else if (which == 1)
-      b->tune.gt_trace2 = path ? path : "";
-    else
-      fail(SMPM_EINVAL, "trace: which must be 0 (per-step phases) or 1 (per-CTA)");
-  });
-}
-
-int smpm_batch_profile(smpm_batch* b, int enable, double* ms, long long* counts, int nclass) {
-  return guard([&] {
-    if (!b) fail(SMPM_EINVAL, "null batch");
-    CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
-    prof_collect(b);
-    if (ms)
-      for (int i = 0; i < std::min(nclass, 10); ++i) ms[i] = b->prof_ms[i];
-    if (counts)
-      for (int i = 0; i < std::min(nclass, 10); ++i) counts[i] = b->prof_n[i];
-    if (enable >= 0) {
-      b->profiling = enable != 0;
-      for (int i = 0; i < 10; ++i) {
-        b->prof_ms[i] = 0.0;
-        b->prof_n[i] = 0;
-      }
-    }
-  });
-}
-
-}  // extern "C"
+#include "batch_abi.inl"

@@ -1,0 +1,413 @@
+// Spectral operator: transform kernel setup / launch, per-mode pass, preconditioned operator (part of batch.cu's translation unit).
+// Included by batch.cu; not a standalone header.
+// --------------------------------------------------------------------------
+// Spectral operator (spectral.cuh): T^{-1} GEMM, per-mode S^ M^^{-1}, T GEMM
+// --------------------------------------------------------------------------
+SpecParams spec_params(const smpm_batch* b) {
+  SpecParams sp{};
+  sp.w = b->w;
+  sp.d = b->d;
+  sp.mx = b->mx;
+  sp.nbf = b->nbf;
+  sp.single = b->single ? 1 : 0;
+  sp.npairs = b->sp_npairs;
+  sp.nmode = b->sp_nmode;
+  sp.k = b->k;
+  sp.gam = reinterpret_cast<const double2*>(b->dgam.p);
+  sp.kinv = reinterpret_cast<const double2*>(b->dkinv.p);
+  sp.omega = b->domega.p;
+  sp.nu = b->dnu.p;
+  sp.cadd = nullptr;
+  sp.nmc = (b->sp_nmode + SP_MODES - 1) / SP_MODES;
+  sp.segb = SP_SEGB;
+  if (b->tune.segb > 0) sp.segb = std::max(1, std::min(SP_SEGB, b->tune.segb));
+  sp.nseg = (b->nbf + (b->single ? 1 : 0) + sp.segb - 1) / sp.segb;
+  return sp;
+}
+
+// ---- shared-matrix transforms (xform.cuh): the largest row slice of T / T^{-1}
+// that fits in shared memory next to a two-deep column ring, P slices per column group
+template <int MB>
+bool xform_try(smpm_batch* b, int P) {
+  const int w = b->w;
+  const size_t smem =
+      sizeof(double) * (static_cast<size_t>(w / 8) * MB * 64 + static_cast<size_t>(XF_NS) * XF_NT * xf_bstr(w / 2));
+  if (smem > 232448 || 8 * MB * P < w || P > b->ctx->num_sms) return false;
+  CUDA_CHECK(cudaFuncSetAttribute(xform_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  std::vector<double> f(static_cast<size_t>(P) * (w / 8) * MB * 64), fi(f.size());
+  xform_frag_order(b->hT.data(), w, P, MB, f.data());
+  xform_frag_order(b->hTi.data(), w, P, MB, fi.data());
+  b->dTfrag.upload(f, b->ctx->stream);
+  b->dTifrag.upload(fi, b->ctx->stream);
+  CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
+  b->xf_P = P;
+  b->xf_MB = MB;
+  b->xf_smem = smem;
+  return true;
+}
+
+// K-streamed kernel (xformk.cuh) for w whose resident slice does not fit
+template <int MB, int NS>
+bool xformk_try(smpm_batch* b, int P) {
+  const int w = b->w;
+  const size_t smem = xformk_smem<MB, NS>();
+  if (smem > 232448 || 8 * MB * P < w || P > b->ctx->num_sms) return false;
+  CUDA_CHECK(cudaFuncSetAttribute(xformk_kernel<MB, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  std::vector<double> f(static_cast<size_t>(P) * (w / 8) * MB * 64), fi(f.size());
+  xform_frag_order(b->hT.data(), w, P, MB, f.data());
+  xform_frag_order(b->hTi.data(), w, P, MB, fi.data());
+  b->dTfrag.upload(f, b->ctx->stream);
+  b->dTifrag.upload(fi, b->ctx->stream);
+  CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
+  b->xf_P = P;
+  b->xf_MB = MB;
+  b->xf_smem = smem;
+  b->xf_stream = true;
+  return true;
+}
+
+// ---- parity-split transforms (xformp.cuh) -----------------------------------
+// True when every column of T (row of T^{-1}) is even or odd under the reversal of
+// the node index and the modes are ordered pairs (even, odd), reals (even, odd);
+// fills the mode segments of each parity.
+bool parity_detect(smpm_batch* b) {
+  const int w = b->w, h = w / 2, np2 = 2 * b->sp_npairs;
+  if (w % 16 != 0) return false;
+  std::vector<int> par(static_cast<size_t>(w), 0);
+  const double tol = 1e-14;
+  for (int m = 0; m < w; ++m) {
+    double amax = 0.0, ce = 0.0, co = 0.0, rmax = 0.0, re = 0.0, ro = 0.0;
+    for (int r = 0; r < w; ++r) {
+      const double x = b->hT[static_cast<size_t>(m) * w + r], y = b->hT[static_cast<size_t>(m) * w + (w - 1 - r)];
+      amax = std::max(amax, std::fabs(x));
+      ce = std::max(ce, std::fabs(x - y));
+      co = std::max(co, std::fabs(x + y));
+      const double p = b->hTi[static_cast<size_t>(r) * w + m], q = b->hTi[static_cast<size_t>(w - 1 - r) * w + m];
+      rmax = std::max(rmax, std::fabs(p));
+      re = std::max(re, std::fabs(p - q));
+      ro = std::max(ro, std::fabs(p + q));
+    }
+    if (ce <= tol * amax && re <= tol * rmax)
+      par[m] = 1;
+    else if (co <= tol * amax && ro <= tol * rmax)
+      par[m] = -1;
+    else
+      return false;
+  }
+  int npe = 0;
+  while (2 * npe < np2 && par[2 * npe] == 1) ++npe;
+  for (int q = 0; q < b->sp_npairs; ++q) {
+    const int want = q < npe ? 1 : -1;
+    if (par[2 * q] != want || par[2 * q + 1] != want) return false;
+  }
+  int nre = 0;
+  while (np2 + nre < w && par[np2 + nre] == 1) ++nre;
+  for (int m = np2 + nre; m < w; ++m)
+    if (par[m] != -1) return false;
+  if (2 * npe + nre != h) return false;
+  b->xp_h = h;
+  b->xp_ks = (h + XK_KS - 1) / XK_KS;
+  b->xp_seg_start[0][0] = 0;
+  b->xp_seg_len0[0] = 2 * npe;
+  b->xp_seg_start[0][1] = np2;
+  b->xp_seg_start[1][0] = 2 * npe;
+  b->xp_seg_len0[1] = np2 - 2 * npe;
+  b->xp_seg_start[1][1] = np2 + nre;
+  return true;
+}
+
+template <int MB, int NS, bool BWD>
+void xformp_attr() {
+  CUDA_CHECK(cudaFuncSetAttribute(xformp_kernel<MB, NS, BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(xformp_smem<MB, NS, BWD>())));
+}
+
+void setup_xformp(smpm_batch* b) {
+  const int w = b->w, h = b->xp_h, ks = b->xp_ks, mbt = h / 8;
+  // forward: Ps single-parity slices per parity of at most 34 m-blocks
+  const int Ps = (mbt + 33) / 34, needf = (mbt + Ps - 1) / Ps;
+  const int MBf = needf <= 11 ? 11 : needf <= 17 ? 17 : needf <= 26 ? 26 : 34;
+  // backward: P slices of rows k < h of at most 17 m-blocks (two accumulator sets)
+  const int Pb = (mbt + 16) / 17, needb = (mbt + Pb - 1) / Pb;
+  const int MBb = needb <= 9 ? 9 : needb <= 11 ? 11 : needb <= 13 ? 13 : 17;
+  if (2 * Ps > b->ctx->num_sms || Pb > b->ctx->num_sms) return;
+  switch (MBf) {
+    case 11: xformp_attr<11, 6, false>(); b->xp_smem_f = xformp_smem<11, 6, false>(); break;
+    case 17: xformp_attr<17, 5, false>(); b->xp_smem_f = xformp_smem<17, 5, false>(); break;
+    case 26: xformp_attr<26, 4, false>(); b->xp_smem_f = xformp_smem<26, 4, false>(); break;
+    default: xformp_attr<34, 3, false>(); b->xp_smem_f = xformp_smem<34, 3, false>(); break;
+  }
+  switch (MBb) {
+    case 9: xformp_attr<9, 8, true>(); b->xp_smem_b = xformp_smem<9, 8, true>(); break;
+    case 11: xformp_attr<11, 8, true>(); b->xp_smem_b = xformp_smem<11, 8, true>(); break;
+    case 13: xformp_attr<13, 8, true>(); b->xp_smem_b = xformp_smem<13, 8, true>(); break;
+    default: xformp_attr<17, 7, true>(); b->xp_smem_b = xformp_smem<17, 7, true>(); break;
+  }
+  auto mode = [&](int par, int kap) { return xp_mode(b->xp_seg_start, b->xp_seg_len0, par, kap); };
+  std::vector<double> f;
+  xformp_image(2 * Ps, ks, MBf, [&](int sl, int r, int kk) {
+    const int par = sl / Ps, kap = (sl % Ps) * 8 * MBf + r;
+    if (kap >= h || kk >= h) return 0.0;
+    return b->hTi[static_cast<size_t>(kk) * w + mode(par, kap)];
+  }, f);
+  b->dTpf.upload(f, b->ctx->stream);
+  xformp_image(Pb, 2 * ks, MBb, [&](int sl, int r, int kk) {
+    const int k = sl * 8 * MBb + r, pq = kk / (XK_KS * ks), kap = kk - pq * XK_KS * ks;
+    if (k >= h || kap >= h) return 0.0;
+    return b->hT[static_cast<size_t>(mode(pq, kap)) * w + k];
+  }, f);
+  b->dTpb.upload(f, b->ctx->stream);
+  CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
+  b->xp_Pf = 2 * Ps;
+  b->xp_MBf = MBf;
+  b->xp_Pb = Pb;
+  b->xp_MBb = MBb;
+  b->xp_on = true;
+}
+
+void setup_xform(smpm_batch* b) {
+  b->xf_P = 0;
+  b->xf_stream = false;
+  b->xp_on = false;
+  if (b->w % 16 != 0 || !b->tune.xform) return;
+  bool found = false;
+  for (int P = 1; P <= 4 && !found; ++P) {
+    const int need = (b->w / 8 + P - 1) / P;
+    found = need <= 4 ? xform_try<4>(b, P) : need <= 8 ? xform_try<8>(b, P) : need <= 11 ? xform_try<11>(b, P) : false;
+  }
+  if (!found) {
+    // w > 176: A streams with the columns; P row slices of at most 34 m-blocks
+    const int K8 = b->w / 8;
+    const int P = (K8 + 33) / 34;
+    const int need = (K8 + P - 1) / P;
+    if (need <= 26)
+      found = xformk_try<26, 5>(b, P);
+    else if (need <= 34)
+      found = xformk_try<34, 4>(b, P);
+  }
+  // parity-pure basis: two half-size contractions instead (half the MMA work)
+  const int pm = b->tune.xform_parity;
+  if (found && pm > 0 && (pm >= 2 || b->xf_stream) && parity_detect(b)) setup_xformp(b);
+}
+
+// one transform launch over the columns described by `a` (a.P set), groups column groups
+// parity-split launch: `a` as for launch_xform (a.Af / a.P are replaced by the direction's image / slices)
+void launch_xformp(smpm_batch* b, const XformArgs& a, bool inverse, cudaStream_t st, bool pdl) {
+  XformPArgs pa;
+  pa.x = a;
+  pa.x.Af = inverse ? b->dTpf.p : b->dTpb.p;
+  pa.x.P = inverse ? b->xp_Pf : b->xp_Pb;
+  pa.h = b->xp_h;
+  pa.ks = b->xp_ks;
+  for (int p = 0; p < 2; ++p) {
+    pa.seg_start[p][0] = b->xp_seg_start[p][0];
+    pa.seg_start[p][1] = b->xp_seg_start[p][1];
+    pa.seg_len0[p] = b->xp_seg_len0[p];
+  }
+  const long long nch = (static_cast<long long>(a.nslots) * a.ncol_sys * a.nv + 15) / 16;
+  const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / pa.x.P, nch)));
+  const dim3 grid(groups * pa.x.P), blk(XF_THREADS);
+  const size_t smem = inverse ? b->xp_smem_f : b->xp_smem_b;
+  auto go = [&](auto kern) {
+    if (pdl) {
+      launch_pdl(b, kern, grid, blk, smem, st, pa);
+    } else {
+      kern<<<grid, blk, smem, st>>>(pa);
+      check_launch(b);
+    }
+  };
+  if (inverse) {
+    switch (b->xp_MBf) {
+      case 11: go(xformp_kernel<11, 6, false>); break;
+      case 17: go(xformp_kernel<17, 5, false>); break;
+      case 26: go(xformp_kernel<26, 4, false>); break;
+      default: go(xformp_kernel<34, 3, false>); break;
+    }
+  } else {
+    switch (b->xp_MBb) {
+      case 9: go(xformp_kernel<9, 8, true>); break;
+      case 11: go(xformp_kernel<11, 8, true>); break;
+      case 13: go(xformp_kernel<13, 8, true>); break;
+      default: go(xformp_kernel<17, 7, true>); break;
+    }
+  }
+}
+
+void launch_xform(smpm_batch* b, const XformArgs& a, int groups, cudaStream_t st, bool pdl) {
+  const dim3 grid(groups * a.P), blk(XF_THREADS);
+  auto go = [&](auto kern) {
+    if (pdl) {
+      launch_pdl(b, kern, grid, blk, b->xf_smem, st, a);
+    } else {
+      kern<<<grid, blk, b->xf_smem, st>>>(a);
+      check_launch(b);
+    }
+  };
+  if (b->xf_stream) {
+    if (b->xf_MB == 26)
+      go(xformk_kernel<26, 5>);
+    else
+      go(xformk_kernel<34, 4>);
+    return;
+  }
+  switch (b->xf_MB) {
+    case 4: go(xform_kernel<4>); break;
+    case 8: go(xform_kernel<8>); break;
+    default: go(xform_kernel<11>); break;
+  }
+}
+
+// out = A in (and out2 = A in2) for every w-block of the live systems, A = T^{-1} (inverse) or T
+void run_xform(smpm_batch* b, bool inverse, const double* in, double* out, const Live& lv, cudaStream_t st,
+               const double* in2 = nullptr, double* out2 = nullptr) {
+  if (lv.nslots == 0) return;
+  ProfScope psx(b, 8, st);  // class 8: shared-matrix transforms
+  if (b->xf_P == 0) {
+    run_plan(b, inverse ? b->pF : b->pB, in, out, nullptr, lv, st);
+    if (in2) run_plan(b, inverse ? b->pF : b->pB, in2, out2, nullptr, lv, st);
+    return;
+  }
+  XformArgs a;
+  a.Af = inverse ? b->dTifrag.p : b->dTfrag.p;
+  a.w = b->w;
+  a.ncol_sys = 2 * b->d;
+  a.k = b->k;
+  a.alist = lv.alist;
+  a.acount = lv.acount;
+  a.nslots = lv.nslots;
+  a.nv = in2 ? 2 : 1;
+  a.in[0] = in;
+  a.out[0] = out;
+  a.in[1] = in2;
+  a.out[1] = out2;
+  a.P = b->xf_P;
+  // column groups: every SM busy unless a group's share would drop below 16 columns
+  const long long nch = (static_cast<long long>(lv.nslots) * a.ncol_sys * a.nv + 15) / 16;
+  const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / a.P, nch)));
+  if (b->xp_on)
+    launch_xformp(b, a, inverse, st, true);
+  else
+    launch_xform(b, a, groups, st, true);
+}
+
+// th = S^ M^^{-1} vh (bj) or S^ vh in T-coordinates; with cout, also
+// c = C^{-1} Z^T (T th) per system (deflation coarse solve)
+void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* cout, const Live& lv, cudaStream_t st,
+                double* uh = nullptr, const double* cadd = nullptr) {
+  if (lv.nslots == 0) return;
+  ProfScope ps(b, 7, st);  // class 7: per-mode pass
+  SpecParams sp = spec_params(b);
+  sp.cadd = cadd;
+  DeflateParams P = deflate_params(b, lv.active);
+  P.alist = lv.alist;
+  P.acount = lv.acount;
+  double* zp = cout ? b->dzpart.p : nullptr;
+  if (b->tune.spec_v2) {
+    // pipelined pass (spec_op2_kernel): segments as long as ~32 warps per SM
+    // still allow (shorter halo), at least 4 and at most 16 blocks
+    const long long nbk = b->nbf + (b->single ? 1 : 0);
+    const long long warps = nbk * sp.nmc * lv.nslots;
+    int segb = static_cast<int>(std::max(4LL, std::min(16LL, warps / (32LL * b->ctx->num_sms))));
+    if (b->tune.segb > 0) segb = b->tune.segb;
+    sp.segb = segb;
+    sp.nseg = static_cast<int>((nbk + segb - 1) / segb);
+    const dim3 grid2(sp.nmc * ((sp.nseg + SP_WARPS - 1) / SP_WARPS), lv.nslots);
+    const size_t shm2 = cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0;
+    if (bj)
+      launch_pdl(b, spec_op2_kernel<true>, grid2, dim3(SP_THREADS), shm2, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);
+    else
+      launch_pdl(b, spec_op2_kernel<false>, grid2, dim3(SP_THREADS), shm2, st, sp, vh, th, P, zp, b->dcount.p, cout,
+                 uh);
+    return;
+  }
+  const dim3 grid(sp.nmc * ((sp.nseg + SP_WARPS - 1) / SP_WARPS), lv.nslots);
+  // staged slot rows (tuning sp_stage = 0: direct loads)
+  sp.stage = sp.segb <= SP_SEGB && b->tune.sp_stage ? 1 : 0;
+  const size_t shm = (cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0) +
+                     (sp.stage ? sizeof(double) * SP_STAGE_DOUBLES : 0);
+  if (sp.stage && !b->sp_smem_set) {
+    const int mx = static_cast<int>(sizeof(double) * (SP_STAGE_DOUBLES + 2 * 256));
+    CUDA_CHECK(cudaFuncSetAttribute(spec_op_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CUDA_CHECK(cudaFuncSetAttribute(spec_op_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    b->sp_smem_set = true;
+  }
+  if (bj)
+    launch_pdl(b, spec_op_kernel<true>, grid, dim3(SP_THREADS), shm, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);
+  else
+    launch_pdl(b, spec_op_kernel<false>, grid, dim3(SP_THREADS), shm, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);
+}
+
+// u = M^{-1} v through the spectral form, and (su != nullptr) S u as well
+void spec_Minv(smpm_batch* b, const double* v, double* u, double* su, const Live& lv, cudaStream_t st) {
+  run_xform(b, true, v, b->dvh.p, lv, st);
+  spec_apply(b, true, b->dvh.p, su ? b->dth.p : nullptr, nullptr, lv, st, b->dvh2.p);
+  run_xform(b, false, b->dvh2.p, u, lv, st, su ? b->dth.p : nullptr, su);
+}
+
+bool spec_on(const smpm_batch* b) { return b->spectral && b->tune.spectral; }
+
+bool spec_ok(const smpm_batch* b, const SolveCfg& c) {
+  return spec_on(b) && (c.method == SMPM_SCHUR || c.method == SMPM_BJ || c.method == SMPM_DBJ);
+}
+// 2LAS through the spectral form in the per-stage steps (many live systems); the grid
+// tail keeps its dense stages for 2LAS (a coarse solve before the per-mode pass would
+// add two grid barriers per step; measured: per-stage spectral 2LAS with one live
+// system is slower than the dense tail, 12.1 vs 10.2 ms on C3)
+bool spec_2las(const smpm_batch* b, const SolveCfg& c) {
+  return spec_on(b) && c.method == SMPM_2LAS && b->tune.spec_2las;
+}
+
+// S M^{-1} v (bj) or S v through the spectral form; out may be any buffer
+void spec_SMinv(smpm_batch* b, bool bj, const double* v, double* out, double* cout, const Live& lv, cudaStream_t st) {
+  run_xform(b, true, v, b->dvh.p, lv, st);
+  spec_apply(b, bj, b->dvh.p, b->dth.p, cout, lv, st);
+  run_xform(b, false, b->dth.p, out, lv, st);
+}
+
+// the preconditioned operator GMRES iterates on (proj/src/deflation.cpp:105-107,131; proj/src/gmres.cpp:144-150)
+// returns the number of S applications it made per system
+int apply_op(smpm_batch* b, const SolveCfg& c, const double* vin, double* wout, const Live& act, cudaStream_t st) {
+  double* u = b->vbuf[4].p;
+  double* t = b->vbuf[5].p;
+  if (spec_ok(b, c)) {
+    if (c.method == SMPM_DBJ) {
+      spec_SMinv(b, true, vin, t, nullptr, act, st);
+      op_P(b, t, wout, c.fused, act, st);
+      return c.fused ? 1 : 2;
+    }
+    spec_SMinv(b, c.method == SMPM_BJ, vin, wout, nullptr, act, st);
+    return 1;
+  }
+  if (spec_2las(b, c)) {
+    // S (M^{-1} + Z C^{-1} Z^T) v: c = C^{-1} Z^T v, then one per-mode pass of
+    // T^{-1} v that adds Z c before S^ (proj/src/deflation.cpp:127-131)
+    double* cb = b->dcoarse.p + static_cast<size_t>(b->nsys) * b->d;
+    run_deflate(b, DEFL_COARSE, vin, nullptr, nullptr, cb, act, st);
+    run_xform(b, true, vin, b->dvh.p, act, st);
+    spec_apply(b, true, b->dvh.p, b->dth.p, nullptr, act, st, nullptr, cb);
+    run_xform(b, false, b->dth.p, wout, act, st);
+    return 1;
+  }
+  switch (c.method) {
+    case SMPM_SCHUR:
+      op_S(b, vin, wout, act, st);
+      return 1;
+    case SMPM_BJ:
+      op_BJ(b, vin, u, act, st);
+      op_S(b, u, wout, act, st);
+      return 1;
+    case SMPM_DBJ:
+      op_BJ(b, vin, u, act, st);
+      op_S(b, u, t, act, st);
+      op_P(b, t, wout, c.fused, act, st);
+      return c.fused ? 1 : 2;
+    case SMPM_2LAS: {
+      op_BJ(b, vin, u, act, st);
+      run_deflate(b, DEFL_ADD_ZC, vin, u, t, nullptr, act, st);  // minv = M^{-1} + Z C^{-1} Z^T
+      op_S(b, t, wout, act, st);
+      return 1;
+    }
+  }
+  fail(SMPM_EINVAL, "unknown method");
+}
