@@ -29,6 +29,7 @@
 #include "vec4.cuh"
 #include "grid.cuh"
 #include "spectral.cuh"
+#include "spectral3.cuh"
 #include "xform.cuh"
 #include "xformk.cuh"
 #include "xformp.cuh"
@@ -250,7 +251,7 @@ struct Tuning {
   int xform_parity = 1;  // parity-split transforms (xformp.cuh) when T is parity-pure: 0 off, 1 where the
                          // K-streamed kernel would run (w > 176), 2 wherever w % 16 == 0
   int sp_stage = 1;      // per-mode pass stages slot rows in shared memory (spec_v2 = 0)
-  int spec_v2 = 1;       // pipelined per-mode pass (spec_op2_kernel)
+  int spec_v2 = 2;       // pipelined per-mode pass: 2 spec_op3_kernel (16 bytes per lane), 1 spec_op2_kernel, 0 staged
   int spectral = 1;      // spectral operator when its factors are set
   int spec_2las = 1;     // spectral operator for 2LAS
   int p2fuse = 1;        // CGS2 pass 2 single-read fusion
@@ -311,9 +312,13 @@ struct smpm_batch {
   // parity-split transforms (xformp.cuh): forward = T^{-1}, backward = T
   bool xp_on = false;
   int xp_h = 0, xp_ks = 0, xp_seg_start[2][2] = {{0, 0}, {0, 0}}, xp_seg_len0[2] = {0, 0};
-  int xp_Pf = 0, xp_MBf = 0, xp_Pb = 0, xp_MBb = 0;
-  size_t xp_smem_f = 0, xp_smem_b = 0;
-  DevArray<double> dTpf, dTpb;
+  // slicing variants per direction ([0] forward = T^{-1}, [1] backward = T): more, thinner row slices
+  // for launches with few columns (the slow-mode tail), so every SM still gets a full 64-column chunk
+  struct XpVariant {
+    int P = 0, MB = 0;  // row slices (forward: both parities), m-blocks per slice
+    DevArray<double> img;
+  };
+  std::vector<std::unique_ptr<XpVariant>> xp_var[2];
   long long cgs3_res = 0;  // resident CTAs of the CGS2 pass kernels (device)
   long long cgs3_kres[3] = {0, 0, 0};  // per kernel: pass 1, pass 2', pass 3' (norm-from-h2 path)
   long long p2t_res[V2_MAXCOL + 1] = {};  // resident CTAs of the tiled pass 2' per column capacity

@@ -587,7 +587,7 @@ void finalize(smpm_batch* b) {
       for (int r = 0; r < w; ++r) nu[r] += b->hTi[static_cast<size_t>(c2) * w + r];
     b->dnu.upload(nu, st);
     const int nmc = (b->sp_nmode + SP_MODES - 1) / SP_MODES;
-    b->dzpart.alloc(static_cast<size_t>(b->nsys) * nmc * d);
+    b->dzpart.alloc(static_cast<size_t>(b->nsys) * std::max(nmc, spec3_chunks(b->sp_npairs, b->sp_nmode)) * d);
     b->dkinv.alloc(static_cast<size_t>(b->nsys) * 20 * b->sp_nmode * 2);
     b->dvh.alloc(static_cast<size_t>(b->nsys) * b->k);
     b->dth.alloc(static_cast<size_t>(b->nsys) * b->k);

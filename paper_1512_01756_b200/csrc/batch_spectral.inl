@@ -117,53 +117,80 @@ bool parity_detect(smpm_batch* b) {
   return true;
 }
 
+// the xformp_kernel instances: (m-blocks per slice, ring depth) per direction
+struct XpKernel {
+  int MB;
+  void (*fn)(XformPArgs);
+  size_t smem;
+};
 template <int MB, int NS, bool BWD>
-void xformp_attr() {
-  CUDA_CHECK(cudaFuncSetAttribute(xformp_kernel<MB, NS, BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(xformp_smem<MB, NS, BWD>())));
+XpKernel xp_instance() {
+  return XpKernel{MB, xformp_kernel<MB, NS, BWD>, xformp_smem<MB, NS, BWD>()};
+}
+const XpKernel* xp_kernels(bool bwd, int& count) {
+  static const XpKernel fwd[] = {xp_instance<9, 6, false>(), xp_instance<11, 6, false>(), xp_instance<17, 5, false>(),
+                                 xp_instance<26, 4, false>(), xp_instance<34, 3, false>()};
+  static const XpKernel back[] = {xp_instance<5, 8, true>(), xp_instance<9, 8, true>(), xp_instance<11, 8, true>(),
+                                  xp_instance<13, 8, true>(), xp_instance<17, 7, true>()};
+  count = 5;
+  return bwd ? back : fwd;
+}
+const XpKernel& xp_kernel_for(bool bwd, int MB) {
+  int n = 0;
+  const XpKernel* ks = xp_kernels(bwd, n);
+  for (int i = 0; i < n; ++i)
+    if (ks[i].MB == MB) return ks[i];
+  fail(SMPM_ERUNTIME, "no parity transform kernel instance for this slice height");
 }
 
 void setup_xformp(smpm_batch* b) {
   const int w = b->w, h = b->xp_h, ks = b->xp_ks, mbt = h / 8;
-  // forward: Ps single-parity slices per parity of at most 34 m-blocks
-  const int Ps = (mbt + 33) / 34, needf = (mbt + Ps - 1) / Ps;
-  const int MBf = needf <= 11 ? 11 : needf <= 17 ? 17 : needf <= 26 ? 26 : 34;
-  // backward: P slices of rows k < h of at most 17 m-blocks (two accumulator sets)
-  const int Pb = (mbt + 16) / 17, needb = (mbt + Pb - 1) / Pb;
-  const int MBb = needb <= 9 ? 9 : needb <= 11 ? 11 : needb <= 13 ? 13 : 17;
-  if (2 * Ps > b->ctx->num_sms || Pb > b->ctx->num_sms) return;
-  switch (MBf) {
-    case 11: xformp_attr<11, 6, false>(); b->xp_smem_f = xformp_smem<11, 6, false>(); break;
-    case 17: xformp_attr<17, 5, false>(); b->xp_smem_f = xformp_smem<17, 5, false>(); break;
-    case 26: xformp_attr<26, 4, false>(); b->xp_smem_f = xformp_smem<26, 4, false>(); break;
-    default: xformp_attr<34, 3, false>(); b->xp_smem_f = xformp_smem<34, 3, false>(); break;
-  }
-  switch (MBb) {
-    case 9: xformp_attr<9, 8, true>(); b->xp_smem_b = xformp_smem<9, 8, true>(); break;
-    case 11: xformp_attr<11, 8, true>(); b->xp_smem_b = xformp_smem<11, 8, true>(); break;
-    case 13: xformp_attr<13, 8, true>(); b->xp_smem_b = xformp_smem<13, 8, true>(); break;
-    default: xformp_attr<17, 7, true>(); b->xp_smem_b = xformp_smem<17, 7, true>(); break;
-  }
   auto mode = [&](int par, int kap) { return xp_mode(b->xp_seg_start, b->xp_seg_len0, par, kap); };
   std::vector<double> f;
-  xformp_image(2 * Ps, ks, MBf, [&](int sl, int r, int kk) {
-    const int par = sl / Ps, kap = (sl % Ps) * 8 * MBf + r;
-    if (kap >= h || kk >= h) return 0.0;
-    return b->hTi[static_cast<size_t>(kk) * w + mode(par, kap)];
-  }, f);
-  b->dTpf.upload(f, b->ctx->stream);
-  xformp_image(Pb, 2 * ks, MBb, [&](int sl, int r, int kk) {
-    const int k = sl * 8 * MBb + r, pq = kk / (XK_KS * ks), kap = kk - pq * XK_KS * ks;
-    if (k >= h || kap >= h) return 0.0;
-    return b->hT[static_cast<size_t>(mode(pq, kap)) * w + k];
-  }, f);
-  b->dTpb.upload(f, b->ctx->stream);
+  for (int dir = 0; dir < 2; ++dir) {
+    const bool bwd = dir == 1;
+    b->xp_var[dir].clear();
+    int n = 0;
+    const XpKernel* kern = xp_kernels(bwd, n);
+    const int mbmax = kern[n - 1].MB;
+    // slice counts S = S0, 2 S0, 4 S0 (per parity in the forward direction): the instance of least
+    // padding for each; variants whose padding exceeds 15 % of the rows are skipped
+    const int S0 = (mbt + mbmax - 1) / mbmax;
+    for (int S = S0; S <= 4 * S0; S *= 2) {
+      const int need = (mbt + S - 1) / S;
+      int MB = 0;
+      for (int i = 0; i < n; ++i)
+        if (kern[i].MB >= need) {
+          MB = kern[i].MB;
+          break;
+        }
+      if (MB == 0) continue;
+      if (S > S0 && static_cast<long long>(MB) * S * 100 > 115LL * mbt) continue;
+      const int P = bwd ? S : 2 * S;
+      if (P > b->ctx->num_sms) continue;
+      const XpKernel& kk = xp_kernel_for(bwd, MB);
+      CUDA_CHECK(cudaFuncSetAttribute(kk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kk.smem)));
+      b->xp_var[dir].push_back(std::make_unique<smpm_batch::XpVariant>());
+      smpm_batch::XpVariant& v = *b->xp_var[dir].back();
+      v.P = P;
+      v.MB = MB;
+      if (!bwd)
+        xformp_image(2 * S, ks, MB, [&](int sl, int r, int kk2) {
+          const int par = sl / S, kap = (sl % S) * 8 * MB + r;
+          if (kap >= h || kk2 >= h) return 0.0;
+          return b->hTi[static_cast<size_t>(kk2) * w + mode(par, kap)];
+        }, f);
+      else
+        xformp_image(S, 2 * ks, MB, [&](int sl, int r, int kk2) {
+          const int k = sl * 8 * MB + r, pq = kk2 / (XK_KS * ks), kap = kk2 - pq * XK_KS * ks;
+          if (k >= h || kap >= h) return 0.0;
+          return b->hT[static_cast<size_t>(mode(pq, kap)) * w + k];
+        }, f);
+      v.img.upload(f, b->ctx->stream);
+    }
+  }
   CUDA_CHECK(cudaStreamSynchronize(b->ctx->stream));
-  b->xp_Pf = 2 * Ps;
-  b->xp_MBf = MBf;
-  b->xp_Pb = Pb;
-  b->xp_MBb = MBb;
-  b->xp_on = true;
+  b->xp_on = !b->xp_var[0].empty() && !b->xp_var[1].empty();
 }
 
 void setup_xform(smpm_batch* b) {
@@ -192,12 +219,34 @@ void setup_xform(smpm_batch* b) {
 }
 
 // one transform launch over the columns described by `a` (a.P set), groups column groups
-// parity-split launch: `a` as for launch_xform (a.Af / a.P are replaced by the direction's image / slices)
+// parity-split launch: `a` as for launch_xform (a.Af / a.P are replaced by the direction's image / slices).
+// The slicing variant is the one with the least estimated time for this many columns: a CTA's time is
+// (chunks of 64 columns in its share) x (stages) x (fixed cost per stage + cost per m-block).
 void launch_xformp(smpm_batch* b, const XformArgs& a, bool inverse, cudaStream_t st, bool pdl) {
+  const int dir = inverse ? 0 : 1;
+  const long long ncols = static_cast<long long>(a.nslots) * a.ncol_sys * a.nv;
+  const long long nch = (ncols + 15) / 16;
+  const smpm_batch::XpVariant* best = nullptr;
+  int best_groups = 1;
+  double best_t = 0.0;
+  for (const auto& vp : b->xp_var[dir]) {
+    const smpm_batch::XpVariant& v = *vp;
+    const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / v.P, nch)));
+    const long long share = ((ncols + groups - 1) / groups + 7) / 8 * 8;
+    const long long full = share / XF_NT, rem = share % XF_NT;
+    // a trailing chunk of <= 32 columns runs one n-block per warp: half the MMA work
+    const double chunks = static_cast<double>(full) + (rem == 0 ? 0.0 : rem <= 32 ? 0.6 : 1.0);
+    const double t = chunks * (inverse ? 1.0 : 2.0) * (0.25 + 0.065 * v.MB);  // backward: two K sweeps (E, O)
+    if (!best || t < best_t) {
+      best = &v;
+      best_t = t;
+      best_groups = groups;
+    }
+  }
   XformPArgs pa;
   pa.x = a;
-  pa.x.Af = inverse ? b->dTpf.p : b->dTpb.p;
-  pa.x.P = inverse ? b->xp_Pf : b->xp_Pb;
+  pa.x.Af = best->img.p;
+  pa.x.P = best->P;
   pa.h = b->xp_h;
   pa.ks = b->xp_ks;
   for (int p = 0; p < 2; ++p) {
@@ -205,32 +254,13 @@ void launch_xformp(smpm_batch* b, const XformArgs& a, bool inverse, cudaStream_t
     pa.seg_start[p][1] = b->xp_seg_start[p][1];
     pa.seg_len0[p] = b->xp_seg_len0[p];
   }
-  const long long nch = (static_cast<long long>(a.nslots) * a.ncol_sys * a.nv + 15) / 16;
-  const int groups = static_cast<int>(std::max(1LL, std::min<long long>(b->ctx->num_sms / pa.x.P, nch)));
-  const dim3 grid(groups * pa.x.P), blk(XF_THREADS);
-  const size_t smem = inverse ? b->xp_smem_f : b->xp_smem_b;
-  auto go = [&](auto kern) {
-    if (pdl) {
-      launch_pdl(b, kern, grid, blk, smem, st, pa);
-    } else {
-      kern<<<grid, blk, smem, st>>>(pa);
-      check_launch(b);
-    }
-  };
-  if (inverse) {
-    switch (b->xp_MBf) {
-      case 11: go(xformp_kernel<11, 6, false>); break;
-      case 17: go(xformp_kernel<17, 5, false>); break;
-      case 26: go(xformp_kernel<26, 4, false>); break;
-      default: go(xformp_kernel<34, 3, false>); break;
-    }
+  const XpKernel& kk = xp_kernel_for(!inverse, best->MB);
+  const dim3 grid(best_groups * best->P), blk(XF_THREADS);
+  if (pdl) {
+    launch_pdl(b, kk.fn, grid, blk, kk.smem, st, pa);
   } else {
-    switch (b->xp_MBb) {
-      case 9: go(xformp_kernel<9, 8, true>); break;
-      case 11: go(xformp_kernel<11, 8, true>); break;
-      case 13: go(xformp_kernel<13, 8, true>); break;
-      default: go(xformp_kernel<17, 7, true>); break;
-    }
+    kk.fn<<<grid, blk, kk.smem, st>>>(pa);
+    check_launch(b);
   }
 }
 
@@ -304,16 +334,28 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
   P.acount = lv.acount;
   double* zp = cout ? b->dzpart.p : nullptr;
   if (b->tune.spec_v2) {
-    // pipelined pass (spec_op2_kernel): segments as long as ~32 warps per SM
-    // still allow (shorter halo), at least 4 and at most 16 blocks
+    // pipelined pass: segments as long as ~32 warps per SM still allow (shorter halo), at
+    // least 4 and at most 16 blocks.  spec_v2 = 2 (default): spec_op3_kernel, 16 bytes per
+    // lane for every mode (a pair, or two real modes); 1: spec_op2_kernel, one mode per lane
+    const bool v3 = b->tune.spec_v2 >= 2;
+    const int nch = v3 ? spec3_chunks(sp.npairs, sp.nmode) : sp.nmc;
     const long long nbk = b->nbf + (b->single ? 1 : 0);
-    const long long warps = nbk * sp.nmc * lv.nslots;
+    const long long warps = nbk * nch * lv.nslots;
     int segb = static_cast<int>(std::max(4LL, std::min(16LL, warps / (32LL * b->ctx->num_sms))));
     if (b->tune.segb > 0) segb = b->tune.segb;
     sp.segb = segb;
     sp.nseg = static_cast<int>((nbk + segb - 1) / segb);
-    const dim3 grid2(sp.nmc * ((sp.nseg + SP_WARPS - 1) / SP_WARPS), lv.nslots);
+    const dim3 grid2(nch * ((sp.nseg + SP_WARPS - 1) / SP_WARPS), lv.nslots);
     const size_t shm2 = cout ? sizeof(double) * 2 * static_cast<size_t>(b->d) : 0;
+    if (v3) {
+      if (bj)
+        launch_pdl(b, spec_op3_kernel<true>, grid2, dim3(SP_THREADS), shm2, st, sp, vh, th, P, zp, b->dcount.p, cout,
+                   uh);
+      else
+        launch_pdl(b, spec_op3_kernel<false>, grid2, dim3(SP_THREADS), shm2, st, sp, vh, th, P, zp, b->dcount.p, cout,
+                   uh);
+      return;
+    }
     if (bj)
       launch_pdl(b, spec_op2_kernel<true>, grid2, dim3(SP_THREADS), shm2, st, sp, vh, th, P, zp, b->dcount.p, cout, uh);
     else

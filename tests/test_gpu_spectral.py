@@ -149,3 +149,32 @@ def test_parity_split_transforms(ctx, n, m_z):
             a, c = a - a.mean(), c - c.mean()
         assert np.linalg.norm(a - c) <= 2e-8 * np.linalg.norm(a), i
     assert max(abs(a - c) for a, c in zip(it0, it2)) <= 1
+
+
+@pytest.mark.parametrize("method", ["dbj", "2las", "bj"])
+def test_per_mode_pass_variants_agree(ctx, method):
+    """The three per-mode pass kernels — spec_op3 (16 bytes per lane: a pair or two
+    real modes, default), spec_op2 (one mode per lane), spec_op (staged) — run the
+    same per-mode arithmetic: same iteration counts, solutions to rounding; each
+    also holds the oracle's bars (check_solve on the default)."""
+    import torch
+
+    mus = [(2 * np.pi * j / 6.0) ** 2 for j in range(20)]
+    case = build_case(9, 7, 4, 7.0, 1.0, mus, kmax=4, decay=True)
+    assert _pairs(case) > 0
+    b = gpu_batch(ctx, case, spectral=True)
+    b.tune(grid=0)
+    check_solve(case, b, method, max_iter=100)
+    rhs = torch.tensor(case.b_S, device="cuda")
+    out = {}
+    for v in (2, 1, 0):
+        b.tune(spec_v2=v)
+        r = b.solve(rhs, method, 1e-10, 100, 0)
+        out[v] = (list(r.iterations), r.x_S.cpu().numpy())
+    for v in (1, 0):
+        assert max(abs(a - c) for a, c in zip(out[2][0], out[v][0])) <= 1, v
+        for i in range(len(mus)):
+            a, c = out[2][1][i], out[v][1][i]
+            if mus[i] == 0.0:
+                a, c = a - a.mean(), c - c.mean()
+            assert np.linalg.norm(a - c) <= 1e-8 * np.linalg.norm(a), (v, i)
