@@ -33,6 +33,7 @@
 #include "xform.cuh"
 #include "xformk.cuh"
 #include "xformp.cuh"
+#include "xformq.cuh"
 #include "strip.cuh"
 #include "fourier.cuh"
 
@@ -248,6 +249,8 @@ struct smpm_ctx {
 struct Tuning {
   int segb = 0;          // per-mode pass: blocks per warp item (0: SP_SEGB)
   int xform = 1;         // resident-slice transform kernel (xform.cuh) where it applies
+  int xform_ws = 2;      // parity transforms: 0 CTA barrier per stage (xformp.cuh); 2 / 3 producer warp + mbarrier ring
+                         // with that many consumer warpgroups (xformq.cuh; 2 measured best)
   int xform_parity = 1;  // parity-split transforms (xformp.cuh) when T is parity-pure: 0 off, 1 where the
                          // K-streamed kernel would run (w > 176), 2 wherever w % 16 == 0
   int sp_stage = 1;      // per-mode pass stages slot rows in shared memory (spec_v2 = 0)
@@ -336,7 +339,7 @@ struct smpm_batch {
   bool pending = false;  // deferred CGS2: the newest basis vector is still the pending pair (w', h2) (vec4.cuh)
   bool p1bt_attr = false;
   long long p1b_res = 0, p1bt_res[V2_MAXCOL + 1] = {};  // resident CTAs of the pass 1B kernels
-  long long p2l_res = 0, p1bl_res = 0;                  // ... of the lane-shared-row kernels
+  long long p2l_res[2] = {0, 0}, p1bl_res[2] = {0, 0};  // ... of the lane-shared-row kernels ([1]: > 64 columns)
   bool pythag = true;  // norm from the second CGS2 reduction (cgs3_pass2n / cgs3_pass3s); tuning pythag
   bool pdl = true;  // programmatic dependent launch for the Arnoldi step chain (tuning pdl)
   size_t xf_smem = 0;

@@ -652,7 +652,7 @@ int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
       t.tail_rows = value;
       return;
     }
-    const Knob knobs[] = {{"segb", &t.segb}, {"spec_v2", &t.spec_v2}, {"xform", &t.xform}, {"xform_parity", &t.xform_parity},
+    const Knob knobs[] = {{"segb", &t.segb}, {"spec_v2", &t.spec_v2}, {"xform", &t.xform}, {"xform_parity", &t.xform_parity}, {"xform_ws", &t.xform_ws},
                           {"sp_stage", &t.sp_stage},
                           {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse}, {"cgs_defer", &t.cgs_defer}, {"cgs_lanes", &t.cgs_lanes},
                           {"gt_vblock", &t.gt_vblock}, {"grid_per_sm", &t.grid_per_sm}, {"gt_ctas", &t.gt_ctas},

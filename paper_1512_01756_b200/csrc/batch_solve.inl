@@ -175,15 +175,16 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
           launch_pdl(b, cgs4_pass1b_kernel, gb, dim3(V3_THREADS), 0, st, Gb, V, wv, tdefl, 1, P,
                      static_cast<const double*>(cbuf));
         } else if (b->tune.cgs_lanes) {
-          if (b->p1bl_res == 0) {
+          const int wide = nold > 64 ? 1 : 0;
+          auto kern = wide ? cgs5_pass1bl_kernel<true> : cgs5_pass1bl_kernel<false>;
+          if (b->p1bl_res[wide] == 0) {
             int o = 0;
-            CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs5_pass1bl_kernel, V3_THREADS, 0));
-            b->p1bl_res = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
+            CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, V3_THREADS, 0));
+            b->p1bl_res[wide] = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
           }
           dim3 gb;
-          const GmState_ Gb = chunked(b->p1bl_res, gb);
-          launch_pdl(b, cgs5_pass1bl_kernel, gb, dim3(V3_THREADS), 0, st, Gb, V, wv, tdefl, 1, P,
-                     static_cast<const double*>(cbuf));
+          const GmState_ Gb = chunked(b->p1bl_res[wide], gb);
+          launch_pdl(b, kern, gb, dim3(V3_THREADS), 0, st, Gb, V, wv, tdefl, 1, P, static_cast<const double*>(cbuf));
         } else {
           const size_t smem = sizeof(double) * p1bt_smem_doubles(nold);
           if (!b->p1bt_attr) {
@@ -209,14 +210,16 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
       if (b->tune.p2fuse && b->tune.cgs_lanes && ncols_h > 2 * V3_GRP && ncols_h <= LN_MAXCOL &&
           ncols_h <= G.m + 1) {
         // more than 16 columns: update and dots in one read of V, eight lanes per row (cgs5_pass2l_kernel)
-        if (b->p2l_res == 0) {
+        const int wide = ncols_h > 64 ? 1 : 0;
+        auto kern = wide ? cgs5_pass2l_kernel<true> : cgs5_pass2l_kernel<false>;
+        if (b->p2l_res[wide] == 0) {
           int o = 0;
-          CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, cgs5_pass2l_kernel, V3_THREADS, 0));
-          b->p2l_res = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
+          CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, V3_THREADS, 0));
+          b->p2l_res[wide] = static_cast<long long>(std::max(1, o)) * b->ctx->num_sms;
         }
         dim3 g2l;
-        const GmState_ G2l = chunked(b->p2l_res, g2l);
-        launch_pdl(b, cgs5_pass2l_kernel, g2l, dim3(V3_THREADS), 0, st, G2l, static_cast<const double*>(V), wv);
+        const GmState_ G2l = chunked(b->p2l_res[wide], g2l);
+        launch_pdl(b, kern, g2l, dim3(V3_THREADS), 0, st, G2l, static_cast<const double*>(V), wv);
       } else if (b->tune.p2fuse && ncols_h > 2 * V3_GRP && ncols_h <= 8 * P2T_MAXC && ncols_h <= G.m + 1) {
         // more than 16 columns: update and dots in one read of V through
         // shared-memory row tiles (cgs3_pass2t_kernel)
@@ -681,9 +684,11 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   int* lflag = ecount + 1;
   int* llist = lflag + ns;
   int* lcount = llist + ns;
-  auto launch_tail = [&](int nrun) {
-    const bool early = early_ok && !early_done && nrun < ns;
-    if (early) {
+  // (per-stage path without a tail, e.g. C5: the same early epilogue once at most an eighth of
+  // the systems is still running; the slow low-wavenumber modes then iterate for tens of steps
+  // while the finished rows travel)
+  auto do_early = [&](int nslots_bound) {
+    {
       if (!b->st2) {
         int lo = 0, hi = 0;
         CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -697,7 +702,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       Live le;
       le.alist = elist;
       le.acount = ecount;
-      le.nslots = ns - nrun;
+      le.nslots = nslots_bound;
       le.active = eflag;
       epilogue_dbj(le, eflag, st);
       CUDA_CHECK(cudaEventRecord(b->eev[1], st));
@@ -707,6 +712,9 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
       CUDA_CHECK(cudaEventRecord(b->eev[2], b->st2));
       early_done = true;
     }
+  };
+  auto launch_tail = [&](int nrun) {
+    if (early_ok && !early_done && nrun < ns) do_early(ns - nrun);
     flush_pending(b, nrun, st);  // the tail starts from a materialised v_j
     return arnoldi_grid(b, c, alist, acount, st);
   };
@@ -748,6 +756,10 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     CUDA_CHECK(cudaEventSynchronize(ev[cur]));
     const int nrun = hcnt[2 * cur], ncyc = hcnt[2 * cur + 1];
     bound = std::min(bound, nrun);
+    // no tail ahead: early epilogue of the systems that have stopped (a later step may be in
+    // flight, so the early list is bounded by all systems)
+    if (early_ok && !early_done && !(use_grid && grid_max > 0) && c.restart == 0 && nrun > 0 && 8 * nrun <= ns)
+      do_early(ns);
     cur ^= 1;
     if (nrun > 0 && more) continue;
     if (more) CUDA_CHECK(cudaEventSynchronize(ev[cur]));  // drain the speculative step

@@ -122,10 +122,13 @@ struct XpKernel {
   int MB;
   void (*fn)(XformPArgs);
   size_t smem;
+  void (*fn_ws[2])(XformPArgs);  // warp-specialised variants (xformq.cuh): 2 or 3 consumer warpgroups
+  size_t smem_ws;
 };
 template <int MB, int NS, bool BWD>
 XpKernel xp_instance() {
-  return XpKernel{MB, xformp_kernel<MB, NS, BWD>, xformp_smem<MB, NS, BWD>()};
+  return XpKernel{MB, xformp_kernel<MB, NS, BWD>, xformp_smem<MB, NS, BWD>(),
+                  {xformq_kernel<MB, NS, BWD, 2>, xformq_kernel<MB, NS, BWD, 3>}, xformq_smem<MB, NS, BWD>()};
 }
 const XpKernel* xp_kernels(bool bwd, int& count) {
   static const XpKernel fwd[] = {xp_instance<9, 6, false>(), xp_instance<11, 6, false>(), xp_instance<17, 5, false>(),
@@ -170,6 +173,8 @@ void setup_xformp(smpm_batch* b) {
       if (P > b->ctx->num_sms) continue;
       const XpKernel& kk = xp_kernel_for(bwd, MB);
       CUDA_CHECK(cudaFuncSetAttribute(kk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kk.smem)));
+      for (auto fw : kk.fn_ws)
+        CUDA_CHECK(cudaFuncSetAttribute(fw, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kk.smem_ws)));
       b->xp_var[dir].push_back(std::make_unique<smpm_batch::XpVariant>());
       smpm_batch::XpVariant& v = *b->xp_var[dir].back();
       v.P = P;
@@ -255,11 +260,17 @@ void launch_xformp(smpm_batch* b, const XformArgs& a, bool inverse, cudaStream_t
     pa.seg_len0[p] = b->xp_seg_len0[p];
   }
   const XpKernel& kk = xp_kernel_for(!inverse, best->MB);
-  const dim3 grid(best_groups * best->P), blk(XF_THREADS);
+  // xform_ws: 0 CTA barrier per stage (xformp.cuh), 2 / 3: producer warp + that many consumer
+  // warpgroups (xformq.cuh); slices of fewer than 3 m-blocks keep two
+  const int nw = b->tune.xform_ws >= 3 && best->MB >= 3 ? 3 : 2;
+  const bool ws = b->tune.xform_ws != 0;
+  const dim3 grid(best_groups * best->P), blk(ws ? 128 * nw + 128 : XF_THREADS);
+  auto fn = ws ? kk.fn_ws[nw - 2] : kk.fn;
+  const size_t smem = ws ? kk.smem_ws : kk.smem;
   if (pdl) {
-    launch_pdl(b, kk.fn, grid, blk, kk.smem, st, pa);
+    launch_pdl(b, fn, grid, blk, smem, st, pa);
   } else {
-    kk.fn<<<grid, blk, kk.smem, st>>>(pa);
+    fn<<<grid, blk, smem, st>>>(pa);
     check_launch(b);
   }
 }

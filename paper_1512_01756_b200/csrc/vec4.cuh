@@ -442,7 +442,7 @@ __device__ __forceinline__ void lanes_reduce(double (&acc)[CPT], double sq, int 
   }
 }
 
-template <bool P1B, class XS>
+template <bool P1B, bool WIDE, class XS>
 __device__ __forceinline__ void lanes_dispatch(const double* __restrict__ Vs, long long k, int ncols, const double* hsm,
                                                double* ws, const double* __restrict__ ts, XS xs, double inv, double* col,
                                                int r0, int r1, double* part, double* red) {
@@ -454,27 +454,36 @@ __device__ __forceinline__ void lanes_dispatch(const double* __restrict__ Vs, lo
     const double sq = lanes_rows<G, CPT, NR, P1B>(Vs, k, ncols, hsm, ws, ts, xs, inv, col, r0, r1, acc);
     lanes_reduce<G, CPT>(acc, sq, ncols, part, red);
   };
-  // G lanes x CPT columns >= ncols; CPT x NR ~ 12-16 independent 16-byte loads per
-  // thread in flight (2 CTAs/SM: 100-130 KB per SM)
+  // G lanes x CPT columns >= ncols; CPT x NR independent 16-byte loads per thread in flight.
+  // Up to 64 columns (WIDE = false): 2 CTAs per SM at 128 registers, 12-16 loads per thread
+  // (100-130 KB per SM).  Beyond (WIDE = true): eight lanes per row pair leave only 64 rows per
+  // CTA iteration at NR = 1, and each iteration costs a full memory latency (2.6 TB/s measured
+  // with the few systems that run this deep); one CTA per SM at up to 255 registers holds NR = 2-3
+  // row groups (28-36 loads per thread, 115-150 KB per SM in flight, half to a third of the iterations)
   using std::integral_constant;
 #define SMPM_LANES_CASE(LIM, G_, CPT_, NR_)                                                            \
   if (ncols <= LIM) {                                                                                  \
     run(integral_constant<int, G_>{}, integral_constant<int, CPT_>{}, integral_constant<int, NR_>{}); \
     return;                                                                                            \
   }
-  SMPM_LANES_CASE(24, 4, 6, 2)
-  SMPM_LANES_CASE(32, 4, 8, 2)
-  SMPM_LANES_CASE(48, 4, 12, 1)
-  SMPM_LANES_CASE(64, 4, 16, 1)
-  SMPM_LANES_CASE(80, 8, 10, 1)
-  SMPM_LANES_CASE(96, 8, 12, 1)
-  SMPM_LANES_CASE(112, 8, 14, 1)
-  SMPM_LANES_CASE(128, 8, 16, 1)
+  if (!WIDE) {
+    SMPM_LANES_CASE(24, 4, 6, 2)
+    SMPM_LANES_CASE(32, 4, 8, 2)
+    SMPM_LANES_CASE(48, 4, 12, 1)
+    SMPM_LANES_CASE(64, 4, 16, 1)
+  } else {
+    SMPM_LANES_CASE(80, 8, 10, 3)
+    SMPM_LANES_CASE(96, 8, 12, (P1B ? 2 : 3))
+    SMPM_LANES_CASE(112, 8, 14, 2)
+    SMPM_LANES_CASE(128, 8, 16, 2)
+  }
 #undef SMPM_LANES_CASE
 }
 
 // pass 2' for 16 < ncols <= 128 (w -= V h1; h2 = V^T w; ||w||^2; Givens in the last CTA)
-__global__ void __launch_bounds__(V3_THREADS, 2) cgs5_pass2l_kernel(GmState_ G, const double* __restrict__ V, double* w) {
+template <bool WIDE>
+__global__ void __launch_bounds__(V3_THREADS, WIDE ? 1 : 2) cgs5_pass2l_kernel(GmState_ G, const double* __restrict__ V,
+                                                                              double* w) {
   pdl_wait();
   __shared__ double hs[V2_MAXCOL];
   __shared__ double red[(V3_THREADS / 32) * LN_RED];
@@ -492,7 +501,7 @@ __global__ void __launch_bounds__(V3_THREADS, 2) cgs5_pass2l_kernel(GmState_ G, 
   const double* Vs = V + s * G.vstride;
   double* ws = w + s * G.k;
   double* part = G.part + (static_cast<long long>(s) * G.nchunk + ch) * stride;
-  lanes_dispatch<false>(Vs, G.k, ncols, hs, ws, nullptr, XVal{}, 1.0, nullptr, r0, r1, part, red);
+  lanes_dispatch<false, WIDE>(Vs, G.k, ncols, hs, ws, nullptr, XVal{}, 1.0, nullptr, r0, r1, part, red);
   pdl_launch();  // the row work is done: dependents may start launching
   if (!last_cta(G.counter + s, G.nchunk)) return;
   double* h2 = G.h2 + static_cast<long long>(s) * stride;
@@ -510,7 +519,8 @@ __global__ void __launch_bounds__(V3_THREADS, 2) cgs5_pass2l_kernel(GmState_ G, 
 }
 
 // pass 1B for 16 < old columns <= 128
-__global__ void __launch_bounds__(V3_THREADS, 2) cgs5_pass1bl_kernel(GmState_ G, double* __restrict__ V, double* w,
+template <bool WIDE>
+__global__ void __launch_bounds__(V3_THREADS, WIDE ? 1 : 2) cgs5_pass1bl_kernel(GmState_ G, double* __restrict__ V, double* w,
                                                                      const double* __restrict__ t, int defl,
                                                                      DeflateParams P, const double* __restrict__ cbuf) {
   pdl_wait();
@@ -536,9 +546,9 @@ __global__ void __launch_bounds__(V3_THREADS, 2) cgs5_pass1bl_kernel(GmState_ G,
     const int wd = P.w, w2 = 2 * wd;
     const double* rs = P.rowsum + static_cast<long long>(s) * 6 * wd;
     const XDeflVal xd{cbuf + static_cast<long long>(s) * P.d, rs, rs + w2, rs + 2 * w2, rs + 2 * w2 + wd, wd, P.mx};
-    lanes_dispatch<true>(Vs, G.k, nold, hs, ws, ts, xd, inv, col, r0, r1, part, red);
+    lanes_dispatch<true, WIDE>(Vs, G.k, nold, hs, ws, ts, xd, inv, col, r0, r1, part, red);
   } else {
-    lanes_dispatch<true>(Vs, G.k, nold, hs, ws, ts, XVal{}, inv, col, r0, r1, part, red);
+    lanes_dispatch<true, WIDE>(Vs, G.k, nold, hs, ws, ts, XVal{}, inv, col, r0, r1, part, red);
   }
   pdl_launch();  // the row work is done: dependents may start launching
   if (last_cta(G.counter + s, G.nchunk))
