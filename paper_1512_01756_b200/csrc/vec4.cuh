@@ -472,10 +472,17 @@ __device__ __forceinline__ void lanes_dispatch(const double* __restrict__ Vs, lo
     SMPM_LANES_CASE(48, 4, 12, 1)
     SMPM_LANES_CASE(64, 4, 16, 1)
   } else {
+#ifdef SMPM_WIDE_G8
     SMPM_LANES_CASE(80, 8, 10, 3)
     SMPM_LANES_CASE(96, 8, 12, (P1B ? 2 : 3))
     SMPM_LANES_CASE(112, 8, 14, 2)
     SMPM_LANES_CASE(128, 8, 16, 2)
+#else
+    SMPM_LANES_CASE(80, 4, 20, 1)
+    SMPM_LANES_CASE(96, 4, 24, 1)
+    SMPM_LANES_CASE(112, 4, 28, 1)
+    SMPM_LANES_CASE(128, 4, 32, 1)
+#endif
   }
 #undef SMPM_LANES_CASE
 }
