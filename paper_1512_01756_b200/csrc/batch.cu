@@ -251,6 +251,7 @@ struct Tuning {
   int xform = 1;         // resident-slice transform kernel (xform.cuh) where it applies
   int xform_ws = 2;      // parity transforms: 0 CTA barrier per stage (xformp.cuh); 2 / 3 producer warp + mbarrier ring
                          // with that many consumer warpgroups (xformq.cuh; 2 measured best)
+  int xform_ares = 1;    // parity transforms keep the slice's matrix resident in shared memory when it fits (small w)
   int xform_parity = 1;  // parity-split transforms (xformp.cuh) when T is parity-pure: 0 off, 1 where the
                          // K-streamed kernel would run (w > 176), 2 wherever w % 16 == 0
   int sp_stage = 1;      // per-mode pass stages slot rows in shared memory (spec_v2 = 0)
@@ -319,6 +320,7 @@ struct smpm_batch {
   // for launches with few columns (the slow-mode tail), so every SM still gets a full 64-column chunk
   struct XpVariant {
     int P = 0, MB = 0;  // row slices (forward: both parities), m-blocks per slice
+    size_t ares_smem = 0;  // > 0: the slice's matrix fits in shared memory next to a ring of column slabs
     DevArray<double> img;
   };
   std::vector<std::unique_ptr<XpVariant>> xp_var[2];

@@ -652,7 +652,7 @@ int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
       t.tail_rows = value;
       return;
     }
-    const Knob knobs[] = {{"segb", &t.segb}, {"spec_v2", &t.spec_v2}, {"xform", &t.xform}, {"xform_parity", &t.xform_parity}, {"xform_ws", &t.xform_ws},
+    const Knob knobs[] = {{"segb", &t.segb}, {"spec_v2", &t.spec_v2}, {"xform", &t.xform}, {"xform_parity", &t.xform_parity}, {"xform_ws", &t.xform_ws}, {"xform_ares", &t.xform_ares},
                           {"sp_stage", &t.sp_stage},
                           {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse}, {"cgs_defer", &t.cgs_defer}, {"cgs_lanes", &t.cgs_lanes},
                           {"gt_vblock", &t.gt_vblock}, {"grid_per_sm", &t.grid_per_sm}, {"gt_ctas", &t.gt_ctas},
@@ -664,7 +664,7 @@ int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
         *kb.field = v;
         // grid geometry and transform plans depend on some knobs: recompute lazily
         if (k == "gt_vblock" || k == "grid_per_sm" || k == "gt_ctas") b->gt_blocks = 0;
-        if ((k == "xform" || k == "xform_parity") && b->finalized && b->spectral) setup_xform(b);
+        if ((k == "xform" || k == "xform_parity" || k == "xform_ares") && b->finalized && b->spectral) setup_xform(b);
         return;
       }
     fail(SMPM_EINVAL, "unknown tuning key '" + k + "'");

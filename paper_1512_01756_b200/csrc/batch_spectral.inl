@@ -124,11 +124,16 @@ struct XpKernel {
   size_t smem;
   void (*fn_ws[2])(XformPArgs);  // warp-specialised variants (xformq.cuh): 2 or 3 consumer warpgroups
   size_t smem_ws;
+  void (*fn_ares)(XformPArgs);   // ... with the slice's matrix resident in shared memory (small w)
+  size_t (*smem_ares)(int nstage);
 };
 template <int MB, int NS, bool BWD>
 XpKernel xp_instance() {
+  // resident-matrix variant: the ring carries column slabs only (forward 24.6 KB, backward 12.3 KB a stage)
+  constexpr int NSA = BWD ? 6 : 4;
   return XpKernel{MB, xformp_kernel<MB, NS, BWD>, xformp_smem<MB, NS, BWD>(),
-                  {xformq_kernel<MB, NS, BWD, 2>, xformq_kernel<MB, NS, BWD, 3>}, xformq_smem<MB, NS, BWD>()};
+                  {xformq_kernel<MB, NS, BWD, 2>, xformq_kernel<MB, NS, BWD, 3>}, xformq_smem<MB, NS, BWD>(),
+                  xformq_kernel<MB, NSA, BWD, 2, true>, xformq_ares_smem<MB, NSA, BWD>};
 }
 const XpKernel* xp_kernels(bool bwd, int& count) {
   static const XpKernel fwd[] = {xp_instance<9, 6, false>(), xp_instance<11, 6, false>(), xp_instance<17, 5, false>(),
@@ -175,10 +180,17 @@ void setup_xformp(smpm_batch* b) {
       CUDA_CHECK(cudaFuncSetAttribute(kk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kk.smem)));
       for (auto fw : kk.fn_ws)
         CUDA_CHECK(cudaFuncSetAttribute(fw, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kk.smem_ws)));
+      const size_t sa = kk.smem_ares(bwd ? 2 * ks : ks);
+      const bool ares = sa <= 232448 && b->tune.xform_ares;
       b->xp_var[dir].push_back(std::make_unique<smpm_batch::XpVariant>());
       smpm_batch::XpVariant& v = *b->xp_var[dir].back();
       v.P = P;
       v.MB = MB;
+      v.ares_smem = 0;
+      if (ares) {
+        CUDA_CHECK(cudaFuncSetAttribute(kk.fn_ares, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sa)));
+        v.ares_smem = sa;
+      }
       if (!bwd)
         xformp_image(2 * S, ks, MB, [&](int sl, int r, int kk2) {
           const int par = sl / S, kap = (sl % S) * 8 * MB + r;
@@ -241,7 +253,8 @@ void launch_xformp(smpm_batch* b, const XformArgs& a, bool inverse, cudaStream_t
     const long long full = share / XF_NT, rem = share % XF_NT;
     // a trailing chunk of <= 32 columns runs one n-block per warp: half the MMA work
     const double chunks = static_cast<double>(full) + (rem == 0 ? 0.0 : rem <= 32 ? 0.6 : 1.0);
-    const double t = chunks * (inverse ? 1.0 : 2.0) * (0.25 + 0.065 * v.MB);  // backward: two K sweeps (E, O)
+    // backward: two K sweeps (E, O); resident matrix: no A slab traffic per stage
+    const double t = chunks * (inverse ? 1.0 : 2.0) * ((v.ares_smem ? 0.15 : 0.25) + 0.065 * v.MB);
     if (!best || t < best_t) {
       best = &v;
       best_t = t;
@@ -264,9 +277,10 @@ void launch_xformp(smpm_batch* b, const XformArgs& a, bool inverse, cudaStream_t
   // warpgroups (xformq.cuh); slices of fewer than 3 m-blocks keep two
   const int nw = b->tune.xform_ws >= 3 && best->MB >= 3 ? 3 : 2;
   const bool ws = b->tune.xform_ws != 0;
-  const dim3 grid(best_groups * best->P), blk(ws ? 128 * nw + 128 : XF_THREADS);
-  auto fn = ws ? kk.fn_ws[nw - 2] : kk.fn;
-  const size_t smem = ws ? kk.smem_ws : kk.smem;
+  const bool ares = ws && best->ares_smem != 0;
+  const dim3 grid(best_groups * best->P), blk(ares ? 384 : ws ? 128 * nw + 128 : XF_THREADS);
+  auto fn = ares ? kk.fn_ares : ws ? kk.fn_ws[nw - 2] : kk.fn;
+  const size_t smem = ares ? best->ares_smem : ws ? kk.smem_ws : kk.smem;
   if (pdl) {
     launch_pdl(b, fn, grid, blk, smem, st, pa);
   } else {

@@ -27,7 +27,7 @@ __device__ __forceinline__ void cp_async_arrive_noinc(unsigned long long* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int MB, int NS, bool BWD>
+template <int MB, int NS, bool BWD, bool ARES>
 __device__ __forceinline__ void xq_producer(const XformPArgs& pa, double* ring, unsigned long long* full,
                                             unsigned long long* empty, int c0, int c1, int cps, const double* Aslice) {
   const XformArgs& a = pa.x;
@@ -38,7 +38,8 @@ __device__ __forceinline__ void xq_producer(const XformPArgs& pa, double* ring, 
   const int nst = nch * KS;
   constexpr int ASTAGE = xk_astage(MB);
   constexpr int BSTAGE = BWD ? XK_BSTAGE : 2 * XK_BSTAGE;
-  constexpr int STAGE = ASTAGE + BSTAGE;
+  constexpr int AOFF = ARES ? 0 : ASTAGE;  // resident A: the ring holds the column slabs only
+  constexpr int STAGE = AOFF + BSTAGE;
   constexpr unsigned ABYTES = static_cast<unsigned>(ASTAGE * sizeof(double));
   const double* col[2] = {nullptr, nullptr};  // this lane's columns lane, lane + 32 of the chunk
   for (int sidx = 0; sidx < nst; ++sidx) {
@@ -50,13 +51,13 @@ __device__ __forceinline__ void xq_producer(const XformPArgs& pa, double* ring, 
     }
     if (use > 0) mbar_wait(empty + slot, static_cast<unsigned>((use - 1) & 1));
     double* st = ring + static_cast<size_t>(slot) * STAGE;
-    if (lane == 0) {
+    if (!ARES && lane == 0) {
       mbar_expect_tx(full + slot, ABYTES);
       bulk_g2s(st, Aslice + static_cast<size_t>(kq) * ASTAGE, ABYTES, full + slot);
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      double* dst = st + ASTAGE + (lane + 32 * u) * XK_BSTR;
+      double* dst = st + AOFF + (lane + 32 * u) * XK_BSTR;
       const bool ok = col[u] != nullptr;
       const double* src = ok ? col[u] : a.in[0];
       if constexpr (BWD) {
@@ -83,9 +84,10 @@ __device__ __forceinline__ void xq_producer(const XformPArgs& pa, double* ring, 
   }
 }
 
-template <int MB, int NMB, int NS, bool BWD>
+template <int MB, int NMB, int NS, bool BWD, bool ARES>
 __device__ __forceinline__ void xq_consumer(const XformPArgs& pa, const double* ring, unsigned long long* full,
-                                            unsigned long long* empty, int c0, int c1, int slice, int mb0, int cps) {
+                                            unsigned long long* empty, int c0, int c1, int slice, int mb0, int cps,
+                                            const double* Ares) {
   const XformArgs& a = pa.x;
   const int t = threadIdx.x, lane = t & 31, nb = (t >> 5) & 3;
   const int w = a.w, h = pa.h;
@@ -94,7 +96,8 @@ __device__ __forceinline__ void xq_consumer(const XformPArgs& pa, const double* 
   const int nst = nch * KS;
   constexpr int ASTAGE = xk_astage(MB);
   constexpr int BSTAGE = BWD ? XK_BSTAGE : 2 * XK_BSTAGE;
-  constexpr int STAGE = ASTAGE + BSTAGE;
+  constexpr int AOFF = ARES ? 0 : ASTAGE;
+  constexpr int STAGE = AOFF + BSTAGE;
   const int Ps = BWD ? a.P : a.P / 2;
   const int par = BWD ? 0 : slice / Ps;
   const int row0 = (BWD ? slice : slice % Ps) * 8 * MB;
@@ -118,8 +121,8 @@ __device__ __forceinline__ void xq_consumer(const XformPArgs& pa, const double* 
     }
     mbar_wait(full + slot, static_cast<unsigned>(use & 1));
     const double* st = ring + static_cast<size_t>(slot) * STAGE;
-    const double* Ap = st + (mb0 * 32 + lane) * 2;
-    const double* Bp = st + ASTAGE + (nb * 8 + (lane >> 2)) * XK_BSTR + 2 * (lane & 3);
+    const double* Ap = (ARES ? Ares + static_cast<size_t>(kq) * ASTAGE : st) + (mb0 * 32 + lane) * 2;
+    const double* Bp = st + AOFF + (nb * 8 + (lane >> 2)) * XK_BSTR + 2 * (lane & 3);
     const bool wide = cb + 32 < c1;
     if constexpr (BWD) {
       if (kq < pa.ks) {
@@ -134,7 +137,7 @@ __device__ __forceinline__ void xq_consumer(const XformPArgs& pa, const double* 
           xf_stage<MB, NMB, 1, 2>(Ap, Bp, XK_BSTR, 0, 2, acc[NSET - 1]);
       }
     } else {
-      const double* Bh = st + ASTAGE + XK_BSTAGE + (nb * 8 + (lane >> 2)) * XK_BSTR + 14 - 2 * (lane & 3);
+      const double* Bh = st + AOFF + XK_BSTAGE + (nb * 8 + (lane >> 2)) * XK_BSTR + 14 - 2 * (lane & 3);
       if (wide)
         xp_stage_fwd<MB, NMB, 2>(Ap, Bp, Bh, sg, acc[0]);
       else
@@ -172,12 +175,14 @@ __device__ __forceinline__ void xq_consumer(const XformPArgs& pa, const double* 
 // NW consumer warpgroups split the slice's m-blocks NW ways (warp (s, hh): n-blocks s, s + 4, part hh):
 // NW = 3 puts three DMMA-issuing warps on every scheduler, so one warp's fragment loads hide under
 // the other two's MMAs (two left the fp64 tensor pipe idle 30 % of the time)
-template <int MB, int NS, bool BWD, int NW>
+// ARES: the slice's whole matrix image (all K stages) is resident in shared memory after the ring
+// (small w: C4's 176 x 88 per direction fits), the ring then carries the column slabs only
+template <int MB, int NS, bool BWD, int NW, bool ARES = false>
 __global__ void __launch_bounds__(128 * NW + 128, 1) xformq_kernel(XformPArgs pa) {
   pdl_wait();
   extern __shared__ __align__(128) double xq_smem[];
   const XformArgs& a = pa.x;
-  constexpr int STAGE = xk_astage(MB) + (BWD ? XK_BSTAGE : 2 * XK_BSTAGE);
+  constexpr int STAGE = (ARES ? 0 : xk_astage(MB)) + (BWD ? XK_BSTAGE : 2 * XK_BSTAGE);
   constexpr int NCW = 4 * NW;  // consumer warps
   double* ring = xq_smem;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(xq_smem + static_cast<size_t>(NS) * STAGE);
@@ -192,35 +197,43 @@ __global__ void __launch_bounds__(128 * NW + 128, 1) xformq_kernel(XformPArgs pa
   if (c0 >= c1) return;
   if (t == 0) {
     for (int s = 0; s < NS; ++s) {
-      mbar_init(full + s, 33);  // 32 cp.async arrivals of the producer lanes + the bulk copy's expect_tx arrival
+      // 32 cp.async arrivals of the producer lanes (+ the bulk copy's expect_tx arrival)
+      mbar_init(full + s, ARES ? 32 : 33);
       mbar_init(empty + s, NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
   const int nstage = BWD ? 2 * pa.ks : pa.ks;
   const double* Aslice = a.Af + static_cast<size_t>(slice) * nstage * xk_astage(MB);
+  double* Ares = reinterpret_cast<double*>(empty + NS);
+  if (ARES) {
+    const int pieces = nstage * xk_astage(MB) / 2;
+    for (int e = t; e < pieces; e += blockDim.x) cp_async16(Ares + 2 * e, Aslice + 2 * e, true);
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
+  __syncthreads();
   // register budget: the kernel is compiled for (128 NW + 128) threads; the producer's warpgroup
   // hands its registers to the consumers (setmaxnreg)
   if (warp >= NCW) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
-    if (warp == NCW) xq_producer<MB, NS, BWD>(pa, ring, full, empty, c0, c1, cps, Aslice);
+    if (warp == NCW) xq_producer<MB, NS, BWD, ARES>(pa, ring, full, empty, c0, c1, cps, Aslice);
   } else if (NW == 2) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
     constexpr int MB0 = (MB + 1) / 2;
     if (warp < 4)
-      xq_consumer<MB, MB0, NS, BWD>(pa, ring, full, empty, c0, c1, slice, 0, cps);
+      xq_consumer<MB, MB0, NS, BWD, ARES>(pa, ring, full, empty, c0, c1, slice, 0, cps, Ares);
     else
-      xq_consumer<MB, MB - MB0, NS, BWD>(pa, ring, full, empty, c0, c1, slice, MB0, cps);
+      xq_consumer<MB, MB - MB0, NS, BWD, ARES>(pa, ring, full, empty, c0, c1, slice, MB0, cps, Ares);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
     constexpr int M0 = (MB + 2) / 3, M1 = (MB - M0 + 1) / 2, M2 = MB - M0 - M1;
     if (warp < 4)
-      xq_consumer<MB, M0, NS, BWD>(pa, ring, full, empty, c0, c1, slice, 0, cps);
+      xq_consumer<MB, M0, NS, BWD, ARES>(pa, ring, full, empty, c0, c1, slice, 0, cps, Ares);
     else if (warp < 8)
-      xq_consumer<MB, M1, NS, BWD>(pa, ring, full, empty, c0, c1, slice, M0, cps);
+      xq_consumer<MB, M1, NS, BWD, ARES>(pa, ring, full, empty, c0, c1, slice, M0, cps, Ares);
     else
-      xq_consumer<MB, (M2 > 0 ? M2 : 1), NS, BWD>(pa, ring, full, empty, c0, c1, slice, M0 + M1, cps);
+      xq_consumer<MB, (M2 > 0 ? M2 : 1), NS, BWD, ARES>(pa, ring, full, empty, c0, c1, slice, M0 + M1, cps, Ares);
   }
   pdl_launch();
 }
@@ -228,6 +241,12 @@ __global__ void __launch_bounds__(128 * NW + 128, 1) xformq_kernel(XformPArgs pa
 template <int MB, int NS, bool BWD>
 constexpr size_t xformq_smem() {
   return xformp_smem<MB, NS, BWD>() + NS * sizeof(unsigned long long);
+}
+// resident-matrix variant: ring of column slabs, barriers, then nstage A slabs
+template <int MB, int NS, bool BWD>
+inline size_t xformq_ares_smem(int nstage) {
+  return sizeof(double) * (static_cast<size_t>(NS) * (BWD ? XK_BSTAGE : 2 * XK_BSTAGE) +
+                           static_cast<size_t>(nstage) * xk_astage(MB)) + 2 * NS * sizeof(unsigned long long);
 }
 
 }  // namespace smpm

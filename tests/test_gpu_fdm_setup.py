@@ -74,3 +74,39 @@ def test_device_setup_rejects_unaligned_width(ctx):
     b = SchurBatch(ctx, 5, 4, 3, 1)
     with pytest.raises(SmpmError):
         b.set_fdm(npairs, T, Ti, F.strip_factors([1.0]))
+
+
+@pytest.mark.slow
+def test_device_setup_at_c5_scale(ctx):
+    """The bench's own setup path at C5 size (w = 544, k = 277,440; modes 0, 3, 8,
+    255): operators of the device-built batch against the host-built one (which
+    test_gpu_parity / test_gpu_configs hold to the oracle), the singular mode's
+    compatibility, and solves whose true residual is at the tolerance."""
+    import torch
+
+    from paper_1512_01756_b200 import configs
+    from paper_1512_01756_b200.problems import build_problem, load_batch
+
+    cfg = configs.C5
+    modes = [0, 3, 8, 255]
+    host = build_problem(cfg, modes, device="cuda", device_rhs=True)
+    dev = build_problem(cfg, modes, device="cuda", device_rhs=True, device_setup=True)
+    bh = load_batch(ctx, host)
+    bd = load_batch(ctx, dev)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    v = torch.randn((len(modes), bh.k), device="cuda", dtype=torch.float64, generator=gen)
+
+    def close(a, b, tol):
+        r = torch.linalg.norm(a - b, dim=1) / torch.linalg.norm(b, dim=1)
+        assert float(r.max()) <= tol, float(r.max())
+
+    close(bd.apply_S(v), bh.apply_S(v), 1e-10)
+    close(bd.apply_block_jacobi_inv(v), bh.apply_block_jacobi_inv(v), 1e-8)
+    close(bd.apply_P(v, fused=True), bh.apply_P(v, fused=True), 1e-9)
+    for i in range(len(modes)):
+        assert np.linalg.norm(dev.b_S[i] - host.b_S[i]) <= 1e-10 * np.linalg.norm(host.b_S[i]), i
+    bS = torch.tensor(dev.b_S, device="cuda")
+    res = bd.solve(bS, "dbj", 1e-10, 400, 0, history=False)
+    assert all(res.converged)
+    r = bd.apply_S(res.x_S) - bS
+    assert float((torch.linalg.norm(r, dim=1) / torch.linalg.norm(bS, dim=1)).max()) < 1e-9

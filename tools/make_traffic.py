@@ -34,7 +34,7 @@ def main():
     res = {"config": cfg.name, "note": "ncu --set full, --clock-control none, cold per-launch replay; bytes per "
            "launch group at the stated point", "classes": {}}
     if a.cgs:
-        ls = [x for x in launches(a.cgs) if x["kernel"].startswith("cgs")][:2]
+        ls = [x for x in launches(a.cgs) if "cgs" in x["kernel"]][:2]
         live, j = a.cgs_live, a.cgs_j
         dram = sum(x["dram_bytes"] for x in ls)
         t = sum(x["duration_s"] for x in ls)
@@ -51,8 +51,8 @@ def main():
     if a.xform:
         ls = launches(a.xform)
         live = a.xform_live
-        xf = [x for x in ls if x["kernel"].startswith(("void xformp", "xformp"))][:2]
-        spo = [x for x in ls if "spec_op2" in x["kernel"]][:1]
+        xf = [x for x in ls if "xformp" in x["kernel"] or "xformq" in x["kernel"]][:2]
+        spo = [x for x in ls if "spec_op" in x["kernel"]][:1]
         vec = live * 2.0 * k * 8
         res["classes"]["transform"] = {
             "live": live, "dram_bytes": sum(x["dram_bytes"] for x in xf),
