@@ -506,7 +506,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   // programmatic dependent launch hides launch latency when the step's kernels are short
   // (C4: +4 %); at C5 sizes (k = 277,440, ms-scale kernels) dependents that become resident
   // early only take SM resources from the running kernel (measured -5 %): auto = off above
-  // 100,000 unknowns per system
+  // 100,000 unknowns per system (also measured: chaining only the few-live-system steps of C5, -3.5 %)
   b->pdl = b->tune.pdl < 0 ? b->k <= 100000 : b->tune.pdl != 0;
   b->pythag = b->tune.pythag != 0;
   if (c.max_iter < 1) fail(SMPM_EINVAL, "max_iter must be >= 1");

@@ -162,7 +162,9 @@ void setup_xformp(smpm_batch* b) {
     const XpKernel* kern = xp_kernels(bwd, n);
     const int mbmax = kern[n - 1].MB;
     // slice counts S = S0, 2 S0, 4 S0 (per parity in the forward direction): the instance of least
-    // padding for each; variants whose padding exceeds 15 % of the rows are skipped
+    // padding for each; variants whose padding exceeds 45 % of the rows are skipped (the cost model
+    // below charges a variant its padded height, so a padded thin variant is only picked when the
+    // launch has so few columns that spreading the rows over more SMs still wins: single 2D systems)
     const int S0 = (mbt + mbmax - 1) / mbmax;
     for (int S = S0; S <= 4 * S0; S *= 2) {
       const int need = (mbt + S - 1) / S;
@@ -173,7 +175,7 @@ void setup_xformp(smpm_batch* b) {
           break;
         }
       if (MB == 0) continue;
-      if (S > S0 && static_cast<long long>(MB) * S * 100 > 115LL * mbt) continue;
+      if (S > S0 && static_cast<long long>(MB) * S * 100 > 145LL * mbt) continue;
       const int P = bwd ? S : 2 * S;
       if (P > b->ctx->num_sms) continue;
       const XpKernel& kk = xp_kernel_for(bwd, MB);
