@@ -247,6 +247,14 @@ int smpm_batch_set_allreduce(smpm_batch* b, smpm_allreduce_fn fn, void* user);
  * the call (the reference-facing end-to-end path). */
 int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x_S_host,
                     const smpm_solve_options* opt, smpm_report* reports, double* history);
+/* Starts the host -> device copy of a right-hand-side array (nsys x k, ideally
+ * pinned) on a side stream and returns at once; a later smpm_solve_host with the
+ * SAME host pointer uses that upload instead of copying.  Called for the next
+ * batch before the current smpm_solve_host, it hides the upload behind the
+ * current solve (two uploads may be outstanding; the host buffer must stay
+ * unchanged until its solve has started).  No reference counterpart: the
+ * reference's solve_3d is host-resident. */
+int smpm_prefetch_rhs(smpm_batch* b, const double* b_S_host);
 
 /* Number of kernels this library launched since the batch was created
  * (instrumentation for bench.py's gpu_launches). */

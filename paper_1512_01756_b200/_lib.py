@@ -24,7 +24,7 @@ EXPORTS = [
     "smpm_batch_set_interface_blocks", "smpm_batch_set_nullspace", "smpm_batch_set_spectral", "smpm_batch_finalize",
     "smpm_batch_coarse_info", "smpm_apply_S", "smpm_apply_St", "smpm_apply_block_jacobi_inv", "smpm_apply_Z",
     "smpm_apply_Zt", "smpm_coarse_solve", "smpm_apply_P", "smpm_apply_Q", "smpm_project_out", "smpm_solve",
-    "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_batch_launch_count",
+    "smpm_deflated_solve", "smpm_two_level_schwarz_solve", "smpm_solve_host", "smpm_prefetch_rhs", "smpm_batch_launch_count",
     "smpm_batch_profile", "smpm_fp64_peak", "smpm_batch_set_strip_factors", "smpm_batch_set_fdm", "smpm_schur_rhs",
     "smpm_recover_solution", "smpm_solve_stacked", "smpm_fourier_y", "smpm_inverse_fourier_y",
     "smpm_batch_load_schur_blocks", "smpm_batch_set_tuning", "smpm_batch_query", "smpm_batch_set_trace", "smpm_batch_set_allreduce",
@@ -123,6 +123,7 @@ def lib():
     L.smpm_deflated_solve.argtypes = [vp, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp, vp]
     L.smpm_two_level_schwarz_solve.argtypes = [vp, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp, vp]
     L.smpm_solve_host.argtypes = [vp, ip, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp]
+    L.smpm_prefetch_rhs.argtypes = [vp, dp]
     L.smpm_solve_stacked.argtypes = [vp, ip, dp, dp, C.POINTER(SolveOptions), C.POINTER(Report), dp, vp]
     L.smpm_batch_launch_count.restype = llp
     L.smpm_batch_launch_count.argtypes = [vp]

@@ -379,6 +379,12 @@ struct smpm_batch {
   // (x' = V y, M^{-1}, residual, x_S) on a side stream while the tail runs
   cudaStream_t st2 = nullptr;
   cudaEvent_t eev[3] = {nullptr, nullptr, nullptr};  // early list ready, early epilogue done, host copy done
+  // right-hand sides uploaded ahead of their solve (smpm_prefetch_rhs): two device buffers in turn
+  DevArray<double> dpf[2];
+  cudaStream_t st3 = nullptr;
+  cudaEvent_t pfev[2] = {nullptr, nullptr};
+  const double* pf_host[2] = {nullptr, nullptr};
+  int pf_next = 0;
   int* hearly = nullptr;      // pinned + mapped: nsys flags of the early set (read by solve_host)
   int* hearly_dev = nullptr;
   DevArray<int> dearly;       // [early flags, early list, count, late flags, late list, count]

@@ -623,9 +623,40 @@ int smpm_solve_host(smpm_batch* b, int method, const double* b_S_host, double* x
     const size_t bytes = sizeof(double) * b->nsys * static_cast<size_t>(b->k);
     double* din = b->vbuf[10].p;
     double* dout = b->vbuf[11].p;
-    CUDA_CHECK(cudaMemcpyAsync(din, b_S_host, bytes, cudaMemcpyHostToDevice, st));
+    // an upload started ahead by smpm_prefetch_rhs for this host buffer: wait for it instead of copying
+    // (the older of two outstanding uploads of the same buffer first: slot pf_next is the next to be refilled)
+    int hit = -1;
+    for (int i = 0; i < 2 && hit < 0; ++i) {
+      const int q = (b->pf_next + i) & 1;
+      if (b_S_host && b->pf_host[q] == b_S_host) hit = q;
+    }
+    if (hit >= 0) {
+      CUDA_CHECK(cudaStreamWaitEvent(st, b->pfev[hit], 0));
+      din = b->dpf[hit].p;
+      b->pf_host[hit] = nullptr;
+    } else {
+      CUDA_CHECK(cudaMemcpyAsync(din, b_S_host, bytes, cudaMemcpyHostToDevice, st));
+    }
     solve(b, cfg_from(method, opt), din, dout, reports, history, st, x_S_host);
     CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int smpm_prefetch_rhs(smpm_batch* b, const double* b_S_host) {
+  return guard([&] {
+    need_final(b);
+    if (!b_S_host) fail(SMPM_EINVAL, "null right-hand side");
+    const size_t n = static_cast<size_t>(b->nsys) * static_cast<size_t>(b->k);
+    if (!b->st3) {
+      CUDA_CHECK(cudaStreamCreateWithFlags(&b->st3, cudaStreamNonBlocking));
+      for (auto& e : b->pfev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int q = b->pf_next;
+    b->pf_next ^= 1;
+    b->dpf[q].alloc(n);
+    CUDA_CHECK(cudaMemcpyAsync(b->dpf[q].p, b_S_host, sizeof(double) * n, cudaMemcpyHostToDevice, b->st3));
+    CUDA_CHECK(cudaEventRecord(b->pfev[q], b->st3));
+    b->pf_host[q] = b_S_host;
   });
 }
 

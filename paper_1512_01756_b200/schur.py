@@ -353,6 +353,15 @@ class SchurBatch:
         check(lib().smpm_solve_host(self.h, METHODS[method], _hptr(b), _hptr(x), C.byref(o), reps, None))
         return self._collect(x, reps, None, 0)
 
+    def prefetch_rhs(self, b_S_host):
+        """Start the upload of a host right-hand-side array ahead of its solve_host
+        (smpm_prefetch_rhs); the array must be the very object later passed to
+        solve_host (same memory) and stay unchanged until then."""
+        b = np.ascontiguousarray(b_S_host, dtype=np.float64).reshape(self.nsys, self.k)
+        if b.ctypes.data != np.asarray(b_S_host).ctypes.data:
+            raise SmpmError(1, "prefetch_rhs needs a C-contiguous float64 array (no copy)")
+        check(lib().smpm_prefetch_rhs(self.h, _hptr(b)))
+
     def tune(self, **knobs):
         """Performance knobs (smpm_batch_set_tuning), e.g. tune(grid_max=4, pdl=0)."""
         for k, v in knobs.items():
