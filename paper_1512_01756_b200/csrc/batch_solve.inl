@@ -443,6 +443,7 @@ bool arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
   A.acount = acount;
   A.method = c.method;
   A.pythag = b->pythag ? 1 : 0;
+  A.defer = b->tune.cgs_defer && b->pythag ? 1 : 0;
   A.vcap = b->gt_vcap;
   A.G = G;
   A.P = deflate_params(b, nullptr);

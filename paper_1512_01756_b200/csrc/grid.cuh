@@ -81,6 +81,8 @@ struct GridArgs {
   const int* acount;
   int method;              // smpm_method
   int pythag;              // ||w|| from the second CGS2 reduction (as cgs3_pass2n)
+  int defer;               // spectral + pythag: the next step's T^{-1} runs on w' (before the reorthogonalisation
+                           // update, vec4.cuh), so pass 3 and that transform share one barrier interval
   int vcap;                // doubles of the tile-ring region (>= GT_SMEM / 8); with pythag, a CTA whose
                            // V rows (ncols x rows) fit there stages them once per step (gt_vblock)
   unsigned long long* trace;  // debug: 64 steps x 16 phase timestamps of CTA 0 (nullable)
@@ -464,7 +466,8 @@ __device__ __forceinline__ double gt_update(const double* Vs, long long k, int n
 // pass 3 with the norm known: w -= V h for this CTA's rows, then
 // v_{j+1} = w * inv into the basis column and the operator input (when col != nullptr)
 __device__ __forceinline__ void gt_update_scale(const double* Vs, long long k, int ncols, const double* h, double* ws,
-                                                int r0, int r1, double inv, double* col, double* vin) {
+                                                int r0, int r1, double inv, double* col, double* vin,
+                                                bool store_w = true) {
   for (int r = r0 + static_cast<int>(threadIdx.x); r < r1; r += blockDim.x) {
     double a4[4] = {0.0, 0.0, 0.0, 0.0};
     for (int i0 = 0; i0 < ncols; i0 += 16) {
@@ -475,7 +478,7 @@ __device__ __forceinline__ void gt_update_scale(const double* Vs, long long k, i
       for (int u = 0; u < 16; ++u) a4[u & 3] = fma(v[u], i0 + u < ncols ? h[i0 + u] : 0.0, a4[u & 3]);
     }
     const double nv = __ldcg(ws + r) - ((a4[0] + a4[1]) + (a4[2] + a4[3]));
-    ws[r] = nv;
+    if (store_w) ws[r] = nv;
     if (col) {
       col[r] = nv * inv;
       vin[r] = nv * inv;
@@ -837,9 +840,13 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
     // ---- pass 2: w -= V h1 ; h2 = V^T w (and ||w||^2 of the updated w)
     double sq1 = 0.0;
     if (vc) {
+      // deferred form: w' goes to global memory here, before the reduction's barrier — the next
+      // step's transform reads it right after that barrier (otherwise pass 3 writes w)
+      const bool w1_out = a.defer && a.spectral && a.pythag;
       for (int r = threadIdx.x; r < nr; r += blockDim.x) {
         const double nv = wb[r] - gt_vblock_row(vb, nr, ncols, hs, r);
         wb[r] = nv;
+        if (w1_out) ws[r0 + r] = nv;
         sq1 = fma(nv, nv, sq1);
       }
       __syncthreads();
@@ -887,26 +894,30 @@ __global__ void __launch_bounds__(G2_THREADS, GT_MINB) arnoldi_grid_kernel(GridA
         if (threadIdx.x < 32) givens_step(G, s, j, nrm);
       }
       // ---- pass 3: w -= V h2 ; v_{j+1} = w / ||w|| (own rows; unused if the system stops)
+      // deferred form (spectral): w keeps w' — the next step's transform runs on it without
+      // waiting for this update (the operator is linear; the O(eps) term is dropped exactly
+      // as in the per-stage path, vec4.cuh) — and only the basis column takes the update
       double* col = a.V + s * G.vstride + static_cast<long long>(j + 1) * k;
       const bool wr = j + 1 <= G.m;
+      const bool dfr = a.defer && a.spectral;
       if (vc) {
         const double inv = 1.0 / nrm;
         double* vs = a.vin + so;
         for (int r = threadIdx.x; r < nr; r += blockDim.x) {
           const double nv = wb[r] - gt_vblock_row(vb, nr, ncols, h2s, r);
-          ws[r0 + r] = nv;
+          if (!dfr) ws[r0 + r] = nv;
           if (wr) {
             col[r0 + r] = nv * inv;
             vs[r0 + r] = nv * inv;
           }
         }
       } else {
-        gt_update_scale(Vs, k, ncols, h2s, ws, r0, r1, 1.0 / nrm, wr ? col : nullptr, a.vin + so);
+        gt_update_scale(Vs, k, ncols, h2s, ws, r0, r1, 1.0 / nrm, wr ? col : nullptr, a.vin + so, !dfr);
       }
       mark(9);
       if (a.spectral) {
         // next step's T^{-1} v_{j+1} = T^{-1} w / ||w|| (1/||w|| applied in the per-mode pass)
-        grid_sync(a.bar, epoch);
+        if (!dfr) grid_sync(a.bar, epoch);
         BufTable f;
         f.p[BUF_IN] = a.w;
         f.p[BUF_OUT] = a.vh;
