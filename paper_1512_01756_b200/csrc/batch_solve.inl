@@ -720,12 +720,21 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     return arnoldi_grid(b, c, alist, acount, st);
   };
   int cur = 0;
-  issue(cur);
+  // a batch small enough for the tail from the start (single 2D systems) skips the per-stage
+  // first step and its host round trip: the tail's first step transforms v_0 itself
+  bool tail_first = use_grid && ns <= grid_max;
+  if (!tail_first) issue(cur);
   for (;;) {
-    // invariant here: exactly one step is in flight, in slot `cur`
+    // invariant here: exactly one step is in flight, in slot `cur` (none when tail_first)
     if (use_grid && bound <= grid_max) {
-      CUDA_CHECK(cudaEventSynchronize(ev[cur]));
-      int nrun = hcnt[2 * cur], ncyc = hcnt[2 * cur + 1];
+      int nrun = ns, ncyc = 0;
+      if (tail_first) {
+        tail_first = false;
+      } else {
+        CUDA_CHECK(cudaEventSynchronize(ev[cur]));
+        nrun = hcnt[2 * cur];
+        ncyc = hcnt[2 * cur + 1];
+      }
       if (nrun > 0) {
         if (!launch_tail(nrun)) {
           // no cooperative launch: the per-step kernels finish the solve
@@ -734,12 +743,19 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
           continue;
         }
         ++steps;
-        compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->hcnt_dev + 2 * cur);
-        check_launch(b);
-        CUDA_CHECK(cudaStreamSynchronize(st));
-        nrun = hcnt[2 * cur];
-        ncyc = hcnt[2 * cur + 1];
-        if (nrun > 0) fail(SMPM_ERUNTIME, "grid tail launch returned with running systems");
+        if (m >= mtot) {
+          // one cycle holds every allowed iteration: the tail leaves no system running or waiting
+          // for a restart, so the epilogue is queued right behind it (no host round trip)
+          nrun = 0;
+          ncyc = 0;
+        } else {
+          compact_kernel<<<1, 1024, 0, st>>>(G.active, G.state, ns, alist, acount, b->hcnt_dev + 2 * cur);
+          check_launch(b);
+          CUDA_CHECK(cudaStreamSynchronize(st));
+          nrun = hcnt[2 * cur];
+          ncyc = hcnt[2 * cur + 1];
+          if (nrun > 0) fail(SMPM_ERUNTIME, "grid tail launch returned with running systems");
+        }
       }
       if (ncyc > 0) {
         restart(ncyc);
