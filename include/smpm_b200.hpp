@@ -105,6 +105,13 @@ class System {
     check(smpm_batch_set_spectral(b_, npairs, T, T_inv, gamma));
   }
   void set_strip_factors(const smpm_strip_factors& f) { check(smpm_batch_set_strip_factors(b_, &f)); }
+  // device-side setup instead of set_couplings + set_spectral + set_strip_factors: the library
+  // builds couplings, block-Jacobi inverses and coarse data from the fast-diagonalisation factors
+  // (replaces build_kind_coupling / build_block_jacobi / build_coarse, proj/src/schur.cpp:19-69,
+  // 188-216, proj/src/deflation.cpp:24-69); w % 16 == 0
+  void set_fdm(int npairs, const double* T, const double* T_inv, const smpm_strip_factors& f) {
+    check(smpm_batch_set_fdm(b_, npairs, T, T_inv, &f));
+  }
   void finalize() { check(smpm_batch_finalize(b_)); }
 
   long long k() const { return k_; }
