@@ -110,3 +110,29 @@ def test_device_setup_at_c5_scale(ctx):
     assert all(res.converged)
     r = bd.apply_S(res.x_S) - bS
     assert float((torch.linalg.norm(r, dim=1) / torch.linalg.norm(bS, dim=1)).max()) < 1e-9
+
+
+@pytest.mark.parametrize("m_x", [2, 3, 4])
+def test_device_setup_block_edges(ctx, m_x):
+    """d = 1 (a single one-interface block, no strip solver), d = 2 (first == last
+    block) and d = 3 (a full block plus the trailing single one): the device-built
+    pool against the host-built one."""
+    import torch
+
+    from paper_1512_01756_b200.configs import Config
+    from paper_1512_01756_b200.problems import build_problem, load_batch
+
+    cfg = Config(f"edge{m_x}", 8, m_x, 4, 1.5 * m_x, 1.0, 3, True, 100, modes=3, l_y=3.0)
+    host = build_problem(cfg, [1, 2], device="cuda")
+    dev = build_problem(cfg, [1, 2], device="cuda", device_setup=True)
+    dev.b_S = host.b_S
+    bh, bd = load_batch(ctx, host), load_batch(ctx, dev)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    v = torch.randn((2, bh.k), device="cuda", dtype=torch.float64, generator=gen)
+    for op in ("apply_S", "apply_block_jacobi_inv"):
+        a, c = getattr(bd, op)(v), getattr(bh, op)(v)
+        rel = float((torch.linalg.norm(a - c, dim=1) / torch.linalg.norm(c, dim=1)).max())
+        assert rel <= 1e-10, (op, rel)
+    bS = torch.tensor(host.b_S, device="cuda")
+    rh, rd = bh.solve(bS, "dbj", 1e-10, 100, 0), bd.solve(bS, "dbj", 1e-10, 100, 0)
+    assert all(rd.converged) and max(abs(a - c) for a, c in zip(rh.iterations, rd.iterations)) <= 1
