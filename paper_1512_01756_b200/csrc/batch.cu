@@ -355,6 +355,7 @@ struct smpm_batch {
   size_t gt_smem = 0;  // tail dynamic shared memory (tile ring / V-row block region + vectors)
   int gt_vcap = 0;     // doubles of the ring / V-row block region
   DevArray<unsigned> dgbar;   // grid barrier counter
+  bool gbar_clean = false;    // zeroed by the solve prologue (gm_v0_kernel), no tail launched since
   DevArray<double> dgtpart, dgtzsum, dgtzp, dgtcg;
 
   // vectors (nsys x k each)
@@ -372,7 +373,8 @@ struct smpm_batch {
   DevArray<int> dalist;  // two compacted live lists + counts: [alist, acount, alist2, acount2]
   int* hcnt = nullptr;      // pinned + mapped, 4 ints (two in-flight step counters)
   int* hcnt_dev = nullptr;  // device alias of hcnt: compact_kernel writes the counters straight to the host
-  void* hrep = nullptr;  // pinned report staging
+  void* hrep = nullptr;  // pinned + mapped report staging (written by report_pack_kernel)
+  void* hrep_dev = nullptr;  // its device alias
   size_t hrep_bytes = 0;
   cudaEvent_t sev[4] = {nullptr, nullptr, nullptr, nullptr};  // solve events (timing x2, step polling x2)
   // early epilogue: the systems already stopped when the grid tail starts are finished

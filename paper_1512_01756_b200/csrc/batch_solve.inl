@@ -265,6 +265,29 @@ void arnoldi_step(smpm_batch* b, const SolveCfg& c, const Live& lv, cudaStream_t
   ++b->jhost;
 }
 
+// Report staging: four double arrays and one int array gathered into one mapped host block
+__global__ void report_pack_kernel(const double* __restrict__ a0, long long n0, const double* __restrict__ a1,
+                                   long long n1, const double* __restrict__ a2, long long n2,
+                                   const double* __restrict__ a3, long long n3, const int* __restrict__ ai,
+                                   long long ni, double* __restrict__ outd, int* __restrict__ outi) {
+  pdl_wait();
+  pdl_launch();
+  const long long nd = n0 + n1 + n2 + n3;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < nd + ni;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (e < n0)
+      outd[e] = a0[e];
+    else if (e < n0 + n1)
+      outd[e] = a1[e - n0];
+    else if (e < n0 + n1 + n2)
+      outd[e] = a2[e - n0 - n1];
+    else if (e < nd)
+      outd[e] = a3[e - n0 - n1 - n2];
+    else
+      outi[e - nd] = ai[e - nd];
+  }
+}
+
 // Compacted list of live systems (ascending index, so deterministic) from a
 // flag array, plus RUN / CYCLE state counts for the host; single CTA.
 __global__ void __launch_bounds__(1024) compact_kernel(const int* flags, const int* state, int nsys, int* alist,
@@ -461,7 +484,9 @@ bool arnoldi_grid(smpm_batch* b, const SolveCfg& c, const int* alist, const int*
     CUDA_CHECK(cudaMemsetAsync(dtr2.p, 0, dtr2.n * sizeof(unsigned long long), st));
     A.trace2 = dtr2.p;
   }
-  CUDA_CHECK(cudaMemsetAsync(b->dgbar.p, 0, sizeof(unsigned), st));
+  // the first tail of a solve finds the barrier word zeroed by gm_v0_kernel
+  if (!b->gbar_clean) CUDA_CHECK(cudaMemsetAsync(b->dgbar.p, 0, sizeof(unsigned), st));
+  b->gbar_clean = false;
   cfg.gridDim = dim3(nb);
   // opt-in plain cluster launch (profilers only: co-residency is then not guaranteed)
   cfg.numAttrs = b->tune.grid_nocoop ? 1 : 2;
@@ -555,28 +580,45 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   int* acount2 = alist2 + ns;
 
   // ---- right-hand side
+  const bool keep_cb = c.method == SMPM_DBJ && c.fused && !c.stacked;
   if (c.method == SMPM_DBJ) {
     op_P(b, bS, rhs, c.fused, all, st);  // pb = P b_S (proj/src/deflation.cpp:110)
-    // keep c_b = C^{-1} Z^T b_S for the solution (proj/src/deflation.cpp:118-120)
-    if (c.fused)
+    // keep c_b = C^{-1} Z^T b_S for the solution (proj/src/deflation.cpp:118-120):
+    // copied by norm2_start_kernel (stacked: here)
+    if (c.fused && c.stacked)
       CUDA_CHECK(cudaMemcpyAsync(b->dczb.p, b->dcoarse.p + static_cast<size_t>(ns) * b->d,
                                  sizeof(double) * ns * b->d, cudaMemcpyDeviceToDevice, st));
   } else {
     CUDA_CHECK(cudaMemcpyAsync(rhs, bS, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
   }
-  batched_dot(b, bS, bS, nb2, nullptr, st);
-  batched_dot(b, rhs, rhs, nr2, nullptr, st);
-  if (c.stacked) {  // ||b|| and ||rhs|| of the stacked vector (proj/src/helmholtz.cpp:193-201)
+  dim3 vg(std::max(1, std::min(G.nchunk, 64)), ns);
+  if (c.stacked) {
+    batched_dot(b, bS, bS, nb2, nullptr, st);
+    batched_dot(b, rhs, rhs, nr2, nullptr, st);
+    // ||b|| and ||rhs|| of the stacked vector (proj/src/helmholtz.cpp:193-201)
     stack_sum(b, nb2, st);
     stack_sum(b, nr2, st);
+    launch_pdl(b, gm_start_kernel, dim3((ns + 127) / 128), dim3(128), 0, st, G, static_cast<const double*>(nr2),
+               static_cast<const double*>(nb2), c.tol, 1, static_cast<const int*>(nullptr));
+  } else {
+    // both norms, the GMRES start of each system and the copy of c_b in one launch
+    // (the same bits as two batched_dot launches + gm_start_kernel)
+    const Chunking ck = chunking(b);
+    b->dpart.alloc(std::max<size_t>(b->dpart.n, 2 * static_cast<size_t>(ns) * ck.nchunk));
+    launch_pdl(b, norm2_start_kernel, dim3(ck.nchunk, ns), dim3(VEC_THREADS), 0, st, G, b->k, ck.chunk, ck.nchunk, bS,
+               static_cast<const double*>(rhs), b->dpart.p, b->dcount.p, nb2, nr2, c.tol,
+               static_cast<const double*>(keep_cb ? b->dcoarse.p + static_cast<size_t>(ns) * b->d : nullptr),
+               keep_cb ? b->dczb.p : static_cast<double*>(nullptr), b->d);
   }
-  CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double) * nk, st));
-  launch_pdl(b, gm_start_kernel, dim3((ns + 127) / 128), dim3(128), 0, st, G, static_cast<const double*>(nr2),
-             static_cast<const double*>(nb2), c.tol, 1, static_cast<const int*>(nullptr));
-  dim3 vg(std::max(1, std::min(G.nchunk, 64)), ns);
-  launch_pdl(b, gm_v0_kernel, vg, dim3(256), 0, st, G, b->dV.p, static_cast<const double*>(rhs), vin);
-  launch_pdl(b, compact_kernel, dim3(1), dim3(1024), 0, st, static_cast<const int*>(G.active),
-             static_cast<const int*>(nullptr), ns, alist, acount, static_cast<int*>(nullptr));
+  // v_0, x = 0 and the tail's barrier word in one launch
+  // (and the list of live systems, up to one block's worth of systems)
+  const bool v0_lists = ns <= 256;
+  launch_pdl(b, gm_v0_kernel, vg, dim3(256), 0, st, G, b->dV.p, static_cast<const double*>(rhs), vin, x,
+             b->dgbar.p, v0_lists ? alist : static_cast<int*>(nullptr), v0_lists ? acount : static_cast<int*>(nullptr));
+  b->gbar_clean = true;
+  if (!v0_lists)
+    launch_pdl(b, compact_kernel, dim3(1), dim3(1024), 0, st, static_cast<const int*>(G.active),
+               static_cast<const int*>(nullptr), ns, alist, acount, static_cast<int*>(nullptr));
   G.alist = alist;
   G.acount = acount;
   b->jhost = 0;
@@ -642,7 +684,7 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
     if (c.stacked) stack_sum(b, nr2, st);
     gm_start_kernel<<<(ns + 127) / 128, 128, 0, st>>>(G, nr2, nb2, c.tol, 0, G.state);
     check_launch(b);
-    gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, r, vin);
+    gm_v0_kernel<<<vg, 256, 0, st>>>(G, b->dV.p, r, vin, nullptr, nullptr, nullptr, nullptr);
     check_launch(b);
     compact_kernel<<<1, 1024, 0, st>>>(G.active, nullptr, ns, alist, acount, nullptr);
     check_launch(b);
@@ -903,7 +945,9 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   if (b->hrep_bytes < rep_bytes) {
     if (b->hrep) cudaFreeHost(b->hrep);
     b->hrep = nullptr;
-    CUDA_CHECK(cudaMallocHost(&b->hrep, rep_bytes));
+    b->hrep_dev = nullptr;
+    CUDA_CHECK(cudaHostAlloc(&b->hrep, rep_bytes, cudaHostAllocMapped));
+    CUDA_CHECK(cudaHostGetDevicePointer(&b->hrep_dev, b->hrep, 0));
     b->hrep_bytes = rep_bytes;
   }
   double* hsc_p = reinterpret_cast<double*>(b->hrep);
@@ -912,12 +956,16 @@ void solve(smpm_batch* b, const SolveCfg& c, const double* bS, double* xS, smpm_
   double* hh_p = hsm_p + static_cast<size_t>(ns) * 3;
   int* hint_p = reinterpret_cast<int*>(hh_p + rep_hist);
   if (reps || history) {
-    CUDA_CHECK(cudaMemcpyAsync(hint_p, b->dgint.p, sizeof(int) * ns * 8, cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaMemcpyAsync(hsc_p, b->dscal.p, sizeof(double) * ns * 8, cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaMemcpyAsync(hg_p, b->dg.p, sizeof(double) * ns * (m + 1), cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaMemcpyAsync(hsm_p, sc, sizeof(double) * ns * 3, cudaMemcpyDeviceToHost, st));
-    if (history)
-      CUDA_CHECK(cudaMemcpyAsync(hh_p, b->dhist.p, sizeof(double) * rep_hist, cudaMemcpyDeviceToHost, st));
+    // one kernel writes the five report arrays straight into the mapped staging block
+    // (was: one device-to-host copy each)
+    double* dd = reinterpret_cast<double*>(b->hrep_dev);
+    const long long n0 = static_cast<long long>(ns) * 8, n1 = static_cast<long long>(ns) * (m + 1),
+                    n2 = static_cast<long long>(ns) * 3, n3 = static_cast<long long>(rep_hist);
+    const long long tot = n0 + n1 + n2 + n3 + n0;
+    launch_pdl(b, report_pack_kernel, dim3(static_cast<unsigned>(std::min<long long>((tot + 255) / 256, 64))), dim3(256),
+               0, st, static_cast<const double*>(b->dscal.p), n0, static_cast<const double*>(b->dg.p), n1,
+               static_cast<const double*>(sc), n2, static_cast<const double*>(history ? b->dhist.p : nullptr), n3,
+               static_cast<const int*>(b->dgint.p), n0, dd, reinterpret_cast<int*>(dd + n0 + n1 + n2 + n3));
   }
   CUDA_CHECK(cudaEventRecord(e1, st));
   CUDA_CHECK(cudaEventSynchronize(e1));

@@ -602,19 +602,13 @@ __global__ void project_kernel(int nsys, long long k, const double* __restrict__
 
 // ---- GMRES cycle start: bnorm/target on the first cycle, g0, v0 = r / ||r|| ----
 // nrm2sq: ||r||^2 per system; first: 1 on the first cycle.
-__global__ void gm_start_kernel(GmState_ G, const double* __restrict__ nrm2sq, const double* __restrict__ bs_nrm2sq,
-                                double tol, int first, const int* __restrict__ restart_mask) {
-  pdl_wait();
-  pdl_launch();
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= G.nsys) return;
-  if (!first && !(restart_mask && restart_mask[s] == GM_CYCLE)) return;
-  const double rn = sqrt(nrm2sq[s]);
+__device__ __forceinline__ void gm_start_one(GmState_& G, int s, double nrm2sq, double bs_nrm2sq, double tol, int first) {
+  const double rn = sqrt(nrm2sq);
   const int m = G.m;
   if (first) {
     G.bnorm[s] = rn;
     // abs target = tol * ||b_S|| (proj/src/deflation.cpp:109)
-    G.target[s] = tol * sqrt(bs_nrm2sq[s]);
+    G.target[s] = tol * sqrt(bs_nrm2sq);
     G.hmax[s] = 0.0;
     G.iters[s] = 0;
     G.hist_len[s] = 1;
@@ -630,12 +624,108 @@ __global__ void gm_start_kernel(GmState_ G, const double* __restrict__ nrm2sq, c
   G.active[s] = go ? 1 : 0;
 }
 
-// v0 = r / ||r|| into V[:,0] and vin, for systems just (re)started
+__global__ void gm_start_kernel(GmState_ G, const double* __restrict__ nrm2sq, const double* __restrict__ bs_nrm2sq,
+                                double tol, int first, const int* __restrict__ restart_mask) {
+  pdl_wait();
+  pdl_launch();
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= G.nsys) return;
+  if (!first && !(restart_mask && restart_mask[s] == GM_CYCLE)) return;
+  gm_start_one(G, s, nrm2sq[s], first ? bs_nrm2sq[s] : 0.0, tol, first);
+}
+
+// First cycle of an independent (not stacked) solve in one launch: ||b_S||^2 and ||rhs||^2
+// per system (same chunks and summation order as two batched_dot_kernel launches, so the
+// same bits), then the last CTA of each system starts its GMRES state (gm_start_one) and
+// keeps c_b (csrc -> cdst, d doubles per system; nullable)
+__global__ void __launch_bounds__(VEC_THREADS) norm2_start_kernel(GmState_ G, long long k, int chunk, int nchunk,
+                                                                  const double* __restrict__ bs,
+                                                                  const double* __restrict__ rhs,
+                                                                  double* __restrict__ part, int* counter,
+                                                                  double* __restrict__ nb2, double* __restrict__ nr2,
+                                                                  double tol, const double* __restrict__ csrc,
+                                                                  double* __restrict__ cdst, int d) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ double red[2][32];
+  const int s = blockIdx.y;
+  const int ch = blockIdx.x;
+  const long long r0 = static_cast<long long>(ch) * chunk, r1 = min(k, r0 + chunk);
+  const double* xs = bs + s * k;
+  const double* ys = rhs + s * k;
+  double a0 = 0.0, a1 = 0.0;
+  for (long long r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const double xv = xs[r], yv = ys[r];
+    a0 = fma(xv, xv, a0);
+    a1 = fma(yv, yv, a1);
+  }
+  a0 = warp_sum(a0);
+  a1 = warp_sum(a1);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = a0;
+    red[1][threadIdx.x >> 5] = a1;
+  }
+  __syncthreads();
+  double* p0 = part + static_cast<long long>(s) * nchunk;
+  double* p1 = part + (static_cast<long long>(G.nsys) + s) * nchunk;
+  if (threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int q = 0; q < (blockDim.x >> 5); ++q) {
+      t0 += red[0][q];
+      t1 += red[1][q];
+    }
+    p0[ch] = t0;
+    p1[ch] = t1;
+  }
+  if (last_cta(counter + s, nchunk)) {
+    if (threadIdx.x == 0) {
+      double t0 = 0.0, t1 = 0.0;
+      for (int c = 0; c < nchunk; ++c) {
+        t0 += p0[c];
+        t1 += p1[c];
+      }
+      nb2[s] = t0;
+      nr2[s] = t1;
+      gm_start_one(G, s, t1, t0, tol, 1);
+    }
+    if (cdst)
+      for (int i = threadIdx.x; i < d; i += blockDim.x)
+        cdst[static_cast<long long>(s) * d + i] = csrc[static_cast<long long>(s) * d + i];
+  }
+}
+
+// v0 = r / ||r|| into V[:,0] and vin, for systems just (re)started; first cycle: also
+// x = 0 for every system (xzero) and the grid tail's barrier word (zero_word)
+// and the compacted list of the live systems (alist / acount, ascending; nsys <= blockDim.x)
 __global__ void gm_v0_kernel(GmState_ G, double* __restrict__ V, const double* __restrict__ r,
-                             double* __restrict__ vin) {
+                             double* __restrict__ vin, double* __restrict__ xzero, unsigned* zero_word,
+                             int* __restrict__ alist, int* __restrict__ acount) {
   pdl_wait();
   pdl_launch();
   const int s = blockIdx.y;
+  if (zero_word && blockIdx.x == 0 && s == 0 && threadIdx.x == 0) *zero_word = 0u;
+  if (alist && blockIdx.x == 0 && s == 0) {
+    __shared__ int wsum[32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int f = (t < G.nsys && G.active[t]) ? 1 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0;
+    for (int q = 0; q < warp; ++q) off += wsum[q];
+    if (f) alist[off + __popc(bal & ((1u << lane) - 1u))] = t;
+    if (t == 0) {
+      int tot = 0;
+      for (int q = 0; q < (blockDim.x >> 5); ++q) tot += wsum[q];
+      *acount = tot;
+    }
+  }
+  if (xzero) {
+    double* xs = xzero + s * G.k;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < G.k;
+         e += static_cast<long long>(gridDim.x) * blockDim.x)
+      xs[e] = 0.0;
+  }
   if (!G.active[s] || G.jcyc[s] != 0) return;
   const double inv = 1.0 / G.nrm[s];
   double* col = V + s * G.vstride;
