@@ -83,16 +83,26 @@ __device__ void coarse_solve_block(const DeflateParams& P, int s, double* sums, 
       for (int i = t; i < 3 * d; i += blockDim.x) band[i] = gsrc[i];
     __syncthreads();
     if (t == 0) {
-      const double* sub = staged ? band : gsrc;
-      const double* cp = sub + d;
-      const double* rpiv = cp + d;
-      double yprev = sums[0] * rpiv[0];
-      c[0] = yprev;
+      // the recurrences carry their value in a register (one fma, or fma + mul, per step on
+      // the serial chain); every load is independent of the chain and unrolled ahead of it
+      const double* __restrict__ sub = staged ? band : gsrc;
+      const double* __restrict__ cp = sub + d;
+      const double* __restrict__ rpiv = cp + d;
+      const double* __restrict__ rhs = sums;
+      double* __restrict__ co = c;
+      double yprev = rhs[0] * rpiv[0];
+      co[0] = yprev;
+#pragma unroll 8
       for (int i = 1; i < d; ++i) {
-        yprev = (sums[i] - sub[i - 1] * yprev) * rpiv[i];
-        c[i] = yprev;
+        yprev = fma(-sub[i - 1], yprev, rhs[i]) * rpiv[i];
+        co[i] = yprev;
       }
-      for (int i = d - 2; i >= 0; --i) c[i] -= cp[i] * c[i + 1];
+      double cn = yprev;
+#pragma unroll 8
+      for (int i = d - 2; i >= 0; --i) {
+        cn = fma(-cp[i], cn, co[i]);
+        co[i] = cn;
+      }
     }
   } else {
     const double* ci = P.cinv + static_cast<long long>(s) * d * d;
