@@ -30,7 +30,7 @@ EXPORTS = [
     "smpm_batch_load_schur_blocks", "smpm_batch_set_tuning", "smpm_batch_query", "smpm_batch_set_trace", "smpm_batch_set_allreduce",
 ]
 # smpm_batch_set_tuning keys (include/smpm_b200.h)
-TUNING_KEYS = ["segb", "spec_v2", "xform", "xform_parity", "xform_ws", "xform_ares", "sp_stage", "spectral", "spec_2las", "p2fuse", "cgs_defer", "cgs_lanes", "gt_vblock", "grid_per_sm", "gt_ctas",
+TUNING_KEYS = ["segb", "spec_v2", "xform", "xform_parity", "xform_ws", "xform_ares", "sp_stage", "spectral", "spec_2las", "p2fuse", "cgs_defer", "cgs_lanes", "gt_vblock", "grid_per_sm", "gt_ctas", "coarse_fork",
                "grid_nocoop", "pdl", "pythag", "grid", "grid_max", "tail_rows", "post_fuse", "early"]
 PROFILE_CLASSES = ["schur_gemm", "bj_gemm", "deflation", "orthogonalization", "other", "reserved5", "grid_tail",
                    "spectral_op", "transform", "reserved"]

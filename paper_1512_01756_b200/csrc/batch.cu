@@ -265,6 +265,7 @@ struct Tuning {
   int gt_vblock = 2;     // grid tail V-row block: 0 off, 1 ring size, 2 as large as 2 CTAs/SM allow
   int grid_per_sm = 2;   // grid tail CTAs per SM (cap)
   int gt_ctas = 0;       // grid tail CTA cap (0: none)
+  int coarse_fork = 1;   // per-stage steps without PDL: coarse solve on a side stream beside the T transform
   int grid_nocoop = 0;   // opt-in: plain (non-cooperative) cluster launch of the tail, for profilers only
   int pdl = -1;          // programmatic dependent launch of the step chain: 1 on, 0 off, -1 auto (on for k <= 100,000)
   int pythag = 1;        // norm from the second CGS2 reduction
@@ -380,6 +381,9 @@ struct smpm_batch {
   // early epilogue: the systems already stopped when the grid tail starts are finished
   // (x' = V y, M^{-1}, residual, x_S) on a side stream while the tail runs
   cudaStream_t st2 = nullptr;
+  cudaStream_t st4 = nullptr;              // coarse solves beside the T transform (spec_SMinv)
+  cudaEvent_t cfev[2] = {nullptr, nullptr};
+  DevArray<double> dzsum;                  // nsys x d coarse right-hand sides for that kernel
   cudaEvent_t eev[3] = {nullptr, nullptr, nullptr};  // early list ready, early epilogue done, host copy done
   // right-hand sides uploaded ahead of their solve (smpm_prefetch_rhs): two device buffers in turn
   DevArray<double> dpf[2];
@@ -396,6 +400,9 @@ struct smpm_batch {
     for (auto e : eev)
       if (e) cudaEventDestroy(e);
     if (st2) cudaStreamDestroy(st2);
+    if (st4) cudaStreamDestroy(st4);
+    for (auto e : cfev)
+      if (e) cudaEventDestroy(e);
     if (hearly) cudaFreeHost(hearly);
     if (hcnt) cudaFreeHost(hcnt);
     if (hrep) cudaFreeHost(hrep);

@@ -686,7 +686,7 @@ int smpm_batch_set_tuning(smpm_batch* b, const char* key, long long value) {
     const Knob knobs[] = {{"segb", &t.segb}, {"spec_v2", &t.spec_v2}, {"xform", &t.xform}, {"xform_parity", &t.xform_parity}, {"xform_ws", &t.xform_ws}, {"xform_ares", &t.xform_ares},
                           {"sp_stage", &t.sp_stage},
                           {"spectral", &t.spectral}, {"spec_2las", &t.spec_2las}, {"p2fuse", &t.p2fuse}, {"cgs_defer", &t.cgs_defer}, {"cgs_lanes", &t.cgs_lanes},
-                          {"gt_vblock", &t.gt_vblock}, {"grid_per_sm", &t.grid_per_sm}, {"gt_ctas", &t.gt_ctas},
+                          {"gt_vblock", &t.gt_vblock}, {"grid_per_sm", &t.grid_per_sm}, {"gt_ctas", &t.gt_ctas}, {"coarse_fork", &t.coarse_fork},
                           {"grid_nocoop", &t.grid_nocoop}, {"pdl", &t.pdl}, {"pythag", &t.pythag},
                           {"grid", &t.grid}, {"grid_max", &t.grid_max}, {"post_fuse", &t.post_fuse},
                           {"early", &t.early}};

@@ -350,8 +350,9 @@ void run_xform(smpm_batch* b, bool inverse, const double* in, double* out, const
 
 // th = S^ M^^{-1} vh (bj) or S^ vh in T-coordinates; with cout, also
 // c = C^{-1} Z^T (T th) per system (deflation coarse solve)
+// (sums_only, spec_op3_kernel only: cout receives the coarse right-hand sides instead)
 void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* cout, const Live& lv, cudaStream_t st,
-                double* uh = nullptr, const double* cadd = nullptr) {
+                double* uh = nullptr, const double* cadd = nullptr, bool sums_only = false) {
   if (lv.nslots == 0) return;
   ProfScope ps(b, 7, st);  // class 7: per-mode pass
   SpecParams sp = spec_params(b);
@@ -377,10 +378,10 @@ void spec_apply(smpm_batch* b, bool bj, const double* vh, double* th, double* co
     if (v3) {
       if (bj)
         launch_pdl(b, spec_op3_kernel<true>, grid2, dim3(SP_THREADS), shm2, st, sp, vh, th, P, zp, b->dcount.p, cout,
-                   uh);
+                   uh, sums_only ? 1 : 0);
       else
         launch_pdl(b, spec_op3_kernel<false>, grid2, dim3(SP_THREADS), shm2, st, sp, vh, th, P, zp, b->dcount.p, cout,
-                   uh);
+                   uh, sums_only ? 1 : 0);
       return;
     }
     if (bj)
@@ -430,8 +431,36 @@ bool spec_2las(const smpm_batch* b, const SolveCfg& c) {
 // S M^{-1} v (bj) or S v through the spectral form; out may be any buffer
 void spec_SMinv(smpm_batch* b, bool bj, const double* v, double* out, double* cout, const Live& lv, cudaStream_t st) {
   run_xform(b, true, v, b->dvh.p, lv, st);
-  spec_apply(b, bj, b->dvh.p, b->dth.p, cout, lv, st);
+  // The coarse solve is a serial recurrence (Thomas, d steps of dependent fp64 operations: 20 us
+  // at d = 255) that the per-mode pass's last CTA per system ran with the rest of the GPU idle
+  // (ncu: SMs active 28 % of a launch with two live systems).  Its result is first needed after
+  // the T transform (fused P of pass 1B), so without programmatic launch chaining (large
+  // systems) it runs in zt_coarse_kernel on a side stream beside that transform.
+  const bool fork = cout && !b->pdl && b->tune.coarse_fork && b->tune.spec_v2 >= 2 && lv.nslots > 0;
+  if (!fork) {
+    spec_apply(b, bj, b->dvh.p, b->dth.p, cout, lv, st);
+    run_xform(b, false, b->dth.p, out, lv, st);
+    return;
+  }
+  if (!b->st4) {
+    int lo = 0, hi = 0;
+    CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_CHECK(cudaStreamCreateWithPriority(&b->st4, cudaStreamNonBlocking, hi));
+    for (auto& e : b->cfev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  b->dzsum.alloc(std::max<size_t>(b->dzsum.n, static_cast<size_t>(b->nsys) * b->d));
+  spec_apply(b, bj, b->dvh.p, b->dth.p, b->dzsum.p, lv, st, nullptr, nullptr, true);
+  CUDA_CHECK(cudaEventRecord(b->cfev[0], st));
+  CUDA_CHECK(cudaStreamWaitEvent(b->st4, b->cfev[0], 0));
+  DeflateParams P = deflate_params(b, lv.active);
+  P.alist = lv.alist;
+  P.acount = lv.acount;
+  zt_coarse_kernel<<<dim3(1, lv.nslots), V2_THREADS, sizeof(double) * 2 * static_cast<size_t>(b->d), b->st4>>>(
+      P, b->dzsum.p, b->dcoarse.p, cout, b->dcount.p, 1);
+  check_launch(b);
+  CUDA_CHECK(cudaEventRecord(b->cfev[1], b->st4));
   run_xform(b, false, b->dth.p, out, lv, st);
+  CUDA_CHECK(cudaStreamWaitEvent(st, b->cfev[1], 0));
 }
 
 // the preconditioned operator GMRES iterates on (proj/src/deflation.cpp:105-107,131; proj/src/gmres.cpp:144-150)

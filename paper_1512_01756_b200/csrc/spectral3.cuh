@@ -208,11 +208,13 @@ __host__ __device__ __forceinline__ int spec3_chunks(int npairs, int nmode) {
   return spec3_pair_chunks(npairs) + (((nmode - npairs) >> 1) + 31) / 32;
 }
 
-// grid (chunks * ceil(nseg / SP_WARPS), live slots); zpart: nsys x chunks x d
+// grid (chunks * ceil(nseg / SP_WARPS), live slots); zpart: nsys x chunks x d; cout: the coarse
+// solutions c = C^{-1} Z^T t, or (sums_only) the coarse right-hand sides Z^T t
 template <bool BJ>
 __global__ void __launch_bounds__(SP_THREADS, 4) spec_op3_kernel(SpecParams sp, const double* __restrict__ vh,
                                                               double* __restrict__ th, DeflateParams P, double* zpart,
-                                                              int* counter, double* cout, double* __restrict__ uh) {
+                                                              int* counter, double* cout, double* __restrict__ uh,
+                                                              int sums_only) {
   pdl_wait();
   extern __shared__ double sm3[];  // 2 d doubles (coarse solve)
   int s;
@@ -236,7 +238,11 @@ __global__ void __launch_bounds__(SP_THREADS, 4) spec_op3_kernel(SpecParams sp, 
     double v = 0.0;
     for (int q = 0; q < nch; ++q) v += __ldcg(zpart + (static_cast<long long>(s) * nch + q) * sp.d + i);
     sums[i] = v;
+    // sums_only: the coarse right-hand side goes out as it is; the (serial) coarse solve runs in
+    // zt_coarse_kernel on a side stream beside the T transform (spec_SMinv)
+    if (sums_only) cout[static_cast<long long>(s) * sp.d + i] = v;
   }
+  if (sums_only) return;
   __syncthreads();
   coarse_solve_block(P, s, sums, c);
   for (int i = threadIdx.x; i < sp.d; i += blockDim.x) cout[static_cast<long long>(s) * sp.d + i] = c[i];

@@ -62,6 +62,24 @@ def test_helmholtz_modes_batched(ctx):
     check_solve(case, b, "2las", max_iter=100)
 
 
+def test_more_systems_than_one_block(ctx):
+    # 300 systems: beyond the 256 the solve prologue lists inside gm_v0_kernel, so the
+    # compact_kernel fallback builds the live list (batch_solve.inl); oracle on a sample
+    mus = [(2 * np.pi * j / 400.0) ** 2 for j in range(300)]
+    case = build_case(5, 4, 2, 4.0, 1.0, mus, kmax=3, decay=True)
+    b = gpu_batch(ctx, case)
+    import torch
+
+    res = b.solve(torch.tensor(case.b_S, device="cuda"), "dbj", 1e-10, 100, 0, history=False)
+    x = res.x_S.cpu().numpy()
+    assert all(res.converged)
+    for i in (0, 1, 128, 255, 256, 257, 299):
+        ref = case.systems[i].solve(case.b_S[i], "dbj", 1e-10, 100, 0)
+        assert abs(res.iterations[i] - ref.iterations) <= 1, (i, res.iterations[i], ref.iterations)
+        a, r = (x[i] - x[i].mean(), ref.x_S - ref.x_S.mean()) if case.mus[i] == 0.0 else (x[i], ref.x_S)
+        assert rel(a, r) < 1e-9, (i, rel(a, r))
+
+
 def test_restart(ctx):
     # GMRES(m) restart extension: oracle and GPU restart identically
     case = build_case(6, 6, 4, 24.0, 4.0, (0.0,))
