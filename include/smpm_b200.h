@@ -271,7 +271,7 @@ int smpm_batch_profile(smpm_batch* b, int enable, double* ms, long long* counts,
 
 /* Performance knobs of a batch (no reference counterpart; defaults are the
  * measured-best settings). Keys: segb, spec_v2, xform, sp_stage, spectral, spec_2las,
- * p2fuse, cgs_defer, cgs_lanes, xform_parity, gt_vblock, grid_per_sm, gt_ctas, grid_nocoop (profilers only: the
+ * p2fuse, cgs_defer, cgs_lanes, xform_parity, gt_vblock, grid_per_sm, gt_ctas, coarse_fork, grid_nocoop (profilers only: the
  * tail then launches without the co-residency guarantee of a cooperative
  * launch), pdl, pythag, grid, grid_max, tail_rows (the tail runs only while
  * live systems x k <= tail_rows; default 200000), post_fuse, early; with b = NULL:
