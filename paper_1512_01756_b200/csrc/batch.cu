@@ -265,7 +265,7 @@ struct Tuning {
   int gt_vblock = 2;     // grid tail V-row block: 0 off, 1 ring size, 2 as large as 2 CTAs/SM allow
   int grid_per_sm = 2;   // grid tail CTAs per SM (cap)
   int gt_ctas = 0;       // grid tail CTA cap (0: none)
-  int coarse_fork = 1;   // per-stage steps without PDL: coarse solve on a side stream beside the T transform
+  int coarse_fork = 1;   // per-stage steps: coarse solve on a side stream beside the T transform
   int grid_nocoop = 0;   // opt-in: plain (non-cooperative) cluster launch of the tail, for profilers only
   int pdl = -1;          // programmatic dependent launch of the step chain: 1 on, 0 off, -1 auto (on for k <= 100,000)
   int pythag = 1;        // norm from the second CGS2 reduction

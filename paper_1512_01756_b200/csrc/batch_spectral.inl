@@ -434,9 +434,10 @@ void spec_SMinv(smpm_batch* b, bool bj, const double* v, double* out, double* co
   // The coarse solve is a serial recurrence (Thomas, d steps of dependent fp64 operations: 20 us
   // at d = 255) that the per-mode pass's last CTA per system ran with the rest of the GPU idle
   // (ncu: SMs active 28 % of a launch with two live systems).  Its result is first needed after
-  // the T transform (fused P of pass 1B), so without programmatic launch chaining (large
-  // systems) it runs in zt_coarse_kernel on a side stream beside that transform.
-  const bool fork = cout && !b->pdl && b->tune.coarse_fork && b->tune.spec_v2 >= 2 && lv.nslots > 0;
+  // the T transform (fused P of pass 1B), so it runs in zt_coarse_kernel on a side stream beside
+  // that transform (C5 +1.6 %; C4, where the events cut the programmatic launch chain once per
+  // step, still +3 %).
+  const bool fork = cout && b->tune.coarse_fork && b->tune.spec_v2 >= 2 && lv.nslots > 0;
   if (!fork) {
     spec_apply(b, bj, b->dvh.p, b->dth.p, cout, lv, st);
     run_xform(b, false, b->dth.p, out, lv, st);
